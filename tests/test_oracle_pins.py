@@ -1,0 +1,367 @@
+"""Pins for the fp64 oracle (tier rule ③): each test checks the oracle against
+something other than itself -- a value SPEC/PAPER fixes for a worked example,
+a closed form derived from Eq. 1, an invariant the paper states, a library
+routine (scipy / scikit-learn), or brute force.  CPU only.
+
+P:n = PAPER.md line n, S:n = SPEC.md line n.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import scipy.linalg
+from scipy.sparse import csr_matrix
+from scipy.sparse.csgraph import shortest_path
+
+from oracle import core, layout
+from workloads import graphs
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def gold(key):
+    return GOLD[key]["value"]
+
+
+# ----------------------------------------------------------- Eq. 1 (stress)
+
+def test_stress_worked_examples():
+    """S:134-136 worked examples of Eq. 1 with w = d^-2."""
+    p3 = graphs.path_graph(3)
+    assert core.stress(np.array([[0.0], [1.0], [2.0]]), core.hop_matrix(p3), 1.0) == gold("stress_p3_collinear")
+    c4 = graphs.cycle_graph(4)
+    f = core.stress(np.array([[0.0, 0], [1, 0], [1, 1], [0, 1]]), core.hop_matrix(c4), 1.0)
+    assert f == pytest.approx(3 - 2 * math.sqrt(2), rel=1e-14)
+    assert f == pytest.approx(gold("stress_c4_unit_square"), rel=1e-14)
+    e = graphs.path_graph(2)
+    assert core.stress(np.zeros((2, 2)), core.hop_matrix(e), 1.0) == gold("stress_collapsed_edge")
+
+
+def test_stress_brute_force_tiny():
+    """Eq. 1 re-evaluated by brute force over all i<j with scipy's BFS hops."""
+    rng = np.random.default_rng(7)
+    for t in range(5):
+        g = graphs.random_connected_graph(9, 5, seed=t)
+        X = rng.normal(size=(9, 2))
+        k = 0.7
+        a = csr_matrix((np.ones(g.col.size), g.col, g.row_ptr), shape=(g.n, g.n))
+        D = k * shortest_path(a, unweighted=True)
+        ref = 0.0
+        for i in range(9):
+            for j in range(i + 1, 9):
+                r = math.dist(X[i], X[j])
+                ref += D[i, j] ** -2 * (r - D[i, j]) ** 2
+        assert core.stress(X, core.hop_matrix(g), k) == pytest.approx(ref, rel=1e-13)
+
+
+def test_stress_invariances():
+    """Eq. 1 depends only on pairwise distances: translation, rotation and
+    reflection invariance."""
+    rng = np.random.default_rng(3)
+    g = graphs.random_connected_graph(12, 8, seed=1)
+    hop = core.hop_matrix(g)
+    X = rng.normal(size=(12, 3))
+    f = core.stress(X, hop, 0.5)
+    Q, _ = np.linalg.qr(rng.normal(size=(3, 3)))
+    assert core.stress(X @ Q + rng.normal(size=3), hop, 0.5) == pytest.approx(f, rel=1e-12)
+    assert core.stress(X * np.array([-1, 1, 1]), hop, 0.5) == pytest.approx(f, rel=1e-12)
+
+
+def test_stress_rows_sum_to_twice_eq1():
+    rng = np.random.default_rng(4)
+    g = graphs.random_connected_graph(15, 10, seed=2)
+    hop = core.hop_matrix(g)
+    X = rng.normal(size=(15, 2))
+    s = core.stress_rows(X, np.arange(15), hop, 0.3)
+    assert 0.5 * s.sum() == pytest.approx(core.stress(X, hop, 0.3), rel=1e-13)
+
+
+# ----------------------------------------------------- Laplacians, Prop. 2.1
+
+def test_weight_laplacian_p3():
+    """S:144 and S:208 worked examples (L^W definition, reduction P:125)."""
+    hop = core.hop_matrix(graphs.path_graph(3))
+    np.testing.assert_allclose(core.lw_dense(hop, 1.0), np.array(gold("lw_p3")), rtol=0, atol=1e-15)
+    np.testing.assert_allclose(core.lw_red_dense(hop, 1.0), np.array(gold("lw_p3_reduced")), rtol=0, atol=1e-15)
+    # (L^W X) rows equal the dense matrix times X
+    X = np.random.default_rng(0).normal(size=(3, 2))
+    np.testing.assert_allclose(core.lw_rows(X, np.arange(3), hop, 1.0), np.array(gold("lw_p3")) @ X, atol=1e-14)
+
+
+def test_iteration_laplacian_example_and_coincident_rule():
+    """single edge, w = 1 (alpha = 0), d = 2, ||y_0 - y_1|| = 4 ->
+    off-diagonal -0.5; coincident y_0 = y_1 -> zero matrix."""
+    hop = core.hop_matrix(graphs.path_graph(2))
+    Y = np.array([[0.0], [4.0]])
+    R = core.ly_rows(Y, np.arange(2), hop, k=2.0, alpha=0.0)
+    l01 = gold("ly_edge_d2_r4_offdiag")
+    np.testing.assert_allclose(R[:, 0], [l01 * 4.0 + 0.5 * 0.0, -l01 * 4.0 * 1.0 + (-0.5) * 0.0 + 0.0], atol=1e-15)
+    Yc = np.array([[1.5, 2.0], [1.5, 2.0]])
+    assert np.all(core.ly_rows(Yc, np.arange(2), hop, k=2.0) == 0.0)
+
+
+def test_dominance_prop_2_1():
+    """Prop. 2.1: f(X) <= g(X, Y) and f(X) = g(X, X); S:541 criterion 1."""
+    rng = np.random.default_rng(11)
+    for t in range(40):
+        n = int(rng.integers(3, 12))
+        dim = int(rng.integers(1, 4))
+        g = graphs.random_connected_graph(n, int(rng.integers(0, n)), seed=100 + t)
+        hop = core.hop_matrix(g)
+        k = float(rng.uniform(0.2, 2.0))
+        for _ in range(5):
+            X = rng.normal(size=(n, dim))
+            Y = rng.normal(size=(n, dim))
+            f = core.stress(X, hop, k)
+            gxy = core.dominant_value(X, Y, hop, k)
+            gxx = core.dominant_value(X, X, hop, k)
+            assert f <= gxy + 1e-9 * (1 + abs(gxy))
+            assert abs(f - gxx) <= 1e-9 * (1 + f)
+
+
+def test_force_is_half_negative_gradient():
+    """F = R - A = L^X X - L^W X = -1/2 grad f (gradient of Eq. 1; the zero
+    of F is the fixed point of Eq. 5).  Central finite differences of the
+    stress alone, so a sign or factor slip in R or A fails."""
+    rng = np.random.default_rng(5)
+    g = graphs.random_connected_graph(10, 6, seed=9)
+    hop = core.hop_matrix(g)
+    k = 0.8
+    X = rng.normal(size=(10, 2))
+    R, A, F = core.forces(X, hop, k)
+    h = 1e-6
+    grad = np.zeros_like(X)
+    for i in range(10):
+        for c in range(2):
+            Xp = X.copy(); Xp[i, c] += h
+            Xm = X.copy(); Xm[i, c] -= h
+            grad[i, c] = (core.stress(Xp, hop, k) - core.stress(Xm, hop, k)) / (2 * h)
+    np.testing.assert_allclose(F, -0.5 * grad, rtol=1e-6, atol=1e-7)
+
+
+def test_zero_net_force():
+    """Both Laplacians have zero row (and column) sums, so the net
+    'repulsion' and net 'attraction' vanish."""
+    rng = np.random.default_rng(6)
+    g = graphs.random_connected_graph(30, 40, seed=3)
+    hop = core.hop_matrix(g)
+    X = rng.random((30, 2))
+    R, A, _ = core.forces(X, hop, 0.2)
+    scale = np.abs(R).sum()
+    assert np.abs(R.sum(axis=0)).max() < 1e-13 * scale
+    assert np.abs(A.sum(axis=0)).max() < 1e-13 * np.abs(A).sum()
+
+
+# ------------------------------------------------------------------ BFS hops
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_hops_match_scipy_shortest_path(seed):
+    """Ideal-distance reading d = k*hop: the oracle's BFS equals scipy's
+    unweighted shortest_path (library routine), bit-exact integers."""
+    g = graphs.random_connected_graph(60, 40, seed=seed)
+    a = csr_matrix((np.ones(g.col.size), g.col, g.row_ptr), shape=(g.n, g.n))
+    ref = shortest_path(a, unweighted=True, directed=False).astype(np.int64)
+    assert np.array_equal(core.hop_matrix(g).astype(np.int64), ref)
+
+
+def test_hops_disconnected_raises():
+    g = graphs.csr_from_edges(4, np.array([[0, 1], [2, 3]]))
+    with pytest.raises(core.DisconnectedGraph):
+        core.hop_matrix(g)
+
+
+# ------------------------------------------------------------------- solves
+
+def test_reduced_solve_worked_example():
+    """[[2,-1],[-1,1.25]] z = (1, 0) -> (5/6, 2/3), by Cholesky and CG."""
+    g = graphs.path_graph(3)
+    for solver in ("cholesky", "cg"):
+        prob = layout.Problem(g, 1, 1.0, solver=solver)
+        Z = prob.solve_reduced(np.array([[0.0], [1.0], [0.0]]))
+        np.testing.assert_allclose(Z[1:, 0], gold("solve_p3_reduced_rhs_10"), rtol=1e-12)
+        assert Z[0, 0] == 0.0
+
+
+def test_cg_matches_cholesky():
+    """S:544 criterion 4: Cholesky vs CG (1e-12) agree to 1e-8."""
+    rng = np.random.default_rng(8)
+    for t in range(5):
+        g = graphs.random_connected_graph(80, 60, seed=50 + t)
+        hop = core.hop_matrix(g)
+        B = rng.normal(size=(80, 2))
+        za = layout.Problem(g, 2, 0.4, solver="cholesky", hop=hop).solve_reduced(B)
+        zb = layout.Problem(g, 2, 0.4, solver="cg", hop=hop).solve_reduced(B, rng.normal(size=(80, 2)))
+        np.testing.assert_allclose(zb, za, rtol=1e-8, atol=1e-8 * np.abs(za).max())
+        # residual of the reduced system
+        Lr = core.lw_red_dense(hop, 0.4)
+        assert np.linalg.norm(Lr @ za[1:] - B[1:]) <= 1e-10 * (1 + np.linalg.norm(B[1:]))
+
+
+# ---------------------------------------------------- one majorization step
+
+def test_majorize_single_edge_1d():
+    """single edge, d = 1, x = (0, 3) -> next placement has distance 1."""
+    prob = layout.Problem(graphs.path_graph(2), 1, 1.0)
+    Xn = prob.H(np.array([[0.0], [3.0]]))
+    assert abs(Xn[1, 0] - Xn[0, 0]) == pytest.approx(gold("majorize_edge_1d"), rel=1e-14)
+
+
+def test_majorize_p2_closed_form_2d():
+    """P2: H(Y) puts x_1 at k * y_1/||y_1|| from the pinned x_0 = 0."""
+    rng = np.random.default_rng(1)
+    for k in (0.1, 1.0, 3.0):
+        prob = layout.Problem(graphs.path_graph(2), 2, k)
+        Y = np.vstack([np.zeros(2), rng.normal(size=2)])
+        np.testing.assert_allclose(prob.H(Y)[1], k * Y[1] / np.linalg.norm(Y[1]), rtol=1e-14)
+
+
+def test_majorize_complete_graph_equals_sklearn_smacof():
+    """K_n has uniform weights, so H is the textbook Guttman transform; one
+    step equals sklearn.manifold.smacof(max_iter=1) up to the translation that
+    pins x_0 = 0 (library-routine pin of Eq. 4/5 and L^Y, L^W)."""
+    from sklearn.manifold import smacof
+
+    rng = np.random.default_rng(2)
+    for n, dim in ((5, 2), (8, 3)):
+        k = 0.7
+        prob = layout.Problem(graphs.complete_graph(n), dim, k)
+        X = rng.normal(size=(n, dim))
+        ours = prob.H(X)
+        D = k * (1.0 - np.eye(n))
+        sk, _ = smacof(D, metric=True, n_components=dim, init=X.copy(), n_init=1, max_iter=1,
+                       normalized_stress=False, eps=0.0)
+        np.testing.assert_allclose(ours, sk - sk[0], rtol=1e-12, atol=1e-13)
+
+
+# -------------------------------------------------------- Algorithm 2 runs
+
+def _best_final(g, dim, seeds, omega=1.5, k=1.0, tol=1e-13, max_iter=3000):
+    prob = layout.Problem(g, dim, k)
+    best = math.inf
+    for s in seeds:
+        X0 = graphs.init_positions(g.n, dim, s)
+        best = min(best, layout.run_algorithm2(prob, X0, omega, tol, max_iter).f)
+    return best
+
+
+def test_equilibria_closed_forms():
+    """Closed-form optima of Eq. 1 (derivations in golden/spec_examples.json)."""
+    assert _best_final(graphs.path_graph(2), 2, [1]) == pytest.approx(0.0, abs=1e-20)
+    assert _best_final(graphs.complete_graph(3), 2, [1, 2]) < 1e-18
+    assert _best_final(graphs.complete_graph(4), 3, [1, 2, 3]) < 1e-14
+    assert _best_final(graphs.complete_graph(4), 2, range(1, 8)) == pytest.approx(gold("equilibrium_K4_2d"), rel=1e-9)
+    assert _best_final(graphs.cycle_graph(4), 2, range(1, 11)) == pytest.approx(gold("equilibrium_C4_2d"), rel=1e-9)
+
+
+@pytest.mark.parametrize("omega", [0.0, 0.5, 1.0, 1.5, 3.0, 9.0])
+def test_stress_monotone_every_omega(omega):
+    """Prop. 2.2 ('non-decreasing' at P:89 read as non-increasing) plus
+    the guard of Algorithm 2 lines 6-8: f never increases."""
+    g = graphs.grid_graph(5, 5)
+    prob = layout.Problem(g, 2, 0.2)
+    for s in (1, 2):
+        r = layout.run_algorithm2(prob, graphs.init_positions(g.n, 2, s), omega, 1e-9, 200)
+        fs = [r.f_initial] + [t.f_after for t in r.trace]
+        assert all(b <= a * (1 + 1e-12) for a, b in zip(fs, fs[1:]))
+        for t in r.trace:  # guard correctness
+            if t.accepted:
+                assert t.f_relaxed <= t.f_next
+
+
+def test_omega_zero_is_algorithm_1():
+    """w = 0 degenerates into Algorithm 1 -- identical traces and
+    placements (S:543 criterion 3)."""
+    g = graphs.grid_graph(4, 6)
+    prob = layout.Problem(g, 2, 0.3)
+    X0 = graphs.init_positions(g.n, 2, 4)
+    a = layout.run_algorithm2(prob, X0, 0.0, 1e-7, 300)
+    b = layout.run_algorithm1(prob, X0, 1e-7, 300)
+    assert a.iterations == b.iterations
+    assert [t.f_after for t in a.trace] == [t.f_after for t in b.trace]
+    assert np.array_equal(a.X, b.X)
+
+
+def test_scale_equivariance_in_k():
+    """For w = d^-2, f_{kD}(kY) = f_D(Y) and H_{kD}(kY) = k H_D(Y), so k is a
+    pure unit: identical iteration counts and stresses."""
+    g = graphs.grid_graph(5, 4)
+    X0 = graphs.init_positions(g.n, 2, 3)
+    r1 = layout.run_algorithm2(layout.Problem(g, 2, 1.0), X0, 1.5, 1e-6, 400)
+    r2 = layout.run_algorithm2(layout.Problem(g, 2, 0.1), 0.1 * X0, 1.5, 1e-6, 400)
+    assert r1.iterations == r2.iterations
+    assert r2.f == pytest.approx(r1.f, rel=1e-9)
+    np.testing.assert_allclose(r2.X, 0.1 * r1.X, rtol=1e-7, atol=1e-9)
+
+
+def test_step_cap():
+    """cap_step: +inf is the identity (paper-exact); a finite cap bounds every
+    vertex move and the guard keeps f monotone."""
+    rng = np.random.default_rng(0)
+    Xn = rng.normal(size=(6, 2)); Xt = Xn + rng.normal(size=(6, 2))
+    assert np.array_equal(layout.cap_step(Xt, Xn, math.inf), Xt)
+    capped = layout.cap_step(Xt, Xn, 0.1)
+    assert np.all(np.linalg.norm(capped - Xn, axis=1) <= 0.1 + 1e-15)
+    g = graphs.grid_graph(4, 4)
+    r = layout.run_algorithm2(layout.Problem(g, 2, 0.25), graphs.init_positions(16, 2, 1), 1.5, 1e-8, 100, step=0.01)
+    fs = [r.f_initial] + [t.f_after for t in r.trace]
+    assert all(b <= a for a, b in zip(fs, fs[1:]))
+
+
+def test_convergence_rate_theorem_3_2():
+    """Theorem 3.2: the w = 0 iteration converges linearly at rate
+    1 - lambda_n, lambda_n the smallest eigenvalue of D^2 f z = lambda D_11 g z
+    (Eq. 7), D_11 g = 2 L^W (x) I.  Hessian of f by finite differences of Eq. 1
+    alone; the rotation mode (lambda = 0) is dropped.  Observed rate from the
+    oracle's own trajectory.  grid 3x3 (0.8034)."""
+    g = graphs.grid_graph(3, 3)
+    n, dim, k = 9, 2, 1.0
+    prob = layout.Problem(g, dim, k)
+    X0 = graphs.init_positions(n, dim, 1)
+    Xs = layout.pin(X0)
+    for _ in range(600):          # X* = limit of the w = 0 iteration (errors reach ~1e-16)
+        Xs = prob.H(Xs)
+    # Hessian of f in the reduced coordinates (vertices 1..n-1), central differences
+    m = (n - 1) * dim
+    h = 1e-4
+    x0 = Xs[1:].ravel().copy()
+
+    def fr(v):
+        X = np.vstack([np.zeros(dim), v.reshape(n - 1, dim)])
+        return prob.f(X)
+
+    H = np.zeros((m, m))
+    for a in range(m):
+        for b in range(a, m):
+            ea = np.zeros(m); ea[a] = h
+            eb = np.zeros(m); eb[b] = h
+            val = (fr(x0 + ea + eb) - fr(x0 + ea - eb) - fr(x0 - ea + eb) + fr(x0 - ea - eb)) / (4 * h * h)
+            H[a, b] = H[b, a] = val
+    B = 2.0 * np.kron(core.lw_red_dense(prob.hop, k), np.eye(dim))
+    lam = scipy.linalg.eigh(H, B, eigvals_only=True)
+    lam_pos = lam[lam > 1e-5]
+    predicted = 1.0 - lam_pos.min()
+    # observed: e_k = ||X^k - X*|| along a fresh trajectory
+    # the rotation about the pinned vertex is a neutral (lambda = 0) direction:
+    # align each iterate to X* by orthogonal Procrustes first
+    def aligned_err(X):
+        U, _, Vt = np.linalg.svd(X.T @ Xs)
+        Q = U @ Vt
+        if np.linalg.det(Q) < 0:
+            U[:, -1] *= -1
+            Q = U @ Vt
+        return np.linalg.norm(X @ Q - Xs)
+
+    X = layout.pin(X0)
+    errs = []
+    for _ in range(400):
+        X = prob.H(X)
+        errs.append(aligned_err(X))
+    errs = np.array(errs)
+    win = np.flatnonzero((errs < 1e-5) & (errs > 1e-10))
+    assert win.size >= 10
+    slope = np.polyfit(win, np.log(errs[win]), 1)[0]
+    observed = math.exp(slope)
+    assert observed == pytest.approx(predicted, abs=0.01)
+    assert 0.0 < predicted < 1.0
