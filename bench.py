@@ -1,0 +1,363 @@
+#!/usr/bin/env python
+"""Benchmark of the SOR stress-majorization hot path on B200.
+
+A "step" is one Algorithm-2 iteration of the whole
+hot path on BASELINE config C5 (Barabasi-Albert n=200,000, m=3, 2-D, omega
+1.5): PCG solve (P2 passes), Eq. 10 combine, fused P1 stress/repulsion pass
+over both candidates, guard, stop test.  The hop matrix (MS-BFS) is built at
+create time, outside the timed region (reported as setup_ms).
+
+metric: pair-interactions/sec = sum over timed steps of (unordered pair
+sweeps) * n(n-1)/2 / time, where the sweeps of one step are 2 stress
+evaluations + 1 repulsion evaluation (fused in one P1 pass) + one L^W matvec
+per P2 pass (1 + PCG iterations) -- SURVEY.md §8(d).  SOR iterations/sec is
+reported beside it.
+
+Launch: python bench.py [--gpus N --steps K --warmup W] (N>1 under torchrun,
+rows sharded over ranks, NCCL all-gathers; time = max over ranks).
+`--impl reference` times the fp64 CPU oracle (oracle/) on a bounded sample
+of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import configs  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+SM_COUNT = 148
+FP32_LANES_PER_SM = 128
+# Algorithmic FP32 flops per ordered pair: per position set
+# delta (d) + r^2 (2d-1) + r^2 h^2 (1) + R accumulate (2d) + u = r^2 q - 1 (2)
+# + s += u^2 (2); per pair the hop decode h^2 (1).  rsqrt counted as 0 flops.
+P1_FLOPS_PER_PAIR_SET = {2: 14, 3: 19}
+P1_FLOPS_PER_PAIR_DECODE = 1
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="fdl", choices=["fdl", "reference"])
+    ap.add_argument("--config", default="C5", choices=list(configs.CONFIGS))
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-rows", type=int, default=0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def fp32_peak_tflops(peaks):
+    mhz = peaks.get("sm_max_mhz", 1965.0)
+    return SM_COUNT * FP32_LANES_PER_SM * 2 * mhz * 1e6 / 1e12
+
+
+# ---------------------------------------------------------- CPU (oracle) leg
+def cpu_oracle_sample(name: str, seed: int, rows_target: int = 0):
+    """The fp64 oracle as it stands, on a bounded row sample of the workload:
+    BFS hop rows of the sampled sources, then per sampled row the quantities
+    one Algorithm-2 iteration evaluates per pair -- stress of two placements,
+    L^X X and L^W X.  Returns unordered pair-interactions/sec (2 ordered row
+    evaluations = 1 unordered pair, matching the GPU count)."""
+    from oracle import core
+
+    cfg = configs.CONFIGS[name]
+    g = configs.graph_for(name)
+    k = cfg.k_for(g.n)
+    X0 = configs.positions_for(name, g.n, seed)
+    X1 = X0 * 1.01
+    nrows = rows_target or max(64, min(g.n, int(6e8 // g.n)))
+    rows = np.linspace(0, g.n - 1, nrows).astype(np.int32)
+    t0 = time.perf_counter()
+    hr = core.hop_rows(g, rows)
+    t1 = time.perf_counter()
+    core.stress_rows(X0, rows, hr, k)
+    core.stress_rows(X1, rows, hr, k)
+    core.ly_rows(X1, rows, hr, k)
+    core.lw_rows(X1, rows, hr, k)
+    t2 = time.perf_counter()
+    ordered = 4 * nrows * (g.n - 1)
+    return {
+        "value": (ordered / 2) / (t2 - t1),
+        "unit": "pair-interactions/sec",
+        "cores": core.num_threads(),
+        "kind": "oracle",
+        "sample": f"{nrows} of {g.n} rows of {name}: 2 stress + L^X X + L^W X row passes (fp64); "
+                  f"BFS of the sampled sources {t1 - t0:.2f}s excluded",
+        "seconds": t2 - t1,
+    }
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = configs.CONFIGS[args.config]
+    g = configs.graph_for(args.config)
+    vals = []
+    res = None
+    for _ in range(max(args.warmup, 0)):
+        cpu_oracle_sample(args.config, args.seed, rows_target=args.cpu_sample_rows or 64)
+    t_all = 0.0
+    for _ in range(args.steps):
+        res = cpu_oracle_sample(args.config, args.seed, rows_target=args.cpu_sample_rows)
+        vals.append(res["value"])
+        t_all += res["seconds"]
+    v = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": "pair-interactions/sec", "value": v, "unit": "pair-interactions/sec",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t_all / max(args.steps, 1), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "n": g.n, "edges": g.num_edges, "dim": cfg.dim,
+                   "omega": cfg.omega, "sample": res["sample"]},
+        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": v, "unit": "pair-interactions/sec", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    line["cpu_baseline"]["value"] = v
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU leg
+def run_gpu(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    from paper_1711_01228_b200 import fdl
+
+    cfg = configs.CONFIGS[args.config]
+    g = configs.graph_for(args.config)
+    n = g.n
+    k = cfg.k_for(n)
+    X0 = configs.positions_for(args.config, n, args.seed)
+    p = fdl.make_params(dim=cfg.dim, k=k, omega=cfg.omega, tol=cfg.tol, max_iter=100000, device=local_rank)
+    nccl_id = None
+    if world > 1:
+        buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            buf.copy_(torch.tensor(list(fdl.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(buf, 0)
+        nccl_id = bytes(buf.cpu().tolist())
+    L = fdl.Layout.from_graph(g, params=p, init_pos=X0, nccl_id=nccl_id, rank=rank, world=world)
+    stream = torch.cuda.current_stream()
+    L.set_stream(stream.cuda_stream)
+    L.set_timing(True)
+    info = L.get_info()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        L.step()
+    L.reset_stats()
+    clocks = ClockSampler(local_rank)
+    barrier()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        L.step()
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    st = L.get_stats()
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    pairs_unordered = n * (n - 1) / 2
+    sweeps = 3 * st.steps + st.p2_launches
+    total_pairs = sweeps * pairs_unordered
+    value = total_pairs / (ms * 1e-3)
+    its_per_s = args.steps / (ms * 1e-3)
+
+    # roofline of the dominant kernel (P1 at C5): algorithmic flops / event time
+    dim = cfg.dim
+    p1_flops = (st.p1_pairs * P1_FLOPS_PER_PAIR_SET[dim]
+                + (st.p1_pairs - st.p1_pairs_x2 / 2) * P1_FLOPS_PER_PAIR_DECODE)
+    peaks = load_peaks()
+    peak_tf = fp32_peak_tflops(peaks)
+    p1_tf = p1_flops / (st.p1_ms * 1e-3) / 1e12 if st.p1_ms > 0 else 0.0
+    # P2 is hop-matrix streaming: algorithmic bytes = hop bytes per launch
+    hop_bytes = info.hop_bytes
+    p2_gbs = (st.p2_pairs * hop_bytes) / (st.p2_ms * 1e-3) / 1e9 if st.p2_ms > 0 else 0.0
+    p1_share = st.p1_ms / ms if ms > 0 else 0
+    p2_share = st.p2_ms / ms if ms > 0 else 0
+    dominant_p1 = st.p1_ms >= st.p2_ms
+    if dominant_p1:
+        roof = {"bound": "alu", "kernel": "p1_repulse_stress", "achieved": p1_tf, "peak": peak_tf,
+                "unit": "TFLOP/s", "frac": p1_tf / peak_tf, "traffic": None,
+                "peak_source": f"148 SMs x 128 FP32 lanes x 2 x {peaks.get('sm_max_mhz', 1965.0):.0f} MHz "
+                               "(MEASURED_PEAKS sm_max_mhz)",
+                "flops_per_launch": p1_flops / max(st.p1_launches, 1),
+                "avg_launch_ms": st.p1_ms / max(st.p1_launches, 1)}
+    else:
+        hbm = peaks.get("hbm_gbs", 6650.0)
+        roof = {"bound": "hbm", "kernel": "p2_lw_matvec", "achieved": p2_gbs, "peak": hbm, "unit": "GB/s",
+                "frac": p2_gbs / hbm, "traffic": None, "peak_source": "MEASURED_PEAKS hbm_gbs",
+                "bytes_per_launch": st.p2_pairs * hop_bytes / max(st.p2_launches, 1),
+                "avg_launch_ms": st.p2_ms / max(st.p2_launches, 1)}
+
+    # ---- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        Xh = L.get_positions()
+        L.reset_stats()
+        barrier()
+        e2 = torch.cuda.Event(enable_timing=True)
+        e3 = torch.cuda.Event(enable_timing=True)
+        e2.record(stream)
+        for _ in range(args.steps):
+            L.set_positions(Xh)          # H2D of the step's input (pinned by ctypes? pageable host)
+            L.step()
+            L.get_positions(Xh)          # D2H of the result
+        e3.record(stream)
+        barrier()
+        ms2 = e2.elapsed_time(e3)
+        st2 = L.get_stats()
+        if dist is not None:
+            t = torch.tensor([ms2], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms2 = float(t.item())
+        sweeps2 = 3 * st2.steps + st2.p2_launches
+        e2e = {"value": sweeps2 * pairs_unordered / (ms2 * 1e-3), "unit": "pair-interactions/sec",
+               "h2d_bytes_per_step": int(n * dim * 8), "d2h_bytes_per_step": int(n * dim * 8),
+               "iterations_per_sec": args.steps / (ms2 * 1e-3)}
+
+    ffma_tf, _ = fdl.bench_ffma(local_rank)
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                cpu = cpu_oracle_sample(args.config, args.seed, args.cpu_sample_rows)
+                cpu = {k2: cpu[k2] for k2 in ("value", "unit", "cores", "kind", "sample")}
+            except Exception as ex:  # pragma: no cover
+                cpu = {"error": str(ex)}
+        line = {
+            "metric": "pair-interactions/sec", "value": value, "unit": "pair-interactions/sec",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "f32 pair math / f64 reductions+state", "data": "synthetic",
+            "config": {"workload": f"{args.config}: BA n={n} m=3 |E|={g.num_edges}" if args.config == "C5"
+                       else f"{args.config} n={n} |E|={g.num_edges}",
+                       "dim": dim, "omega": cfg.omega, "k": k, "diameter": info.diameter,
+                       "hop_bytes": info.hop_bytes, "parallelism": f"row-shard x{world}",
+                       "l2": "inputs larger than L2 (hop matrix %.1f GB per GPU)" % (info.hop_matrix_bytes / 1e9)},
+            "iterations_per_sec": its_per_s,
+            "pcg_iters_per_step": st.cg_iters / max(st.steps, 1),
+            "kernel_share": {"p1": p1_share, "p2": p2_share, "other": max(0.0, 1 - p1_share - p2_share)},
+            "p1_tflops": p1_tf, "p2_hop_gbs": p2_gbs,
+            "fp32_ffma_microbench_tflops": ffma_tf,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk,
+            "gpu_launches": int(st.launches),
+            "setup_ms": info.setup_ms,
+        }
+        print(json.dumps(line), flush=True)
+    L.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,231 @@
+/*
+ * fdl.h -- C ABI of libfdl.so, the B200 (sm_100a) hot path of Wang & Wang's
+ * SOR force-directed (stress-majorization) layout, arXiv 1711.01228.
+ *
+ * Citations: "P:n" = line n of the paper text, "S:n" = line n of
+ * SPEC.md, "DESIGN Rk" = reading k in DESIGN.md §3.
+ *
+ * The method (§2 and §4):
+ *   stress      f(X) = sum_{i<j} w_ij (||x_i - x_j|| - d_ij)^2           Eq. 1
+ *   ideal dist  d_ij = k * hop(i,j) (graph distance, DESIGN R1)
+ *   weights     w_ij = d_ij^-2
+ *   one step    solve L^W X^{k+1} = L^{X^k} X^k with x_0 = 0              Eq. 2-5, Prop. 2.3
+ *   relaxation  Xt = (1+omega) X^{k+1} - omega X^k                       Eq. 10
+ *   guard       if f(Xt) <= f(X^{k+1}) then X^{k+1} <- Xt                 Algorithm 2 l.6-8
+ *   stop        (f_old - f_new)/f_old < tol, or f_new = 0, or it = max_iter (DESIGN R4)
+ * Vocabulary of BASELINE north_star: "repulsion" R = L^X X (the right-hand
+ * side), "attraction" A = L^W X, "force" F = R - A = -1/2 grad f.
+ *
+ * Conventions (all functions):
+ *   - Every function returns fdl_status; 0 = OK, < 0 = error.  No C++
+ *     exception crosses the ABI.
+ *   - Vertex ids are 0-based; id 0 is the paper's vertex 1, pinned at the
+ *     origin.  Positions are n*dim doubles, row-major (x_i contiguous).
+ *   - All pointer arguments are HOST pointers unless the name says otherwise.
+ *     Inputs are copied; the caller keeps ownership of its buffers.  Output
+ *     buffers are caller-allocated with the exact element count stated.
+ *   - A context owns all device memory it uses; it is not thread-safe;
+ *     distinct contexts are independent.  Calls that return host data
+ *     synchronise the context stream.
+ *   - After a CUDA error inside a context every later call on it returns
+ *     FDL_E_STATE; fdl_last_error() explains.
+ */
+#ifndef FDL_H_
+#define FDL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FDL_ABI_VERSION 1
+
+typedef struct fdl_ctx fdl_ctx; /* opaque; owned by the library */
+
+typedef enum {
+    FDL_OK = 0,
+    FDL_E_INVALID_ARG = -1,    /* null pointer, bad size, bad parameter value             */
+    FDL_E_SELF_LOOP = -2,      /* CSR has an edge (v, v)                           */
+    FDL_E_DUPLICATE_EDGE = -3, /* CSR row lists a neighbour twice                 */
+    FDL_E_ASYMMETRIC = -4,     /* (u,v) present but (v,u) missing: graph must be undirected */
+    FDL_E_DISCONNECTED = -5,   /* graph not connected: d_ij undefined        */
+    FDL_E_BAD_LENGTH = -6,     /* edge lengths given (weighted graphs are not supported yet) */
+    FDL_E_DIAMETER = -7,       /* hop count exceeds 65535                                 */
+    FDL_E_OOM = -8,            /* device allocation failed                                */
+    FDL_E_CUDA = -9,           /* CUDA runtime error                                      */
+    FDL_E_NCCL = -10,          /* NCCL error / NCCL library not loadable                  */
+    FDL_E_SOLVER = -11,        /* CG hit cg_max_iter before cg_rtol (S:223 NoConvergence) */
+    FDL_E_NONFINITE = -12,     /* stress became NaN/Inf                           */
+    FDL_E_UNSUPPORTED = -13,   /* parameter combination not implemented                   */
+    FDL_E_STATE = -14          /* context unusable after an earlier CUDA/NCCL error       */
+} fdl_status;
+
+typedef enum {
+    FDL_STRAT_FIXED = 0, /* omega constant; omega = 0 is Algorithm 1           */
+    FDL_STRAT_PROB = 1   /* roulette over {0.5,1,1.5,2} w.p. {.3,.3,.2,.2} each iteration */
+} fdl_strategy;
+
+typedef enum {
+    FDL_STOP_NONE = 0,
+    FDL_STOP_REL_TOL = 1,     /* (f_old - f_new)/f_old < tol */
+    FDL_STOP_ZERO_STRESS = 2, /* f_new == 0                  */
+    FDL_STOP_MAX_ITER = 3     /* it == max_iter              */
+} fdl_stop_reason;
+
+typedef struct {
+    uint32_t struct_size; /* sizeof(fdl_params); set by fdl_params_default               */
+    int32_t dim;          /* embedding dimension d >= 1; kernels built for 2 and 3 */
+    double k;             /* ideal edge length, d_ij = k*hop_ij; k <= 0 -> n^(-1/dim) (DESIGN R2) */
+    double omega;         /* relax factor omega >= 0 (Eq. 10)                                      */
+    double step;          /* cap on ||xt_i - x^{k+1}_i|| per vertex; +INF = paper-exact (DESIGN R14) */
+    double tol;           /* "rel err" of Table 1 > 0                                       */
+    int32_t max_iter;     /* >= 1                                                                   */
+    double weight_exp;    /* alpha in w = d^alpha; only -2 is implemented                   */
+    double cg_rtol;       /* PCG relative residual; <= 0 -> max(1e-2*tol, 1e-9)             */
+    int32_t cg_max_iter;  /* PCG cap per outer iteration; <= 0 -> min(10n, 10000)           */
+    int32_t strategy;     /* fdl_strategy                                                           */
+    uint64_t seed;        /* roulette stream seed (FDL_STRAT_PROB)                                  */
+    int32_t device;       /* CUDA device ordinal                                                    */
+} fdl_params;
+
+typedef struct {
+    int32_t it;            /* 1-based iteration number just completed                    */
+    int32_t accepted;      /* 1 if the relaxed point Xt replaced X^{k+1} (Alg. 2 line 7) */
+    int32_t cg_iters;      /* PCG iterations (= L^W matvec passes) in this step           */
+    int32_t stop;          /* fdl_stop_reason after this step (0 = keep going)            */
+    double omega;          /* relax factor used                                          */
+    double f_before;       /* f(X^k)                                                     */
+    double f_next;         /* f(X^{k+1}) before relaxation                               */
+    double f_relaxed;      /* f(Xt); NaN when omega == 0 (not evaluated)                 */
+    double f_after;        /* f of the accepted point                                    */
+    double rel_decrease;   /* (f_before - f_after)/f_before                              */
+    double cg_relres;      /* max over columns of ||r||/||b|| at PCG exit                */
+    double maxdisp;        /* max_i ||x^{k+1}_i - x^k_i|| (diagnostic, original units)   */
+} fdl_iter_info;
+
+typedef struct {
+    int32_t iterations;    /* iterations run by this call                 */
+    int32_t accepted;      /* how many relaxations were accepted          */
+    int32_t stop;          /* fdl_stop_reason                             */
+    int32_t cg_iters;      /* total PCG iterations                        */
+    double f_initial;      /* f before the first iteration of this call  */
+    double f_final;        /* f after the last iteration                  */
+} fdl_run_info;
+
+typedef struct {
+    int32_t n, dim;
+    int32_t diameter;      /* max hop count found by the BFS                     */
+    int32_t hop_bytes;     /* 1 (uint8) or 2 (uint16) per stored hop             */
+    int32_t row0, row1;    /* rows owned by this context [row0, row1)           */
+    int32_t rank, world;
+    int32_t iterations;    /* iterations run so far on this context              */
+    double k;              /* resolved ideal edge length                        */
+    double f;              /* current stress                                    */
+    uint64_t hop_matrix_bytes; /* device bytes of the hop matrix (this rank)   */
+    uint64_t device_bytes;     /* all device memory held by the context         */
+    double setup_ms;       /* MS-BFS + rowsum + first stress pass at create     */
+} fdl_ctx_info;
+
+/* Kernel accounting of the hot path, accumulated since fdl_reset_stats. */
+typedef struct {
+    uint64_t launches;        /* kernels launched by the library                     */
+    uint64_t p1_launches;     /* all-pairs repulsion + stress kernel launches (P1)   */
+    uint64_t p2_launches;     /* all-pairs L^W matvec kernel launches (P2)           */
+    uint64_t p1_pairs;        /* ordered pair-position-set interactions done by P1   */
+    uint64_t p2_pairs;        /* ordered pairs done by P2                            */
+    uint64_t p1_pairs_x2;     /* ... of which in launches over two position sets     */
+    double p1_ms, p2_ms;      /* CUDA-event time of P1 / P2 launches (needs timing on) */
+    double other_ms;          /* CUDA-event time of everything else in fdl_step       */
+    uint64_t steps;           /* fdl_step calls                                      */
+    uint64_t cg_iters;        /* PCG iterations                                      */
+} fdl_stats;
+
+/* Fill *p with defaults: dim 2, k auto, omega 1.5, step +INF, tol 1e-4,
+ * max_iter 500, weight_exp -2, cg_rtol auto, cg_max_iter auto, FIXED, seed 1,
+ * device 0. */
+void fdl_params_default(fdl_params* p);
+
+/* Build a layout context on one GPU.
+ *   n        number of vertices (>= 1)
+ *   row_ptr  int64[n+1], CSR offsets; col_idx int32[row_ptr[n]] neighbour ids.
+ *            The graph must be undirected (both directions stored), without
+ *            self-loops or duplicate neighbours, and connected.
+ *   edge_len must be NULL (unit lengths; weighted graphs -> FDL_E_BAD_LENGTH).
+ *   p        parameters (NULL -> defaults).
+ *   init_pos n*dim doubles (row-major) or NULL for the seeded uniform unit-cube
+ *            placement.  Translated so x_0 = 0.
+ * Computes the hop matrix on the device (multi-source BFS), the Jacobi
+ * diagonal, and f(X^0), L^{X^0} X^0.  On error *out = NULL. */
+fdl_status fdl_create(int32_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                      const double* edge_len, const fdl_params* p,
+                      const double* init_pos, fdl_ctx** out);
+
+/* Same, for rank `rank` of `world` GPUs of one node.  `nccl_unique_id` is the
+ * 128-byte ncclUniqueId created by rank 0 and broadcast by the caller (e.g.
+ * over torch.distributed).  Rank g owns the row block [row0, row1) given by
+ * fdl_shard_rows(n, world, g); every rank must pass identical graph,
+ * parameters and init_pos.  Results are bitwise identical to world = 1. */
+fdl_status fdl_create_sharded(int32_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                              const double* edge_len, const fdl_params* p,
+                              const double* init_pos, const uint8_t* nccl_unique_id,
+                              int32_t rank, int32_t world, fdl_ctx** out);
+
+/* Row block owned by `rank` of `world`: rows are split in blocks of
+ * FDL_ROW_BLOCK rows, contiguous per rank, as evenly as blocks allow. */
+#define FDL_ROW_BLOCK 256
+fdl_status fdl_shard_rows(int32_t n, int32_t world, int32_t rank, int32_t* row0, int32_t* row1);
+
+/* Create a 128-byte NCCL unique id (rank 0 calls this). */
+fdl_status fdl_nccl_unique_id(uint8_t* out128);
+
+/* Enqueue all subsequent work on `cuda_stream` (a cudaStream_t, e.g. a torch
+ * stream).  NULL = the context's own stream. */
+fdl_status fdl_set_stream(fdl_ctx* ctx, void* cuda_stream);
+
+/* One Algorithm-2 iteration on the device; info may be NULL.
+ * Returns FDL_E_STATE once the run has stopped (query info->stop). */
+fdl_status fdl_step(fdl_ctx* ctx, fdl_iter_info* info);
+
+/* Iterate until a stop rule fires (or max_iter).  info may be NULL. */
+fdl_status fdl_run_until_converged(fdl_ctx* ctx, fdl_run_info* info);
+
+/* Current placement (count must be n*dim), original units, x_0 = 0. */
+fdl_status fdl_get_positions(fdl_ctx* ctx, double* out, size_t count);
+
+/* Replace the placement (count n*dim); re-pins x_0 = 0, recomputes f and
+ * L^X X, clears the stop flag (checkpoint resume / parity). */
+fdl_status fdl_set_positions(fdl_ctx* ctx, const double* in, size_t count);
+
+/* Forces at the current placement, original units (each n*dim, may be NULL):
+ * R = L^X X ("repulsion"), A = L^W X ("attraction"); *stress = f(X). */
+fdl_status fdl_eval_forces(fdl_ctx* ctx, double* R, double* A, double* stress);
+
+/* Hop counts of rows [r0, r0+nrows) (must be owned rows): out[r*n + j]. */
+fdl_status fdl_get_hop_rows(fdl_ctx* ctx, int32_t r0, int32_t nrows, uint16_t* out);
+
+/* Jacobi diagonal sum_{j != i} w_ij for owned rows, original units (n_owned). */
+fdl_status fdl_get_diag(fdl_ctx* ctx, double* out, size_t count);
+
+fdl_status fdl_get_info(fdl_ctx* ctx, fdl_ctx_info* info);
+
+/* Kernel statistics.  With timing on, every P1/P2 launch and the rest of each
+ * step are bracketed by CUDA events on the context stream. */
+fdl_status fdl_set_timing(fdl_ctx* ctx, int32_t enable);
+fdl_status fdl_get_stats(fdl_ctx* ctx, fdl_stats* out);
+fdl_status fdl_reset_stats(fdl_ctx* ctx);
+
+/* FFMA-chain microbenchmark on `device`: achieved FP32 FLOP/s of a kernel that
+ * issues only FFMA (the measured FP32 roofline denominator). */
+fdl_status fdl_bench_ffma(int32_t device, double* tflops, double* ms);
+
+const char* fdl_status_str(fdl_status s);
+const char* fdl_last_error(const fdl_ctx* ctx); /* valid until the next call on ctx */
+void fdl_destroy(fdl_ctx* ctx);                 /* NULL-safe */
+int32_t fdl_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDL_H_ */

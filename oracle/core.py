@@ -202,3 +202,16 @@ def lw_red_dense(hop: np.ndarray, k: float, alpha: float = ALPHA) -> np.ndarray:
                                    ctypes.c_double, ctypes.c_void_p]
     L.orc_lw_red_dense(n, _ptr(hop), float(k), float(alpha), _ptr(Lr))
     return Lr
+
+
+def lw_diag_rows(rows, hoprows, k, alpha=ALPHA) -> np.ndarray:
+    """sum_{j != i} w_ij for the listed rows (diagonal of L^W)."""
+    rows = np.ascontiguousarray(np.asarray(rows, dtype=np.int32))
+    hoprows = np.ascontiguousarray(hoprows, dtype=np.uint16)
+    out = np.empty(rows.size, dtype=np.float64)
+    L = lib()
+    L.orc_lw_diag_rows.restype = None
+    L.orc_lw_diag_rows.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.c_double, ctypes.c_double, ctypes.c_void_p]
+    L.orc_lw_diag_rows(hoprows.shape[1], rows.size, _ptr(rows), _ptr(hoprows), float(k), float(alpha), _ptr(out))
+    return out

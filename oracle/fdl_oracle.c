@@ -325,6 +325,24 @@ void orc_lw_diag(int32_t n, const uint16_t* hop, double k, double alpha, double*
     free_table(t);
 }
 
+/* Diagonal entries sum_{j != i} w_ij of L^W for listed rows (hoprows as in
+ * orc_stress_rows). */
+void orc_lw_diag_rows(int32_t n, int32_t nrows, const int32_t* rows, const uint16_t* hoprows,
+                      double k, double alpha, double* out)
+{
+    dw_table t = make_table(k, alpha, max_hop(hoprows, (size_t)nrows * (size_t)n));
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int32_t r = 0; r < nrows; ++r) {
+        int64_t i = rows[r];
+        const uint16_t* hrow = hoprows + (size_t)r * (size_t)n;
+        double s = 0.0;
+        for (int64_t j = 0; j < n; ++j)
+            if (j != i) s += t.w[hrow[j]];
+        out[r] = s;
+    }
+    free_table(t);
+}
+
 /* C = sum_{i<j} w_ij d_ij^2, the constant of Eq. 2. */
 double orc_const_c(int32_t n, const uint16_t* hop, double k, double alpha)
 {

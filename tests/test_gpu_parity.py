@@ -1,0 +1,241 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the
+same seeded inputs.  Gates (BASELINE north_star):
+  * hops: bit-exact;
+  * single-iteration forces at X0: relL2(R), relL2(A), relL2(F) <= 1e-5;
+  * stress at X0: relative 1e-6 (fp32 pair math, fp64 reductions);
+  * end-to-end: |f_gpu - f_oracle| / f_oracle <= 1e-3 and
+    |it_gpu - it_oracle| <= max(1, ceil(0.02 it_oracle)).
+Full matrices at C1-C3 (several tiles and a ragged tail: n = 100, 1000, 9828);
+sampled rows at C4 (n = 49012, u16 hops, 3-D) and C5 (n = 200000), in the
+launch configuration bench.py times.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import core, layout
+from paper_1711_01228_b200 import fdl
+from workloads import configs, graphs
+
+pytestmark = pytest.mark.gpu
+
+FORCE_TOL = 1e-5
+STRESS_TOL = 1e-6
+
+
+def relL2(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+def make(name, seed=1, omega=None, **kw):
+    cfg = configs.CONFIGS[name]
+    g = configs.graph_for(name)
+    k = cfg.k_for(g.n)
+    X0 = configs.positions_for(name, g.n, seed)
+    p = fdl.make_params(dim=cfg.dim, k=k, omega=cfg.omega if omega is None else omega, tol=cfg.tol,
+                        max_iter=cfg.max_iter, **kw)
+    return g, k, X0, fdl.Layout.from_graph(g, params=p, init_pos=X0)
+
+
+def sample_rows(n, count=40, seed=0):
+    rng = np.random.default_rng(seed)
+    fixed = [0, 1, 31, 32, 255, 256, 257, n // 2, n - 2, n - 1]
+    rows = np.unique(np.concatenate([[r for r in fixed if 0 <= r < n], rng.integers(0, n, count)]))
+    return rows.astype(np.int32)
+
+
+_ctx_cache = {}
+
+
+def big_ctx(name):
+    if name not in _ctx_cache:
+        _ctx_cache[name] = make(name)
+    return _ctx_cache[name]
+
+
+# ------------------------------------------------------------------ a1: hops
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_hops_bit_exact_full(name):
+    g, k, X0, L = make(name)
+    ref = core.hop_matrix(g)
+    got = L.get_hop_rows(0, g.n)
+    assert np.array_equal(got, ref)
+    assert L.info.diameter == int(ref.max())
+    assert L.info.hop_bytes == 1
+
+
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_hops_bit_exact_sampled(name):
+    g, k, X0, L = big_ctx(name)
+    rows = sample_rows(g.n)
+    ref = core.hop_rows(g, rows)
+    for r, want in zip(rows, ref):
+        assert np.array_equal(L.get_hop_rows(int(r), 1)[0], want), r
+    assert L.info.hop_bytes == (2 if name == "C4" else 1)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_jacobi_diagonal(name):
+    g, k, X0, L = big_ctx(name) if name in ("C4", "C5") else make(name)
+    rows = sample_rows(g.n) if g.n > 20000 else np.arange(g.n, dtype=np.int32)
+    ref = core.lw_diag_rows(rows, core.hop_rows(g, rows), k)
+    got = L.get_diag()[rows]
+    # GPU sums fp32-rounded weights in fp64: relative 1e-7
+    np.testing.assert_allclose(got, ref, rtol=1e-7)
+
+
+# ------------------------------------------------- a2/a3 forces at X0 (single iteration)
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_forces_full(name):
+    g, k, X0, L = make(name)
+    R, A, f = L.eval_forces()
+    hop = core.hop_matrix(g)
+    Ro, Ao, Fo = core.forces(X0, hop, k)
+    assert relL2(R, Ro) <= FORCE_TOL
+    assert relL2(A, Ao) <= FORCE_TOL
+    assert relL2(R - A, Fo) <= FORCE_TOL
+    fo = core.stress(X0, hop, k)
+    assert abs(f - fo) / fo <= STRESS_TOL
+    # zero net force (symmetric zero-row-sum Laplacians)
+    assert np.abs(R.sum(axis=0)).max() <= 1e-5 * np.abs(R).sum()
+
+
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_forces_sampled(name):
+    g, k, X0, L = big_ctx(name)
+    L.set_positions(X0)
+    rows = sample_rows(g.n)
+    hr = core.hop_rows(g, rows)
+    R, A, f = L.eval_forces()
+    Ro = core.ly_rows(X0, rows, hr, k)
+    Ao = core.lw_rows(X0, rows, hr, k)
+    assert relL2(R[rows], Ro) <= FORCE_TOL
+    assert relL2(A[rows], Ao) <= FORCE_TOL
+    assert relL2((R - A)[rows], Ro - Ao) <= FORCE_TOL
+    # f at full size: 1/2 sum of row stresses; sampled rows of the oracle bound
+    # nothing alone, so check the full-size invariant instead: zero net force
+    assert np.abs(R.sum(axis=0)).max() <= 1e-5 * np.abs(R).sum()
+    assert np.isfinite(f) and f > 0
+
+
+# ------------------------------------------------------------- one iteration
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_first_iteration(name):
+    cfg = configs.CONFIGS[name]
+    g, k, X0, L = make(name, cg_rtol=1e-10)
+    info = L.step()
+    prob = layout.Problem(g, cfg.dim, k)
+    o = layout.run_algorithm2(prob, X0, cfg.omega, 0.0, 1)
+    t = o.trace[0]
+    assert abs(info.f_next - t.f_next) / t.f_next <= 1e-6
+    assert abs(info.f_relaxed - t.f_relaxed) / t.f_relaxed <= 1e-6
+    assert bool(info.accepted) == t.accepted
+    X1 = L.get_positions()
+    assert relL2(X1, o.X) <= FORCE_TOL
+    assert info.cg_iters > 0 and info.cg_relres <= 1e-10
+
+
+# --------------------------------------------------------------- end to end
+def _gates(gpu_it, gpu_f, o):
+    assert abs(gpu_f - o.f) / o.f <= 1e-3, (gpu_f, o.f)
+    assert abs(gpu_it - o.iterations) <= max(1, math.ceil(0.02 * o.iterations)), (gpu_it, o.iterations)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+@pytest.mark.parametrize("omega", [0.0, 1.5])
+def test_end_to_end_C1(seed, omega):
+    cfg = configs.CONFIGS["C1"]
+    g, k, X0, L = make("C1", seed=seed, omega=omega)
+    trace = []
+    while True:
+        info = L.step()
+        trace.append(info.f_after)
+        if info.stop:
+            break
+    prob = layout.Problem(g, 2, k)
+    o = layout.run_algorithm2(prob, X0, omega, cfg.tol, cfg.max_iter)
+    _gates(len(trace), trace[-1], o)
+    fs = [L.info.f] + trace
+    assert all(b <= a * (1 + 1e-9) for a, b in zip(fs, fs[1:]))
+
+
+@pytest.mark.parametrize("omega", [1.0, 1.3, 1.6, 1.9])
+def test_end_to_end_C2_sweep(omega):
+    cfg = configs.CONFIGS["C2"]
+    g, k, X0, L = make("C2", seed=1, omega=omega)
+    r = L.run_until_converged()
+    o = layout.run_algorithm2(layout.Problem(g, 2, k), X0, omega, cfg.tol, cfg.max_iter)
+    _gates(r.iterations, r.f_final, o)
+
+
+def test_omega_zero_matches_algorithm_1():
+    cfg = configs.CONFIGS["C1"]
+    g, k, X0, L = make("C1", seed=4, omega=0.0)
+    r = L.run_until_converged()
+    o = layout.run_algorithm1(layout.Problem(g, 2, k), X0, cfg.tol, cfg.max_iter)
+    _gates(r.iterations, r.f_final, o)
+
+
+def test_bitwise_determinism():
+    a = make("C2", seed=2)[3]
+    b = make("C2", seed=2)[3]
+    for _ in range(5):
+        ia, ib = a.step(), b.step()
+        assert ia.f_after == ib.f_after
+    assert np.array_equal(a.get_positions(), b.get_positions())
+
+
+# ------------------------------------------------- closed forms and edge cases
+def _run_small(g, dim, X0, omega=1.5, tol=1e-12, k=1.0, max_iter=2000):
+    p = fdl.make_params(dim=dim, k=k, omega=omega, tol=tol, max_iter=max_iter, cg_rtol=1e-12)
+    L = fdl.Layout.from_graph(g, params=p, init_pos=X0)
+    r = L.run_until_converged()
+    return L, r
+
+
+def test_closed_form_equilibria_on_gpu():
+    """GPU path reaches the closed-form optima of Eq. 1 (fp32 pair math:
+    relative 1e-5): K4 in 2-D -> 3 - 2 sqrt 2; C4 -> 4(3 - 2 sqrt 2)/5."""
+    best = min(_run_small(graphs.complete_graph(4), 2, graphs.init_positions(4, 2, s))[1].f_final
+               for s in range(1, 6))
+    assert best == pytest.approx(3 - 2 * math.sqrt(2), rel=1e-5)
+    best = min(_run_small(graphs.cycle_graph(4), 2, graphs.init_positions(4, 2, s))[1].f_final
+               for s in range(1, 9))
+    assert best == pytest.approx(4 * (3 - 2 * math.sqrt(2)) / 5, rel=1e-5)
+
+
+def test_single_vertex_and_single_edge():
+    L, r = _run_small(graphs.csr_from_edges(1, np.zeros((0, 2))), 2, np.zeros((1, 2)))
+    assert r.f_final == 0.0 and r.iterations == 1
+    L, r = _run_small(graphs.path_graph(2), 2, np.array([[0.0, 0.0], [3.0, 4.0]]), omega=0.0)
+    X = L.get_positions()
+    assert np.linalg.norm(X[1] - X[0]) == pytest.approx(1.0, rel=1e-6)  # S:235 / P2 closed form
+
+
+def test_coincident_start():
+    """All vertices at one point: L^X X = 0, so X^{k+1} = 0, f stays
+    n(n-1)/2 and the stop rule fires after one iteration (as in the oracle)."""
+    g = graphs.grid_graph(3, 3)
+    X0 = np.zeros((9, 2))
+    L, r = _run_small(g, 2, X0, tol=1e-6)
+    o = layout.run_algorithm2(layout.Problem(g, 2, 1.0), X0, 1.5, 1e-6, 2000)
+    assert r.iterations == o.iterations == 1
+    assert r.f_final == pytest.approx(o.f, rel=1e-12) and o.f == pytest.approx(36.0)
+
+
+def test_stopped_context_refuses_step_until_reset():
+    g, k, X0, L = make("C1", seed=1)
+    L.run_until_converged()
+    with pytest.raises(fdl.FdlError) as e:
+        L.step()
+    assert e.value.name == "FDL_E_STATE"
+    L.set_positions(X0)
+    L.step()
+
+
+def test_set_positions_roundtrip_and_pin():
+    g, k, X0, L = make("C2", seed=3)
+    Y = X0 + 0.25
+    L.set_positions(Y)
+    np.testing.assert_allclose(L.get_positions(), Y - Y[0], rtol=0, atol=1e-15)
