@@ -103,6 +103,7 @@ struct fdl_ctx {
     double *cr = nullptr, *cz = nullptr, *cp = nullptr, *cy = nullptr;
     float *posf = nullptr, *pvec = nullptr, *lut = nullptr;
     double *part = nullptr, *blk_f = nullptr, *blk_max = nullptr, *blk_cg = nullptr;
+    double* pin_slots = nullptr;  // world x 4: x_0 of the CG solution
     DevScalars* sc = nullptr;
     HostScalars* hs = nullptr;      // host-mapped (host pointer)
     HostScalars* hs_dev = nullptr;  // same memory, device pointer
@@ -510,8 +511,11 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
     cudaFree(fb);
     cudaFree(vis);
     if (st != FDL_OK) return st;
+    FDL_CUDA(cudaMemsetAsync(ctx->blk_f, 0, (size_t)ctx->nblk * sizeof(double), ctx->stream));
     if (ctx->nloc > 0)
-        FDL_LAUNCH(launch_diag(ctx->D, ctx->Np, ctx->hb, n, ctx->nloc, ctx->row0, ctx->diag, ctx->stream));
+        FDL_LAUNCH(launch_diag(ctx->D, ctx->Np, ctx->hb, n, ctx->nloc, ctx->row0, ctx->diag, ctx->blk_f, ctx->stream));
+    FDL_TRY(gather_blocks(ctx, ctx->blk_f, 1));
+    FDL_LAUNCH(launch_set_sigma(ctx->blk_f, ctx->nblk, n, ctx->sc, ctx->stream));
     // w'_h = fp32(1/h^2) (P2 u8 table)
     float lut[256];
     lut[0] = 0.0f;
@@ -647,11 +651,12 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     FDL_ALLOC(ctx->part, (size_t)ctx->NC * 2 * (dim + 1) * ctx->Mrows);
     FDL_ALLOC(ctx->blk_f, (size_t)2 * ctx->nblk);
     FDL_ALLOC(ctx->blk_max, (size_t)ctx->nblk);
-    FDL_ALLOC(ctx->blk_cg, (size_t)12 * ctx->nblk);
+    FDL_ALLOC(ctx->blk_cg, (size_t)16 * ctx->nblk);
+    FDL_ALLOC(ctx->pin_slots, (size_t)4 * world);
     FDL_CUDA(cudaMemsetAsync(ctx->posf, 0, (size_t)ctx->Np * 8 * sizeof(float), ctx->stream));
     FDL_CUDA(cudaMemsetAsync(ctx->pvec, 0, (size_t)ctx->Np * 4 * sizeof(float), ctx->stream));
     FDL_CUDA(cudaMemsetAsync(ctx->blk_f, 0, (size_t)2 * ctx->nblk * sizeof(double), ctx->stream));
-    FDL_CUDA(cudaMemsetAsync(ctx->blk_cg, 0, (size_t)12 * ctx->nblk * sizeof(double), ctx->stream));
+    FDL_CUDA(cudaMemsetAsync(ctx->blk_cg, 0, (size_t)16 * ctx->nblk * sizeof(double), ctx->stream));
 
     const int items = ctx->nrb * ctx->NC;
     for (int s = 1; s <= 2; ++s)
@@ -702,14 +707,14 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
     const int pq = ps_p2(dim), ps = ps_p1(dim, nsets);
     cudaStream_t s = ctx->stream;
     const int mstep = mark_begin(ctx, 0);
-    // ---- line 4: X^{k+1} = H(X^k) by PCG on the reduced system, warm start X^k
+    // ---- line 4: X^{k+1} = H(X^k): PCG on Eq. 5 (zero-mean gauge), warm start X^k
     if (nloc > 0) FDL_LAUNCH(launch_cg_begin(ctx->Xk, ctx->Xn, ctx->pvec, nloc, row0, dim, pq, s));
     FDL_TRY(allgather_inplace(ctx, ctx->pvec, (size_t)ctx->Mrows * pq, ncclFloat32, 4));
     FDL_TRY(run_p2(ctx));
     if (nloc > 0)
         FDL_LAUNCH(launch_cg_init(ctx->part, ctx->NC, ctx->Mrows, ctx->Rk, ctx->Xn, ctx->diag, ctx->cr, ctx->cz,
                                   ctx->cp, ctx->pvec, ctx->blk_cg, ctx->nblk, nloc, row0, dim, pq, s));
-    FDL_TRY(gather_blocks(ctx, ctx->blk_cg, 12));
+    FDL_TRY(gather_blocks(ctx, ctx->blk_cg, 16));
     FDL_TRY(allgather_inplace(ctx, ctx->pvec, (size_t)ctx->Mrows * pq, ncclFloat32, 4));
     FDL_LAUNCH(launch_cg_finalize(ctx->blk_cg, ctx->nblk, dim, 0, ctx->p.cg_rtol, ctx->sc, ctx->hs_dev, s));
     FDL_CUDA(cudaStreamSynchronize(s));
@@ -722,23 +727,25 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
         FDL_TRY(run_p2(ctx));
         if (nloc > 0)
             FDL_LAUNCH(launch_cg_ap(ctx->part, ctx->NC, ctx->Mrows, ctx->cp, ctx->cy, ctx->blk_cg, ctx->nblk, nloc,
-                                    row0, dim, s));
+                                    row0, dim, ctx->sc, s));
         FDL_TRY(gather_blocks(ctx, ctx->blk_cg, 4));
         FDL_LAUNCH(launch_cg_finalize(ctx->blk_cg, ctx->nblk, dim, 1, ctx->p.cg_rtol, ctx->sc, ctx->hs_dev, s));
         if (nloc > 0)
             FDL_LAUNCH(launch_cg_update(ctx->Xn, ctx->cr, ctx->cz, ctx->cp, ctx->cy, ctx->diag, ctx->blk_cg,
                                         ctx->nblk, ctx->sc, nloc, row0, dim, s));
-        FDL_TRY(gather_blocks(ctx, ctx->blk_cg, 8));
+        FDL_TRY(gather_blocks(ctx, ctx->blk_cg, 16));
         FDL_LAUNCH(launch_cg_finalize(ctx->blk_cg, ctx->nblk, dim, 2, ctx->p.cg_rtol, ctx->sc, ctx->hs_dev, s));
         if (nloc > 0) FDL_LAUNCH(launch_cg_p(ctx->cp, ctx->cz, ctx->pvec, ctx->sc, nloc, row0, dim, pq, s));
         FDL_TRY(allgather_inplace(ctx, ctx->pvec, (size_t)ctx->Mrows * pq, ncclFloat32, 4));
         FDL_CUDA(cudaStreamSynchronize(s));
         ++cg;
     }
-    // ---- line 5: Xt = (1+w) X^{k+1} - w X^k  (Eq. 10), staged with X^{k+1} for P1
+    // ---- pin x_0 = 0, then line 5: Xt = (1+w) X^{k+1} - w X^k (Eq. 10)
+    FDL_LAUNCH(launch_get_pin(ctx->Xn, ctx->pin_slots, ctx->rank, dim, ctx->row0 == 0 && nloc > 0, s));
+    FDL_TRY(allgather_inplace(ctx, ctx->pin_slots, 4, ncclFloat64, 8));
     if (nloc > 0)
-        FDL_LAUNCH(launch_combine(ctx->Xk, ctx->Xn, ctx->Xt, ctx->posf, ctx->blk_max, nloc, row0, dim, omega,
-                                  ctx->cap, nsets, ps, s));
+        FDL_LAUNCH(launch_combine(ctx->Xk, ctx->Xn, ctx->Xt, ctx->posf, ctx->blk_max, ctx->pin_slots, nloc, row0,
+                                  dim, omega, ctx->cap, nsets, ps, s));
     FDL_TRY(allgather_inplace(ctx, ctx->posf, (size_t)ctx->Mrows * ps, ncclFloat32, 4));
     // ---- line 6: f(Xt), f(X^{k+1}) and the next right-hand side, one fused pass
     FDL_TRY(run_p1(ctx, nsets));

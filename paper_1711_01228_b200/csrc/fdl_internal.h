@@ -63,6 +63,8 @@ struct DevScalars {
     double maxdisp;        // scaled units
     // PCG (per column, up to 3)
     double rz[4], bb[4], rr[4], alpha[4], beta[4], pap[4];
+    double S[4];           // sum_i p_i per column (rank-one term of the regularised operator)
+    double sigma;          // regularisation weight: (L + sigma 1 1^T), sigma = mean(diag)/n
     int active[4];
     int done;
     int cg_iters;
@@ -98,14 +100,16 @@ cudaError_t launch_bfs_level(const int64_t* row_ptr, const int32_t* col, const u
                              int level, int row0, int row1, int64_t Np, int hb, unsigned int* anynew,
                              cudaStream_t s);
 cudaError_t launch_diag(const uint8_t* D, int64_t Np, int hb, int n, int nloc, int row0, double* diag,
-                        cudaStream_t s);
+                        double* blk, cudaStream_t s);
+cudaError_t launch_set_sigma(const double* blk, int nblk, int n, DevScalars* sc, cudaStream_t s);
 
 // staging / vector kernels (dim columns, local rows, global row = row0 + lr)
 cudaError_t launch_stage_pos1(const double* X, float* posf, int nloc, int row0, int dim, int ps,
                               cudaStream_t s);
-cudaError_t launch_combine(const double* Xk, const double* Xn, double* Xt, float* posf, double* blk_max,
-                           int nloc, int row0, int dim, double omega, double cap, int nsets, int ps,
-                           cudaStream_t s);
+cudaError_t launch_combine(const double* Xk, double* Xn, double* Xt, float* posf, double* blk_max,
+                           const double* xpin, int nloc, int row0, int dim, double omega, double cap,
+                           int nsets, int ps, cudaStream_t s);
+cudaError_t launch_get_pin(const double* x, double* slots, int rank, int dim, int owns_row0, cudaStream_t s);
 cudaError_t launch_select(double* Xk, double* Rk, const double* Xn, const double* Xt, const double* R1,
                           const double* R2, const double* blk_f, const double* blk_max, int nblk,
                           int nloc, int dim, int nsets, DevScalars* sc, cudaStream_t s);
@@ -115,7 +119,7 @@ cudaError_t launch_cg_init(const double* part, int NC, int Mrows, const double* 
                            const double* diag, double* r, double* z, double* p, float* pvec,
                            double* blk, int nblk, int nloc, int row0, int dim, int pq, cudaStream_t s);
 cudaError_t launch_cg_ap(const double* part, int NC, int Mrows, const double* p, double* y, double* blk,
-                         int nblk, int nloc, int row0, int dim, cudaStream_t s);
+                         int nblk, int nloc, int row0, int dim, const DevScalars* sc, cudaStream_t s);
 cudaError_t launch_cg_update(double* x, double* r, double* z, const double* p, const double* y,
                              const double* diag, double* blk, int nblk, const DevScalars* sc, int nloc,
                              int row0, int dim, cudaStream_t s);

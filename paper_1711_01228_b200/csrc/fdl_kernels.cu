@@ -770,8 +770,10 @@ cudaError_t launch_bfs_level(const int64_t* row_ptr, const int32_t* col, const u
 // thread per local row summing its row sequentially in fp64 (row-group
 // coalesced 16-byte cell reads).
 template <int HB>
-__global__ void __launch_bounds__(256) k_diag(const uint8_t* __restrict__ D, int64_t Np, int nloc, double* diag)
+__global__ void __launch_bounds__(256) k_diag(const uint8_t* __restrict__ D, int64_t Np, int nloc, double* diag,
+                                              double* blk, int row0)
 {
+    __shared__ double red[8];
     const int64_t lr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     constexpr int V = kVecBytes / HB;
     const int64_t cells = Np / V;
@@ -787,19 +789,19 @@ __global__ void __launch_bounds__(256) k_diag(const uint8_t* __restrict__ D, int
         }
     }
     if (lr < nloc) diag[lr] = s;
+    const double t = block_sum_256(lr < nloc ? s : 0.0, red);
+    if (threadIdx.x == 0) blk[row0 / kRB + blockIdx.x] = t;
 }
 
-cudaError_t launch_diag(const uint8_t* D, int64_t Np, int hb, int n, int nloc, int row0, double* diag,
+cudaError_t launch_diag(const uint8_t* D, int64_t Np, int hb, int n, int nloc, int row0, double* diag, double* blk,
                         cudaStream_t s)
 {
     (void)n;
-    (void)row0;
-    const int rows = ((nloc + kRowGroup - 1) / kRowGroup) * kRowGroup;
-    const unsigned grid = (unsigned)((rows + 255) / 256);
+    const unsigned grid = (unsigned)((nloc + 255) / 256);
     if (hb == 1)
-        k_diag<1><<<grid, 256, 0, s>>>(D, Np, nloc, diag);
+        k_diag<1><<<grid, 256, 0, s>>>(D, Np, nloc, diag, blk, row0);
     else
-        k_diag<2><<<grid, 256, 0, s>>>(D, Np, nloc, diag);
+        k_diag<2><<<grid, 256, 0, s>>>(D, Np, nloc, diag, blk, row0);
     return cudaGetLastError();
 }
 
@@ -818,12 +820,14 @@ cudaError_t launch_stage_pos1(const double* X, float* posf, int nloc, int row0, 
     return cudaGetLastError();
 }
 
-// Eq. 10: Xt = (1 + w) X^{k+1} - w X^k, optional per-vertex cap of
+// Pin: X^{k+1} <- x - x_0 ("always taking x_1 = 0").  Then Eq. 10:
+// Xt = (1 + w) X^{k+1} - w X^k, optional per-vertex cap of
 // ||Xt_i - X^{k+1}_i|| (DESIGN R14), staging of the P1 input and the
-// max-displacement diagnostic.
-__global__ void __launch_bounds__(kRB) k_combine(const double* __restrict__ Xk, const double* __restrict__ Xn,
-                                                 double* __restrict__ Xt, float* posf, double* blk_max, int nloc,
-                                                 int row0, int dim, double omega, double cap, int nsets, int ps)
+// max-displacement diagnostic.  xpin = x_0 of the CG solution.
+__global__ void __launch_bounds__(kRB) k_combine(const double* __restrict__ Xk, double* __restrict__ Xn,
+                                                 double* __restrict__ Xt, float* posf, double* blk_max,
+                                                 const double* __restrict__ xpin, int nloc, int row0, int dim,
+                                                 double omega, double cap, int nsets, int ps)
 {
     __shared__ double red[8];
     const int lr = blockIdx.x * kRB + threadIdx.x;
@@ -832,7 +836,8 @@ __global__ void __launch_bounds__(kRB) k_combine(const double* __restrict__ Xk, 
         const int64_t g = (int64_t)row0 + lr;
         double v[3], xn[3], n2 = 0.0;
         for (int q = 0; q < dim; ++q) {
-            xn[q] = Xn[(size_t)lr * dim + q];
+            xn[q] = Xn[(size_t)lr * dim + q] - xpin[q];
+            Xn[(size_t)lr * dim + q] = xn[q];
             const double xk = Xk[(size_t)lr * dim + q];
             const double dq = xn[q] - xk;
             disp2 += dq * dq;
@@ -854,11 +859,26 @@ __global__ void __launch_bounds__(kRB) k_combine(const double* __restrict__ Xk, 
     if (threadIdx.x == 0) blk_max[blockIdx.x] = m;
 }
 
-cudaError_t launch_combine(const double* Xk, const double* Xn, double* Xt, float* posf, double* blk_max, int nloc,
-                           int row0, int dim, double omega, double cap, int nsets, int ps, cudaStream_t s)
+cudaError_t launch_combine(const double* Xk, double* Xn, double* Xt, float* posf, double* blk_max,
+                           const double* xpin, int nloc, int row0, int dim, double omega, double cap, int nsets,
+                           int ps, cudaStream_t s)
 {
-    k_combine<<<(nloc + kRB - 1) / kRB, kRB, 0, s>>>(Xk, Xn, Xt, posf, blk_max, nloc, row0, dim, omega, cap, nsets,
-                                                     ps);
+    k_combine<<<(nloc + kRB - 1) / kRB, kRB, 0, s>>>(Xk, Xn, Xt, posf, blk_max, xpin, nloc, row0, dim, omega, cap,
+                                                     nsets, ps);
+    return cudaGetLastError();
+}
+
+// x_0 of the CG solution (global row 0 lives on the rank with row0 == 0) into
+// slot `rank` of a world x 4 buffer (all-gathered across ranks afterwards).
+__global__ void k_get_pin(const double* __restrict__ x, double* slots, int rank, int dim, int owns_row0)
+{
+    const int q = threadIdx.x;
+    if (q < 4) slots[rank * 4 + q] = (owns_row0 && q < dim) ? x[q] : 0.0;
+}
+
+cudaError_t launch_get_pin(const double* x, double* slots, int rank, int dim, int owns_row0, cudaStream_t s)
+{
+    k_get_pin<<<1, 32, 0, s>>>(x, slots, rank, dim, owns_row0);
     return cudaGetLastError();
 }
 
@@ -905,9 +925,20 @@ cudaError_t launch_select(double* Xk, double* Rk, const double* Xn, const double
 }
 
 // ------------------------------------------------------------------- PCG
-// Jacobi-preconditioned CG on the reduced system (vertex 0 pinned, its
-// row/column deleted), all d columns at once with per-column scalars (the d
-// systems of Eq. 2-5 are independent).  Global row 0 is held at zero.
+// Jacobi-preconditioned CG on Eq. 5, L^W X = L^{X^k} X^k, over all n rows
+// (consistent singular system: L^W 1 = 0 and sum_i (L^X X)_i = 0).  CG from a
+// warm start converges to a solution of Eq. 5; the translation is fixed
+// afterwards by x_0 = 0 in k_combine.  The result is the paper's
+// X^{k+1} (unique up to translation); the gauge is chosen after the
+// solve instead of by deleting row/column 0, which removes the small
+// eigenvalue mean_i w_i0 that pinning introduces (R7).
+// All d columns at once with per-column scalars (the d systems of Eq. 2-5
+// are independent).
+// The correction d = x - x0 solves (L + sigma 1 1^T) d = r0 with r0 = b - L x0:
+// r0 is orthogonal to 1 (up to rounding), so d is the zero-mean solution of
+// L d = r0 and the rank-one term only makes the operator nonsingular (fp32
+// rounding leaves sum_i r_i != 0 otherwise, an unreachable residual floor).
+// sum_i p_i is carried by the recurrence S <- sum z + beta S.
 __global__ void k_cg_begin(const double* __restrict__ Xk, double* x, float* pvec, int nloc, int row0, int dim,
                            int pq)
 {
@@ -917,7 +948,7 @@ __global__ void k_cg_begin(const double* __restrict__ Xk, double* x, float* pvec
     for (int q = 0; q < pq; ++q) {
         double v = 0.0;
         if (q < dim) {
-            v = g == 0 ? 0.0 : Xk[(size_t)lr * dim + q];
+            v = Xk[(size_t)lr * dim + q];
             x[(size_t)lr * dim + q] = v;
         }
         pvec[g * pq + q] = (float)v;
@@ -949,16 +980,13 @@ __global__ void __launch_bounds__(kRB) k_cg_init(const double* __restrict__ part
     __shared__ double red[8];
     const int lr = blockIdx.x * kRB + threadIdx.x;
     const int64_t g = (int64_t)row0 + lr;
-    double rz[3] = {0, 0, 0}, rr[3] = {0, 0, 0}, bb[3] = {0, 0, 0};
+    double rz[3] = {0, 0, 0}, rr[3] = {0, 0, 0}, bb[3] = {0, 0, 0}, zs[3] = {0, 0, 0};
     if (lr < nloc) {
         for (int q = 0; q < dim; ++q) {
             const size_t i = (size_t)lr * dim + q;
-            double rv = 0.0, zv = 0.0, bv = 0.0;
-            if (g != 0) {
-                bv = b[i];
-                rv = bv - chunk_sum(part, NC, Mrows, dim, q, lr);
-                zv = rv / diag[lr];
-            }
+            const double bv = b[i];
+            const double rv = bv - chunk_sum(part, NC, Mrows, dim, q, lr);
+            const double zv = rv / diag[lr];
             r[i] = rv;
             z[i] = zv;
             p[i] = zv;
@@ -966,6 +994,7 @@ __global__ void __launch_bounds__(kRB) k_cg_init(const double* __restrict__ part
             rz[q] = rv * zv;
             rr[q] = rv * rv;
             bb[q] = bv * bv;
+            zs[q] = zv;
         }
         for (int q = dim; q < pq; ++q) pvec[g * pq + q] = 0.0f;
     }
@@ -977,6 +1006,8 @@ __global__ void __launch_bounds__(kRB) k_cg_init(const double* __restrict__ part
         if (threadIdx.x == 0) blk[(size_t)(1 * 4 + q) * nblk + gb] = t;
         t = block_sum_256(bb[q], red);
         if (threadIdx.x == 0) blk[(size_t)(2 * 4 + q) * nblk + gb] = t;
+        t = block_sum_256(zs[q], red);
+        if (threadIdx.x == 0) blk[(size_t)(3 * 4 + q) * nblk + gb] = t;
     }
 }
 
@@ -989,19 +1020,18 @@ cudaError_t launch_cg_init(const double* part, int NC, int Mrows, const double* 
     return cudaGetLastError();
 }
 
-// y = L p (sum of chunk partials, row 0 -> 0); block partials of p.y
+// y = L p (sum of chunk partials); block partials of p.y
 __global__ void __launch_bounds__(kRB) k_cg_ap(const double* __restrict__ part, int NC, int Mrows,
                                                const double* __restrict__ p, double* y, double* blk, int nloc,
-                                               int row0, int dim, int nblk)
+                                               int row0, int dim, int nblk, const DevScalars* __restrict__ sc)
 {
     __shared__ double red[8];
     const int lr = blockIdx.x * kRB + threadIdx.x;
-    const int64_t g = (int64_t)row0 + lr;
     double py[3] = {0, 0, 0};
     if (lr < nloc) {
         for (int q = 0; q < dim; ++q) {
             const size_t i = (size_t)lr * dim + q;
-            const double yv = g == 0 ? 0.0 : chunk_sum(part, NC, Mrows, dim, q, lr);
+            const double yv = chunk_sum(part, NC, Mrows, dim, q, lr) + sc->sigma * sc->S[q];
             y[i] = yv;
             py[q] = p[i] * yv;
         }
@@ -1014,10 +1044,10 @@ __global__ void __launch_bounds__(kRB) k_cg_ap(const double* __restrict__ part, 
 }
 
 cudaError_t launch_cg_ap(const double* part, int NC, int Mrows, const double* p, double* y, double* blk, int nblk,
-                         int nloc, int row0, int dim, cudaStream_t s)
+                         int nloc, int row0, int dim, const DevScalars* sc, cudaStream_t s)
 {
     const int nb = (nloc + kRB - 1) / kRB;
-    k_cg_ap<<<nb, kRB, 0, s>>>(part, NC, Mrows, p, y, blk, nloc, row0, dim, nblk);
+    k_cg_ap<<<nb, kRB, 0, s>>>(part, NC, Mrows, p, y, blk, nloc, row0, dim, nblk, sc);
     return cudaGetLastError();
 }
 
@@ -1028,20 +1058,20 @@ __global__ void __launch_bounds__(kRB) k_cg_update(double* x, double* r, double*
 {
     __shared__ double red[8];
     const int lr = blockIdx.x * kRB + threadIdx.x;
-    const int64_t g = (int64_t)row0 + lr;
-    double rz[3] = {0, 0, 0}, rr[3] = {0, 0, 0};
+    double rz[3] = {0, 0, 0}, rr[3] = {0, 0, 0}, zs[3] = {0, 0, 0};
     if (lr < nloc) {
         for (int q = 0; q < dim; ++q) {
             const size_t i = (size_t)lr * dim + q;
             const double al = sc->alpha[q];
             const double xv = x[i] + al * p[i];
             const double rv = r[i] - al * y[i];
-            const double zv = g == 0 ? 0.0 : rv / diag[lr];
+            const double zv = rv / diag[lr];
             x[i] = xv;
             r[i] = rv;
             z[i] = zv;
             rz[q] = rv * zv;
             rr[q] = rv * rv;
+            zs[q] = zv;
         }
     }
     const int gb = row0 / kRB + blockIdx.x;
@@ -1050,6 +1080,8 @@ __global__ void __launch_bounds__(kRB) k_cg_update(double* x, double* r, double*
         if (threadIdx.x == 0) blk[(size_t)(0 * 4 + q) * nblk + gb] = t;
         t = block_sum_256(rr[q], red);
         if (threadIdx.x == 0) blk[(size_t)(1 * 4 + q) * nblk + gb] = t;
+        t = block_sum_256(zs[q], red);
+        if (threadIdx.x == 0) blk[(size_t)(3 * 4 + q) * nblk + gb] = t;
     }
 }
 
@@ -1084,16 +1116,19 @@ cudaError_t launch_cg_p(double* p, const double* z, float* pvec, const DevScalar
 }
 
 // Scalar step of PCG from block partials (summed in global block order by
-// one warp, fixed butterfly).  mode 0: init; 1: alpha; 2: beta + stop test.
+// one warp, fixed butterfly).  Slots: 0 r.z | p.y (mode 1), 1 r.r, 2 b.b,
+// 3 sum z.  mode 0: init; 1: alpha; 2: beta + stop test.
 __global__ void k_cg_finalize(const double* __restrict__ blk, int nblk, int dim, int mode, double rtol,
                               DevScalars* sc, HostScalars* hs)
 {
     const int lane = threadIdx.x;
-    const int nq = mode == 0 ? 3 : (mode == 1 ? 1 : 2);
-    double sums[3][3];
-    for (int qq = 0; qq < nq; ++qq)
+    double sums[4][3];
+    for (int qq = 0; qq < 4; ++qq)
         for (int c = 0; c < dim; ++c) {
-            const double* src = mode == 1 ? blk + (size_t)c * nblk : blk + (size_t)(qq * 4 + c) * nblk;
+            sums[qq][c] = 0.0;
+            if (mode == 1 && qq > 0) continue;
+            if (mode == 2 && qq == 2) continue;
+            const double* src = blk + (size_t)(qq * 4 + c) * nblk;
             double v = 0.0;
             for (int b = lane; b < nblk; b += 32) v += src[b];
 #pragma unroll
@@ -1109,6 +1144,7 @@ __global__ void k_cg_finalize(const double* __restrict__ blk, int nblk, int dim,
             sc->rz[c] = sums[0][c];
             sc->rr[c] = sums[1][c];
             sc->bb[c] = sums[2][c];
+            sc->S[c] = sums[3][c];
             const int act = sums[1][c] > rt2 * sums[2][c];
             sc->active[c] = act;
             any |= act;
@@ -1129,9 +1165,11 @@ __global__ void k_cg_finalize(const double* __restrict__ blk, int nblk, int dim,
         for (int c = 0; c < dim; ++c) {
             if (sc->active[c]) {
                 const double rzn = sums[0][c];
-                sc->beta[c] = sc->rz[c] != 0.0 ? rzn / sc->rz[c] : 0.0;
+                const double beta = sc->rz[c] != 0.0 ? rzn / sc->rz[c] : 0.0;
+                sc->beta[c] = beta;
                 sc->rz[c] = rzn;
                 sc->rr[c] = sums[1][c];
+                sc->S[c] = sums[3][c] + beta * sc->S[c];  // sum of p = z + beta p
                 sc->active[c] = sums[1][c] > rt2 * sc->bb[c];
             }
             any |= sc->active[c];
@@ -1142,6 +1180,23 @@ __global__ void k_cg_finalize(const double* __restrict__ blk, int nblk, int dim,
         sc->relres = rel;
         hs->done = !any;
     }
+}
+
+// sigma = (sum_i diag_i) / n^2 from per-block partial sums of diag
+__global__ void k_set_sigma(const double* __restrict__ blk, int nblk, double n, DevScalars* sc)
+{
+    const int lane = threadIdx.x;
+    double v = 0.0;
+    for (int b = lane; b < nblk; b += 32) v += blk[b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) sc->sigma = v / (n * n);
+}
+
+cudaError_t launch_set_sigma(const double* blk, int nblk, int n, DevScalars* sc, cudaStream_t s)
+{
+    k_set_sigma<<<1, 32, 0, s>>>(blk, nblk, (double)n, sc);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_cg_finalize(const double* blk, int nblk, int dim, int mode, double rtol, DevScalars* sc,
