@@ -40,10 +40,11 @@ from workloads import configs  # noqa: E402
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 SM_COUNT = 148
 FP32_LANES_PER_SM = 128
-# Algorithmic FP32 flops per ordered pair: per position set
-# delta (d) + r^2 (2d-1) + r^2 h^2 (1) + R accumulate (2d) + u = r^2 q - 1 (2)
-# + s += u^2 (2); per pair the hop decode h^2 (1).  rsqrt counted as 0 flops.
-P1_FLOPS_PER_PAIR_SET = {2: 14, 3: 19}
+# Algorithmic FP32 flops per UNORDERED pair, symmetric pass: per
+# position set delta (d) + r^2 (2d-1) + r^2 h^2 (1) + R_i += q delta (2d)
+# + R_j -= q delta (2d) + u = r^2 q - 1 (2) + s += u^2 (2); per pair the hop
+# decode h^2 (1), shared by the two sets.  rsqrt counted as 0 flops.
+P1_FLOPS_PER_PAIR_SET = {2: 18, 3: 25}
 P1_FLOPS_PER_PAIR_DECODE = 1
 
 
@@ -263,12 +264,12 @@ def run_gpu(args):
 
     # roofline of the dominant kernel (P1 at C5): algorithmic flops / event time
     dim = cfg.dim
-    p1_flops = (st.p1_pairs * P1_FLOPS_PER_PAIR_SET[dim]
-                + (st.p1_pairs - st.p1_pairs_x2 / 2) * P1_FLOPS_PER_PAIR_DECODE)
+    unique_p1_pairs = (st.p1_pairs - st.p1_pairs_x2) + st.p1_pairs_x2 / 2
+    p1_flops = st.p1_pairs * P1_FLOPS_PER_PAIR_SET[dim] + unique_p1_pairs * P1_FLOPS_PER_PAIR_DECODE
     peaks = load_peaks()
     peak_tf = fp32_peak_tflops(peaks)
     p1_tf = p1_flops / (st.p1_ms * 1e-3) / 1e12 if st.p1_ms > 0 else 0.0
-    # P2 is hop-matrix streaming: algorithmic bytes = hop bytes per launch
+    # P2 streams the stored upper triangle: algorithmic bytes = 1 hop per unordered pair
     hop_bytes = info.hop_bytes
     p2_gbs = (st.p2_pairs * hop_bytes) / (st.p2_ms * 1e-3) / 1e9 if st.p2_ms > 0 else 0.0
     p1_share = st.p1_ms / ms if ms > 0 else 0

@@ -118,12 +118,13 @@ typedef struct {
     int32_t n, dim;
     int32_t diameter;      /* max hop count found by the BFS                     */
     int32_t hop_bytes;     /* 1 (uint8) or 2 (uint16) per stored hop             */
-    int32_t row0, row1;    /* rows owned by this context [row0, row1)           */
     int32_t rank, world;
+    int64_t tile0, tile1;  /* hop tiles stored by this context [tile0, tile1)   */
     int32_t iterations;    /* iterations run so far on this context              */
     double k;              /* resolved ideal edge length                        */
     double f;              /* current stress                                    */
-    uint64_t hop_matrix_bytes; /* device bytes of the hop matrix (this rank)   */
+    uint64_t hop_matrix_bytes; /* device bytes of the hop tiles (this rank)     */
+    uint64_t local_pairs;      /* unordered vertex pairs in this rank's tiles   */
     uint64_t device_bytes;     /* all device memory held by the context         */
     double setup_ms;       /* MS-BFS + rowsum + first stress pass at create     */
 } fdl_ctx_info;
@@ -133,8 +134,8 @@ typedef struct {
     uint64_t launches;        /* kernels launched by the library                     */
     uint64_t p1_launches;     /* all-pairs repulsion + stress kernel launches (P1)   */
     uint64_t p2_launches;     /* all-pairs L^W matvec kernel launches (P2)           */
-    uint64_t p1_pairs;        /* ordered pair-position-set interactions done by P1   */
-    uint64_t p2_pairs;        /* ordered pairs done by P2                            */
+    uint64_t p1_pairs;        /* unordered pair x position-set evaluations by P1     */
+    uint64_t p2_pairs;        /* unordered pairs evaluated by P2                     */
     uint64_t p1_pairs_x2;     /* ... of which in launches over two position sets     */
     double p1_ms, p2_ms;      /* CUDA-event time of P1 / P2 launches (needs timing on) */
     double other_ms;          /* CUDA-event time of everything else in fdl_step       */
@@ -164,18 +165,23 @@ fdl_status fdl_create(int32_t n, const int64_t* row_ptr, const int32_t* col_idx,
 
 /* Same, for rank `rank` of `world` GPUs of one node.  `nccl_unique_id` is the
  * 128-byte ncclUniqueId created by rank 0 and broadcast by the caller (e.g.
- * over torch.distributed).  Rank g owns the row block [row0, row1) given by
- * fdl_shard_rows(n, world, g); every rank must pass identical graph,
- * parameters and init_pos.  Results are bitwise identical to world = 1. */
+ * over torch.distributed).  Rank g stores and evaluates the hop tiles
+ * [t0, t1) given by fdl_shard_tiles(n, world, g) (upper-triangle tiles of
+ * 128 x 128 vertex pairs, row-major); every rank keeps the O(n) state
+ * (positions, forces, PCG vectors) replicated.  After each pair pass the
+ * per-rank partial sums are all-gathered over NCCL and summed in rank order,
+ * so all ranks hold identical state.  Every rank must pass identical graph,
+ * parameters and init_pos. */
 fdl_status fdl_create_sharded(int32_t n, const int64_t* row_ptr, const int32_t* col_idx,
                               const double* edge_len, const fdl_params* p,
                               const double* init_pos, const uint8_t* nccl_unique_id,
                               int32_t rank, int32_t world, fdl_ctx** out);
 
-/* Row block owned by `rank` of `world`: rows are split in blocks of
- * FDL_ROW_BLOCK rows, contiguous per rank, as evenly as blocks allow. */
-#define FDL_ROW_BLOCK 256
-fdl_status fdl_shard_rows(int32_t n, int32_t world, int32_t rank, int32_t* row0, int32_t* row1);
+/* Tile range [t0, t1) of `rank` of `world`: equal shares of the
+ * nb(nb+1)/2 upper-triangle tiles (nb = ceil(n / FDL_TILE)) in row-major
+ * triangle order. */
+#define FDL_TILE 128
+fdl_status fdl_shard_tiles(int32_t n, int32_t world, int32_t rank, int64_t* t0, int64_t* t1);
 
 /* Create a 128-byte NCCL unique id (rank 0 calls this). */
 fdl_status fdl_nccl_unique_id(uint8_t* out128);
@@ -202,10 +208,11 @@ fdl_status fdl_set_positions(fdl_ctx* ctx, const double* in, size_t count);
  * R = L^X X ("repulsion"), A = L^W X ("attraction"); *stress = f(X). */
 fdl_status fdl_eval_forces(fdl_ctx* ctx, double* R, double* A, double* stress);
 
-/* Hop counts of rows [r0, r0+nrows) (must be owned rows): out[r*n + j]. */
+/* Hop counts of rows [r0, r0+nrows): out[r*n + j] = hop(r0 + r, j), gathered from
+ * the stored upper triangle (FDL_E_INVALID_ARG if an entry lives on another rank). */
 fdl_status fdl_get_hop_rows(fdl_ctx* ctx, int32_t r0, int32_t nrows, uint16_t* out);
 
-/* Jacobi diagonal sum_{j != i} w_ij for owned rows, original units (n_owned). */
+/* Jacobi diagonal sum_{j != i} w_ij of all n rows, original units (count = n). */
 fdl_status fdl_get_diag(fdl_ctx* ctx, double* out, size_t count);
 
 fdl_status fdl_get_info(fdl_ctx* ctx, fdl_ctx_info* info);

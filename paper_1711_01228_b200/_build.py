@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libfdl.so")
-SOURCES = ["fdl_kernels.cu", "fdl_api.cu"]
+SOURCES = ["fdl_sym.cu", "fdl_kernels.cu", "fdl_api.cu"]
 HEADERS = ["fdl_internal.h", os.path.join(ROOT, "include", "fdl.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -43,7 +43,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             f.write(r.stderr)
         objs.append(obj)
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "shared", "-ldl"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "shared", "-ldl", "-Xlinker", "--no-undefined"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

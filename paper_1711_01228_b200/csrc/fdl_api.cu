@@ -1,13 +1,17 @@
 // fdl_api.cu -- host runtime behind the C ABI of include/fdl.h.
 //
-// One context = one GPU (rank) holding the hop rows it owns, the fp64 state of
-// those rows and full-length fp32 staging vectors.  fdl_step enqueues one
-// Algorithm-2 iteration on the context stream:
-//   PCG solve of L^W X^{k+1} = L^{X^k} X^k (x_0 = 0)      -> P2 passes + fp64 vector kernels
-//   Eq. 10 combine, P1 fused pass over {X^{k+1}, Xt}      -> f, R of both candidates
-//   guard (line 6) and the stop test (DESIGN R4)          -> device select + one D->H copy
-// The host only sequences launches; every arithmetic step of the path runs in
-// fdl_kernels.cu.
+// A context holds, on one GPU, the upper-triangle hop tiles of its tile range
+// and replicated O(n) state (fp64 positions, R, PCG vectors; fp32 staging).
+// fdl_step enqueues one Algorithm-2 iteration:
+//   PCG solve of L^W X^{k+1} = L^{X^k} X^k          -> symmetric P2 passes + fp64 vector kernels
+//   pin x_0 = 0, Eq. 10 combine              -> k_combine
+//   fused symmetric P1 pass over {X^{k+1}, Xt}       -> f and R of both candidates
+//   guard (lines 6-8) on device, stop test on host   -> one D->H scalar copy
+// With several GPUs each rank evaluates the pairs of its tiles; after every
+// pair pass the dense per-rank partials are all-gathered and summed in rank
+// order, so every rank holds identical state and takes identical decisions.
+// The host only sequences launches; all arithmetic of the path is in the
+// kernels (fdl_sym.cu, fdl_kernels.cu).
 #include <dlfcn.h>
 
 #include <algorithm>
@@ -33,7 +37,7 @@ typedef struct {
     char internal[128];
 } ncclUniqueId;
 typedef int ncclResult_t;
-enum { ncclInt8 = 0, ncclUint8 = 1, ncclFloat32 = 7, ncclFloat64 = 8 };
+enum { ncclInt8 = 0, ncclUint8 = 1, ncclInt32 = 2, ncclFloat32 = 7, ncclFloat64 = 8 };
 
 struct NcclApi {
     void* h = nullptr;
@@ -79,36 +83,60 @@ inline uint64_t splitmix64(uint64_t& s)
 }
 inline double u01(uint64_t& s) { return (double)(splitmix64(s) >> 11) * (1.0 / 9007199254740992.0); }
 
-constexpr int kTargetItems = 8 * 148 * 2;  // work items per all-pairs pass (fixed: results independent of GPU count)
+// (I, J) of triangle index t (row-major upper triangle over nb blocks)
+void tri_coords(int64_t t, int64_t nb, int64_t& I, int64_t& J)
+{
+    int64_t lo = 0, hi = nb - 1;  // largest I with tri_index(I, I) <= t
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) / 2;
+        if (tri_index(mid, mid, nb) <= t)
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    I = lo;
+    J = I + (t - tri_index(I, I, nb));
+}
 
 }  // namespace
 
+extern "C" fdl_status fdl_shard_tiles(int32_t n, int32_t world, int32_t rank, int64_t* t0, int64_t* t1);
+
 struct fdl_ctx {
     fdl_params p{};
-    int n = 0, dim = 0, rank = 0, world = 1, row0 = 0, row1 = 0, nloc = 0;
+    int n = 0, dim = 0, rank = 0, world = 1;
     double k = 1.0, cap = INFINITY;
     int hb = 1;
-    int64_t Np = 0;
-    int Mrows = 0, CK = 0, NC = 0, nrb = 0, nblk = 0, nblk_loc = 0;
+    int nb = 0;              // vertex blocks of kT
+    int64_t npad = 0;        // nb * kT
+    int64_t t0 = 0, t1 = 0;  // local tile range [t0, t1) in triangle order
+    int nitems = 0;
+    uint64_t local_pairs = 0;  // unordered pairs in the local tiles
     int diameter = 0;
     int device = 0;
     int sm_count = 148;
-    int p1_grid[3] = {0, 0, 0};
-    int p2_grid = 0;
+    int nblk = 0;  // 256-row reduction blocks of the vector kernels
+    int grid_p1[3] = {0, 0, 0}, grid_p2 = 0, grid_diag = 0;
     cudaStream_t stream = nullptr, own_stream = nullptr;
     // device memory
     uint8_t* D = nullptr;
+    int4* items = nullptr;
+    int *it_lo = nullptr, *it_hi = nullptr;
+    float* jpart = nullptr;
+    double *ipart = nullptr, *spart = nullptr;
+    double *rparts = nullptr, *sparts = nullptr;  // world x partials
     double *diag = nullptr, *Xk = nullptr, *Xn = nullptr, *Xt = nullptr, *Rk = nullptr, *R1 = nullptr,
            *R2 = nullptr;
     double *cr = nullptr, *cz = nullptr, *cp = nullptr, *cy = nullptr;
-    float *posf = nullptr, *pvec = nullptr, *lut = nullptr;
-    double *part = nullptr, *blk_f = nullptr, *blk_max = nullptr, *blk_cg = nullptr;
-    double* pin_slots = nullptr;  // world x 4: x_0 of the CG solution
+    float *posf = nullptr, *pvec = nullptr;
+    double *blk_max = nullptr, *blk_cg = nullptr;
+    double* pin_slots = nullptr;
     DevScalars* sc = nullptr;
     HostScalars* hs = nullptr;      // host-mapped (host pointer)
     HostScalars* hs_dev = nullptr;  // same memory, device pointer
     DevScalars* sc_host = nullptr;  // pinned copy target
     size_t device_bytes = 0;
+    uint64_t hop_bytes_total = 0;
     std::vector<void*> allocs;
     // run state
     int iterations = 0;
@@ -121,7 +149,11 @@ struct fdl_ctx {
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
-    struct Mark { size_t start; int kind; size_t end; };
+    struct Mark {
+        size_t start;
+        int kind;
+        size_t end;
+    };
     std::vector<Mark> ev_marks;
     double setup_ms = 0.0;
     // errors
@@ -150,17 +182,23 @@ fdl_status cuda_fail(fdl_ctx* c, cudaError_t e, const char* what)
     return (e == cudaErrorMemoryAllocation) ? FDL_E_OOM : FDL_E_CUDA;
 }
 
-#define FDL_CUDA(call)                                              \
-    do {                                                            \
-        cudaError_t e_ = (call);                                    \
-        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call);    \
+#define FDL_CUDA(call)                                           \
+    do {                                                         \
+        cudaError_t e_ = (call);                                 \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
     } while (0)
 
-#define FDL_LAUNCH(call)                                            \
-    do {                                                            \
-        cudaError_t e_ = (call);                                    \
-        ctx->stats.launches++;                                      \
-        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call);    \
+#define FDL_LAUNCH(call)                                         \
+    do {                                                         \
+        cudaError_t e_ = (call);                                 \
+        ctx->stats.launches++;                                   \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
+    } while (0)
+
+#define FDL_TRY(x)                     \
+    do {                               \
+        fdl_status s__ = (x);          \
+        if (s__ != FDL_OK) return s__; \
     } while (0)
 
 template <typename T>
@@ -182,10 +220,10 @@ fdl_status dalloc(fdl_ctx* ctx, T** ptr, size_t count)
     return FDL_OK;
 }
 
-#define FDL_ALLOC(ptr, count)                              \
-    do {                                                   \
-        fdl_status s_ = dalloc(ctx, &(ptr), (count));      \
-        if (s_ != FDL_OK) return s_;                       \
+#define FDL_ALLOC(ptr, count)                         \
+    do {                                              \
+        fdl_status s_ = dalloc(ctx, &(ptr), (count)); \
+        if (s_ != FDL_OK) return s_;                  \
     } while (0)
 
 // --------------------------------------------------------------- validation
@@ -266,28 +304,9 @@ fdl_status validate_graph(int32_t n, const int64_t* rp, const int32_t* col, std:
 int ps_p1(int dim, int nsets) { return dim == 2 ? (nsets == 1 ? 2 : 4) : (nsets == 1 ? 4 : 8); }
 int ps_p2(int dim) { return dim == 2 ? 2 : 4; }
 
-PairArgs pair_args(fdl_ctx* ctx, const float* pos, int ps)
-{
-    PairArgs a;
-    a.D = ctx->D;
-    a.pos = pos;
-    a.part = ctx->part;
-    a.lut = ctx->lut;
-    a.Np = ctx->Np;
-    a.n = ctx->n;
-    a.row0 = ctx->row0;
-    a.nloc = ctx->nloc;
-    a.Mrows = ctx->Mrows;
-    a.CK = ctx->CK;
-    a.NC = ctx->NC;
-    a.nrb = ctx->nrb;
-    a.ps = ps;
-    return a;
-}
-
 // ------------------------------------------------------------ event timing
-// Intervals are (start event, end event, kind): kind 1 = P1 launch, 2 = P2
-// launch, 0 = a whole fdl_step.  Events are recorded on the context stream.
+// Intervals are (start event, end event, kind): kind 1 = P1 pass, 2 = P2
+// pass, 3 = DIAG pass, 0 = a whole fdl_step.  Recorded on the context stream.
 cudaEvent_t next_event(fdl_ctx* ctx)
 {
     if (ctx->ev_used == ctx->ev_pool.size()) {
@@ -323,7 +342,7 @@ void collect_events(fdl_ctx* ctx)
         cudaEventElapsedTime(&ms, ctx->ev_pool[m.start], ctx->ev_pool[m.end]);
         if (m.kind == 1) p1 += ms;
         else if (m.kind == 2) p2 += ms;
-        else step += ms;
+        else if (m.kind == 0) step += ms;
     }
     ctx->stats.p1_ms += p1;
     ctx->stats.p2_ms += p2;
@@ -332,35 +351,8 @@ void collect_events(fdl_ctx* ctx)
     ctx->ev_marks.clear();
 }
 
-// ------------------------------------------------------------ pair passes
-fdl_status run_p1(fdl_ctx* ctx, int nsets)
-{
-    if (ctx->nloc == 0) return FDL_OK;
-    PairArgs a = pair_args(ctx, ctx->posf, ps_p1(ctx->dim, nsets));
-    const int mk = mark_begin(ctx, 1);
-    FDL_LAUNCH(launch_p1(a, ctx->dim, nsets, ctx->hb, ctx->p1_grid[nsets], ctx->stream));
-    mark_end(ctx, mk);
-    ctx->stats.p1_launches++;
-    const uint64_t pairs = (uint64_t)ctx->nloc * (uint64_t)(ctx->n - 1) * (uint64_t)nsets;
-    ctx->stats.p1_pairs += pairs;
-    if (nsets == 2) ctx->stats.p1_pairs_x2 += pairs;
-    return FDL_OK;
-}
-
-fdl_status run_p2(fdl_ctx* ctx)
-{
-    if (ctx->nloc == 0) return FDL_OK;
-    PairArgs a = pair_args(ctx, ctx->pvec, ps_p2(ctx->dim));
-    const int mk = mark_begin(ctx, 2);
-    FDL_LAUNCH(launch_p2(a, ctx->dim, ctx->hb, ctx->p2_grid, ctx->stream));
-    mark_end(ctx, mk);
-    ctx->stats.p2_launches++;
-    ctx->stats.p2_pairs += (uint64_t)ctx->nloc * (uint64_t)(ctx->n - 1);
-    return FDL_OK;
-}
-
-// Multi-GPU exchange: all-gather a per-rank slice of `slice_elems` elements
-// (the rank's slice starts at rank*slice_elems) in place.
+// Multi-GPU: all-gather the rank slices (slice_elems each, rank slice at
+// rank * slice_elems) of `buf` in place.
 fdl_status allgather_inplace(fdl_ctx* ctx, void* buf, size_t slice_elems, int nccl_type, size_t esize)
 {
     if (ctx->world == 1) return FDL_OK;
@@ -375,20 +367,56 @@ fdl_status allgather_inplace(fdl_ctx* ctx, void* buf, size_t slice_elems, int nc
     return FDL_OK;
 }
 
-#define FDL_TRY(x)                         \
-    do {                                   \
-        fdl_status s__ = (x);              \
-        if (s__ != FDL_OK) return s__;     \
-    } while (0)
-
-// block partials live at global block index; with several ranks each rank
-// fills its own blocks, then an all-gather gives every rank all of them.
-fdl_status gather_blocks(fdl_ctx* ctx, double* blk, int nquant)
+// ------------------------------------------------------------ pair passes
+// One symmetric pass over the local tiles + the per-row fixed-order
+// reduction; with several ranks the dense rank partials are all-gathered and
+// summed in rank order.  out0 gets components [0, D0), out1 the rest.
+fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* out0, double* out1, int set_cur)
 {
-    if (ctx->world == 1) return FDL_OK;
-    const size_t per_rank = (size_t)ctx->Mrows / kRB;
-    for (int q = 0; q < nquant; ++q)
-        FDL_TRY(allgather_inplace(ctx, blk + (size_t)q * ctx->nblk, per_rank, ncclFloat64, 8));
+    const int dim = ctx->dim;
+    const int C = mode == kSymP1 ? nsets * dim : (mode == kSymP2 ? dim : 1);
+    const int D0 = mode == kSymP1 ? dim : C;
+    SymArgs a;
+    a.D = ctx->D;
+    a.pos = pos;
+    a.jpart = ctx->jpart;
+    a.ipart = ctx->ipart;
+    a.spart = ctx->spart;
+    a.items = ctx->items;
+    a.nitems = ctx->nitems;
+    a.n = ctx->n;
+    const int grid = mode == kSymP1 ? ctx->grid_p1[nsets] : (mode == kSymP2 ? ctx->grid_p2 : ctx->grid_diag);
+    const int mk = mark_begin(ctx, mode == kSymP1 ? 1 : (mode == kSymP2 ? 2 : 3));
+    if (ctx->nitems > 0) FDL_LAUNCH(launch_sym(a, mode, dim, nsets, ctx->hb, grid, ctx->stream));
+    mark_end(ctx, mk);
+    if (mode == kSymP1) {
+        ctx->stats.p1_launches++;
+        ctx->stats.p1_pairs += ctx->local_pairs * (uint64_t)nsets;
+        if (nsets == 2) ctx->stats.p1_pairs_x2 += ctx->local_pairs * 2;
+    } else if (mode == kSymP2) {
+        ctx->stats.p2_launches++;
+        ctx->stats.p2_pairs += ctx->local_pairs;
+    }
+    if (ctx->world == 1) {
+        FDL_LAUNCH(launch_sym_reduce(ctx->ipart, ctx->jpart, ctx->it_lo, ctx->it_hi, ctx->nb, ctx->t0, ctx->t1, C, D0,
+                                     out0, out1, ctx->stream));
+        if (mode == kSymP1) {
+            FDL_LAUNCH(launch_sym_stress(ctx->spart, ctx->nitems, nsets, ctx->sparts, ctx->stream));
+            FDL_LAUNCH(launch_stress_ranks(ctx->sparts, 1, nsets, ctx->sc, set_cur, ctx->stream));
+        }
+        return FDL_OK;
+    }
+    const size_t slice = (size_t)ctx->npad * C;
+    double* mine = ctx->rparts + (size_t)ctx->rank * slice;
+    FDL_LAUNCH(launch_sym_reduce(ctx->ipart, ctx->jpart, ctx->it_lo, ctx->it_hi, ctx->nb, ctx->t0, ctx->t1, C, C, mine,
+                                 nullptr, ctx->stream));
+    FDL_TRY(allgather_inplace(ctx, ctx->rparts, slice, ncclFloat64, 8));
+    FDL_LAUNCH(launch_rank_sum(ctx->rparts, ctx->world, ctx->npad, C, D0, out0, out1, ctx->stream));
+    if (mode == kSymP1) {
+        FDL_LAUNCH(launch_sym_stress(ctx->spart, ctx->nitems, nsets, ctx->sparts + 2 * ctx->rank, ctx->stream));
+        FDL_TRY(allgather_inplace(ctx, ctx->sparts, 2, ncclFloat64, 8));
+        FDL_LAUNCH(launch_stress_ranks(ctx->sparts, ctx->world, nsets, ctx->sc, set_cur, ctx->stream));
+    }
     return FDL_OK;
 }
 
@@ -397,14 +425,8 @@ fdl_status gather_blocks(fdl_ctx* ctx, double* blk, int nquant)
 fdl_status eval_current(fdl_ctx* ctx)
 {
     const int ps = ps_p1(ctx->dim, 1);
-    if (ctx->nloc > 0) FDL_LAUNCH(launch_stage_pos1(ctx->Xk, ctx->posf, ctx->nloc, ctx->row0, ctx->dim, ps, ctx->stream));
-    FDL_TRY(allgather_inplace(ctx, ctx->posf, (size_t)ctx->Mrows * ps, ncclFloat32, 4));
-    FDL_TRY(run_p1(ctx, 1));
-    if (ctx->nloc > 0)
-        FDL_LAUNCH(launch_p1_reduce(ctx->part, ctx->NC, ctx->Mrows, ctx->nloc, ctx->row0, ctx->dim, 1, ctx->Rk,
-                                    nullptr, ctx->blk_f, ctx->nblk, ctx->stream));
-    FDL_TRY(gather_blocks(ctx, ctx->blk_f, 1));
-    FDL_LAUNCH(launch_stress_finalize(ctx->blk_f, ctx->nblk, 1, ctx->sc, 1, ctx->stream));
+    FDL_LAUNCH(launch_stage_pos1(ctx->Xk, ctx->posf, ctx->n, 0, ctx->dim, ps, ctx->stream));
+    FDL_TRY(run_sym(ctx, kSymP1, 1, ctx->posf, ctx->Rk, nullptr, 1));
     FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, ctx->stream));
     FDL_CUDA(cudaStreamSynchronize(ctx->stream));
     collect_events(ctx);
@@ -413,23 +435,23 @@ fdl_status eval_current(fdl_ctx* ctx)
     return FDL_OK;
 }
 
-// Upload a full n*dim placement (original units): pin x_0 = 0, scale
-// by 1/k, keep the owned rows.
+// Upload a full n*dim placement (original units): pin x_0 = 0, scale by 1/k.
 fdl_status upload_positions(fdl_ctx* ctx, const double* X)
 {
-    std::vector<double> loc((size_t)std::max(ctx->nloc, 1) * ctx->dim);
-    for (int lr = 0; lr < ctx->nloc; ++lr)
+    std::vector<double> loc((size_t)ctx->n * ctx->dim);
+    for (int i = 0; i < ctx->n; ++i)
         for (int q = 0; q < ctx->dim; ++q) {
-            const size_t g = (size_t)(ctx->row0 + lr) * ctx->dim + q;
-            loc[(size_t)lr * ctx->dim + q] = (X[g] - X[q]) / ctx->k;
+            const size_t g = (size_t)i * ctx->dim + q;
+            loc[g] = (X[g] - X[q]) / ctx->k;
         }
-    if (ctx->nloc > 0)
-        FDL_CUDA(cudaMemcpyAsync(ctx->Xk, loc.data(), loc.size() * sizeof(double), cudaMemcpyHostToDevice,
-                                 ctx->stream));
+    FDL_CUDA(cudaMemcpyAsync(ctx->Xk, loc.data(), loc.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     return eval_current(ctx);
 }
 
 // ------------------------------------------------------------------ MS-BFS
+// Sources: the rows of the blocks I of the local tiles.  Writes the upper
+// triangle tiles of the local range; the Jacobi diagonal follows from one
+// symmetric DIAG pass.
 fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int ecc0)
 {
     const int n = ctx->n;
@@ -437,7 +459,6 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
     int32_t* d_col = nullptr;
     uint32_t *fa = nullptr, *fb = nullptr, *vis = nullptr;
     const size_t masks = (size_t)n * kBFSWords;
-    // BFS scratch is freed at the end; allocate outside the context list
     FDL_CUDA(cudaMalloc(&d_rp, sizeof(int64_t) * (n + 1)));
     FDL_CUDA(cudaMalloc(&d_col, sizeof(int32_t) * std::max<int64_t>(rp[n], 1)));
     FDL_CUDA(cudaMalloc(&fa, masks * 4));
@@ -447,18 +468,26 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
     if (rp[n] > 0)
         FDL_CUDA(cudaMemcpyAsync(d_col, col, sizeof(int32_t) * rp[n], cudaMemcpyHostToDevice, ctx->stream));
 
+    int64_t Ilo = 0, Jlo = 0, Ihi = -1, Jhi = 0;
+    if (ctx->t1 > ctx->t0) {
+        tri_coords(ctx->t0, ctx->nb, Ilo, Jlo);
+        tri_coords(ctx->t1 - 1, ctx->nb, Ihi, Jhi);
+    }
+    const int src_lo = (int)std::min<int64_t>(n, Ilo * kT);
+    const int src_hi = (int)std::min<int64_t>(n, (Ihi + 1) * kT);
+    const int64_t ntiles = ctx->t1 - ctx->t0;
+
     // u8 when the diameter provably fits (diam <= 2 ecc0 <= 255); u16 when it
     // provably does not (ecc0 > 255); otherwise try u8 and redo on overflow.
     int hb = (2 * ecc0 <= 255) ? 1 : (ecc0 > 255 ? 2 : 1);
     fdl_status st = FDL_OK;
     for (int attempt = 0; attempt < 2; ++attempt) {
         ctx->hb = hb;
-        const int64_t V = kVecBytes / hb;
-        const size_t dbytes = (size_t)ctx->Mrows * (size_t)ctx->Np * hb;
-        (void)V;
+        const size_t dbytes = (size_t)std::max<int64_t>(ntiles, 1) * kT * kT * hb;
         if (ctx->D) {
             cudaFree(ctx->D);
             ctx->allocs.erase(std::find(ctx->allocs.begin(), ctx->allocs.end(), (void*)ctx->D));
+            ctx->device_bytes -= ctx->hop_bytes_total;
             ctx->D = nullptr;
         }
         void* q = nullptr;
@@ -471,18 +500,19 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
         ctx->D = static_cast<uint8_t*>(q);
         ctx->allocs.push_back(q);
         ctx->device_bytes += dbytes;
+        ctx->hop_bytes_total = dbytes;
         FDL_CUDA(cudaMemsetAsync(ctx->D, 0, dbytes, ctx->stream));
         const int maxhop = hb == 1 ? 255 : 65535;
         bool overflow = false;
         int diam = 0;
-        for (int s0 = 0; s0 < n && !overflow; s0 += 32 * kBFSWords) {
-            const int nsrc = std::min(32 * kBFSWords, n - s0);
+        for (int s0 = src_lo; s0 < src_hi && !overflow; s0 += 32 * kBFSWords) {
+            const int nsrc = std::min(32 * kBFSWords, src_hi - s0);
             FDL_LAUNCH(launch_bfs_init(fa, vis, n, s0, ctx->stream));
             uint32_t *fin = fa, *fout = fb;
             for (int level = 1;; ++level) {
                 FDL_CUDA(cudaMemsetAsync(&ctx->sc->anynew, 0, sizeof(unsigned int), ctx->stream));
-                FDL_LAUNCH(launch_bfs_level(d_rp, d_col, fin, fout, vis, ctx->D, n, s0, nsrc, level, ctx->row0,
-                                            ctx->row1, ctx->Np, hb, &ctx->sc->anynew, ctx->stream));
+                FDL_LAUNCH(launch_bfs_level_sym(d_rp, d_col, fin, fout, vis, ctx->D, n, s0, nsrc, level, ctx->nb,
+                                                ctx->t0, ctx->t1, hb, &ctx->sc->anynew, ctx->stream));
                 FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost,
                                          ctx->stream));
                 FDL_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -511,17 +541,20 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
     cudaFree(fb);
     cudaFree(vis);
     if (st != FDL_OK) return st;
-    FDL_CUDA(cudaMemsetAsync(ctx->blk_f, 0, (size_t)ctx->nblk * sizeof(double), ctx->stream));
-    if (ctx->nloc > 0)
-        FDL_LAUNCH(launch_diag(ctx->D, ctx->Np, ctx->hb, n, ctx->nloc, ctx->row0, ctx->diag, ctx->blk_f, ctx->stream));
-    FDL_TRY(gather_blocks(ctx, ctx->blk_f, 1));
-    FDL_LAUNCH(launch_set_sigma(ctx->blk_f, ctx->nblk, n, ctx->sc, ctx->stream));
-    // w'_h = fp32(1/h^2) (P2 u8 table)
-    float lut[256];
-    lut[0] = 0.0f;
-    for (int h = 1; h < 256; ++h) lut[h] = 1.0f / (float)(h * h);
-    FDL_CUDA(cudaMemcpyAsync(ctx->lut, lut, sizeof lut, cudaMemcpyHostToDevice, ctx->stream));
-    FDL_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->world > 1) {
+        // every rank BFSed only its sources: agree on the diameter and hop width (max over ranks)
+        int* dd = nullptr;
+        FDL_CUDA(cudaMalloc(&dd, sizeof(int) * 2 * ctx->world));
+        int mine[2] = {ctx->diameter, ctx->hb};
+        FDL_CUDA(cudaMemcpyAsync(dd + 2 * ctx->rank, mine, sizeof mine, cudaMemcpyHostToDevice, ctx->stream));
+        fdl_status s2 = allgather_inplace(ctx, dd, 2, ncclInt32, 4);
+        std::vector<int> all(2 * ctx->world);
+        cudaMemcpyAsync(all.data(), dd, sizeof(int) * 2 * ctx->world, cudaMemcpyDeviceToHost, ctx->stream);
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(dd);
+        FDL_TRY(s2);
+        for (int g = 0; g < ctx->world; ++g) ctx->diameter = std::max(ctx->diameter, all[2 * g]);
+    }
     return FDL_OK;
 }
 
@@ -562,6 +595,35 @@ fdl_status check_params(const fdl_params* p, std::string& msg)
     return FDL_OK;
 }
 
+// Work items of the local tile range: strip segments of <= kSeg tiles.
+void build_items(fdl_ctx* ctx, std::vector<int4>& items, std::vector<int>& lo, std::vector<int>& hi)
+{
+    const int64_t nb = ctx->nb;
+    lo.assign(nb, 0);
+    hi.assign(nb, 0);
+    std::vector<char> seen(nb, 0);
+    int64_t t = ctx->t0;
+    ctx->local_pairs = 0;
+    while (t < ctx->t1) {
+        int64_t I, J;
+        tri_coords(t, nb, I, J);
+        const int64_t strip_end = tri_index(I, nb - 1, nb) + 1;
+        const int64_t nt = std::min<int64_t>({(int64_t)kSeg, strip_end - t, ctx->t1 - t});
+        if (!seen[I]) {
+            seen[I] = 1;
+            lo[I] = (int)items.size();
+        }
+        items.push_back(make_int4((int)I, (int)J, (int)nt, (int)(t - ctx->t0)));
+        hi[I] = (int)items.size();
+        const int64_t mi = std::min<int64_t>(kT, ctx->n - I * kT);
+        for (int64_t j = J; j < J + nt; ++j) {
+            const int64_t mj = std::min<int64_t>(kT, ctx->n - j * kT);
+            ctx->local_pairs += (j == I) ? (uint64_t)(mi * (mi - 1) / 2) : (uint64_t)(mi * mj);
+        }
+        t += nt;
+    }
+}
+
 fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const double* edge_len,
                        const fdl_params* pin, const double* init_pos, const uint8_t* nccl_id, int32_t rank,
                        int32_t world, fdl_ctx* ctx)
@@ -573,7 +635,8 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     std::string msg;
     fdl_status st = check_params(&p, msg);
     if (st != FDL_OK) return set_err(ctx, st, msg);
-    if (edge_len) return set_err(ctx, FDL_E_BAD_LENGTH, "weighted edge lengths are not supported yet (unit lengths only)");
+    if (edge_len)
+        return set_err(ctx, FDL_E_BAD_LENGTH, "weighted edge lengths are not supported yet (unit lengths only)");
     if (world < 1 || rank < 0 || rank >= world) return set_err(ctx, FDL_E_INVALID_ARG, "bad rank/world");
     int ecc0 = 0;
     st = validate_graph(n, rp, col, msg, ecc0);
@@ -603,72 +666,74 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
         memcpy(id.internal, nccl_id, 128);
         ncclResult_t r = g_nccl.CommInitRank(&ctx->comm, world, id, rank);
         if (r != 0)
-            return set_err(ctx, FDL_E_NCCL,
-                           std::string("ncclCommInitRank: ") + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
+            return set_err(ctx, FDL_E_NCCL, std::string("ncclCommInitRank: ") +
+                                                 (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
     }
 
-    // ---- sizes (all from n and world; CK from n only, so per-row sums do
-    // not depend on the number of GPUs)
-    const int nblk_total = (n + kRB - 1) / kRB;
-    const int blocks_per_rank = (nblk_total + world - 1) / world;
-    ctx->Mrows = blocks_per_rank * kRB;
-    ctx->nblk = blocks_per_rank * world;
-    ctx->Np = (int64_t)ctx->nblk * kRB;
-    ctx->row0 = rank * ctx->Mrows;
-    ctx->row1 = std::min(n, ctx->row0 + ctx->Mrows);
-    ctx->nloc = std::max(0, ctx->row1 - ctx->row0);
-    if (ctx->nloc == 0) ctx->row0 = ctx->row1 = std::min(n, ctx->row0);
-    ctx->nblk_loc = (ctx->nloc + kRB - 1) / kRB;
-    ctx->nrb = ctx->Mrows / kBM;
-    {
-        const int nt = (n + kColPad - 1) / kColPad;
-        const int nc0 = std::min(std::max((kTargetItems + nblk_total - 1) / nblk_total, 1), nt);
-        ctx->CK = ((nt + nc0 - 1) / nc0) * kColPad;
-        ctx->NC = (n + ctx->CK - 1) / ctx->CK;
-    }
+    // ---- geometry: tiles of kT x kT, this rank's share of the triangle
+    ctx->nb = (n + kT - 1) / kT;
+    ctx->npad = (int64_t)ctx->nb * kT;
+    fdl_shard_tiles(n, world, rank, &ctx->t0, &ctx->t1);
+    std::vector<int4> items;
+    std::vector<int> lo, hi;
+    build_items(ctx, items, lo, hi);
+    ctx->nitems = (int)items.size();
+    ctx->nblk = (int)((ctx->npad + kRB - 1) / kRB);
     const int dim = ctx->dim;
-    const size_t vloc = (size_t)std::max(ctx->nloc, 1) * dim;
+    const size_t vn = (size_t)ctx->npad * dim;
+    const int64_t ntiles = ctx->t1 - ctx->t0;
+    const int Cmax = 2 * dim;
+
     FDL_ALLOC(ctx->sc, 1);
     FDL_CUDA(cudaMemsetAsync(ctx->sc, 0, sizeof(DevScalars), ctx->stream));
     FDL_CUDA(cudaHostAlloc(&ctx->hs, sizeof(HostScalars), cudaHostAllocMapped));
     FDL_CUDA(cudaHostGetDevicePointer((void**)&ctx->hs_dev, ctx->hs, 0));
     FDL_CUDA(cudaHostAlloc(&ctx->sc_host, sizeof(DevScalars), cudaHostAllocDefault));
     memset(ctx->sc_host, 0, sizeof(DevScalars));
-    FDL_ALLOC(ctx->diag, std::max(ctx->nloc, 1));
-    FDL_ALLOC(ctx->Xk, vloc);
-    FDL_ALLOC(ctx->Xn, vloc);
-    FDL_ALLOC(ctx->Xt, vloc);
-    FDL_ALLOC(ctx->Rk, vloc);
-    FDL_ALLOC(ctx->R1, vloc);
-    FDL_ALLOC(ctx->R2, vloc);
-    FDL_ALLOC(ctx->cr, vloc);
-    FDL_ALLOC(ctx->cz, vloc);
-    FDL_ALLOC(ctx->cp, vloc);
-    FDL_ALLOC(ctx->cy, vloc);
-    FDL_ALLOC(ctx->posf, (size_t)ctx->Np * 8);
-    FDL_ALLOC(ctx->pvec, (size_t)ctx->Np * 4);
-    FDL_ALLOC(ctx->lut, 256);
-    FDL_ALLOC(ctx->part, (size_t)ctx->NC * 2 * (dim + 1) * ctx->Mrows);
-    FDL_ALLOC(ctx->blk_f, (size_t)2 * ctx->nblk);
+    FDL_ALLOC(ctx->items, std::max(ctx->nitems, 1));
+    FDL_ALLOC(ctx->it_lo, ctx->nb);
+    FDL_ALLOC(ctx->it_hi, ctx->nb);
+    FDL_ALLOC(ctx->jpart, (size_t)std::max<int64_t>(ntiles, 1) * kT * Cmax);
+    FDL_ALLOC(ctx->ipart, (size_t)std::max(ctx->nitems, 1) * kT * Cmax);
+    FDL_ALLOC(ctx->spart, (size_t)std::max(ctx->nitems, 1) * 2);
+    FDL_ALLOC(ctx->sparts, (size_t)2 * world);
+    if (world > 1) FDL_ALLOC(ctx->rparts, (size_t)world * ctx->npad * Cmax);
+    FDL_ALLOC(ctx->diag, (size_t)ctx->npad);
+    FDL_ALLOC(ctx->Xk, vn);
+    FDL_ALLOC(ctx->Xn, vn);
+    FDL_ALLOC(ctx->Xt, vn);
+    FDL_ALLOC(ctx->Rk, vn);
+    FDL_ALLOC(ctx->R1, vn);
+    FDL_ALLOC(ctx->R2, vn);
+    FDL_ALLOC(ctx->cr, vn);
+    FDL_ALLOC(ctx->cz, vn);
+    FDL_ALLOC(ctx->cp, vn);
+    FDL_ALLOC(ctx->cy, vn);
+    FDL_ALLOC(ctx->posf, (size_t)ctx->npad * 8);
+    FDL_ALLOC(ctx->pvec, (size_t)ctx->npad * 4);
     FDL_ALLOC(ctx->blk_max, (size_t)ctx->nblk);
     FDL_ALLOC(ctx->blk_cg, (size_t)16 * ctx->nblk);
-    FDL_ALLOC(ctx->pin_slots, (size_t)4 * world);
-    FDL_CUDA(cudaMemsetAsync(ctx->posf, 0, (size_t)ctx->Np * 8 * sizeof(float), ctx->stream));
-    FDL_CUDA(cudaMemsetAsync(ctx->pvec, 0, (size_t)ctx->Np * 4 * sizeof(float), ctx->stream));
-    FDL_CUDA(cudaMemsetAsync(ctx->blk_f, 0, (size_t)2 * ctx->nblk * sizeof(double), ctx->stream));
+    FDL_ALLOC(ctx->pin_slots, 4);
+    FDL_CUDA(cudaMemsetAsync(ctx->posf, 0, (size_t)ctx->npad * 8 * sizeof(float), ctx->stream));
+    FDL_CUDA(cudaMemsetAsync(ctx->pvec, 0, (size_t)ctx->npad * 4 * sizeof(float), ctx->stream));
+    FDL_CUDA(cudaMemsetAsync(ctx->Xk, 0, vn * sizeof(double), ctx->stream));
     FDL_CUDA(cudaMemsetAsync(ctx->blk_cg, 0, (size_t)16 * ctx->nblk * sizeof(double), ctx->stream));
+    if (ctx->nitems > 0)
+        FDL_CUDA(cudaMemcpyAsync(ctx->items, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+    FDL_CUDA(cudaMemcpyAsync(ctx->it_lo, lo.data(), sizeof(int) * ctx->nb, cudaMemcpyHostToDevice, ctx->stream));
+    FDL_CUDA(cudaMemcpyAsync(ctx->it_hi, hi.data(), sizeof(int) * ctx->nb, cudaMemcpyHostToDevice, ctx->stream));
 
-    const int items = ctx->nrb * ctx->NC;
-    for (int s = 1; s <= 2; ++s)
-        ctx->p1_grid[s] = std::max(1, std::min(items, ctx->sm_count * p1_max_ctas(dim, s, 1, ctx->device)));
-    ctx->p2_grid = std::max(1, std::min(items, ctx->sm_count * p2_max_ctas(dim, 1, ctx->device)));
-
+    // hop matrix first (fixes the hop width), then grids, then the Jacobi diagonal
     FDL_TRY(build_hops(ctx, rp, col, ecc0));
-    if (ctx->hb == 2) {
-        for (int s = 1; s <= 2; ++s)
-            ctx->p1_grid[s] = std::max(1, std::min(items, ctx->sm_count * p1_max_ctas(dim, s, 2, ctx->device)));
-        ctx->p2_grid = std::max(1, std::min(items, ctx->sm_count * p2_max_ctas(dim, 2, ctx->device)));
-    }
+    const int cap_items = std::max(ctx->nitems, 1);
+    for (int s = 1; s <= 2; ++s)
+        ctx->grid_p1[s] = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymP1, dim, s, ctx->hb)));
+    ctx->grid_p2 = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymP2, dim, 1, ctx->hb)));
+    ctx->grid_diag = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymDiag, dim, 1, ctx->hb)));
+    // Jacobi diagonal sum_{j != i} w'_ij (one symmetric DIAG pass) and sigma = mean(diag)/n
+    FDL_TRY(run_sym(ctx, kSymDiag, 1, ctx->posf, ctx->diag, nullptr, 0));
+    FDL_LAUNCH(launch_set_sigma_rows(ctx->diag, ctx->n, ctx->sc, ctx->stream));
 
     // initial placement: caller's, else seeded uniform on the unit cube
     std::vector<double> X0;
@@ -703,19 +768,15 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
     if (ctx->stopped) return set_err(ctx, FDL_E_STATE, "the run has stopped; call fdl_set_positions to restart");
     const double omega = pick_omega(ctx);
     const int nsets = omega > 0.0 ? 2 : 1;
-    const int dim = ctx->dim, nloc = ctx->nloc, row0 = ctx->row0;
+    const int dim = ctx->dim, n = ctx->n;
     const int pq = ps_p2(dim), ps = ps_p1(dim, nsets);
     cudaStream_t s = ctx->stream;
     const int mstep = mark_begin(ctx, 0);
-    // ---- line 4: X^{k+1} = H(X^k): PCG on Eq. 5 (zero-mean gauge), warm start X^k
-    if (nloc > 0) FDL_LAUNCH(launch_cg_begin(ctx->Xk, ctx->Xn, ctx->pvec, nloc, row0, dim, pq, s));
-    FDL_TRY(allgather_inplace(ctx, ctx->pvec, (size_t)ctx->Mrows * pq, ncclFloat32, 4));
-    FDL_TRY(run_p2(ctx));
-    if (nloc > 0)
-        FDL_LAUNCH(launch_cg_init(ctx->part, ctx->NC, ctx->Mrows, ctx->Rk, ctx->Xn, ctx->diag, ctx->cr, ctx->cz,
-                                  ctx->cp, ctx->pvec, ctx->blk_cg, ctx->nblk, nloc, row0, dim, pq, s));
-    FDL_TRY(gather_blocks(ctx, ctx->blk_cg, 16));
-    FDL_TRY(allgather_inplace(ctx, ctx->pvec, (size_t)ctx->Mrows * pq, ncclFloat32, 4));
+    // ---- line 4: X^{k+1} = H(X^k): PCG on Eq. 5 (zero-mean gauge, R7), warm start X^k
+    FDL_LAUNCH(launch_cg_begin(ctx->Xk, ctx->Xn, ctx->pvec, n, 0, dim, pq, s));
+    FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->cy, nullptr, 0));
+    FDL_LAUNCH(launch_cg_init(ctx->cy, ctx->Rk, ctx->diag, ctx->cr, ctx->cz, ctx->cp, ctx->pvec, ctx->blk_cg, ctx->nblk,
+                              n, dim, pq, s));
     FDL_LAUNCH(launch_cg_finalize(ctx->blk_cg, ctx->nblk, dim, 0, ctx->p.cg_rtol, ctx->sc, ctx->hs_dev, s));
     FDL_CUDA(cudaStreamSynchronize(s));
     int cg = 0;
@@ -724,40 +785,25 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
             collect_events(ctx);
             return set_err(ctx, FDL_E_SOLVER, "PCG reached cg_max_iter before cg_rtol (S:223)");
         }
-        FDL_TRY(run_p2(ctx));
-        if (nloc > 0)
-            FDL_LAUNCH(launch_cg_ap(ctx->part, ctx->NC, ctx->Mrows, ctx->cp, ctx->cy, ctx->blk_cg, ctx->nblk, nloc,
-                                    row0, dim, ctx->sc, s));
-        FDL_TRY(gather_blocks(ctx, ctx->blk_cg, 4));
+        FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->cy, nullptr, 0));
+        FDL_LAUNCH(launch_cg_ap(ctx->cp, ctx->cy, ctx->blk_cg, ctx->nblk, n, dim, ctx->sc, s));
         FDL_LAUNCH(launch_cg_finalize(ctx->blk_cg, ctx->nblk, dim, 1, ctx->p.cg_rtol, ctx->sc, ctx->hs_dev, s));
-        if (nloc > 0)
-            FDL_LAUNCH(launch_cg_update(ctx->Xn, ctx->cr, ctx->cz, ctx->cp, ctx->cy, ctx->diag, ctx->blk_cg,
-                                        ctx->nblk, ctx->sc, nloc, row0, dim, s));
-        FDL_TRY(gather_blocks(ctx, ctx->blk_cg, 16));
+        FDL_LAUNCH(launch_cg_update(ctx->Xn, ctx->cr, ctx->cz, ctx->cp, ctx->cy, ctx->diag, ctx->blk_cg, ctx->nblk,
+                                    ctx->sc, n, 0, dim, s));
         FDL_LAUNCH(launch_cg_finalize(ctx->blk_cg, ctx->nblk, dim, 2, ctx->p.cg_rtol, ctx->sc, ctx->hs_dev, s));
-        if (nloc > 0) FDL_LAUNCH(launch_cg_p(ctx->cp, ctx->cz, ctx->pvec, ctx->sc, nloc, row0, dim, pq, s));
-        FDL_TRY(allgather_inplace(ctx, ctx->pvec, (size_t)ctx->Mrows * pq, ncclFloat32, 4));
+        FDL_LAUNCH(launch_cg_p(ctx->cp, ctx->cz, ctx->pvec, ctx->sc, n, 0, dim, pq, s));
         FDL_CUDA(cudaStreamSynchronize(s));
         ++cg;
     }
     // ---- pin x_0 = 0, then line 5: Xt = (1+w) X^{k+1} - w X^k (Eq. 10)
-    FDL_LAUNCH(launch_get_pin(ctx->Xn, ctx->pin_slots, ctx->rank, dim, ctx->row0 == 0 && nloc > 0, s));
-    FDL_TRY(allgather_inplace(ctx, ctx->pin_slots, 4, ncclFloat64, 8));
-    if (nloc > 0)
-        FDL_LAUNCH(launch_combine(ctx->Xk, ctx->Xn, ctx->Xt, ctx->posf, ctx->blk_max, ctx->pin_slots, nloc, row0,
-                                  dim, omega, ctx->cap, nsets, ps, s));
-    FDL_TRY(allgather_inplace(ctx, ctx->posf, (size_t)ctx->Mrows * ps, ncclFloat32, 4));
+    FDL_LAUNCH(launch_get_pin(ctx->Xn, ctx->pin_slots, 0, dim, 1, s));
+    FDL_LAUNCH(launch_combine(ctx->Xk, ctx->Xn, ctx->Xt, ctx->posf, ctx->blk_max, ctx->pin_slots, n, 0, dim, omega,
+                              ctx->cap, nsets, ps, s));
     // ---- line 6: f(Xt), f(X^{k+1}) and the next right-hand side, one fused pass
-    FDL_TRY(run_p1(ctx, nsets));
-    if (nloc > 0)
-        FDL_LAUNCH(launch_p1_reduce(ctx->part, ctx->NC, ctx->Mrows, nloc, row0, dim, nsets, ctx->R1, ctx->R2,
-                                    ctx->blk_f, ctx->nblk, s));
-    FDL_TRY(gather_blocks(ctx, ctx->blk_f, nsets));
-    FDL_LAUNCH(launch_stress_finalize(ctx->blk_f, ctx->nblk, nsets, ctx->sc, 0, s));
+    FDL_TRY(run_sym(ctx, kSymP1, nsets, ctx->posf, ctx->R1, ctx->R2, 0));
     // ---- lines 6-8: guard
-    if (nloc > 0)
-        FDL_LAUNCH(launch_select(ctx->Xk, ctx->Rk, ctx->Xn, ctx->Xt, ctx->R1, ctx->R2, ctx->blk_f, ctx->blk_max,
-                                 ctx->nblk, nloc, dim, nsets, ctx->sc, s));
+    FDL_LAUNCH(launch_select(ctx->Xk, ctx->Rk, ctx->Xn, ctx->Xt, ctx->R1, ctx->R2, ctx->blk_max, n, dim, nsets,
+                             ctx->sc, s));
     mark_end(ctx, mstep);
     FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, s));
     FDL_CUDA(cudaStreamSynchronize(s));
@@ -767,9 +813,8 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
 
     const DevScalars& h = *ctx->sc_host;
     const double f_before = ctx->f;
-    // With several ranks only rank 0's block partials... all ranks computed the same f.
-    double f_next = h.f_set[0];
-    double f_rel = nsets == 2 ? h.f_set[1] : NAN;
+    const double f_next = h.f_set[0];
+    const double f_rel = nsets == 2 ? h.f_set[1] : NAN;
     const bool accepted = nsets == 2 && (f_rel <= f_next);
     const double f_after = accepted ? f_rel : f_next;
     ctx->iterations++;
@@ -901,14 +946,13 @@ fdl_status fdl_create_sharded(int32_t n, const int64_t* row_ptr, const int32_t* 
     return create_common(n, row_ptr, col_idx, edge_len, p, init_pos, nccl_unique_id, rank, world, out);
 }
 
-fdl_status fdl_shard_rows(int32_t n, int32_t world, int32_t rank, int32_t* row0, int32_t* row1)
+fdl_status fdl_shard_tiles(int32_t n, int32_t world, int32_t rank, int64_t* t0, int64_t* t1)
 {
-    if (n < 1 || world < 1 || rank < 0 || rank >= world || !row0 || !row1) return FDL_E_INVALID_ARG;
-    const int nblk_total = (n + kRB - 1) / kRB;
-    const int bpr = (nblk_total + world - 1) / world;
-    const int r0 = std::min(n, rank * bpr * kRB);
-    *row0 = r0;
-    *row1 = std::min(n, r0 + bpr * kRB);
+    if (n < 1 || world < 1 || rank < 0 || rank >= world || !t0 || !t1) return FDL_E_INVALID_ARG;
+    const int64_t nb = (n + kT - 1) / kT;
+    const int64_t total = nb * (nb + 1) / 2;
+    *t0 = total * rank / world;
+    *t1 = total * (rank + 1) / world;
     return FDL_OK;
 }
 
@@ -965,23 +1009,8 @@ fdl_status fdl_get_positions(fdl_ctx* ctx, double* out, size_t count)
     if (count != (size_t)ctx->n * ctx->dim) return set_err(ctx, FDL_E_INVALID_ARG, "count must be n*dim");
     if (ctx->broken) return FDL_E_STATE;
     cudaSetDevice(ctx->device);
-    const size_t slice = (size_t)ctx->Mrows * ctx->dim;
-    if (ctx->world == 1) {
-        FDL_CUDA(cudaMemcpyAsync(out, ctx->Xk, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-        FDL_CUDA(cudaStreamSynchronize(ctx->stream));
-    } else {
-        double* g = nullptr;
-        FDL_CUDA(cudaMalloc(&g, slice * ctx->world * sizeof(double)));
-        cudaMemcpyAsync(g + ctx->rank * slice, ctx->Xk, (size_t)ctx->nloc * ctx->dim * sizeof(double),
-                        cudaMemcpyDeviceToDevice, ctx->stream);
-        fdl_status st = allgather_inplace(ctx, g, slice, ncclFloat64, 8);
-        if (st == FDL_OK) {
-            cudaMemcpyAsync(out, g, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
-            cudaStreamSynchronize(ctx->stream);
-        }
-        cudaFree(g);
-        FDL_TRY(st);
-    }
+    FDL_CUDA(cudaMemcpyAsync(out, ctx->Xk, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    FDL_CUDA(cudaStreamSynchronize(ctx->stream));
     for (size_t i = 0; i < count; ++i) out[i] *= ctx->k;
     return FDL_OK;
 }
@@ -1005,35 +1034,18 @@ fdl_status fdl_eval_forces(fdl_ctx* ctx, double* R, double* A, double* stress)
     if (ctx->broken) return FDL_E_STATE;
     cudaSetDevice(ctx->device);
     const int dim = ctx->dim;
-    const size_t count = (size_t)ctx->n * dim, slice = (size_t)ctx->Mrows * dim;
-    std::vector<double> tmp;
+    const size_t count = (size_t)ctx->n * dim;
     auto fetch = [&](const double* dev, double* out) -> fdl_status {
-        if (ctx->world == 1) {
-            FDL_CUDA(cudaMemcpyAsync(out, dev, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-        } else {
-            double* g = nullptr;
-            FDL_CUDA(cudaMalloc(&g, slice * ctx->world * sizeof(double)));
-            cudaMemcpyAsync(g + ctx->rank * slice, dev, (size_t)ctx->nloc * dim * sizeof(double),
-                            cudaMemcpyDeviceToDevice, ctx->stream);
-            fdl_status st = allgather_inplace(ctx, g, slice, ncclFloat64, 8);
-            cudaMemcpyAsync(out, g, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
-            cudaStreamSynchronize(ctx->stream);
-            cudaFree(g);
-            FDL_TRY(st);
-        }
+        FDL_CUDA(cudaMemcpyAsync(out, dev, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         FDL_CUDA(cudaStreamSynchronize(ctx->stream));
-        for (size_t i = 0; i < count; ++i) out[i] /= ctx->k;  // R = (1/k) R', A = (1/k) A'
+        for (size_t i = 0; i < count; ++i) out[i] /= ctx->k;  // R = R'/k, A = A'/k
         return FDL_OK;
     };
     if (R) FDL_TRY(fetch(ctx->Rk, R));
     if (A) {
-        const int pq = ps_p2(dim);
-        if (ctx->nloc > 0)
-            FDL_LAUNCH(launch_cg_begin(ctx->Xk, ctx->cy, ctx->pvec, ctx->nloc, ctx->row0, dim, pq, ctx->stream));
-        FDL_TRY(allgather_inplace(ctx, ctx->pvec, (size_t)ctx->Mrows * pq, ncclFloat32, 4));
-        FDL_TRY(run_p2(ctx));
-        if (ctx->nloc > 0)
-            FDL_LAUNCH(launch_reduce_rows(ctx->part, ctx->NC, ctx->Mrows, ctx->nloc, dim, ctx->cy, ctx->stream));
+        // A = L^W X: one symmetric P2 pass with p = X
+        FDL_LAUNCH(launch_cg_begin(ctx->Xk, ctx->cy, ctx->pvec, ctx->n, 0, dim, ps_p2(dim), ctx->stream));
+        FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->cy, nullptr, 0));
         FDL_TRY(fetch(ctx->cy, A));
         collect_events(ctx);
     }
@@ -1043,33 +1055,40 @@ fdl_status fdl_eval_forces(fdl_ctx* ctx, double* R, double* A, double* stress)
 
 fdl_status fdl_get_hop_rows(fdl_ctx* ctx, int32_t r0, int32_t nrows, uint16_t* out)
 {
-    if (!ctx || !out || nrows < 0) return FDL_E_INVALID_ARG;
-    if (r0 < ctx->row0 || r0 + nrows > ctx->row1) return set_err(ctx, FDL_E_INVALID_ARG, "rows not owned");
+    if (!ctx || !out || nrows < 0 || r0 < 0 || r0 + nrows > ctx->n) return FDL_E_INVALID_ARG;
     cudaSetDevice(ctx->device);
     if (nrows == 0) return FDL_OK;
-    const int lr0 = r0 - ctx->row0;
-    const int g0 = lr0 / kRowGroup, g1 = (lr0 + nrows - 1) / kRowGroup;
-    const size_t group_bytes = (size_t)kRowGroup * ctx->Np * ctx->hb;
-    std::vector<uint8_t> buf((size_t)(g1 - g0 + 1) * group_bytes);
-    FDL_CUDA(cudaMemcpyAsync(buf.data(), ctx->D + (size_t)g0 * group_bytes, buf.size(), cudaMemcpyDeviceToHost,
-                             ctx->stream));
-    FDL_CUDA(cudaStreamSynchronize(ctx->stream));
-    for (int r = 0; r < nrows; ++r) {
-        const int64_t lr = lr0 + r;
-        for (int64_t j = 0; j < ctx->n; ++j) {
-            const size_t off = d_offset(lr, j, ctx->Np, ctx->hb) - (size_t)g0 * group_bytes;
-            out[(size_t)r * ctx->n + j] = ctx->hb == 1 ? buf[off] : *reinterpret_cast<const uint16_t*>(&buf[off]);
-        }
+    std::vector<int> rows(nrows);
+    for (int r = 0; r < nrows; ++r) rows[r] = r0 + r;
+    int* d_rows = nullptr;
+    int* d_missing = nullptr;
+    uint16_t* d_out = nullptr;
+    FDL_CUDA(cudaMalloc(&d_rows, sizeof(int) * nrows));
+    FDL_CUDA(cudaMalloc(&d_missing, sizeof(int)));
+    FDL_CUDA(cudaMalloc(&d_out, sizeof(uint16_t) * (size_t)nrows * ctx->n));
+    cudaMemcpyAsync(d_rows, rows.data(), sizeof(int) * nrows, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemsetAsync(d_missing, 0, sizeof(int), ctx->stream);
+    cudaError_t e = launch_hop_rows(ctx->D, ctx->hb, ctx->nb, ctx->t0, ctx->t1, d_rows, nrows, ctx->n, d_out,
+                                    d_missing, ctx->stream);
+    int missing = 0;
+    if (e == cudaSuccess) {
+        cudaMemcpyAsync(out, d_out, sizeof(uint16_t) * (size_t)nrows * ctx->n, cudaMemcpyDeviceToHost, ctx->stream);
+        cudaMemcpyAsync(&missing, d_missing, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+        e = cudaStreamSynchronize(ctx->stream);
     }
+    cudaFree(d_rows);
+    cudaFree(d_missing);
+    cudaFree(d_out);
+    FDL_CUDA(e);
+    if (missing) return set_err(ctx, FDL_E_INVALID_ARG, "some requested entries live in tiles of other ranks");
     return FDL_OK;
 }
 
 fdl_status fdl_get_diag(fdl_ctx* ctx, double* out, size_t count)
 {
     if (!ctx || !out) return FDL_E_INVALID_ARG;
-    if (count != (size_t)ctx->nloc) return set_err(ctx, FDL_E_INVALID_ARG, "count must be the owned row count");
+    if (count != (size_t)ctx->n) return set_err(ctx, FDL_E_INVALID_ARG, "count must be n");
     cudaSetDevice(ctx->device);
-    if (count == 0) return FDL_OK;
     FDL_CUDA(cudaMemcpyAsync(out, ctx->diag, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     FDL_CUDA(cudaStreamSynchronize(ctx->stream));
     const double k2 = ctx->k * ctx->k;
@@ -1085,14 +1104,15 @@ fdl_status fdl_get_info(fdl_ctx* ctx, fdl_ctx_info* info)
     r.dim = ctx->dim;
     r.diameter = ctx->diameter;
     r.hop_bytes = ctx->hb;
-    r.row0 = ctx->row0;
-    r.row1 = ctx->row1;
+    r.tile0 = ctx->t0;
+    r.tile1 = ctx->t1;
     r.rank = ctx->rank;
     r.world = ctx->world;
     r.iterations = ctx->iterations;
     r.k = ctx->k;
     r.f = ctx->f;
-    r.hop_matrix_bytes = (uint64_t)ctx->Mrows * (uint64_t)ctx->Np * ctx->hb;
+    r.hop_matrix_bytes = ctx->hop_bytes_total;
+    r.local_pairs = ctx->local_pairs;
     r.device_bytes = ctx->device_bytes;
     r.setup_ms = ctx->setup_ms;
     *info = r;

@@ -1,0 +1,651 @@
+// fdl_sym.cu -- symmetric (upper-triangle) all-pairs kernels for sm_100a.
+//
+// The pair terms of the method are symmetric in (i, j): d_ij = d_ji, w_ij = w_ji
+// (P:48), the stress term of Eq. 1 is counted once per unordered pair
+// (sum over i < j), and the L^Y / L^W products are antisymmetric
+// (x_i - x_j) sums.  So each unordered pair is evaluated ONCE and feeds both
+// rows: R_i += q (x_i - x_j) and R_j -= q (x_i - x_j) (Newton's third law),
+// s += u^2.  Only the upper triangle of the hop matrix is stored: half the
+// HBM bytes and half the pair arithmetic of a row-by-row evaluation.
+//
+// Geometry: tiles of kT x kT (128 x 128) vertices, tile (I, J) with I <= J,
+// numbered row-major over the triangle.  A CTA of 256 threads = 16 x 16 grid;
+// thread (ty, tx) owns the 8 x 8 sub-block rows 8 ty.., cols 8 tx.. of the
+// tile; its 64 (u8) / 128 (u16) hop bytes are stored as 16-byte chunks
+// interleaved across threads ((chunk * 256 + thread) * 16), so both the TMA
+// bulk copy (one contiguous 16/32 KB run per tile) and the LDS.128 reads are
+// conflict-free.
+//
+// Work item = strip segment: row block I and up to kSeg consecutive column
+// blocks J (the rank's tile range in triangle order).  i-side sums stay in
+// registers over the segment; j-side sums are reduced across the 16 thread
+// rows through padded shared memory after every tile.  Outputs are fp32 tile
+// partials (j side, per tile) and fp64 segment partials (i side, stress),
+// summed per row in a fixed order by k_sym_reduce: deterministic, no atomics.
+#include <cfloat>
+#include <cstdint>
+
+#include "fdl_internal.h"
+
+namespace fdl {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity)
+{
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
+{
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ float rsqrt_approx(float x)
+{
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx(float x)
+{
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ uint32_t word_of(const uint4& v, int q)
+{
+    return q == 0 ? v.x : (q == 1 ? v.y : (q == 2 ? v.z : v.w));
+}
+
+// hop of entry (row r, column cc of the chunk) of one 16-byte chunk as an
+// exact float: one PRMT builds 0x4B0000hh (= 2^23 + h), one FADD removes 2^23.
+// u8 chunk: columns 2k, 2k+1, byte cc*8 + r; u16 chunk: column k, bytes 2r, 2r+1.
+template <int HB>
+__device__ __forceinline__ float chunk_hop(const uint4& ch, int r, int cc)
+{
+    uint32_t bits;
+    if (HB == 1) {
+        const int byte = cc * 8 + r;
+        bits = __byte_perm(word_of(ch, byte >> 2), 0x4B000000u, 0x7650u + (uint32_t)(byte & 3));
+    } else {
+        bits = __byte_perm(word_of(ch, r >> 1), 0x4B000000u, (r & 1) ? 0x7632u : 0x7610u);
+    }
+    return __uint_as_float(bits) - 8388608.0f;
+}
+
+}  // namespace
+
+// number of output components per mode
+template <int MODE, int DIM, int NSETS>
+__host__ __device__ constexpr int sym_ncomp()
+{
+    return MODE == kSymP1 ? NSETS * DIM : (MODE == kSymP2 ? DIM : 1);
+}
+
+// floats per vertex in the staged position vector
+template <int MODE, int DIM, int NSETS>
+__host__ __device__ constexpr int sym_ps()
+{
+    return MODE == kSymP1 ? (DIM == 2 ? (NSETS == 1 ? 2 : 4) : (NSETS == 1 ? 4 : 8))
+                          : (MODE == kSymP2 ? (DIM == 2 ? 2 : 4) : 4);
+}
+
+template <int MODE, int DIM, int NSETS, int HB>
+__host__ __device__ constexpr int sym_stage_bytes()
+{
+    return kT * kT * HB + kT * sym_ps<MODE, DIM, NSETS>() * 4;
+}
+
+template <int MODE, int DIM, int NSETS>
+__host__ __device__ constexpr int sym_red_pitch()  // floats per (ty, tx) cell in the reduction buffer
+{
+    return 8 * sym_ncomp<MODE, DIM, NSETS>() + 4;
+}
+
+template <int MODE, int DIM, int NSETS, int HB>
+__host__ __device__ constexpr size_t sym_smem_bytes()
+{
+    return (size_t)kSymStages * sym_stage_bytes<MODE, DIM, NSETS, HB>() +
+           (size_t)256 * sym_red_pitch<MODE, DIM, NSETS>() * 4;
+}
+
+// One evaluation of an unordered pair for one position set.
+// MODE P1: acc_i += q d, acc_j += q d (stored negated), s += u^2
+// MODE P2: acc_i += w d, acc_j += w d
+// MODE DIAG: acc_i += w, acc_j += w
+template <int MODE, int DIM, bool SAFE>
+__device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float h2, bool valid, float* ai,
+                                         float* aj, float& s)
+{
+    if (MODE == kSymP1) {
+        float d[DIM];
+        float r2 = FLT_MIN;
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+            d[c] = xi[c] - xj[c];
+            r2 = fmaf(d[c], d[c], r2);
+        }
+        float q = rsqrt_approx(r2 * h2);  // 1/(h r) = w' d' / r
+        float u = fmaf(r2, q, -1.0f);     // r/h - 1
+        if (SAFE) {
+            q = valid ? q : 0.0f;
+            u = valid ? u : 0.0f;
+        }
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+            ai[c] = fmaf(q, d[c], ai[c]);
+            aj[c] = fmaf(q, d[c], aj[c]);
+        }
+        s = fmaf(u, u, s);
+    } else if (MODE == kSymP2) {
+        float w = rcp_approx(h2);  // w' = 1/h^2
+        if (SAFE) w = valid ? w : 0.0f;
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+            const float d = xi[c] - xj[c];
+            ai[c] = fmaf(w, d, ai[c]);
+            aj[c] = fmaf(w, d, aj[c]);
+        }
+    } else {
+        float w = __frcp_rn(h2);
+        if (SAFE) w = valid ? w : 0.0f;
+        ai[0] += w;
+        aj[0] += w;
+    }
+}
+
+template <int MODE, int DIM, int NSETS, int HB, bool SAFE>
+__device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, int ty, int tx, bool diag,
+                                         const float (&xi)[8][NSETS * DIM], float (&ai)[8][sym_ncomp<MODE, DIM, NSETS>()],
+                                         float* red, float (&sf)[NSETS])
+{
+    constexpr int C = sym_ncomp<MODE, DIM, NSETS>();
+    constexpr int PS = sym_ps<MODE, DIM, NSETS>();
+    constexpr int NCH = 4 * HB;  // 16-byte chunks per thread
+    constexpr int PITCH = sym_red_pitch<MODE, DIM, NSETS>();
+    constexpr int CPC = 2 / HB;  // columns per chunk
+    const int tid = ty * 16 + tx;
+    float* myred = red + (size_t)tid * PITCH;
+#pragma unroll 1
+    for (int kc = 0; kc < NCH; ++kc) {
+        const uint4 ch = *reinterpret_cast<const uint4*>(sD + ((size_t)kc * 256 + tid) * 16);
+#pragma unroll
+        for (int cc = 0; cc < CPC; ++cc) {
+            const int c = kc * CPC + cc;
+            const int jl = tx * 8 + c;
+            float xj[PS];
+            if (PS == 2) {
+                const float2 t = *reinterpret_cast<const float2*>(sP + jl * PS);
+                xj[0] = t.x; xj[1] = t.y;
+            } else {
+#pragma unroll
+                for (int q = 0; q < PS / 4; ++q) {
+                    const float4 t = *reinterpret_cast<const float4*>(sP + jl * PS + 4 * q);
+                    xj[4 * q] = t.x; xj[4 * q + 1] = t.y; xj[4 * q + 2] = t.z; xj[4 * q + 3] = t.w;
+                }
+            }
+            float aj[C];
+#pragma unroll
+            for (int v = 0; v < C; ++v) aj[v] = 0.0f;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const float hf = chunk_hop<HB>(ch, r, cc);
+                const float h2 = hf * hf;
+                bool valid = true;
+                if (SAFE) valid = (h2 > 0.0f) && (!diag || (ty * 8 + r < jl));
+                if (MODE == kSymP1) {
+#pragma unroll
+                    for (int s = 0; s < NSETS; ++s)
+                        sym_pair<MODE, DIM, SAFE>(&xi[r][s * DIM], xj + s * DIM, h2, valid, &ai[r][s * DIM],
+                                                  &aj[s * DIM], sf[s]);
+                } else {
+                    float dummy = 0.0f;
+                    sym_pair<MODE, DIM, SAFE>(&xi[r][0], xj, h2, valid, &ai[r][0], &aj[0], dummy);
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < C; ++v) myred[c * C + v] = aj[v];
+        }
+    }
+}
+
+// Reduction of the per-thread j-side partials of one tile over the 16 thread
+// rows (fixed order, fp64) and store as fp32 jpart[tile][col][C].  The
+// j-side sign: P1 and P2 accumulate +term for row i and -term for row j
+// (antisymmetric); DIAG is symmetric.
+template <int MODE, int DIM, int NSETS>
+__device__ __forceinline__ void sym_flush_j(const float* red, float* jpart_tile, int tid)
+{
+    constexpr int C = sym_ncomp<MODE, DIM, NSETS>();
+    constexpr int PITCH = sym_red_pitch<MODE, DIM, NSETS>();
+    constexpr float SIGN = MODE == kSymDiag ? 1.0f : -1.0f;
+    for (int e = tid; e < kT * C; e += 256) {
+        const int tx = e / (8 * C), rem = e % (8 * C);  // rem = c*C + v
+        double s = 0.0;
+#pragma unroll 4
+        for (int ty = 0; ty < 16; ++ty) s += (double)red[(size_t)(ty * 16 + tx) * PITCH + rem];
+        jpart_tile[tx * 8 * C + rem] = SIGN * (float)s;  // col = tx*8 + c, comp v
+    }
+}
+
+template <int MODE, int DIM, int NSETS, int HB>
+__global__ void __launch_bounds__(256, 1) k_sym(const SymArgs a)
+{
+    constexpr int C = sym_ncomp<MODE, DIM, NSETS>();
+    constexpr int PS = sym_ps<MODE, DIM, NSETS>();
+    constexpr int STAGE = sym_stage_bytes<MODE, DIM, NSETS, HB>();
+    constexpr int DT = kT * kT * HB;
+    constexpr int PITCH = sym_red_pitch<MODE, DIM, NSETS>();
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t full[kSymStages];
+    __shared__ double sred[8][NSETS > 0 ? NSETS : 1];
+    float* red = reinterpret_cast<float*>(smem + (size_t)kSymStages * STAGE);
+
+    const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+    if ((int)blockIdx.x >= a.nitems) return;
+    if (tid == 0) {
+        for (int s = 0; s < kSymStages; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    // producer: tiles of this CTA's items, in order
+    int p_item = blockIdx.x, p_t = 0;
+    auto issue = [&](int stage) {
+        const int4 it = a.items[p_item];  // {I, J0, ntiles, first local tile}
+        const int J = it.y + p_t;
+        const int64_t lt = (int64_t)it.w + p_t;
+        uint8_t* base = smem + (size_t)stage * STAGE;
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&full[stage], STAGE);
+        tma_load_1d(base, a.D + lt * DT, DT, &full[stage]);
+        tma_load_1d(base + DT, a.pos + (int64_t)J * kT * PS, kT * PS * 4, &full[stage]);
+        if (++p_t == it.z) {
+            p_t = 0;
+            p_item += gridDim.x;
+        }
+    };
+    if (tid == 0)
+        for (int s = 0; s < kSymStages - 1 && p_item < a.nitems; ++s) issue(s);
+
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
+        const int4 it = a.items[item];
+        const int I = it.x;
+        float xi[8][NSETS * DIM];
+        float ai[8][C];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int64_t gi = (int64_t)I * kT + ty * 8 + r;
+#pragma unroll
+            for (int q = 0; q < NSETS * DIM; ++q) xi[r][q] = a.pos[gi * PS + q];
+#pragma unroll
+            for (int v = 0; v < C; ++v) ai[r][v] = 0.0f;
+        }
+        double s64[NSETS];
+#pragma unroll
+        for (int s = 0; s < NSETS; ++s) s64[s] = 0.0;
+        for (int t = 0; t < it.z; ++t) {
+            if (tid == 0 && p_item < a.nitems) issue((stage + kSymStages - 1) % kSymStages);
+            const int J = it.y + t;
+            const bool diag = (J == I);
+            const bool safe = diag || (int64_t)(J + 1) * kT > a.n || (int64_t)(I + 1) * kT > a.n;
+            mbar_wait(&full[stage], phase);
+            const uint8_t* sD = smem + (size_t)stage * STAGE;
+            const float* sP = reinterpret_cast<const float*>(sD + DT);
+            float sf[NSETS];
+#pragma unroll
+            for (int s = 0; s < NSETS; ++s) sf[s] = 0.0f;
+            if (safe)
+                sym_tile<MODE, DIM, NSETS, HB, true>(sD, sP, ty, tx, diag, xi, ai, red, sf);
+            else
+                sym_tile<MODE, DIM, NSETS, HB, false>(sD, sP, ty, tx, diag, xi, ai, red, sf);
+#pragma unroll
+            for (int s = 0; s < NSETS; ++s) s64[s] += (double)sf[s];
+            __syncthreads();  // j partials complete; stage consumed
+            sym_flush_j<MODE, DIM, NSETS>(red, a.jpart + ((size_t)it.w + t) * kT * C, tid);
+            __syncthreads();  // red free again
+            if (++stage == kSymStages) {
+                stage = 0;
+                phase ^= 1u;
+            }
+        }
+        // i-side: reduce over the 16 thread columns (fixed order, fp64)
+        float* myred = red + (size_t)(tx * 16 + ty) * PITCH;  // [tx][ty] layout
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int v = 0; v < C; ++v) myred[r * C + v] = ai[r][v];
+        __syncthreads();
+        for (int e = tid; e < kT * C; e += 256) {
+            const int ty2 = e / (8 * C), rem = e % (8 * C);  // rem = r*C + v, row = ty2*8 + r
+            double s = 0.0;
+#pragma unroll 4
+            for (int tx2 = 0; tx2 < 16; ++tx2) s += (double)red[(size_t)(tx2 * 16 + ty2) * PITCH + rem];
+            a.ipart[(size_t)item * kT * C + ty2 * 8 * C + rem] = s;
+        }
+        if (MODE == kSymP1) {
+            // stress of the segment: fixed-order block reduction of the fp64 thread sums
+#pragma unroll
+            for (int s = 0; s < NSETS; ++s) {
+                double v = s64[s];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if ((tid & 31) == 0) sred[tid >> 5][s] = v;
+            }
+        }
+        __syncthreads();
+        if (MODE == kSymP1 && tid == 0) {
+            for (int s = 0; s < NSETS; ++s) {
+                double v = 0.0;
+                for (int w = 0; w < 8; ++w) v += sred[w][s];
+                a.spart[(size_t)item * NSETS + s] = v;
+            }
+        }
+    }
+}
+
+template <int MODE, int DIM, int NSETS, int HB>
+static cudaError_t launch_sym_t(const SymArgs& a, int grid, cudaStream_t s)
+{
+    const size_t sm = sym_smem_bytes<MODE, DIM, NSETS, HB>();
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e =
+            cudaFuncSetAttribute(k_sym<MODE, DIM, NSETS, HB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_sym<MODE, DIM, NSETS, HB><<<grid, 256, sm, s>>>(a);
+    return cudaGetLastError();
+}
+
+#define FDL_SYM_CASE(M_, D_, S_, H_) \
+    if (mode == M_ && dim == D_ && nsets == S_ && hb == H_) return launch_sym_t<M_, D_, S_, H_>(a, grid, s);
+#define FDL_SYM_ALLHB(M_, D_, S_) FDL_SYM_CASE(M_, D_, S_, 1) FDL_SYM_CASE(M_, D_, S_, 2)
+
+cudaError_t launch_sym(const SymArgs& a, int mode, int dim, int nsets, int hb, int grid, cudaStream_t s)
+{
+    FDL_SYM_ALLHB(kSymP1, 2, 1) FDL_SYM_ALLHB(kSymP1, 2, 2) FDL_SYM_ALLHB(kSymP1, 3, 1) FDL_SYM_ALLHB(kSymP1, 3, 2)
+    FDL_SYM_ALLHB(kSymP2, 2, 1) FDL_SYM_ALLHB(kSymP2, 3, 1)
+    FDL_SYM_ALLHB(kSymDiag, 2, 1) FDL_SYM_ALLHB(kSymDiag, 3, 1)
+    return cudaErrorInvalidValue;
+}
+
+template <int MODE, int DIM, int NSETS, int HB>
+static int sym_occ_t()
+{
+    const size_t sm = sym_smem_bytes<MODE, DIM, NSETS, HB>();
+    int n = 0;
+    cudaFuncSetAttribute(k_sym<MODE, DIM, NSETS, HB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_sym<MODE, DIM, NSETS, HB>, 256, sm) != cudaSuccess) n = 1;
+    return n > 0 ? n : 1;
+}
+
+#define FDL_SYM_OCC(M_, D_, S_, H_) \
+    if (mode == M_ && dim == D_ && nsets == S_ && hb == H_) return sym_occ_t<M_, D_, S_, H_>();
+int sym_max_ctas(int mode, int dim, int nsets, int hb)
+{
+    FDL_SYM_OCC(kSymP1, 2, 1, 1) FDL_SYM_OCC(kSymP1, 2, 2, 1) FDL_SYM_OCC(kSymP1, 3, 1, 1) FDL_SYM_OCC(kSymP1, 3, 2, 1)
+    FDL_SYM_OCC(kSymP1, 2, 1, 2) FDL_SYM_OCC(kSymP1, 2, 2, 2) FDL_SYM_OCC(kSymP1, 3, 1, 2) FDL_SYM_OCC(kSymP1, 3, 2, 2)
+    FDL_SYM_OCC(kSymP2, 2, 1, 1) FDL_SYM_OCC(kSymP2, 3, 1, 1) FDL_SYM_OCC(kSymP2, 2, 1, 2) FDL_SYM_OCC(kSymP2, 3, 1, 2)
+    FDL_SYM_OCC(kSymDiag, 2, 1, 1) FDL_SYM_OCC(kSymDiag, 3, 1, 1) FDL_SYM_OCC(kSymDiag, 2, 1, 2)
+    FDL_SYM_OCC(kSymDiag, 3, 1, 2)
+    return 1;
+}
+
+// ---------------------------------------------------------------- reduction
+// Per row (one thread per row of block B): sum, in a fixed order, the i-side
+// segment partials of strip B (items it_lo[B]..it_hi[B]) and the j-side tile
+// partials of the local tiles (I, B), I = 0..B.  Output: dense fp64 rank
+// partial out[row][C] for all n_pad rows.
+__global__ void __launch_bounds__(kT) k_sym_reduce(const double* __restrict__ ipart, const float* __restrict__ jpart,
+                                                   const int* __restrict__ it_lo, const int* __restrict__ it_hi,
+                                                   int nb, int64_t t0, int64_t t1, int C, int D, double* out0,
+                                                   double* out1)
+{
+    const int B = blockIdx.x;
+    const int r = threadIdx.x;
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int item = it_lo[B]; item < it_hi[B]; ++item)
+        for (int v = 0; v < C; ++v) acc[v] += ipart[((size_t)item * kT + r) * C + v];
+    for (int I = 0; I <= B; ++I) {
+        const int64_t t = tri_index(I, B, nb);
+        if (t < t0 || t >= t1) continue;
+        const float* src = jpart + ((size_t)(t - t0) * kT + r) * C;
+        for (int v = 0; v < C; ++v) acc[v] += (double)src[v];
+    }
+    const size_t row = (size_t)B * kT + r;
+    for (int v = 0; v < C; ++v) {
+        if (v < D)
+            out0[row * D + v] = acc[v];
+        else
+            out1[row * (C - D) + (v - D)] = acc[v];
+    }
+}
+
+cudaError_t launch_sym_reduce(const double* ipart, const float* jpart, const int* it_lo, const int* it_hi, int nb,
+                              int64_t t0, int64_t t1, int C, int D, double* out0, double* out1, cudaStream_t s)
+{
+    k_sym_reduce<<<nb, kT, 0, s>>>(ipart, jpart, it_lo, it_hi, nb, t0, t1, C, D, out0, out1);
+    return cudaGetLastError();
+}
+
+// sum of rank partials in rank order (multi-GPU): parts[world][rows][C]
+__global__ void k_rank_sum(const double* __restrict__ parts, int world, int64_t rows, int C, int D, double* out0,
+                           double* out1)
+{
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= rows * C) return;
+    const int64_t row = idx / C;
+    const int v = (int)(idx % C);
+    double s = 0.0;
+    for (int g = 0; g < world; ++g) s += parts[(size_t)g * rows * C + idx];
+    if (v < D)
+        out0[row * D + v] = s;
+    else
+        out1[row * (C - D) + (v - D)] = s;
+}
+
+cudaError_t launch_rank_sum(const double* parts, int world, int64_t rows, int C, int D, double* out0, double* out1,
+                            cudaStream_t s)
+{
+    const int64_t total = rows * C;
+    k_rank_sum<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(parts, world, rows, C, D, out0, out1);
+    return cudaGetLastError();
+}
+
+// f = sum over ranks (rank order) of the rank stress partials; Eq. 1 counts
+// each unordered pair once, as the symmetric pass does.
+__global__ void k_stress_ranks(const double* __restrict__ parts, int world, int nsets, DevScalars* sc, int set_cur)
+{
+    if (threadIdx.x != 0) return;
+    for (int s = 0; s < nsets; ++s) {
+        double v = 0.0;
+        for (int g = 0; g < world; ++g) v += parts[g * 2 + s];
+        sc->f_set[s] = v;
+        if (set_cur && s == 0) {
+            sc->f_cur = v;
+            sc->nonfinite = !isfinite(v);
+        }
+    }
+}
+
+cudaError_t launch_stress_ranks(const double* parts, int world, int nsets, DevScalars* sc, int set_cur,
+                                cudaStream_t s)
+{
+    k_stress_ranks<<<1, 32, 0, s>>>(parts, world, nsets, sc, set_cur);
+    return cudaGetLastError();
+}
+
+// sigma = (sum_i diag_i) / n^2, one block, fixed order
+__global__ void k_sigma_rows(const double* __restrict__ diag, int n, DevScalars* sc)
+{
+    __shared__ double red[32];
+    double v = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) v += diag[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+        sc->sigma = s / ((double)n * (double)n);
+    }
+}
+
+cudaError_t launch_set_sigma_rows(const double* diag, int n, DevScalars* sc, cudaStream_t s)
+{
+    k_sigma_rows<<<1, 1024, 0, s>>>(diag, n, sc);
+    return cudaGetLastError();
+}
+
+// Dense hop rows (uint16) gathered from the triangle tiles: out[r][j] = hop(rows[r], j);
+// entries whose tile is not local set *missing.
+__global__ void k_hop_rows(const uint8_t* __restrict__ D, int hb, int nb, int64_t t0, int64_t t1,
+                           const int* __restrict__ rows, int nrows, int n, uint16_t* out, int* missing)
+{
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)nrows * n) return;
+    const int r = (int)(idx / n), j = (int)(idx % n);
+    int a = rows[r], b = j;
+    if (a / kT > b / kT) {
+        const int tmp = a;
+        a = b;
+        b = tmp;
+    }
+    const int64_t t = tri_index(a / kT, b / kT, nb);
+    if (t < t0 || t >= t1) {
+        *missing = 1;
+        out[idx] = 0;
+        return;
+    }
+    const size_t off = sym_offset(t - t0, a % kT, b % kT, hb);
+    out[idx] = hb == 1 ? D[off] : (uint16_t)(D[off] | (D[off + 1] << 8));
+}
+
+cudaError_t launch_hop_rows(const uint8_t* D, int hb, int nb, int64_t t0, int64_t t1, const int* rows, int nrows,
+                            int n, uint16_t* out, int* missing, cudaStream_t s)
+{
+    const int64_t total = (int64_t)nrows * n;
+    k_hop_rows<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(D, hb, nb, t0, t1, rows, nrows, n, out, missing);
+    return cudaGetLastError();
+}
+
+// stress partial of the rank: sum of segment partials in item order (one warp, fixed butterfly)
+__global__ void k_sym_stress(const double* __restrict__ spart, int nitems, int nsets, double* out)
+{
+    const int lane = threadIdx.x;
+    for (int s = 0; s < nsets; ++s) {
+        double v = 0.0;
+        for (int i = lane; i < nitems; i += 32) v += spart[(size_t)i * nsets + s];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) out[s] = v;
+    }
+}
+
+cudaError_t launch_sym_stress(const double* spart, int nitems, int nsets, double* out, cudaStream_t s)
+{
+    k_sym_stress<<<1, 32, 0, s>>>(spart, nitems, nsets, out);
+    return cudaGetLastError();
+}
+
+// MS-BFS level writing into the triangle tile layout: entry (s, v) goes to tile
+// (s/kT, v/kT) when s/kT <= v/kT and that tile is in [t0, t1).
+template <int HB>
+__global__ void __launch_bounds__(256) k_bfs_level_sym(const int64_t* __restrict__ row_ptr,
+                                                       const int32_t* __restrict__ col,
+                                                       const uint32_t* __restrict__ fin, uint32_t* __restrict__ fout,
+                                                       uint32_t* __restrict__ visited, uint8_t* __restrict__ D, int n,
+                                                       int s0, int nsrc, int level, int nb, int64_t t0, int64_t t1,
+                                                       unsigned int* anynew)
+{
+    const int v = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (v >= n) return;
+    const int nl = min(max(nsrc - 32 * lane, 0), 32);
+    const uint32_t full = nl == 32 ? 0xffffffffu : ((1u << nl) - 1u);
+    const uint32_t vis = visited[(int64_t)v * kBFSWords + lane];
+    if (__all_sync(0xffffffffu, (vis & full) == full)) {
+        fout[(int64_t)v * kBFSWords + lane] = 0u;
+        return;
+    }
+    uint32_t acc = 0;
+    const int64_t beg = row_ptr[v], end = row_ptr[v + 1];
+    for (int64_t e0 = beg; e0 < end; e0 += 32) {
+        const int myu = (e0 + lane < end) ? col[e0 + lane] : 0;
+        const int cnt = (int)min((int64_t)32, end - e0);
+#pragma unroll 4
+        for (int k = 0; k < cnt; ++k) {
+            const int u = __shfl_sync(0xffffffffu, myu, k);
+            acc |= fin[(int64_t)u * kBFSWords + lane];
+        }
+    }
+    uint32_t nw = acc & ~vis & full;
+    fout[(int64_t)v * kBFSWords + lane] = nw;
+    if (nw) visited[(int64_t)v * kBFSWords + lane] = vis | nw;
+    if (__any_sync(0xffffffffu, nw != 0u) && lane == 0) *anynew = 1u;
+    const int J = v / kT, cl = v % kT;
+    while (nw) {
+        const int b = __ffs(nw) - 1;
+        nw &= nw - 1u;
+        const int s = s0 + 32 * lane + b;
+        const int I = s / kT, rl = s % kT;
+        if (I > J) continue;
+        const int64_t t = tri_index(I, J, nb);
+        if (t < t0 || t >= t1) continue;
+        D[sym_offset(t - t0, rl, cl, HB)] = (uint8_t)level;
+        if (HB == 2) D[sym_offset(t - t0, rl, cl, HB) + 1] = (uint8_t)(level >> 8);
+    }
+}
+
+cudaError_t launch_bfs_level_sym(const int64_t* row_ptr, const int32_t* col, const uint32_t* fin, uint32_t* fout,
+                                 uint32_t* visited, uint8_t* D, int n, int s0, int nsrc, int level, int nb, int64_t t0,
+                                 int64_t t1, int hb, unsigned int* anynew, cudaStream_t s)
+{
+    const int64_t threads = (int64_t)n * 32;
+    const unsigned grid = (unsigned)((threads + 255) / 256);
+    if (hb == 1)
+        k_bfs_level_sym<1><<<grid, 256, 0, s>>>(row_ptr, col, fin, fout, visited, D, n, s0, nsrc, level, nb, t0, t1,
+                                                anynew);
+    else
+        k_bfs_level_sym<2><<<grid, 256, 0, s>>>(row_ptr, col, fin, fout, visited, D, n, s0, nsrc, level, nb, t0, t1,
+                                                anynew);
+    return cudaGetLastError();
+}
+
+}  // namespace fdl

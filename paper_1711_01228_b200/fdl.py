@@ -15,7 +15,7 @@ import numpy as np
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "lib", "libfdl.so")
 
-FDL_ROW_BLOCK = 256
+FDL_TILE = 128
 STATUS = {
     0: "FDL_OK", -1: "FDL_E_INVALID_ARG", -2: "FDL_E_SELF_LOOP", -3: "FDL_E_DUPLICATE_EDGE",
     -4: "FDL_E_ASYMMETRIC", -5: "FDL_E_DISCONNECTED", -6: "FDL_E_BAD_LENGTH", -7: "FDL_E_DIAMETER",
@@ -26,7 +26,7 @@ STOP = {0: "none", 1: "rel_tol", 2: "zero_stress", 3: "max_iter"}
 STRAT_FIXED, STRAT_PROB = 0, 1
 
 EXPORTS = [
-    "fdl_abi_version", "fdl_params_default", "fdl_create", "fdl_create_sharded", "fdl_shard_rows",
+    "fdl_abi_version", "fdl_params_default", "fdl_create", "fdl_create_sharded", "fdl_shard_tiles",
     "fdl_nccl_unique_id", "fdl_set_stream", "fdl_step", "fdl_run_until_converged", "fdl_get_positions",
     "fdl_set_positions", "fdl_eval_forces", "fdl_get_hop_rows", "fdl_get_diag", "fdl_get_info",
     "fdl_set_timing", "fdl_get_stats", "fdl_reset_stats", "fdl_bench_ffma", "fdl_status_str",
@@ -73,10 +73,10 @@ class RunInfo(ctypes.Structure):
 class CtxInfo(ctypes.Structure):
     _fields_ = [
         ("n", ctypes.c_int32), ("dim", ctypes.c_int32), ("diameter", ctypes.c_int32),
-        ("hop_bytes", ctypes.c_int32), ("row0", ctypes.c_int32), ("row1", ctypes.c_int32),
-        ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("iterations", ctypes.c_int32),
+        ("hop_bytes", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+        ("tile0", ctypes.c_int64), ("tile1", ctypes.c_int64), ("iterations", ctypes.c_int32),
         ("k", ctypes.c_double), ("f", ctypes.c_double), ("hop_matrix_bytes", ctypes.c_uint64),
-        ("device_bytes", ctypes.c_uint64), ("setup_ms", ctypes.c_double),
+        ("local_pairs", ctypes.c_uint64), ("device_bytes", ctypes.c_uint64), ("setup_ms", ctypes.c_double),
     ]
 
 
@@ -103,7 +103,7 @@ def _load():
         "fdl_params_default": (None, [ctypes.POINTER(Params)]),
         "fdl_create": (i32, [i32, P, P, P, ctypes.POINTER(Params), P, ctypes.POINTER(P)]),
         "fdl_create_sharded": (i32, [i32, P, P, P, ctypes.POINTER(Params), P, P, i32, i32, ctypes.POINTER(P)]),
-        "fdl_shard_rows": (i32, [i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]),
+        "fdl_shard_tiles": (i32, [i32, i32, i32, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
         "fdl_nccl_unique_id": (i32, [P]),
         "fdl_set_stream": (i32, [P, P]),
         "fdl_step": (i32, [P, ctypes.POINTER(IterInfo)]),
@@ -150,9 +150,9 @@ def make_params(dim=2, k=0.0, omega=1.5, step=math.inf, tol=1e-4, max_iter=500, 
     return p
 
 
-def shard_rows(n: int, world: int, rank: int):
-    a, b = ctypes.c_int32(), ctypes.c_int32()
-    _check(None, lib.fdl_shard_rows(n, world, rank, ctypes.byref(a), ctypes.byref(b)))
+def shard_tiles(n: int, world: int, rank: int):
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    _check(None, lib.fdl_shard_tiles(n, world, rank, ctypes.byref(a), ctypes.byref(b)))
     return a.value, b.value
 
 
@@ -257,9 +257,8 @@ class Layout:
         return out
 
     def get_diag(self) -> np.ndarray:
-        cnt = self.info.row1 - self.info.row0
-        out = np.empty(cnt, dtype=np.float64)
-        _check(self._h, lib.fdl_get_diag(self._h, _ptr(out), cnt))
+        out = np.empty(self.n, dtype=np.float64)
+        _check(self._h, lib.fdl_get_diag(self._h, _ptr(out), self.n))
         return out
 
     def get_info(self) -> CtxInfo:

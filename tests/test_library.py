@@ -81,12 +81,17 @@ def test_parameter_validation():
 
 
 @pytest.mark.parametrize("n,world", [(1, 1), (100, 2), (1000, 3), (9828, 8), (200000, 8), (300, 8)])
-def test_shard_rows_partition(n, world):
-    """Rows split in whole 256-row blocks, contiguous, covering [0, n) once."""
+def test_shard_tiles_partition(n, world):
+    """Upper-triangle tiles split into contiguous, near-equal ranges covering
+    [0, nb(nb+1)/2) exactly once."""
+    nb = -(-n // fdl.FDL_TILE)
+    total = nb * (nb + 1) // 2
     prev = 0
+    sizes = []
     for r in range(world):
-        a, b = fdl.shard_rows(n, world, r)
-        assert a == prev and a <= b <= n
-        assert a % fdl.FDL_ROW_BLOCK == 0 or a == n
+        a, b = fdl.shard_tiles(n, world, r)
+        assert a == prev and a <= b <= total
+        sizes.append(b - a)
         prev = b
-    assert prev == n
+    assert prev == total
+    assert max(sizes) - min(sizes) <= 1
