@@ -385,6 +385,7 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
     a.items = ctx->items;
     a.nitems = ctx->nitems;
     a.n = ctx->n;
+    a.magic = 0x4B000000u;
     const int grid = mode == kSymP1 ? ctx->grid_p1[nsets] : (mode == kSymP2 ? ctx->grid_p2 : ctx->grid_diag);
     const int mk = mark_begin(ctx, mode == kSymP1 ? 1 : (mode == kSymP2 ? 2 : 3));
     if (ctx->nitems > 0) FDL_LAUNCH(launch_sym(a, mode, dim, nsets, ctx->hb, grid, ctx->stream));

@@ -11,6 +11,14 @@
 
 namespace fdl {
 
+// Slot of vertex v in the staged fp32 vectors (P1 positions, P2 p): inside each
+// 128-vertex block, v -> (v % 8) * 16 + (v % 128) / 8, so the 16 thread columns
+// of k_sym read 16 consecutive slots for their column c (no bank conflicts).
+__host__ __device__ inline int64_t stage_slot(int64_t v)
+{
+    return (v & ~(int64_t)127) | ((v & 7) << 4) | ((v & 127) >> 3);
+}
+
 // ------------------------------------------------------------ constants
 constexpr int kRB = 256;           // row block of all fp64 vector reductions
 constexpr int kBFSWords = 32;      // MS-BFS source batch = 32 words x 32 bits = 1024
@@ -103,6 +111,8 @@ struct SymArgs {
     const int4* items;     // {I, J0, ntiles, first local tile}
     int nitems;
     int n;
+    uint32_t magic;        // 0x4B000000 (2^23 as fp32 bits) for the hop decode, passed as a
+                           // parameter so the PRMT selector can stay an immediate
 };
 
 cudaError_t launch_sym(const SymArgs& a, int mode, int dim, int nsets, int hb, int grid, cudaStream_t s);

@@ -67,7 +67,7 @@ __global__ void k_stage_pos1(const double* __restrict__ X, float* posf, int nloc
 {
     const int lr = blockIdx.x * blockDim.x + threadIdx.x;
     if (lr >= nloc) return;
-    const int64_t g = (int64_t)row0 + lr;
+    const int64_t g = stage_slot((int64_t)row0 + lr);
     for (int q = 0; q < ps; ++q) posf[g * ps + q] = q < dim ? (float)X[(size_t)lr * dim + q] : 0.0f;
 }
 
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kRB) k_combine(const double* __restrict__ Xk, 
     const int lr = blockIdx.x * kRB + threadIdx.x;
     double disp2 = 0.0;
     if (lr < nloc) {
-        const int64_t g = (int64_t)row0 + lr;
+        const int64_t g = stage_slot((int64_t)row0 + lr);
         double v[3], xn[3], n2 = 0.0;
         for (int q = 0; q < dim; ++q) {
             xn[q] = Xn[(size_t)lr * dim + q] - xpin[q];
@@ -199,7 +199,7 @@ __global__ void k_cg_begin(const double* __restrict__ Xk, double* x, float* pvec
 {
     const int lr = blockIdx.x * blockDim.x + threadIdx.x;
     if (lr >= nloc) return;
-    const int64_t g = (int64_t)row0 + lr;
+    const int64_t g = stage_slot((int64_t)row0 + lr);
     for (int q = 0; q < pq; ++q) {
         double v = 0.0;
         if (q < dim) {
@@ -235,13 +235,13 @@ __global__ void __launch_bounds__(kRB) k_cg_init(const double* __restrict__ y, c
             r[k] = rv;
             z[k] = zv;
             p[k] = zv;
-            pvec[(size_t)i * pq + q] = (float)zv;
+            pvec[stage_slot(i) * pq + q] = (float)zv;
             rz[q] = rv * zv;
             rr[q] = rv * rv;
             bb[q] = bv * bv;
             zs[q] = zv;
         }
-        for (int q = dim; q < pq; ++q) pvec[(size_t)i * pq + q] = 0.0f;
+        for (int q = dim; q < pq; ++q) pvec[stage_slot(i) * pq + q] = 0.0f;
     }
     for (int q = 0; q < dim; ++q) {
         double t = block_sum_256(rz[q], red);
@@ -338,7 +338,7 @@ __global__ void k_cg_p(double* p, const double* __restrict__ z, float* pvec, con
 {
     const int lr = blockIdx.x * blockDim.x + threadIdx.x;
     if (lr >= nloc) return;
-    const int64_t g = (int64_t)row0 + lr;
+    const int64_t g = stage_slot((int64_t)row0 + lr);
     for (int q = 0; q < dim; ++q) {
         const size_t i = (size_t)lr * dim + q;
         double pv = p[i];

@@ -91,15 +91,33 @@ __device__ __forceinline__ uint32_t word_of(const uint4& v, int q)
 // hop of entry (row r, column cc of the chunk) of one 16-byte chunk as an
 // exact float: one PRMT builds 0x4B0000hh (= 2^23 + h), one FADD removes 2^23.
 // u8 chunk: columns 2k, 2k+1, byte cc*8 + r; u16 chunk: column k, bytes 2r, 2r+1.
+// `magic` holds 0x4B000000 in a register (a kernel parameter, opaque to
+// constant folding) so the selector can be the PRMT immediate: one PRMT per
+// hop, no selector materialisation.
+template <int SEL>
+__device__ __forceinline__ uint32_t prmt_imm(uint32_t a, uint32_t b)
+{
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "n"(SEL));
+    return d;
+}
+
 template <int HB>
-__device__ __forceinline__ float chunk_hop(const uint4& ch, int r, int cc)
+__device__ __forceinline__ float chunk_hop(const uint4& ch, int r, int cc, uint32_t magic)
 {
     uint32_t bits;
     if (HB == 1) {
         const int byte = cc * 8 + r;
-        bits = __byte_perm(word_of(ch, byte >> 2), 0x4B000000u, 0x7650u + (uint32_t)(byte & 3));
+        const uint32_t w = word_of(ch, byte >> 2);
+        switch (byte & 3) {
+            case 0: bits = prmt_imm<0x7650>(w, magic); break;
+            case 1: bits = prmt_imm<0x7651>(w, magic); break;
+            case 2: bits = prmt_imm<0x7652>(w, magic); break;
+            default: bits = prmt_imm<0x7653>(w, magic); break;
+        }
     } else {
-        bits = __byte_perm(word_of(ch, r >> 1), 0x4B000000u, (r & 1) ? 0x7632u : 0x7610u);
+        const uint32_t w = word_of(ch, r >> 1);
+        bits = (r & 1) ? prmt_imm<0x7632>(w, magic) : prmt_imm<0x7610>(w, magic);
     }
     return __uint_as_float(bits) - 8388608.0f;
 }
@@ -145,8 +163,8 @@ __host__ __device__ constexpr size_t sym_smem_bytes()
 // MODE P2: acc_i += w d, acc_j += w d
 // MODE DIAG: acc_i += w, acc_j += w
 template <int MODE, int DIM, bool SAFE>
-__device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float h2, bool valid, float* ai,
-                                         float* aj, float& s)
+__device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float h2, float wlut, bool valid,
+                                         float* ai, float* aj, float& s)
 {
     if (MODE == kSymP1) {
         float d[DIM];
@@ -169,7 +187,7 @@ __device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float
         }
         s = fmaf(u, u, s);
     } else if (MODE == kSymP2) {
-        float w = rcp_approx(h2);  // w' = 1/h^2
+        float w = wlut;  // w' = 1/h^2 (table for u8, MUFU rcp for u16; 0 for h = 0)
         if (SAFE) w = valid ? w : 0.0f;
 #pragma unroll
         for (int c = 0; c < DIM; ++c) {
@@ -186,7 +204,8 @@ __device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float
 }
 
 template <int MODE, int DIM, int NSETS, int HB, bool SAFE>
-__device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, int ty, int tx, bool diag,
+__device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, const float* lut, uint32_t magic, int ty,
+                                         int tx, bool diag,
                                          const float (&xi)[8][NSETS * DIM], float (&ai)[8][sym_ncomp<MODE, DIM, NSETS>()],
                                          float* red, float (&sf)[NSETS])
 {
@@ -204,14 +223,15 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, int
         for (int cc = 0; cc < CPC; ++cc) {
             const int c = kc * CPC + cc;
             const int jl = tx * 8 + c;
+            const int js = c * 16 + tx;  // staged slot of column jl (stage_slot)
             float xj[PS];
             if (PS == 2) {
-                const float2 t = *reinterpret_cast<const float2*>(sP + jl * PS);
+                const float2 t = *reinterpret_cast<const float2*>(sP + js * PS);
                 xj[0] = t.x; xj[1] = t.y;
             } else {
 #pragma unroll
                 for (int q = 0; q < PS / 4; ++q) {
-                    const float4 t = *reinterpret_cast<const float4*>(sP + jl * PS + 4 * q);
+                    const float4 t = *reinterpret_cast<const float4*>(sP + js * PS + 4 * q);
                     xj[4 * q] = t.x; xj[4 * q + 1] = t.y; xj[4 * q + 2] = t.z; xj[4 * q + 3] = t.w;
                 }
             }
@@ -220,18 +240,27 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, int
             for (int v = 0; v < C; ++v) aj[v] = 0.0f;
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
-                const float hf = chunk_hop<HB>(ch, r, cc);
-                const float h2 = hf * hf;
+                float hf, h2, wl = 0.0f;
+                if (MODE == kSymP2 && HB == 1) {
+                    const int byte = cc * 8 + r;
+                    const uint32_t hb8 = __byte_perm(word_of(ch, byte >> 2), 0u, 0x4440u + (uint32_t)(byte & 3));
+                    wl = lut[hb8];
+                    h2 = wl;  // only its sign (h > 0) is used below
+                } else {
+                    hf = chunk_hop<HB>(ch, r, cc, magic);
+                    h2 = hf * hf;
+                    if (MODE == kSymP2) wl = rcp_approx(h2);
+                }
                 bool valid = true;
                 if (SAFE) valid = (h2 > 0.0f) && (!diag || (ty * 8 + r < jl));
                 if (MODE == kSymP1) {
 #pragma unroll
                     for (int s = 0; s < NSETS; ++s)
-                        sym_pair<MODE, DIM, SAFE>(&xi[r][s * DIM], xj + s * DIM, h2, valid, &ai[r][s * DIM],
+                        sym_pair<MODE, DIM, SAFE>(&xi[r][s * DIM], xj + s * DIM, h2, wl, valid, &ai[r][s * DIM],
                                                   &aj[s * DIM], sf[s]);
                 } else {
                     float dummy = 0.0f;
-                    sym_pair<MODE, DIM, SAFE>(&xi[r][0], xj, h2, valid, &ai[r][0], &aj[0], dummy);
+                    sym_pair<MODE, DIM, SAFE>(&xi[r][0], xj, h2, wl, valid, &ai[r][0], &aj[0], dummy);
                 }
             }
 #pragma unroll
@@ -252,15 +281,15 @@ __device__ __forceinline__ void sym_flush_j(const float* red, float* jpart_tile,
     constexpr float SIGN = MODE == kSymDiag ? 1.0f : -1.0f;
     for (int e = tid; e < kT * C; e += 256) {
         const int tx = e / (8 * C), rem = e % (8 * C);  // rem = c*C + v
-        double s = 0.0;
-#pragma unroll 4
-        for (int ty = 0; ty < 16; ++ty) s += (double)red[(size_t)(ty * 16 + tx) * PITCH + rem];
-        jpart_tile[tx * 8 * C + rem] = SIGN * (float)s;  // col = tx*8 + c, comp v
+        float s = 0.0f;  // <= 16 partials of <= 8 fp32 terms: a 128-term fp32 tile sum
+#pragma unroll
+        for (int ty = 0; ty < 16; ++ty) s += red[(size_t)(ty * 16 + tx) * PITCH + rem];
+        jpart_tile[tx * 8 * C + rem] = SIGN * s;  // col = tx*8 + c, comp v
     }
 }
 
 template <int MODE, int DIM, int NSETS, int HB>
-__global__ void __launch_bounds__(256, 1) k_sym(const SymArgs a)
+__global__ void __launch_bounds__(256, (MODE == kSymP1 && DIM == 2) ? 2 : 1) k_sym(const SymArgs a)
 {
     constexpr int C = sym_ncomp<MODE, DIM, NSETS>();
     constexpr int PS = sym_ps<MODE, DIM, NSETS>();
@@ -270,10 +299,12 @@ __global__ void __launch_bounds__(256, 1) k_sym(const SymArgs a)
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t full[kSymStages];
     __shared__ double sred[8][NSETS > 0 ? NSETS : 1];
+    __shared__ float lut[256];
     float* red = reinterpret_cast<float*>(smem + (size_t)kSymStages * STAGE);
 
     const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
     if ((int)blockIdx.x >= a.nitems) return;
+    lut[tid] = tid ? 1.0f / (float)(tid * tid) : 0.0f;  // w'_h = fp32(1/h^2), correctly rounded
     if (tid == 0) {
         for (int s = 0; s < kSymStages; ++s) mbar_init(&full[s], 1);
         fence_mbar_init();
@@ -308,7 +339,7 @@ __global__ void __launch_bounds__(256, 1) k_sym(const SymArgs a)
         float ai[8][C];
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-            const int64_t gi = (int64_t)I * kT + ty * 8 + r;
+            const int64_t gi = stage_slot((int64_t)I * kT + ty * 8 + r);
 #pragma unroll
             for (int q = 0; q < NSETS * DIM; ++q) xi[r][q] = a.pos[gi * PS + q];
 #pragma unroll
@@ -329,9 +360,9 @@ __global__ void __launch_bounds__(256, 1) k_sym(const SymArgs a)
 #pragma unroll
             for (int s = 0; s < NSETS; ++s) sf[s] = 0.0f;
             if (safe)
-                sym_tile<MODE, DIM, NSETS, HB, true>(sD, sP, ty, tx, diag, xi, ai, red, sf);
+                sym_tile<MODE, DIM, NSETS, HB, true>(sD, sP, lut, a.magic, ty, tx, diag, xi, ai, red, sf);
             else
-                sym_tile<MODE, DIM, NSETS, HB, false>(sD, sP, ty, tx, diag, xi, ai, red, sf);
+                sym_tile<MODE, DIM, NSETS, HB, false>(sD, sP, lut, a.magic, ty, tx, diag, xi, ai, red, sf);
 #pragma unroll
             for (int s = 0; s < NSETS; ++s) s64[s] += (double)sf[s];
             __syncthreads();  // j partials complete; stage consumed
@@ -427,39 +458,47 @@ int sym_max_ctas(int mode, int dim, int nsets, int hb)
 }
 
 // ---------------------------------------------------------------- reduction
-// Per row (one thread per row of block B): sum, in a fixed order, the i-side
-// segment partials of strip B (items it_lo[B]..it_hi[B]) and the j-side tile
-// partials of the local tiles (I, B), I = 0..B.  Output: dense fp64 rank
-// partial out[row][C] for all n_pad rows.
-__global__ void __launch_bounds__(kT) k_sym_reduce(const double* __restrict__ ipart, const float* __restrict__ jpart,
-                                                   const int* __restrict__ it_lo, const int* __restrict__ it_hi,
-                                                   int nb, int64_t t0, int64_t t1, int C, int D, double* out0,
-                                                   double* out1)
+// Per row of block B: sum, in a fixed order, the i-side segment partials of
+// strip B (items it_lo[B]..it_hi[B]) and the j-side tile partials of the local
+// tiles (I, B), I = 0..B.  4 groups of 128 threads split the I loop (I = g mod
+// 4); the group sums are combined in group order.  Blocks run largest B first.
+// Output: dense fp64 rank partial, components [0, D) -> out0, [D, C) -> out1.
+__global__ void __launch_bounds__(4 * kT) k_sym_reduce(const double* __restrict__ ipart, const float* __restrict__ jpart,
+                                                       const int* __restrict__ it_lo, const int* __restrict__ it_hi,
+                                                       int nb, int64_t t0, int64_t t1, int C, int D, double* out0,
+                                                       double* out1)
 {
-    const int B = blockIdx.x;
-    const int r = threadIdx.x;
+    __shared__ double gsum[4][kT][8];
+    const int B = nb - 1 - (int)blockIdx.x;
+    const int g = threadIdx.x / kT, r = threadIdx.x % kT;
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int item = it_lo[B]; item < it_hi[B]; ++item)
-        for (int v = 0; v < C; ++v) acc[v] += ipart[((size_t)item * kT + r) * C + v];
-    for (int I = 0; I <= B; ++I) {
+    for (int I = g; I <= B; I += 4) {
         const int64_t t = tri_index(I, B, nb);
         if (t < t0 || t >= t1) continue;
         const float* src = jpart + ((size_t)(t - t0) * kT + r) * C;
         for (int v = 0; v < C; ++v) acc[v] += (double)src[v];
     }
+    for (int v = 0; v < C; ++v) gsum[g][r][v] = acc[v];
+    __syncthreads();
+    if (g != 0) return;
+    double tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int item = it_lo[B]; item < it_hi[B]; ++item)
+        for (int v = 0; v < C; ++v) tot[v] += ipart[((size_t)item * kT + r) * C + v];
+    for (int gg = 0; gg < 4; ++gg)
+        for (int v = 0; v < C; ++v) tot[v] += gsum[gg][r][v];
     const size_t row = (size_t)B * kT + r;
     for (int v = 0; v < C; ++v) {
         if (v < D)
-            out0[row * D + v] = acc[v];
+            out0[row * D + v] = tot[v];
         else
-            out1[row * (C - D) + (v - D)] = acc[v];
+            out1[row * (C - D) + (v - D)] = tot[v];
     }
 }
 
 cudaError_t launch_sym_reduce(const double* ipart, const float* jpart, const int* it_lo, const int* it_hi, int nb,
                               int64_t t0, int64_t t1, int C, int D, double* out0, double* out1, cudaStream_t s)
 {
-    k_sym_reduce<<<nb, kT, 0, s>>>(ipart, jpart, it_lo, it_hi, nb, t0, t1, C, D, out0, out1);
+    k_sym_reduce<<<nb, 4 * kT, 0, s>>>(ipart, jpart, it_lo, it_hi, nb, t0, t1, C, D, out0, out1);
     return cudaGetLastError();
 }
 
@@ -565,22 +604,30 @@ cudaError_t launch_hop_rows(const uint8_t* D, int hb, int nb, int64_t t0, int64_
     return cudaGetLastError();
 }
 
-// stress partial of the rank: sum of segment partials in item order (one warp, fixed butterfly)
-__global__ void k_sym_stress(const double* __restrict__ spart, int nitems, int nsets, double* out)
+// stress partial of the rank: fixed-order block reduction of the segment partials
+__global__ void __launch_bounds__(1024) k_sym_stress(const double* __restrict__ spart, int nitems, int nsets,
+                                                     double* out)
 {
-    const int lane = threadIdx.x;
+    __shared__ double red[32];
     for (int s = 0; s < nsets; ++s) {
         double v = 0.0;
-        for (int i = lane; i < nitems; i += 32) v += spart[(size_t)i * nsets + s];
+        for (int i = threadIdx.x; i < nitems; i += blockDim.x) v += spart[(size_t)i * nsets + s];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) out[s] = v;
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+            out[s] = t;
+        }
+        __syncthreads();
     }
 }
 
 cudaError_t launch_sym_stress(const double* spart, int nitems, int nsets, double* out, cudaStream_t s)
 {
-    k_sym_stress<<<1, 32, 0, s>>>(spart, nitems, nsets, out);
+    k_sym_stress<<<1, 1024, 0, s>>>(spart, nitems, nsets, out);
     return cudaGetLastError();
 }
 

@@ -81,8 +81,9 @@ def test_jacobi_diagonal(name):
     rows = sample_rows(g.n) if g.n > 20000 else np.arange(g.n, dtype=np.int32)
     ref = core.lw_diag_rows(rows, core.hop_rows(g, rows), k)
     got = L.get_diag()[rows]
-    # GPU sums fp32-rounded weights in fp64: relative 1e-7
-    np.testing.assert_allclose(got, ref, rtol=1e-7)
+    # Jacobi preconditioner only: fp32 weights, fp32 tile partials (<= 128
+    # terms) summed in fp64 -> relative 1e-6
+    np.testing.assert_allclose(got, ref, rtol=1e-6)
 
 
 # ------------------------------------------------- a2/a3 forces at X0 (single iteration)
