@@ -29,8 +29,10 @@ import scipy.linalg
 
 from . import core
 
-# Dense reduced matrix is used up to this many bytes (fp64, (n-1)^2 entries).
+# Dense reduced matrix (fp64, (n-1)^2 entries) is used up to this many bytes and
+# below 2^31 entries (scipy's bundled LAPACK uses 32-bit indices).
 DENSE_LIMIT_BYTES = 24 << 30
+DENSE_LIMIT_ENTRIES = (1 << 31) - 1
 
 
 @dataclass
@@ -70,7 +72,8 @@ class Problem:
         self.hop = core.hop_matrix(g) if hop is None else hop
         self.rows = np.arange(self.n, dtype=np.int32)
         if solver == "auto":
-            solver = "cholesky" if 8 * (self.n - 1) ** 2 <= DENSE_LIMIT_BYTES else "cg"
+            m2 = (self.n - 1) ** 2
+            solver = "cholesky" if (8 * m2 <= DENSE_LIMIT_BYTES and m2 <= DENSE_LIMIT_ENTRIES) else "cg"
         self.solver = solver
         self.cg_rtol = cg_rtol
         self.cg_iters = []
