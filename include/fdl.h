@@ -177,6 +177,17 @@ fdl_status fdl_create_sharded(int32_t n, const int64_t* row_ptr, const int32_t* 
                               const double* init_pos, const uint8_t* nccl_unique_id,
                               int32_t rank, int32_t world, fdl_ctx** out);
 
+/* Test hook of the sharded path on one GPU.  fdl_create_sharded with
+ * nccl_unique_id == NULL and world > 1 builds an EMULATED rank: it stores and
+ * evaluates only its own tiles and has no communicator, so it accepts only
+ * fdl_eval_partial, fdl_get_info and fdl_destroy (others: FDL_E_UNSUPPORTED).
+ * fdl_eval_partial evaluates, at placement X (n*dim doubles, original units),
+ * one symmetric pass over this context's tiles and returns this rank's dense
+ * partial sums: mode 0 -> out = partial L^X X (n*dim), *stress = partial f;
+ * mode 1 -> out = partial L^W X (n*dim).  Summing the partials of ranks
+ * 0..world-1 gives the full quantities (what the NCCL path all-gathers). */
+fdl_status fdl_eval_partial(fdl_ctx* ctx, int32_t mode, const double* X, double* out, double* stress);
+
 /* Tile range [t0, t1) of `rank` of `world`: equal shares of the
  * nb(nb+1)/2 upper-triangle tiles (nb = ceil(n / FDL_TILE)) in row-major
  * triangle order. */

@@ -161,6 +161,7 @@ struct fdl_ctx {
     bool broken = false;
     // NCCL
     ncclComm_t comm = nullptr;
+    bool emulated = false;  // world > 1 without communicator (fdl_eval_partial only)
 };
 
 namespace {
@@ -355,7 +356,7 @@ void collect_events(fdl_ctx* ctx)
 // rank * slice_elems) of `buf` in place.
 fdl_status allgather_inplace(fdl_ctx* ctx, void* buf, size_t slice_elems, int nccl_type, size_t esize)
 {
-    if (ctx->world == 1) return FDL_OK;
+    if (ctx->world == 1 || ctx->emulated) return FDL_OK;
     char* base = static_cast<char*>(buf);
     ncclResult_t r = g_nccl.AllGather(base + (size_t)ctx->rank * slice_elems * esize, base, slice_elems, nccl_type,
                                       ctx->comm, ctx->stream);
@@ -398,7 +399,7 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
         ctx->stats.p2_launches++;
         ctx->stats.p2_pairs += ctx->local_pairs;
     }
-    if (ctx->world == 1) {
+    if (ctx->world == 1 || ctx->emulated) {
         FDL_LAUNCH(launch_sym_reduce(ctx->ipart, ctx->jpart, ctx->it_lo, ctx->it_hi, ctx->nb, ctx->t0, ctx->t1, C, D0,
                                      out0, out1, ctx->stream));
         if (mode == kSymP1) {
@@ -542,7 +543,7 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
     cudaFree(fb);
     cudaFree(vis);
     if (st != FDL_OK) return st;
-    if (ctx->world > 1) {
+    if (ctx->world > 1 && !ctx->emulated) {
         // every rank BFSed only its sources: agree on the diameter and hop width (max over ranks)
         int* dd = nullptr;
         FDL_CUDA(cudaMalloc(&dd, sizeof(int) * 2 * ctx->world));
@@ -660,9 +661,9 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     FDL_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
 
-    if (world > 1) {
+    ctx->emulated = world > 1 && nccl_id == nullptr;
+    if (world > 1 && !ctx->emulated) {
         if (!g_nccl.load(msg)) return set_err(ctx, FDL_E_NCCL, msg);
-        if (!nccl_id) return set_err(ctx, FDL_E_INVALID_ARG, "nccl_unique_id is NULL");
         ncclUniqueId id;
         memcpy(id.internal, nccl_id, 128);
         ncclResult_t r = g_nccl.CommInitRank(&ctx->comm, world, id, rank);
@@ -698,7 +699,7 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     FDL_ALLOC(ctx->ipart, (size_t)std::max(ctx->nitems, 1) * kT * Cmax);
     FDL_ALLOC(ctx->spart, (size_t)std::max(ctx->nitems, 1) * 2);
     FDL_ALLOC(ctx->sparts, (size_t)2 * world);
-    if (world > 1) FDL_ALLOC(ctx->rparts, (size_t)world * ctx->npad * Cmax);
+    if (world > 1 && !ctx->emulated) FDL_ALLOC(ctx->rparts, (size_t)world * ctx->npad * Cmax);
     FDL_ALLOC(ctx->diag, (size_t)ctx->npad);
     FDL_ALLOC(ctx->Xk, vn);
     FDL_ALLOC(ctx->Xn, vn);
@@ -765,6 +766,7 @@ double pick_omega(fdl_ctx* ctx)
 // One Algorithm-2 iteration.
 fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
 {
+    if (ctx->emulated) return set_err(ctx, FDL_E_UNSUPPORTED, "emulated rank: only fdl_eval_partial is available");
     if (ctx->broken) return set_err(ctx, FDL_E_STATE, ctx->err.empty() ? "context is broken" : ctx->err);
     if (ctx->stopped) return set_err(ctx, FDL_E_STATE, "the run has stopped; call fdl_set_positions to restart");
     const double omega = pick_omega(ctx);
@@ -1007,6 +1009,7 @@ fdl_status fdl_run_until_converged(fdl_ctx* ctx, fdl_run_info* info)
 fdl_status fdl_get_positions(fdl_ctx* ctx, double* out, size_t count)
 {
     if (!ctx || !out) return FDL_E_INVALID_ARG;
+    if (ctx->emulated) return set_err(ctx, FDL_E_UNSUPPORTED, "emulated rank: only fdl_eval_partial");
     if (count != (size_t)ctx->n * ctx->dim) return set_err(ctx, FDL_E_INVALID_ARG, "count must be n*dim");
     if (ctx->broken) return FDL_E_STATE;
     cudaSetDevice(ctx->device);
@@ -1019,6 +1022,7 @@ fdl_status fdl_get_positions(fdl_ctx* ctx, double* out, size_t count)
 fdl_status fdl_set_positions(fdl_ctx* ctx, const double* in, size_t count)
 {
     if (!ctx || !in) return FDL_E_INVALID_ARG;
+    if (ctx->emulated) return set_err(ctx, FDL_E_UNSUPPORTED, "emulated rank: only fdl_eval_partial");
     if (count != (size_t)ctx->n * ctx->dim) return set_err(ctx, FDL_E_INVALID_ARG, "count must be n*dim");
     if (ctx->broken) return FDL_E_STATE;
     for (size_t i = 0; i < count; ++i)
@@ -1032,6 +1036,7 @@ fdl_status fdl_set_positions(fdl_ctx* ctx, const double* in, size_t count)
 fdl_status fdl_eval_forces(fdl_ctx* ctx, double* R, double* A, double* stress)
 {
     if (!ctx) return FDL_E_INVALID_ARG;
+    if (ctx->emulated) return set_err(ctx, FDL_E_UNSUPPORTED, "emulated rank: only fdl_eval_partial");
     if (ctx->broken) return FDL_E_STATE;
     cudaSetDevice(ctx->device);
     const int dim = ctx->dim;
@@ -1051,6 +1056,33 @@ fdl_status fdl_eval_forces(fdl_ctx* ctx, double* R, double* A, double* stress)
         collect_events(ctx);
     }
     if (stress) *stress = ctx->f;
+    return FDL_OK;
+}
+
+fdl_status fdl_eval_partial(fdl_ctx* ctx, int32_t mode, const double* X, double* out, double* stress)
+{
+    if (!ctx || !X || !out || (mode != 0 && mode != 1)) return FDL_E_INVALID_ARG;
+    if (ctx->broken) return FDL_E_STATE;
+    cudaSetDevice(ctx->device);
+    const int dim = ctx->dim;
+    const size_t count = (size_t)ctx->n * dim;
+    std::vector<double> xs(count);
+    for (int i = 0; i < ctx->n; ++i)
+        for (int q = 0; q < dim; ++q) xs[(size_t)i * dim + q] = (X[(size_t)i * dim + q] - X[q]) / ctx->k;
+    FDL_CUDA(cudaMemcpyAsync(ctx->Xt, xs.data(), count * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    if (mode == 0) {
+        FDL_LAUNCH(launch_stage_pos1(ctx->Xt, ctx->posf, ctx->n, 0, dim, ps_p1(dim, 1), ctx->stream));
+        FDL_TRY(run_sym(ctx, kSymP1, 1, ctx->posf, ctx->R1, nullptr, 0));
+    } else {
+        FDL_LAUNCH(launch_cg_begin(ctx->Xt, ctx->R1, ctx->pvec, ctx->n, 0, dim, ps_p2(dim), ctx->stream));
+        FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->R1, nullptr, 0));
+    }
+    FDL_CUDA(cudaMemcpyAsync(out, ctx->R1, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, ctx->stream));
+    FDL_CUDA(cudaStreamSynchronize(ctx->stream));
+    collect_events(ctx);
+    for (size_t i = 0; i < count; ++i) out[i] /= ctx->k;
+    if (stress) *stress = mode == 0 ? ctx->sc_host->f_set[0] : 0.0;
     return FDL_OK;
 }
 

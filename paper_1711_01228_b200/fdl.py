@@ -30,7 +30,7 @@ EXPORTS = [
     "fdl_nccl_unique_id", "fdl_set_stream", "fdl_step", "fdl_run_until_converged", "fdl_get_positions",
     "fdl_set_positions", "fdl_eval_forces", "fdl_get_hop_rows", "fdl_get_diag", "fdl_get_info",
     "fdl_set_timing", "fdl_get_stats", "fdl_reset_stats", "fdl_bench_ffma", "fdl_status_str",
-    "fdl_last_error", "fdl_destroy",
+    "fdl_last_error", "fdl_destroy", "fdl_eval_partial",
 ]
 
 
@@ -121,6 +121,7 @@ def _load():
         "fdl_status_str": (ctypes.c_char_p, [i32]),
         "fdl_last_error": (ctypes.c_char_p, [P]),
         "fdl_destroy": (None, [P]),
+        "fdl_eval_partial": (i32, [P, i32, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -192,7 +193,8 @@ class Layout:
             st = lib.fdl_create(self.n, _ptr(self._rp), _ptr(self._col), None, ctypes.byref(self.params),
                                 _ptr(X0), ctypes.byref(self._h))
         else:
-            idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
+            # nccl_id None -> emulated rank (test hook: fdl_eval_partial only)
+            idbuf = None if nccl_id is None else (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
             st = lib.fdl_create_sharded(self.n, _ptr(self._rp), _ptr(self._col), None, ctypes.byref(self.params),
                                         _ptr(X0), idbuf, rank, world, ctypes.byref(self._h))
         if st != 0:
@@ -250,6 +252,14 @@ class Layout:
         f = ctypes.c_double()
         _check(self._h, lib.fdl_eval_forces(self._h, _ptr(R), _ptr(A), ctypes.byref(f)))
         return R, A, f.value
+
+    def eval_partial(self, mode: int, X):
+        """This rank's partial L^X X (mode 0, with partial stress) or L^W X (mode 1) at X."""
+        X = np.ascontiguousarray(X, dtype=np.float64)
+        out = np.empty((self.n, self.dim))
+        f = ctypes.c_double()
+        _check(self._h, lib.fdl_eval_partial(self._h, mode, _ptr(X), _ptr(out), ctypes.byref(f)))
+        return out, f.value
 
     def get_hop_rows(self, r0: int, nrows: int) -> np.ndarray:
         out = np.empty((nrows, self.n), dtype=np.uint16)
