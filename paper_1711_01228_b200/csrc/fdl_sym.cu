@@ -139,6 +139,12 @@ __host__ __device__ constexpr int sym_ps()
                           : (MODE == kSymP2 ? (DIM == 2 ? 2 : 4) : 4);
 }
 
+template <int MODE>
+__host__ __device__ constexpr int sym_stages()  // P1 is compute-bound: double buffering suffices
+{
+    return MODE == kSymP1 ? 2 : kSymStages;
+}
+
 template <int MODE, int DIM, int NSETS, int HB>
 __host__ __device__ constexpr int sym_stage_bytes()
 {
@@ -154,8 +160,8 @@ __host__ __device__ constexpr int sym_red_pitch()  // floats per (ty, tx) cell i
 template <int MODE, int DIM, int NSETS, int HB>
 __host__ __device__ constexpr size_t sym_smem_bytes()
 {
-    return (size_t)kSymStages * sym_stage_bytes<MODE, DIM, NSETS, HB>() +
-           (size_t)256 * sym_red_pitch<MODE, DIM, NSETS>() * 4;
+    return (size_t)sym_stages<MODE>() * sym_stage_bytes<MODE, DIM, NSETS, HB>() +
+           (size_t)2 * 256 * sym_red_pitch<MODE, DIM, NSETS>() * 4;  // double-buffered reduction
 }
 
 // One evaluation of an unordered pair for one position set.
@@ -296,17 +302,19 @@ __global__ void __launch_bounds__(256, (MODE == kSymP1 && DIM == 2) ? 2 : 1) k_s
     constexpr int STAGE = sym_stage_bytes<MODE, DIM, NSETS, HB>();
     constexpr int DT = kT * kT * HB;
     constexpr int PITCH = sym_red_pitch<MODE, DIM, NSETS>();
+    constexpr int NST = sym_stages<MODE>();
     extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ uint64_t full[kSymStages];
+    __shared__ uint64_t full[NST];
     __shared__ double sred[8][NSETS > 0 ? NSETS : 1];
     __shared__ float lut[256];
-    float* red = reinterpret_cast<float*>(smem + (size_t)kSymStages * STAGE);
+    float* red0 = reinterpret_cast<float*>(smem + (size_t)NST * STAGE);
+    float* red1 = red0 + 256 * PITCH;
 
     const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
     if ((int)blockIdx.x >= a.nitems) return;
     lut[tid] = tid ? 1.0f / (float)(tid * tid) : 0.0f;  // w'_h = fp32(1/h^2), correctly rounded
     if (tid == 0) {
-        for (int s = 0; s < kSymStages; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < NST; ++s) mbar_init(&full[s], 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -328,10 +336,11 @@ __global__ void __launch_bounds__(256, (MODE == kSymP1 && DIM == 2) ? 2 : 1) k_s
         }
     };
     if (tid == 0)
-        for (int s = 0; s < kSymStages - 1 && p_item < a.nitems; ++s) issue(s);
+        for (int s = 0; s < NST - 1 && p_item < a.nitems; ++s) issue(s);
 
     int stage = 0;
     uint32_t phase = 0;
+    int tcount = 0;  // tiles done by this CTA: selects the reduction buffer
     for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
         const int4 it = a.items[item];
         const int I = it.x;
@@ -349,7 +358,9 @@ __global__ void __launch_bounds__(256, (MODE == kSymP1 && DIM == 2) ? 2 : 1) k_s
 #pragma unroll
         for (int s = 0; s < NSETS; ++s) s64[s] = 0.0;
         for (int t = 0; t < it.z; ++t) {
-            if (tid == 0 && p_item < a.nitems) issue((stage + kSymStages - 1) % kSymStages);
+            // stage (stage-1) was consumed before the previous tile's barrier
+            if (tid == 0 && p_item < a.nitems) issue((stage + NST - 1) % NST);
+            float* red = (tcount & 1) ? red1 : red0;
             const int J = it.y + t;
             const bool diag = (J == I);
             const bool safe = diag || (int64_t)(J + 1) * kT > a.n || (int64_t)(I + 1) * kT > a.n;
@@ -365,15 +376,20 @@ __global__ void __launch_bounds__(256, (MODE == kSymP1 && DIM == 2) ? 2 : 1) k_s
                 sym_tile<MODE, DIM, NSETS, HB, false>(sD, sP, lut, a.magic, ty, tx, diag, xi, ai, red, sf);
 #pragma unroll
             for (int s = 0; s < NSETS; ++s) s64[s] += (double)sf[s];
-            __syncthreads();  // j partials complete; stage consumed
+            // One barrier per tile: red[tcount&1] complete, stage consumed, and every
+            // thread finished flushing the other buffer (previous tile) before arriving.
+            __syncthreads();
             sym_flush_j<MODE, DIM, NSETS>(red, a.jpart + ((size_t)it.w + t) * kT * C, tid);
-            __syncthreads();  // red free again
-            if (++stage == kSymStages) {
+            ++tcount;
+            if (++stage == NST) {
                 stage = 0;
                 phase ^= 1u;
             }
         }
-        // i-side: reduce over the 16 thread columns (fixed order, fp64)
+        // i-side: reduce over the 16 thread columns (fixed order, fp64), in the
+        // buffer the next tile would write (its last reader finished before the
+        // last tile's barrier)
+        float* red = (tcount & 1) ? red1 : red0;
         float* myred = red + (size_t)(tx * 16 + ty) * PITCH;  // [tx][ty] layout
 #pragma unroll
         for (int r = 0; r < 8; ++r)
