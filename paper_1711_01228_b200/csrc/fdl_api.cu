@@ -377,6 +377,7 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
     const int dim = ctx->dim;
     const int C = mode == kSymP1 ? nsets * dim : (mode == kSymP2 ? dim : 1);
     const int D0 = mode == kSymP1 ? dim : C;
+    const int inter = (mode == kSymP1 && nsets == 2) ? 1 : 0;  // P1 two sets: components interleaved by set
     SymArgs a;
     a.D = ctx->D;
     a.pos = pos;
@@ -401,7 +402,7 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
     }
     if (ctx->world == 1 || ctx->emulated) {
         FDL_LAUNCH(launch_sym_reduce(ctx->ipart, ctx->jpart, ctx->it_lo, ctx->it_hi, ctx->nb, ctx->t0, ctx->t1, C, D0,
-                                     out0, out1, ctx->stream));
+                                     inter, out0, out1, ctx->stream));
         if (mode == kSymP1) {
             FDL_LAUNCH(launch_sym_stress(ctx->spart, ctx->nitems, nsets, ctx->sparts, ctx->stream));
             FDL_LAUNCH(launch_stress_ranks(ctx->sparts, 1, nsets, ctx->sc, set_cur, ctx->stream));
@@ -410,10 +411,10 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
     }
     const size_t slice = (size_t)ctx->npad * C;
     double* mine = ctx->rparts + (size_t)ctx->rank * slice;
-    FDL_LAUNCH(launch_sym_reduce(ctx->ipart, ctx->jpart, ctx->it_lo, ctx->it_hi, ctx->nb, ctx->t0, ctx->t1, C, C, mine,
-                                 nullptr, ctx->stream));
+    FDL_LAUNCH(launch_sym_reduce(ctx->ipart, ctx->jpart, ctx->it_lo, ctx->it_hi, ctx->nb, ctx->t0, ctx->t1, C, C, 0,
+                                 mine, nullptr, ctx->stream));
     FDL_TRY(allgather_inplace(ctx, ctx->rparts, slice, ncclFloat64, 8));
-    FDL_LAUNCH(launch_rank_sum(ctx->rparts, ctx->world, ctx->npad, C, D0, out0, out1, ctx->stream));
+    FDL_LAUNCH(launch_rank_sum(ctx->rparts, ctx->world, ctx->npad, C, D0, inter, out0, out1, ctx->stream));
     if (mode == kSymP1) {
         FDL_LAUNCH(launch_sym_stress(ctx->spart, ctx->nitems, nsets, ctx->sparts + 2 * ctx->rank, ctx->stream));
         FDL_TRY(allgather_inplace(ctx, ctx->sparts, 2, ncclFloat64, 8));
@@ -952,10 +953,27 @@ fdl_status fdl_create_sharded(int32_t n, const int64_t* row_ptr, const int32_t* 
 fdl_status fdl_shard_tiles(int32_t n, int32_t world, int32_t rank, int64_t* t0, int64_t* t1)
 {
     if (n < 1 || world < 1 || rank < 0 || rank >= world || !t0 || !t1) return FDL_E_INVALID_ARG;
+    // Boundaries fall on global work-item boundaries (strip segments of <= kSeg
+    // tiles), nearest to equal tile shares: every item -- and so every fp32
+    // segment sum -- is the same for any number of GPUs.
     const int64_t nb = (n + kT - 1) / kT;
     const int64_t total = nb * (nb + 1) / 2;
-    *t0 = total * rank / world;
-    *t1 = total * (rank + 1) / world;
+    auto boundary = [&](int64_t target) -> int64_t {
+        if (target <= 0) return 0;
+        if (target >= total) return total;
+        int64_t best = 0;
+        for (int64_t I = 0; I < nb; ++I) {
+            const int64_t s0 = tri_index(I, I, nb), len = nb - I;
+            if (s0 + len < target) continue;  // strip entirely before the target
+            // segment starts inside strip I: s0, s0 + kSeg, ...
+            const int64_t k = (target - s0 + kSeg / 2) / kSeg;
+            best = std::min(s0 + k * kSeg, s0 + len);
+            break;
+        }
+        return best;
+    };
+    *t0 = boundary(total * rank / world);
+    *t1 = boundary(total * (rank + 1) / world);
     return FDL_OK;
 }
 

@@ -118,7 +118,8 @@ struct SymArgs {
 cudaError_t launch_sym(const SymArgs& a, int mode, int dim, int nsets, int hb, int grid, cudaStream_t s);
 int sym_max_ctas(int mode, int dim, int nsets, int hb);
 cudaError_t launch_sym_reduce(const double* ipart, const float* jpart, const int* it_lo, const int* it_hi, int nb,
-                              int64_t t0, int64_t t1, int C, int D, double* out0, double* out1, cudaStream_t s);
+                              int64_t t0, int64_t t1, int C, int D, int inter, double* out0, double* out1,
+                              cudaStream_t s);
 cudaError_t launch_sym_stress(const double* spart, int nitems, int nsets, double* out, cudaStream_t s);
 cudaError_t launch_bfs_level_sym(const int64_t* row_ptr, const int32_t* col, const uint32_t* fin, uint32_t* fout,
                                  uint32_t* visited, uint8_t* D, int n, int s0, int nsrc, int level, int nb, int64_t t0,
@@ -126,8 +127,8 @@ cudaError_t launch_bfs_level_sym(const int64_t* row_ptr, const int32_t* col, con
 cudaError_t launch_hop_rows(const uint8_t* D, int hb, int nb, int64_t t0, int64_t t1, const int* rows, int nrows,
                             int n, uint16_t* out, int* missing, cudaStream_t s);
 // sum of rank partials (world x len doubles, rank order) into out0/out1 split at D of C
-cudaError_t launch_rank_sum(const double* parts, int world, int64_t rows, int C, int D, double* out0, double* out1,
-                            cudaStream_t s);
+cudaError_t launch_rank_sum(const double* parts, int world, int64_t rows, int C, int D, int inter, double* out0,
+                            double* out1, cudaStream_t s);
 cudaError_t launch_stress_ranks(const double* parts, int world, int nsets, DevScalars* sc, int set_cur,
                                 cudaStream_t s);
 cudaError_t launch_set_sigma_rows(const double* diag, int n, DevScalars* sc, cudaStream_t s);

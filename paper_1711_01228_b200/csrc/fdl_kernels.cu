@@ -107,8 +107,12 @@ __global__ void __launch_bounds__(kRB) k_combine(const double* __restrict__ Xk, 
             const double xt = (sc == 1.0) ? (1.0 + omega) * xn[q] - omega * Xk[(size_t)lr * dim + q]
                                           : xn[q] + sc * v[q];
             Xt[(size_t)lr * dim + q] = xt;
-            posf[g * ps + q] = (float)xn[q];
-            if (nsets == 2) posf[g * ps + dim + q] = (float)xt;
+            if (nsets == 2) {  // sets interleaved per component: {x_n, x_t} pairs for the packed P1
+                posf[g * ps + 2 * q] = (float)xn[q];
+                posf[g * ps + 2 * q + 1] = (float)xt;
+            } else {
+                posf[g * ps + q] = (float)xn[q];
+            }
         }
         for (int q = nsets * dim; q < ps; ++q) posf[g * ps + q] = 0.0f;
     }

@@ -164,15 +164,86 @@ __host__ __device__ constexpr size_t sym_smem_bytes()
            (size_t)2 * 256 * sym_red_pitch<MODE, DIM, NSETS>() * 4;  // double-buffered reduction
 }
 
-// One evaluation of an unordered pair for one position set.
-// MODE P1: acc_i += q d, acc_j += q d (stored negated), s += u^2
-// MODE P2: acc_i += w d, acc_j += w d
-// MODE DIAG: acc_i += w, acc_j += w
-template <int MODE, int DIM, bool SAFE>
-__device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float h2, float wlut, bool valid,
-                                         float* ai, float* aj, float& s)
+// ------------------------------------------------------------ packed FP32x2
+// sm_100 executes fp32 pairs as one instruction (FADD2 / FFMA2 / FMUL2, with
+// free negation, immediate and scalar-broadcast operands).  The two position
+// sets of P1 (X^{k+1}, Xt) and the x/y coordinates of P2 run as pairs: half the
+// issue slots of the scalar code for the same fp32 arithmetic (round-to-nearest
+// per element, bitwise equal to the scalar ops).
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk(float lo, float hi)
 {
-    if (MODE == kSymP1) {
+    u64 d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+    return d;
+}
+__device__ __forceinline__ void upk(u64 v, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); }
+__device__ __forceinline__ u64 fsub2(u64 a, u64 b)
+{
+    u64 d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c)
+{
+    u64 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ u64 fmul2(u64 a, u64 b)
+{
+    u64 d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+// One unordered pair.  Layouts (C components per vertex):
+//   P1, 2 sets: [x_s0, x_s1, y_s0, y_s1 (, z_s0, z_s1)]  (sets interleaved, packed)
+//   P1, 1 set and P2: [x, y (, z)];  DIAG: [w]
+// MODE P1: a_i += q d, a_j += q d (j side negated at the flush), s += u^2
+// MODE P2: a_i += w d, a_j += w d;   MODE DIAG: a_i += w, a_j += w
+template <int MODE, int DIM, int NSETS, bool SAFE>
+__device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float h2, float wlut, bool valid,
+                                         float* ai, float* aj, float* s)
+{
+    if (MODE == kSymP1 && NSETS == 2) {
+        u64 d[DIM];
+        u64 r2 = pk(FLT_MIN, FLT_MIN);  // r^2 > 0 for coincident points: zero R term
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+            d[c] = fsub2(pk(xi[2 * c], xi[2 * c + 1]), pk(xj[2 * c], xj[2 * c + 1]));
+            r2 = ffma2(d[c], d[c], r2);
+        }
+        float t0, t1;
+        upk(fmul2(r2, pk(h2, h2)), t0, t1);
+        float q0 = rsqrt_approx(t0), q1 = rsqrt_approx(t1);  // 1/(h r) per set
+        if (SAFE) {
+            q0 = valid ? q0 : 0.0f;
+            q1 = valid ? q1 : 0.0f;
+        }
+        const u64 q = pk(q0, q1);
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+            float lo, hi;
+            upk(ffma2(q, d[c], pk(ai[2 * c], ai[2 * c + 1])), lo, hi);
+            ai[2 * c] = lo;
+            ai[2 * c + 1] = hi;
+            upk(ffma2(q, d[c], pk(aj[2 * c], aj[2 * c + 1])), lo, hi);
+            aj[2 * c] = lo;
+            aj[2 * c + 1] = hi;
+        }
+        float u0, u1;
+        upk(ffma2(r2, q, pk(-1.0f, -1.0f)), u0, u1);  // r/h - 1 per set
+        if (SAFE) {
+            u0 = valid ? u0 : 0.0f;
+            u1 = valid ? u1 : 0.0f;
+        }
+        const u64 u = pk(u0, u1);
+        float s0, s1;
+        upk(ffma2(u, u, pk(s[0], s[1])), s0, s1);
+        s[0] = s0;
+        s[1] = s1;
+    } else if (MODE == kSymP1) {
         float d[DIM];
         float r2 = FLT_MIN;
 #pragma unroll
@@ -191,15 +262,23 @@ __device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float
             ai[c] = fmaf(q, d[c], ai[c]);
             aj[c] = fmaf(q, d[c], aj[c]);
         }
-        s = fmaf(u, u, s);
+        s[0] = fmaf(u, u, s[0]);
     } else if (MODE == kSymP2) {
         float w = wlut;  // w' = 1/h^2 (table for u8, MUFU rcp for u16; 0 for h = 0)
         if (SAFE) w = valid ? w : 0.0f;
-#pragma unroll
-        for (int c = 0; c < DIM; ++c) {
-            const float d = xi[c] - xj[c];
-            ai[c] = fmaf(w, d, ai[c]);
-            aj[c] = fmaf(w, d, aj[c]);
+        const u64 wp = pk(w, w);
+        const u64 dxy = fsub2(pk(xi[0], xi[1]), pk(xj[0], xj[1]));
+        float lo, hi;
+        upk(ffma2(wp, dxy, pk(ai[0], ai[1])), lo, hi);
+        ai[0] = lo;
+        ai[1] = hi;
+        upk(ffma2(wp, dxy, pk(aj[0], aj[1])), lo, hi);
+        aj[0] = lo;
+        aj[1] = hi;
+        if (DIM == 3) {
+            const float dz = xi[2] - xj[2];
+            ai[2] = fmaf(w, dz, ai[2]);
+            aj[2] = fmaf(w, dz, aj[2]);
         }
     } else {
         float w = __frcp_rn(h2);
@@ -259,15 +338,7 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
                 }
                 bool valid = true;
                 if (SAFE) valid = (h2 > 0.0f) && (!diag || (ty * 8 + r < jl));
-                if (MODE == kSymP1) {
-#pragma unroll
-                    for (int s = 0; s < NSETS; ++s)
-                        sym_pair<MODE, DIM, SAFE>(&xi[r][s * DIM], xj + s * DIM, h2, wl, valid, &ai[r][s * DIM],
-                                                  &aj[s * DIM], sf[s]);
-                } else {
-                    float dummy = 0.0f;
-                    sym_pair<MODE, DIM, SAFE>(&xi[r][0], xj, h2, wl, valid, &ai[r][0], &aj[0], dummy);
-                }
+                sym_pair<MODE, DIM, NSETS, SAFE>(&xi[r][0], xj, h2, wl, valid, &ai[r][0], &aj[0], sf);
             }
 #pragma unroll
             for (int v = 0; v < C; ++v) myred[c * C + v] = aj[v];
@@ -481,8 +552,8 @@ int sym_max_ctas(int mode, int dim, int nsets, int hb)
 // Output: dense fp64 rank partial, components [0, D) -> out0, [D, C) -> out1.
 __global__ void __launch_bounds__(4 * kT) k_sym_reduce(const double* __restrict__ ipart, const float* __restrict__ jpart,
                                                        const int* __restrict__ it_lo, const int* __restrict__ it_hi,
-                                                       int nb, int64_t t0, int64_t t1, int C, int D, double* out0,
-                                                       double* out1)
+                                                       int nb, int64_t t0, int64_t t1, int C, int D, int inter,
+                                                       double* out0, double* out1)
 {
     __shared__ double gsum[4][kT][8];
     const int B = nb - 1 - (int)blockIdx.x;
@@ -504,7 +575,9 @@ __global__ void __launch_bounds__(4 * kT) k_sym_reduce(const double* __restrict_
         for (int v = 0; v < C; ++v) tot[v] += gsum[gg][r][v];
     const size_t row = (size_t)B * kT + r;
     for (int v = 0; v < C; ++v) {
-        if (v < D)
+        if (inter)  // two sets interleaved per component: set v&1, component v>>1
+            ((v & 1) ? out1 : out0)[row * D + (v >> 1)] = tot[v];
+        else if (v < D)
             out0[row * D + v] = tot[v];
         else
             out1[row * (C - D) + (v - D)] = tot[v];
@@ -512,15 +585,16 @@ __global__ void __launch_bounds__(4 * kT) k_sym_reduce(const double* __restrict_
 }
 
 cudaError_t launch_sym_reduce(const double* ipart, const float* jpart, const int* it_lo, const int* it_hi, int nb,
-                              int64_t t0, int64_t t1, int C, int D, double* out0, double* out1, cudaStream_t s)
+                              int64_t t0, int64_t t1, int C, int D, int inter, double* out0, double* out1,
+                              cudaStream_t s)
 {
-    k_sym_reduce<<<nb, 4 * kT, 0, s>>>(ipart, jpart, it_lo, it_hi, nb, t0, t1, C, D, out0, out1);
+    k_sym_reduce<<<nb, 4 * kT, 0, s>>>(ipart, jpart, it_lo, it_hi, nb, t0, t1, C, D, inter, out0, out1);
     return cudaGetLastError();
 }
 
 // sum of rank partials in rank order (multi-GPU): parts[world][rows][C]
-__global__ void k_rank_sum(const double* __restrict__ parts, int world, int64_t rows, int C, int D, double* out0,
-                           double* out1)
+__global__ void k_rank_sum(const double* __restrict__ parts, int world, int64_t rows, int C, int D, int inter,
+                           double* out0, double* out1)
 {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= rows * C) return;
@@ -528,17 +602,19 @@ __global__ void k_rank_sum(const double* __restrict__ parts, int world, int64_t 
     const int v = (int)(idx % C);
     double s = 0.0;
     for (int g = 0; g < world; ++g) s += parts[(size_t)g * rows * C + idx];
-    if (v < D)
+    if (inter)
+        ((v & 1) ? out1 : out0)[row * D + (v >> 1)] = s;
+    else if (v < D)
         out0[row * D + v] = s;
     else
         out1[row * (C - D) + (v - D)] = s;
 }
 
-cudaError_t launch_rank_sum(const double* parts, int world, int64_t rows, int C, int D, double* out0, double* out1,
-                            cudaStream_t s)
+cudaError_t launch_rank_sum(const double* parts, int world, int64_t rows, int C, int D, int inter, double* out0,
+                            double* out1, cudaStream_t s)
 {
     const int64_t total = rows * C;
-    k_rank_sum<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(parts, world, rows, C, D, out0, out1);
+    k_rank_sum<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(parts, world, rows, C, D, inter, out0, out1);
     return cudaGetLastError();
 }
 
