@@ -88,6 +88,9 @@ typedef struct {
     int32_t strategy;     /* fdl_strategy                                                           */
     uint64_t seed;        /* roulette stream seed (FDL_STRAT_PROB)                                  */
     int32_t device;       /* CUDA device ordinal                                                    */
+    int32_t a_refresh;    /* L^W X^k for the PCG warm start is carried forward from the previous
+                             solve (L linear: A' = b - r_cg, A(Xt) = (1+w)A' - wA^k) and recomputed
+                             by a full L^W pass every a_refresh steps; 1 = every step; <= 0 -> 10 */
 } fdl_params;
 
 typedef struct {

@@ -128,6 +128,9 @@ struct fdl_ctx {
     double *diag = nullptr, *Xk = nullptr, *Xn = nullptr, *Xt = nullptr, *Rk = nullptr, *R1 = nullptr,
            *R2 = nullptr;
     double *cr = nullptr, *cz = nullptr, *cp = nullptr, *cy = nullptr;
+    double *Ak = nullptr, *An = nullptr, *At = nullptr;  // carried L^W X^k, L^W X^{k+1}, L^W Xt
+    bool a_valid = false;
+    int a_age = 0;  // steps since Ak was last computed by a full pass
     float *posf = nullptr, *pvec = nullptr;
     double *blk_max = nullptr, *blk_cg = nullptr;
     double* pin_slots = nullptr;
@@ -441,6 +444,7 @@ fdl_status eval_current(fdl_ctx* ctx)
 // Upload a full n*dim placement (original units): pin x_0 = 0, scale by 1/k.
 fdl_status upload_positions(fdl_ctx* ctx, const double* X)
 {
+    ctx->a_valid = false;
     std::vector<double> loc((size_t)ctx->n * ctx->dim);
     for (int i = 0; i < ctx->n; ++i)
         for (int q = 0; q < ctx->dim; ++q) {
@@ -655,6 +659,8 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     ctx->cap = std::isfinite(p.step) ? p.step / ctx->k : INFINITY;
     if (!(p.cg_rtol > 0)) ctx->p.cg_rtol = std::max(1e-2 * p.tol, 1e-9);
     if (p.cg_max_iter <= 0) ctx->p.cg_max_iter = std::min(10 * n, 10000);
+    if (p.a_refresh <= 0) ctx->p.a_refresh = 10;
+    if (std::isfinite(p.step)) ctx->p.a_refresh = 1;  // the cap makes Xt non-linear in X^{k+1}
     ctx->rng = p.seed;
 
     FDL_CUDA(cudaSetDevice(ctx->device));
@@ -712,6 +718,9 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     FDL_ALLOC(ctx->cz, vn);
     FDL_ALLOC(ctx->cp, vn);
     FDL_ALLOC(ctx->cy, vn);
+    FDL_ALLOC(ctx->Ak, vn);
+    FDL_ALLOC(ctx->An, vn);
+    FDL_ALLOC(ctx->At, vn);
     FDL_ALLOC(ctx->posf, (size_t)ctx->npad * 8);
     FDL_ALLOC(ctx->pvec, (size_t)ctx->npad * 4);
     FDL_ALLOC(ctx->blk_max, (size_t)ctx->nblk);
@@ -776,10 +785,18 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
     const int pq = ps_p2(dim), ps = ps_p1(dim, nsets);
     cudaStream_t s = ctx->stream;
     const int mstep = mark_begin(ctx, 0);
-    // ---- line 4: X^{k+1} = H(X^k): PCG on Eq. 5 (zero-mean gauge, R7), warm start X^k
+    // ---- line 4: X^{k+1} = H(X^k): PCG on Eq. 5 (zero-mean gauge, R7), warm start X^k.
+    // The warm-start residual needs L^W X^k: carried from the previous solve, or a full
+    // P2 pass every a_refresh steps (bounds the fp32 drift of the carried value).
+    const bool refresh = !ctx->a_valid || ctx->a_age + 1 >= ctx->p.a_refresh;
     FDL_LAUNCH(launch_cg_begin(ctx->Xk, ctx->Xn, ctx->pvec, n, 0, dim, pq, s));
-    FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->cy, nullptr, 0));
-    FDL_LAUNCH(launch_cg_init(ctx->cy, ctx->Rk, ctx->diag, ctx->cr, ctx->cz, ctx->cp, ctx->pvec, ctx->blk_cg, ctx->nblk,
+    if (refresh) {
+        FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->Ak, nullptr, 0));
+        ctx->a_age = 0;
+    } else {
+        ctx->a_age++;
+    }
+    FDL_LAUNCH(launch_cg_init(ctx->Ak, ctx->Rk, ctx->diag, ctx->cr, ctx->cz, ctx->cp, ctx->pvec, ctx->blk_cg, ctx->nblk,
                               n, dim, pq, s));
     FDL_LAUNCH(launch_cg_finalize(ctx->blk_cg, ctx->nblk, dim, 0, ctx->p.cg_rtol, ctx->sc, ctx->hs_dev, s));
     FDL_CUDA(cudaStreamSynchronize(s));
@@ -799,6 +816,8 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
         FDL_CUDA(cudaStreamSynchronize(s));
         ++cg;
     }
+    // carried L^W X^{k+1} and L^W Xt (before Rk is replaced by the select)
+    FDL_LAUNCH(launch_carry_a(ctx->Rk, ctx->cr, ctx->Ak, ctx->An, ctx->At, ctx->sc, n, dim, omega, s));
     // ---- pin x_0 = 0, then line 5: Xt = (1+w) X^{k+1} - w X^k (Eq. 10)
     FDL_LAUNCH(launch_get_pin(ctx->Xn, ctx->pin_slots, 0, dim, 1, s));
     FDL_LAUNCH(launch_combine(ctx->Xk, ctx->Xn, ctx->Xt, ctx->posf, ctx->blk_max, ctx->pin_slots, n, 0, dim, omega,
@@ -807,7 +826,8 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
     FDL_TRY(run_sym(ctx, kSymP1, nsets, ctx->posf, ctx->R1, ctx->R2, 0));
     // ---- lines 6-8: guard
     FDL_LAUNCH(launch_select(ctx->Xk, ctx->Rk, ctx->Xn, ctx->Xt, ctx->R1, ctx->R2, ctx->blk_max, n, dim, nsets,
-                             ctx->sc, s));
+                             ctx->sc, ctx->Ak, ctx->An, ctx->At, s));
+    ctx->a_valid = true;
     mark_end(ctx, mstep);
     FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, s));
     FDL_CUDA(cudaStreamSynchronize(s));
@@ -880,6 +900,7 @@ void fdl_params_default(fdl_params* p)
     p->strategy = FDL_STRAT_FIXED;
     p->seed = 1;
     p->device = 0;
+    p->a_refresh = 10;
 }
 
 const char* fdl_status_str(fdl_status s)

@@ -143,12 +143,40 @@ cudaError_t launch_get_pin(const double* x, double* slots, int rank, int dim, in
     return cudaGetLastError();
 }
 
+// Carried L^W X: the PCG recursion gives (L + sigma 1 1^T) d =
+// r0 - r_cg with d = x - x0 and r0 = Rk - Ak, so L x = Rk - r_cg - sigma (sum d) 1;
+// L is linear, so L Xt = (1 + w) L X^{k+1} - w L X^k.  (The pin x_0 = 0 is a
+// translation: L 1 = 0.)
+__global__ void k_carry_a(const double* __restrict__ Rk, const double* __restrict__ rcg,
+                          const double* __restrict__ Ak, double* An, double* At, const DevScalars* __restrict__ sc,
+                          int n, int dim, double omega)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int q = 0; q < dim; ++q) {
+        const size_t k = (size_t)i * dim + q;
+        const double an = Rk[k] - rcg[k] - sc->sigma * sc->Sd[q];
+        An[k] = an;
+        At[k] = (1.0 + omega) * an - omega * Ak[k];
+    }
+}
+
+cudaError_t launch_carry_a(const double* Rk, const double* rcg, const double* Ak, double* An, double* At,
+                           const DevScalars* sc, int n, int dim, double omega, cudaStream_t s)
+{
+    k_carry_a<<<(n + kRB - 1) / kRB, kRB, 0, s>>>(Rk, rcg, Ak, An, At, sc, n, dim, omega);
+    return cudaGetLastError();
+}
+
 // Guard of Algorithm 2 lines 6-8: accept Xt iff f(Xt) <= f(X^{k+1}) (ties
-// accept, raw comparison).  Copies the accepted placement and its R.
+// accept, raw comparison).  Copies the accepted placement, its R and (when
+// carried) its L^W X.
 __global__ void __launch_bounds__(kRB) k_select(double* Xk, double* Rk, const double* __restrict__ Xn,
                                                 const double* __restrict__ Xt, const double* __restrict__ R1,
                                                 const double* __restrict__ R2, const double* __restrict__ blk_max,
-                                                int nblk_loc, int nloc, int dim, int nsets, DevScalars* sc)
+                                                int nblk_loc, int nloc, int dim, int nsets, DevScalars* sc,
+                                                double* Ak, const double* __restrict__ An,
+                                                const double* __restrict__ At)
 {
     const double f0 = sc->f_set[0];
     const double f1 = nsets == 2 ? sc->f_set[1] : f0;
@@ -159,6 +187,7 @@ __global__ void __launch_bounds__(kRB) k_select(double* Xk, double* Rk, const do
             const size_t i = (size_t)lr * dim + q;
             Xk[i] = accept ? Xt[i] : Xn[i];
             Rk[i] = accept ? R2[i] : R1[i];
+            if (Ak) Ak[i] = accept ? At[i] : An[i];
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -176,10 +205,10 @@ __global__ void __launch_bounds__(kRB) k_select(double* Xk, double* Rk, const do
 
 cudaError_t launch_select(double* Xk, double* Rk, const double* Xn, const double* Xt, const double* R1,
                           const double* R2, const double* blk_max, int nloc, int dim, int nsets, DevScalars* sc,
-                          cudaStream_t s)
+                          double* Ak, const double* An, const double* At, cudaStream_t s)
 {
     const int nb = (nloc + kRB - 1) / kRB;
-    k_select<<<nb, kRB, 0, s>>>(Xk, Rk, Xn, Xt, R1, R2, blk_max, nb, nloc, dim, nsets, sc);
+    k_select<<<nb, kRB, 0, s>>>(Xk, Rk, Xn, Xt, R1, R2, blk_max, nb, nloc, dim, nsets, sc, Ak, An, At);
     return cudaGetLastError();
 }
 
@@ -389,6 +418,7 @@ __global__ void k_cg_finalize(const double* __restrict__ blk, int nblk, int dim,
             sc->rr[c] = sums[1][c];
             sc->bb[c] = sums[2][c];
             sc->S[c] = sums[3][c];
+            sc->Sd[c] = 0.0;
             const int act = sums[1][c] > rt2 * sums[2][c];
             sc->active[c] = act;
             any |= act;
@@ -402,6 +432,7 @@ __global__ void k_cg_finalize(const double* __restrict__ blk, int nblk, int dim,
         for (int c = 0; c < dim; ++c) {
             sc->pap[c] = sums[0][c];
             sc->alpha[c] = (sc->active[c] && sums[0][c] > 0.0) ? sc->rz[c] / sums[0][c] : 0.0;
+            sc->Sd[c] += sc->alpha[c] * sc->S[c];  // x += alpha p  =>  sum d += alpha sum p
         }
     } else {
         int any = 0;

@@ -279,3 +279,24 @@ def test_end_to_end_vs_oracle_trace(case):
     assert abs(fs[-1] - d["f_final"]) / d["f_final"] <= 1e-3, (fs[-1], d["f_final"])
     assert abs(it - d["iterations"]) <= max(1, math.ceil(0.02 * d["iterations"])), (it, d["iterations"])
     assert all(b <= a * (1 + 1e-9) for a, b in zip(fs, fs[1:]))
+
+
+def test_carried_lw_matches_full_refresh():
+    """The warm-start residual uses L^W X^k carried from the previous solve
+    (a_refresh = 10) instead of a full pass every step (a_refresh = 1): same
+    trajectory to the CG tolerance."""
+    runs = []
+    for refresh in (1, 10):
+        cfg = configs.CONFIGS["C2"]
+        g = configs.graph_for("C2")
+        X0 = configs.positions_for("C2", g.n, 1)
+        p = fdl.make_params(dim=2, k=cfg.k_for(g.n), omega=1.6, tol=cfg.tol, max_iter=cfg.max_iter,
+                            a_refresh=refresh)
+        L = fdl.Layout.from_graph(g, params=p, init_pos=X0)
+        r = L.run_until_converged()
+        st = L.get_stats()
+        runs.append((r.iterations, r.f_final, st.p2_launches, st.cg_iters))
+    (it1, f1, p21, cg1), (it10, f10, p210, cg10) = runs
+    assert abs(it1 - it10) <= 1
+    assert abs(f1 - f10) / f1 <= 1e-5
+    assert p210 < p21  # fewer full L^W passes
