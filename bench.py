@@ -265,7 +265,7 @@ def run_gpu(args):
     peak_tf = fp32_peak_tflops(peaks)
     p1_tf = p1_flops / (st.p1_ms * 1e-3) / 1e12 if st.p1_ms > 0 else 0.0
     # P2 streams the stored upper triangle: algorithmic bytes = 1 hop per unordered pair
-    hop_bytes = info.hop_bytes
+    hop_bytes = info.hop_bits / 8.0
     p2_gbs = (st.p2_pairs * hop_bytes) / (st.p2_ms * 1e-3) / 1e9 if st.p2_ms > 0 else 0.0
     p1_share = st.p1_ms / ms if ms > 0 else 0
     p2_share = st.p2_ms / ms if ms > 0 else 0
@@ -325,7 +325,7 @@ def run_gpu(args):
             "config": {"workload": f"{args.config}: BA n={n} m=3 |E|={g.num_edges}" if args.config == "C5"
                        else f"{args.config} n={n} |E|={g.num_edges}",
                        "dim": dim, "omega": cfg.omega, "k": k, "diameter": info.diameter,
-                       "hop_bytes": info.hop_bytes, "parallelism": f"triangle-tile shard x{world} (NCCL all-gather of partials)",
+                       "hop_bits": info.hop_bits, "parallelism": f"triangle-tile shard x{world} (NCCL all-gather of partials)",
                        "l2": "inputs larger than L2 (hop matrix %.1f GB per GPU)" % (info.hop_matrix_bytes / 1e9)},
             "iterations_per_sec": its_per_s,
             "pcg_iters_per_step": st.cg_iters / max(st.steps, 1),

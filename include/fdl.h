@@ -91,6 +91,9 @@ typedef struct {
     int32_t a_refresh;    /* L^W X^k for the PCG warm start is carried forward from the previous
                              solve (L linear: A' = b - r_cg, A(Xt) = (1+w)A' - wA^k) and recomputed
                              by a full L^W pass every a_refresh steps; 1 = every step; <= 0 -> 10 */
+    int32_t hop_bits;     /* minimum stored hop width: 0 = auto (narrowest that holds the diameter:
+                             4 bits if diam <= 15, 8 if <= 255, else 16), or 4, 8, 16. The decoded
+                             hop, hence every result, is the same for every width   */
 } fdl_params;
 
 typedef struct {
@@ -120,7 +123,7 @@ typedef struct {
 typedef struct {
     int32_t n, dim;
     int32_t diameter;      /* max hop count found by the BFS                     */
-    int32_t hop_bytes;     /* 1 (uint8) or 2 (uint16) per stored hop             */
+    int32_t hop_bits;      /* 4, 8 or 16 bits per stored hop                     */
     int32_t rank, world;
     int64_t tile0, tile1;  /* hop tiles stored by this context [tile0, tile1)   */
     int32_t iterations;    /* iterations run so far on this context              */

@@ -484,13 +484,16 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
     const int src_hi = (int)std::min<int64_t>(n, (Ihi + 1) * kT);
     const int64_t ntiles = ctx->t1 - ctx->t0;
 
-    // u8 when the diameter provably fits (diam <= 2 ecc0 <= 255); u16 when it
-    // provably does not (ecc0 > 255); otherwise try u8 and redo on overflow.
-    int hb = (2 * ecc0 <= 255) ? 1 : (ecc0 > 255 ? 2 : 1);
+    // Narrowest width whose range can hold the diameter (ecc0 <= diam <= 2 ecc0):
+    // the first width with max >= ecc0 is tried (a later attempt widens on
+    // overflow); hop_bits forces a minimum width.
+    int hb = 0;
+    const int min_hb = ctx->p.hop_bits >= 16 ? 2 : (ctx->p.hop_bits >= 8 ? 1 : 0);
+    while (hb < 2 && (hb < min_hb || ecc0 > hb_max_hop(hb))) ++hb;
     fdl_status st = FDL_OK;
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    for (int attempt = 0; attempt < 3; ++attempt) {
         ctx->hb = hb;
-        const size_t dbytes = (size_t)std::max<int64_t>(ntiles, 1) * kT * kT * hb;
+        const size_t dbytes = (size_t)std::max<int64_t>(ntiles, 1) * (size_t)tile_bytes(hb);
         if (ctx->D) {
             cudaFree(ctx->D);
             ctx->allocs.erase(std::find(ctx->allocs.begin(), ctx->allocs.end(), (void*)ctx->D));
@@ -509,7 +512,7 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
         ctx->device_bytes += dbytes;
         ctx->hop_bytes_total = dbytes;
         FDL_CUDA(cudaMemsetAsync(ctx->D, 0, dbytes, ctx->stream));
-        const int maxhop = hb == 1 ? 255 : 65535;
+        const int maxhop = hb_max_hop(hb);
         bool overflow = false;
         int diam = 0;
         for (int s0 = src_lo; s0 < src_hi && !overflow; s0 += 32 * kBFSWords) {
@@ -534,13 +537,14 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
         }
         if (!overflow) {
             ctx->diameter = diam;
+            if (hb == 0) FDL_LAUNCH(launch_nib_encode(ctx->D, dbytes, ctx->stream));
             break;
         }
         if (hb == 2) {
             st = set_err(ctx, FDL_E_DIAMETER, "hop count exceeds 65535");
             break;
         }
-        hb = 2;
+        ++hb;
     }
     cudaFree(d_rp);
     cudaFree(d_col);
@@ -901,6 +905,7 @@ void fdl_params_default(fdl_params* p)
     p->seed = 1;
     p->device = 0;
     p->a_refresh = 10;
+    p->hop_bits = 0;
 }
 
 const char* fdl_status_str(fdl_status s)
@@ -1175,7 +1180,7 @@ fdl_status fdl_get_info(fdl_ctx* ctx, fdl_ctx_info* info)
     r.n = ctx->n;
     r.dim = ctx->dim;
     r.diameter = ctx->diameter;
-    r.hop_bytes = ctx->hb;
+    r.hop_bits = ctx->hb ? 8 * ctx->hb : 4;
     r.tile0 = ctx->t0;
     r.tile1 = ctx->t1;
     r.rank = ctx->rank;

@@ -86,7 +86,6 @@ cudaError_t launch_ffma_bench(float* out, int iters, int blocks, int threads, cu
 // ------------------------------------------------------- symmetric (triangle) passes
 constexpr int kT = 128;            // tile edge: tiles (I, J), I <= J, of kT x kT pairs
 constexpr int kSeg = 16;           // tiles per work item (strip segment)
-constexpr int kSymStages = 3;      // TMA ring depth of k_sym
 enum { kSymP1 = 0, kSymP2 = 1, kSymDiag = 2 };
 
 // triangle index of tile (I, J), I <= J, over nb blocks (row-major upper triangle)
@@ -95,13 +94,28 @@ __host__ __device__ inline int64_t tri_index(int64_t I, int64_t J, int64_t nb)
     return I * nb - I * (I - 1) / 2 + (J - I);
 }
 
-// byte offset of entry (row rl, col cl) inside local tile lt: thread (rl/8, cl/8)
-// of a 16 x 16 grid owns an 8 x 8 sub-block stored as 16-byte chunks
-// interleaved across the 256 threads.
+// Hop width code `hb`: 0 = 4-bit (diameter <= 15), 1 = uint8, 2 = uint16.
+__host__ __device__ constexpr int64_t tile_bytes(int hb) { return hb ? (int64_t)kT * kT * hb : (int64_t)kT * kT / 2; }
+constexpr int hb_max_hop(int hb) { return hb == 0 ? 15 : (hb == 1 ? 255 : 65535); }
+
+// 4-bit tiles store the hops of rows (2p, 2p+1) of one column in one byte.  The
+// byte is a bijective encoding of the pair, chosen so that the shared-memory
+// LUT the kernels index with it (8-byte entries) spreads the common hop pairs
+// over the banks: low nibble = (lo + 4 hi) mod 16, high nibble = hi.
+__host__ __device__ inline uint32_t nib_encode(uint32_t lo, uint32_t hi) { return ((lo + 4u * hi) & 15u) | (hi << 4); }
+__host__ __device__ inline uint32_t nib_decode_lo(uint32_t b) { return ((b & 15u) - 4u * (b >> 4)) & 15u; }
+__host__ __device__ inline uint32_t nib_decode_hi(uint32_t b) { return b >> 4; }
+
+// byte offset of entry (row rl, col cl) inside local tile lt: thread (ty, tx) =
+// (rl/8, cl/8) of a 16 x 16 grid, linear index tx*16 + ty (= k_sym's threadIdx),
+// owns an 8 x 8 sub-block stored as 16-byte chunks interleaved across the 256
+// threads.  4-bit: chunk = 4 columns x 4 row pairs,
+// the entry is nibble (rl & 1) of the returned byte (before nib_encode).
 __host__ __device__ inline size_t sym_offset(int64_t lt, int rl, int cl, int hb)
 {
-    const int tid = (rl >> 3) * 16 + (cl >> 3), r = rl & 7, c = cl & 7;
-    const size_t base = (size_t)lt * kT * kT * hb;
+    const int tid = (cl >> 3) * 16 + (rl >> 3), r = rl & 7, c = cl & 7;
+    const size_t base = (size_t)lt * (size_t)tile_bytes(hb);
+    if (hb == 0) return base + ((size_t)(c >> 2) * 256 + tid) * 16 + (c & 3) * 4 + (r >> 1);
     if (hb == 1) return base + ((size_t)(c >> 1) * 256 + tid) * 16 + (c & 1) * 8 + r;
     return base + ((size_t)c * 256 + tid) * 16 + r * 2;
 }
@@ -128,6 +142,8 @@ cudaError_t launch_sym_stress(const double* spart, int nitems, int nsets, double
 cudaError_t launch_bfs_level_sym(const int64_t* row_ptr, const int32_t* col, const uint32_t* fin, uint32_t* fout,
                                  uint32_t* visited, uint8_t* D, int n, int s0, int nsrc, int level, int nb, int64_t t0,
                                  int64_t t1, int hb, unsigned int* anynew, cudaStream_t s);
+// 4-bit tiles: raw (lo | hi << 4) bytes written by the BFS -> nib_encode bytes
+cudaError_t launch_nib_encode(uint8_t* D, size_t bytes, cudaStream_t s);
 cudaError_t launch_hop_rows(const uint8_t* D, int hb, int nb, int64_t t0, int64_t t1, const int* rows, int nrows,
                             int n, uint16_t* out, int* missing, cudaStream_t s);
 // sum of rank partials (world x len doubles, rank order) into out0/out1 split at D of C

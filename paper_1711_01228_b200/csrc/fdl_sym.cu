@@ -22,6 +22,7 @@
 // rows through padded shared memory after every tile.  Outputs are fp32 tile
 // partials (j side, per tile) and fp64 segment partials (i side, stress),
 // summed per row in a fixed order by k_sym_reduce: deterministic, no atomics.
+#include <algorithm>
 #include <cfloat>
 #include <cstdint>
 
@@ -139,29 +140,45 @@ __host__ __device__ constexpr int sym_ps()
                           : (MODE == kSymP2 ? (DIM == 2 ? 2 : 4) : 4);
 }
 
-template <int MODE>
-__host__ __device__ constexpr int sym_stages()  // P1 is compute-bound: double buffering suffices
+template <int MODE, int HB>
+__host__ __device__ constexpr int sym_stages()  // TMA ring depth (bounded by 2 CTAs per SM for the 2-D passes)
 {
-    return MODE == kSymP1 ? 2 : kSymStages;
+    return MODE == kSymP1 ? (HB == 2 ? 2 : 3) : (HB == 2 ? 3 : 4);
 }
 
 template <int MODE, int DIM, int NSETS, int HB>
 __host__ __device__ constexpr int sym_stage_bytes()
 {
-    return kT * kT * HB + kT * sym_ps<MODE, DIM, NSETS>() * 4;
+    return (int)tile_bytes(HB) + kT * sym_ps<MODE, DIM, NSETS>() * 4;
 }
 
 template <int MODE, int DIM, int NSETS>
-__host__ __device__ constexpr int sym_red_pitch()  // floats per (ty, tx) cell in the reduction buffer
+__host__ __device__ constexpr int sym_red_pitch()  // floats per (ty, tx) cell of the i-side reduction
 {
     return 8 * sym_ncomp<MODE, DIM, NSETS>() + 4;
+}
+
+// floats per lane row of a warp's j-side buffer: 9C keeps the 16 rows of a
+// half-warp on distinct banks for the C-wide vector stores
+template <int MODE, int DIM, int NSETS>
+__host__ __device__ constexpr int sym_jpitch()
+{
+    return 9 * sym_ncomp<MODE, DIM, NSETS>();
+}
+
+template <int MODE, int DIM, int NSETS>
+__host__ __device__ constexpr size_t sym_red_floats()  // j-side warp buffers and the i-side buffer share it
+{
+    return (size_t)8 * 2 * (16 * sym_jpitch<MODE, DIM, NSETS>() + 16) > (size_t)256 * sym_red_pitch<MODE, DIM, NSETS>()
+               ? (size_t)8 * 2 * (16 * sym_jpitch<MODE, DIM, NSETS>() + 16)
+               : (size_t)256 * sym_red_pitch<MODE, DIM, NSETS>();
 }
 
 template <int MODE, int DIM, int NSETS, int HB>
 __host__ __device__ constexpr size_t sym_smem_bytes()
 {
-    return (size_t)sym_stages<MODE>() * sym_stage_bytes<MODE, DIM, NSETS, HB>() +
-           (size_t)2 * 256 * sym_red_pitch<MODE, DIM, NSETS>() * 4;  // double-buffered reduction
+    return (size_t)sym_stages<MODE, HB>() * sym_stage_bytes<MODE, DIM, NSETS, HB>() +
+           sym_red_floats<MODE, DIM, NSETS>() * 4;
 }
 
 // ------------------------------------------------------------ packed FP32x2
@@ -289,18 +306,62 @@ __device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float
 }
 
 template <int MODE, int DIM, int NSETS, int HB, bool SAFE>
-__device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, const float* lut, uint32_t magic, int ty,
-                                         int tx, bool diag,
+__device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, const float* lut, const float2* lut2,
+                                         uint32_t magic, int ty, int tx, bool diag,
                                          const float (&xi)[8][NSETS * DIM], float (&ai)[8][sym_ncomp<MODE, DIM, NSETS>()],
-                                         float* red, float (&sf)[NSETS])
+                                         float* myred, float (&sf)[NSETS])
 {
     constexpr int C = sym_ncomp<MODE, DIM, NSETS>();
     constexpr int PS = sym_ps<MODE, DIM, NSETS>();
-    constexpr int NCH = 4 * HB;  // 16-byte chunks per thread
-    constexpr int PITCH = sym_red_pitch<MODE, DIM, NSETS>();
-    constexpr int CPC = 2 / HB;  // columns per chunk
-    const int tid = ty * 16 + tx;
-    float* myred = red + (size_t)tid * PITCH;
+    constexpr int NCH = HB ? 4 * HB : 2;  // 16-byte chunks per thread
+    constexpr int CPC = HB ? 2 / HB : 4;  // columns per chunk
+    const int tid = tx * 16 + ty;  // chunk owner index of the tile layout (sym_offset)
+    if (HB == 0) {
+        // 4-bit tiles: one byte = hops of rows (2p, 2p+1) of a column, one 8-byte
+        // LUT entry per byte gives both decoded values (h^2 for P1/DIAG, w' = 1/h^2
+        // for P2): 2 ALU ops + 1 LDS.64 per two pairs, no FP32-pipe decode work.
+#pragma unroll 1
+        for (int kc = 0; kc < NCH; ++kc) {
+            const uint4 ch = *reinterpret_cast<const uint4*>(sD + ((size_t)kc * 256 + tid) * 16);
+#pragma unroll
+            for (int cc = 0; cc < CPC; ++cc) {
+                const int c = kc * CPC + cc;
+                const int jl = tx * 8 + c;
+                const int js = c * 16 + tx;
+                float xj[PS];
+                if (PS == 2) {
+                    const float2 t = *reinterpret_cast<const float2*>(sP + js * PS);
+                    xj[0] = t.x; xj[1] = t.y;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < PS / 4; ++q) {
+                        const float4 t = *reinterpret_cast<const float4*>(sP + js * PS + 4 * q);
+                        xj[4 * q] = t.x; xj[4 * q + 1] = t.y; xj[4 * q + 2] = t.z; xj[4 * q + 3] = t.w;
+                    }
+                }
+                float aj[C];
+#pragma unroll
+                for (int v = 0; v < C; ++v) aj[v] = 0.0f;
+                const uint32_t w = word_of(ch, cc);
+#pragma unroll
+                for (int rp = 0; rp < 4; ++rp) {
+                    const uint32_t off = rp == 0 ? ((w << 3) & 0x7f8u) : ((w >> (8 * rp - 3)) & 0x7f8u);
+                    const float2 e = *reinterpret_cast<const float2*>(reinterpret_cast<const char*>(lut2) + off);
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int r = 2 * rp + hh;
+                        const float v = hh ? e.y : e.x;
+                        bool valid = true;
+                        if (SAFE) valid = (v > 0.0f) && (!diag || (ty * 8 + r < jl));
+                        sym_pair<MODE, DIM, NSETS, SAFE>(&xi[r][0], xj, v, v, valid, &ai[r][0], &aj[0], sf);
+                    }
+                }
+#pragma unroll
+                for (int v = 0; v < C; ++v) myred[c * C + v] = aj[v];
+            }
+        }
+        return;
+    }
 #pragma unroll 1
     for (int kc = 0; kc < NCH; ++kc) {
         const uint4 ch = *reinterpret_cast<const uint4*>(sD + ((size_t)kc * 256 + tid) * 16);
@@ -346,53 +407,77 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
     }
 }
 
-// Reduction of the per-thread j-side partials of one tile over the 16 thread
-// rows (fixed order, fp64) and store as fp32 jpart[tile][col][C].  The
-// j-side sign: P1 and P2 accumulate +term for row i and -term for row j
-// (antisymmetric); DIAG is symmetric.
+// j-side flush of one tile by one warp (no CTA barrier): the warp's lanes are
+// (h = tx & 1, ty = 0..15); lane (h, ty) wrote its 8 x C column partials to
+// row ty of half h of the warp buffer.  Output e = h * 8C + c * C + v (column
+// tx * 8 + c, component v) is the fixed-order tree sum over the 16 rows, stored
+// as fp32 jpart[tile][col][C]; the warp's outputs are one contiguous run of 16C
+// floats.  The j-side sign: P1 and P2 accumulate +term for row i and -term for
+// row j (antisymmetric); DIAG is symmetric.
 template <int MODE, int DIM, int NSETS>
-__device__ __forceinline__ void sym_flush_j(const float* red, float* jpart_tile, int tid)
+__device__ __forceinline__ void sym_flush_warp(const float* wbuf, float* jpart_warp, int lane)
 {
     constexpr int C = sym_ncomp<MODE, DIM, NSETS>();
-    constexpr int PITCH = sym_red_pitch<MODE, DIM, NSETS>();
+    constexpr int P = sym_jpitch<MODE, DIM, NSETS>();
     constexpr float SIGN = MODE == kSymDiag ? 1.0f : -1.0f;
-    for (int e = tid; e < kT * C; e += 256) {
-        const int tx = e / (8 * C), rem = e % (8 * C);  // rem = c*C + v
-        float s = 0.0f;  // <= 16 partials of <= 8 fp32 terms: a 128-term fp32 tile sum
+    __syncwarp();
 #pragma unroll
-        for (int ty = 0; ty < 16; ++ty) s += red[(size_t)(ty * 16 + tx) * PITCH + rem];
-        jpart_tile[tx * 8 * C + rem] = SIGN * s;  // col = tx*8 + c, comp v
+    for (int e0 = 0; e0 < 16 * C; e0 += 32) {
+        const int e = e0 + lane;
+        if (16 * C % 32 == 0 || e < 16 * C) {
+            const int h = e / (8 * C), o = e % (8 * C);
+            const float* src = wbuf + h * (16 * P + 16) + o;
+            float v[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = src[r * P];
+#pragma unroll
+            for (int w = 1; w < 16; w *= 2)
+#pragma unroll
+                for (int r = 0; r < 16; r += 2 * w) v[r] += v[r + w];
+            jpart_warp[e] = SIGN * v[0];
+        }
     }
+    __syncwarp();  // the buffer is rewritten by the next tile
 }
 
 template <int MODE, int DIM, int NSETS, int HB>
-__global__ void __launch_bounds__(256, (MODE == kSymP1 && DIM == 2) ? 2 : 1) k_sym(const SymArgs a)
+__global__ void __launch_bounds__(256, (DIM == 2 || MODE != kSymP1) ? 2 : 1) k_sym(const SymArgs a)
 {
     constexpr int C = sym_ncomp<MODE, DIM, NSETS>();
     constexpr int PS = sym_ps<MODE, DIM, NSETS>();
     constexpr int STAGE = sym_stage_bytes<MODE, DIM, NSETS, HB>();
-    constexpr int DT = kT * kT * HB;
+    constexpr int DT = (int)tile_bytes(HB);
     constexpr int PITCH = sym_red_pitch<MODE, DIM, NSETS>();
-    constexpr int NST = sym_stages<MODE>();
+    constexpr int JP = sym_jpitch<MODE, DIM, NSETS>();
+    constexpr int NST = sym_stages<MODE, HB>();
+    constexpr int NW = 8;  // warps
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t full[NST];
+    __shared__ int drained[NST];  // warps done with the stage's current tile
+    __shared__ int prod[2];       // producer cursor {item, tile in item}
     __shared__ double sred[8][NSETS > 0 ? NSETS : 1];
     __shared__ float lut[256];
-    float* red0 = reinterpret_cast<float*>(smem + (size_t)NST * STAGE);
-    float* red1 = red0 + 256 * PITCH;
+    __shared__ float2 lut2[HB == 0 ? 256 : 1];
+    float* red = reinterpret_cast<float*>(smem + (size_t)NST * STAGE);
 
-    const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+    // Thread (ty, tx) owns rows ty*8.. and columns tx*8.. of a tile; a warp holds
+    // two thread columns (tx = 2w, 2w+1) x all 16 thread rows, so the j-side sum
+    // over ty stays inside the warp.
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int ty = lane & 15, tx = tid >> 4;
     if ((int)blockIdx.x >= a.nitems) return;
     lut[tid] = tid ? 1.0f / (float)(tid * tid) : 0.0f;  // w'_h = fp32(1/h^2), correctly rounded
-    if (tid == 0) {
-        for (int s = 0; s < NST; ++s) mbar_init(&full[s], 1);
-        fence_mbar_init();
+    if (HB == 0) {  // entry of encoded byte tid: (row 2p, row 2p+1) -> h^2 (P1, DIAG) or w' (P2)
+        const int lo = (int)nib_decode_lo((uint32_t)tid), hi = (int)nib_decode_hi((uint32_t)tid);
+        lut2[tid] = MODE == kSymP2 ? make_float2(lo ? 1.0f / (float)(lo * lo) : 0.0f,
+                                                 hi ? 1.0f / (float)(hi * hi) : 0.0f)
+                                   : make_float2((float)(lo * lo), (float)(hi * hi));
     }
-    __syncthreads();
-
-    // producer: tiles of this CTA's items, in order
-    int p_item = blockIdx.x, p_t = 0;
+    // producer: the next tile of this CTA's items (cursor in shared memory; it is
+    // advanced by whichever warp frees a stage last, see below)
     auto issue = [&](int stage) {
+        int p_item = prod[0], p_t = prod[1];
+        if (p_item >= a.nitems) return;
         const int4 it = a.items[p_item];  // {I, J0, ntiles, first local tile}
         const int J = it.y + p_t;
         const int64_t lt = (int64_t)it.w + p_t;
@@ -405,13 +490,25 @@ __global__ void __launch_bounds__(256, (MODE == kSymP1 && DIM == 2) ? 2 : 1) k_s
             p_t = 0;
             p_item += gridDim.x;
         }
+        prod[0] = p_item;
+        prod[1] = p_t;
     };
-    if (tid == 0)
-        for (int s = 0; s < NST - 1 && p_item < a.nitems; ++s) issue(s);
+    if (tid == 0) {
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&full[s], 1);
+            drained[s] = 0;
+        }
+        fence_mbar_init();
+        prod[0] = blockIdx.x;
+        prod[1] = 0;
+        for (int s = 0; s < NST; ++s) issue(s);
+    }
+    __syncthreads();
 
+    float* wrow = red + wid * 2 * (16 * JP + 16) + (tx & 1) * (16 * JP + 16) + ty * JP;  // this lane's j row
+    const float* wbuf = red + wid * 2 * (16 * JP + 16);
     int stage = 0;
     uint32_t phase = 0;
-    int tcount = 0;  // tiles done by this CTA: selects the reduction buffer
     for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
         const int4 it = a.items[item];
         const int I = it.x;
@@ -429,9 +526,6 @@ __global__ void __launch_bounds__(256, (MODE == kSymP1 && DIM == 2) ? 2 : 1) k_s
 #pragma unroll
         for (int s = 0; s < NSETS; ++s) s64[s] = 0.0;
         for (int t = 0; t < it.z; ++t) {
-            // stage (stage-1) was consumed before the previous tile's barrier
-            if (tid == 0 && p_item < a.nitems) issue((stage + NST - 1) % NST);
-            float* red = (tcount & 1) ? red1 : red0;
             const int J = it.y + t;
             const bool diag = (J == I);
             const bool safe = diag || (int64_t)(J + 1) * kT > a.n || (int64_t)(I + 1) * kT > a.n;
@@ -442,25 +536,29 @@ __global__ void __launch_bounds__(256, (MODE == kSymP1 && DIM == 2) ? 2 : 1) k_s
 #pragma unroll
             for (int s = 0; s < NSETS; ++s) sf[s] = 0.0f;
             if (safe)
-                sym_tile<MODE, DIM, NSETS, HB, true>(sD, sP, lut, a.magic, ty, tx, diag, xi, ai, red, sf);
+                sym_tile<MODE, DIM, NSETS, HB, true>(sD, sP, lut, lut2, a.magic, ty, tx, diag, xi, ai, wrow, sf);
             else
-                sym_tile<MODE, DIM, NSETS, HB, false>(sD, sP, lut, a.magic, ty, tx, diag, xi, ai, red, sf);
+                sym_tile<MODE, DIM, NSETS, HB, false>(sD, sP, lut, lut2, a.magic, ty, tx, diag, xi, ai, wrow, sf);
 #pragma unroll
             for (int s = 0; s < NSETS; ++s) s64[s] += (double)sf[s];
-            // One barrier per tile: red[tcount&1] complete, stage consumed, and every
-            // thread finished flushing the other buffer (previous tile) before arriving.
-            __syncthreads();
-            sym_flush_j<MODE, DIM, NSETS>(red, a.jpart + ((size_t)it.w + t) * kT * C, tid);
-            ++tcount;
+            // stage consumed by this warp; the last of the 8 warps refills it
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                if (atomicAdd(&drained[stage], 1) == NW - 1) {
+                    __threadfence_block();
+                    drained[stage] = 0;
+                    issue(stage);
+                }
+            }
+            sym_flush_warp<MODE, DIM, NSETS>(wbuf, a.jpart + ((size_t)it.w + t) * kT * C + wid * 16 * C, lane);
             if (++stage == NST) {
                 stage = 0;
                 phase ^= 1u;
             }
         }
-        // i-side: reduce over the 16 thread columns (fixed order, fp64), in the
-        // buffer the next tile would write (its last reader finished before the
-        // last tile's barrier)
-        float* red = (tcount & 1) ? red1 : red0;
+        // i-side: reduce over the 16 thread columns (fixed order, fp64)
+        __syncthreads();  // every warp finished its last j flush (the buffer is shared below)
         float* myred = red + (size_t)(tx * 16 + ty) * PITCH;  // [tx][ty] layout
 #pragma unroll
         for (int r = 0; r < 8; ++r)
@@ -481,7 +579,7 @@ __global__ void __launch_bounds__(256, (MODE == kSymP1 && DIM == 2) ? 2 : 1) k_s
                 double v = s64[s];
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                if ((tid & 31) == 0) sred[tid >> 5][s] = v;
+                if (lane == 0) sred[wid][s] = v;
             }
         }
         __syncthreads();
@@ -512,7 +610,7 @@ static cudaError_t launch_sym_t(const SymArgs& a, int grid, cudaStream_t s)
 
 #define FDL_SYM_CASE(M_, D_, S_, H_) \
     if (mode == M_ && dim == D_ && nsets == S_ && hb == H_) return launch_sym_t<M_, D_, S_, H_>(a, grid, s);
-#define FDL_SYM_ALLHB(M_, D_, S_) FDL_SYM_CASE(M_, D_, S_, 1) FDL_SYM_CASE(M_, D_, S_, 2)
+#define FDL_SYM_ALLHB(M_, D_, S_) FDL_SYM_CASE(M_, D_, S_, 0) FDL_SYM_CASE(M_, D_, S_, 1) FDL_SYM_CASE(M_, D_, S_, 2)
 
 cudaError_t launch_sym(const SymArgs& a, int mode, int dim, int nsets, int hb, int grid, cudaStream_t s)
 {
@@ -536,11 +634,10 @@ static int sym_occ_t()
     if (mode == M_ && dim == D_ && nsets == S_ && hb == H_) return sym_occ_t<M_, D_, S_, H_>();
 int sym_max_ctas(int mode, int dim, int nsets, int hb)
 {
-    FDL_SYM_OCC(kSymP1, 2, 1, 1) FDL_SYM_OCC(kSymP1, 2, 2, 1) FDL_SYM_OCC(kSymP1, 3, 1, 1) FDL_SYM_OCC(kSymP1, 3, 2, 1)
-    FDL_SYM_OCC(kSymP1, 2, 1, 2) FDL_SYM_OCC(kSymP1, 2, 2, 2) FDL_SYM_OCC(kSymP1, 3, 1, 2) FDL_SYM_OCC(kSymP1, 3, 2, 2)
-    FDL_SYM_OCC(kSymP2, 2, 1, 1) FDL_SYM_OCC(kSymP2, 3, 1, 1) FDL_SYM_OCC(kSymP2, 2, 1, 2) FDL_SYM_OCC(kSymP2, 3, 1, 2)
-    FDL_SYM_OCC(kSymDiag, 2, 1, 1) FDL_SYM_OCC(kSymDiag, 3, 1, 1) FDL_SYM_OCC(kSymDiag, 2, 1, 2)
-    FDL_SYM_OCC(kSymDiag, 3, 1, 2)
+#define FDL_SYM_OCC3(M_, D_, S_) FDL_SYM_OCC(M_, D_, S_, 0) FDL_SYM_OCC(M_, D_, S_, 1) FDL_SYM_OCC(M_, D_, S_, 2)
+    FDL_SYM_OCC3(kSymP1, 2, 1) FDL_SYM_OCC3(kSymP1, 2, 2) FDL_SYM_OCC3(kSymP1, 3, 1) FDL_SYM_OCC3(kSymP1, 3, 2)
+    FDL_SYM_OCC3(kSymP2, 2, 1) FDL_SYM_OCC3(kSymP2, 3, 1)
+    FDL_SYM_OCC3(kSymDiag, 2, 1) FDL_SYM_OCC3(kSymDiag, 3, 1)
     return 1;
 }
 
@@ -685,7 +782,10 @@ __global__ void k_hop_rows(const uint8_t* __restrict__ D, int hb, int nb, int64_
         return;
     }
     const size_t off = sym_offset(t - t0, a % kT, b % kT, hb);
-    out[idx] = hb == 1 ? D[off] : (uint16_t)(D[off] | (D[off + 1] << 8));
+    if (hb == 0)
+        out[idx] = (uint16_t)((a & 1) ? nib_decode_hi(D[off]) : nib_decode_lo(D[off]));
+    else
+        out[idx] = hb == 1 ? D[off] : (uint16_t)(D[off] | (D[off + 1] << 8));
 }
 
 cudaError_t launch_hop_rows(const uint8_t* D, int hb, int nb, int64_t t0, int64_t t1, const int* rows, int nrows,
@@ -767,8 +867,15 @@ __global__ void __launch_bounds__(256) k_bfs_level_sym(const int64_t* __restrict
         if (I > J) continue;
         const int64_t t = tri_index(I, J, nb);
         if (t < t0 || t >= t1) continue;
-        D[sym_offset(t - t0, rl, cl, HB)] = (uint8_t)level;
-        if (HB == 2) D[sym_offset(t - t0, rl, cl, HB) + 1] = (uint8_t)(level >> 8);
+        if (HB == 0) {
+            // raw nibble (row parity); both nibbles of a byte belong to sources
+            // s, s^1 = bits of this lane's word, so no other thread writes the byte
+            uint8_t* p = D + sym_offset(t - t0, rl, cl, 0);
+            *p = (uint8_t)(*p | (level << (4 * (rl & 1))));
+        } else {
+            D[sym_offset(t - t0, rl, cl, HB)] = (uint8_t)level;
+            if (HB == 2) D[sym_offset(t - t0, rl, cl, HB) + 1] = (uint8_t)(level >> 8);
+        }
     }
 }
 
@@ -778,12 +885,35 @@ cudaError_t launch_bfs_level_sym(const int64_t* row_ptr, const int32_t* col, con
 {
     const int64_t threads = (int64_t)n * 32;
     const unsigned grid = (unsigned)((threads + 255) / 256);
-    if (hb == 1)
+    if (hb == 0)
+        k_bfs_level_sym<0><<<grid, 256, 0, s>>>(row_ptr, col, fin, fout, visited, D, n, s0, nsrc, level, nb, t0, t1,
+                                                anynew);
+    else if (hb == 1)
         k_bfs_level_sym<1><<<grid, 256, 0, s>>>(row_ptr, col, fin, fout, visited, D, n, s0, nsrc, level, nb, t0, t1,
                                                 anynew);
     else
         k_bfs_level_sym<2><<<grid, 256, 0, s>>>(row_ptr, col, fin, fout, visited, D, n, s0, nsrc, level, nb, t0, t1,
                                                 anynew);
+    return cudaGetLastError();
+}
+
+// raw (lo | hi << 4) -> nib_encode, four bytes per 32-bit word at once (no
+// carries cross a byte: lo + 4 hi <= 75)
+__global__ void k_nib_encode(uint32_t* __restrict__ D, size_t words)
+{
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t w = D[i];
+        const uint32_t lo = w & 0x0F0F0F0Fu, hi = (w >> 4) & 0x0F0F0F0Fu;
+        D[i] = ((lo + (hi << 2)) & 0x0F0F0F0Fu) | (hi << 4);
+    }
+}
+
+cudaError_t launch_nib_encode(uint8_t* D, size_t bytes, cudaStream_t s)
+{
+    const size_t words = bytes / 4;  // tiles are 8 KB: always whole words
+    if (words == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)std::min<size_t>((words + 255) / 256, 148 * 16);
+    k_nib_encode<<<grid, 256, 0, s>>>(reinterpret_cast<uint32_t*>(D), words);
     return cudaGetLastError();
 }
 

@@ -47,7 +47,7 @@ class Params(ctypes.Structure):
         ("omega", ctypes.c_double), ("step", ctypes.c_double), ("tol", ctypes.c_double),
         ("max_iter", ctypes.c_int32), ("weight_exp", ctypes.c_double), ("cg_rtol", ctypes.c_double),
         ("cg_max_iter", ctypes.c_int32), ("strategy", ctypes.c_int32), ("seed", ctypes.c_uint64),
-        ("device", ctypes.c_int32), ("a_refresh", ctypes.c_int32),
+        ("device", ctypes.c_int32), ("a_refresh", ctypes.c_int32), ("hop_bits", ctypes.c_int32),
     ]
 
 
@@ -73,7 +73,7 @@ class RunInfo(ctypes.Structure):
 class CtxInfo(ctypes.Structure):
     _fields_ = [
         ("n", ctypes.c_int32), ("dim", ctypes.c_int32), ("diameter", ctypes.c_int32),
-        ("hop_bytes", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+        ("hop_bits", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
         ("tile0", ctypes.c_int64), ("tile1", ctypes.c_int64), ("iterations", ctypes.c_int32),
         ("k", ctypes.c_double), ("f", ctypes.c_double), ("hop_matrix_bytes", ctypes.c_uint64),
         ("local_pairs", ctypes.c_uint64), ("device_bytes", ctypes.c_uint64), ("setup_ms", ctypes.c_double),
@@ -144,11 +144,12 @@ def params_default() -> Params:
 
 
 def make_params(dim=2, k=0.0, omega=1.5, step=math.inf, tol=1e-4, max_iter=500, cg_rtol=0.0,
-                cg_max_iter=0, strategy=STRAT_FIXED, seed=1, device=0, a_refresh=0) -> Params:
+                cg_max_iter=0, strategy=STRAT_FIXED, seed=1, device=0, a_refresh=0, hop_bits=0) -> Params:
     p = params_default()
     p.dim, p.k, p.omega, p.step, p.tol, p.max_iter = dim, k, omega, step, tol, max_iter
     p.cg_rtol, p.cg_max_iter, p.strategy, p.seed, p.device = cg_rtol, cg_max_iter, strategy, seed, device
     p.a_refresh = a_refresh
+    p.hop_bits = hop_bits
     return p
 
 

@@ -62,7 +62,7 @@ def test_hops_bit_exact_full(name):
     got = L.get_hop_rows(0, g.n)
     assert np.array_equal(got, ref)
     assert L.info.diameter == int(ref.max())
-    assert L.info.hop_bytes == 1
+    assert L.info.hop_bits == (4 if ref.max() <= 15 else 8)
 
 
 @pytest.mark.parametrize("name", ["C4", "C5"])
@@ -72,7 +72,7 @@ def test_hops_bit_exact_sampled(name):
     ref = core.hop_rows(g, rows)
     for r, want in zip(rows, ref):
         assert np.array_equal(L.get_hop_rows(int(r), 1)[0], want), r
-    assert L.info.hop_bytes == (2 if name == "C4" else 1)
+    assert L.info.hop_bits == {"C4": 16, "C5": 4}[name]
 
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
@@ -300,3 +300,34 @@ def test_carried_lw_matches_full_refresh():
     assert abs(it1 - it10) <= 1
     assert abs(f1 - f10) / f1 <= 1e-5
     assert p210 < p21  # fewer full L^W passes
+
+
+@pytest.mark.parametrize("name,dim", [("C3", 2), ("C3", 3), ("C1", 2)])
+def test_hop_width_invariance(name, dim):
+    """The stored hop width (4/8/16 bits) changes only the encoding:
+    the decoded hops, h^2 and the correctly rounded w' = 1/h^2 are identical,
+    so R, A, f and one step are bitwise equal for 4 and 8 bits; 16 bits uses
+    the MUFU reciprocal in P2 (A within 1e-6)."""
+    cfg = configs.CONFIGS[name]
+    g = configs.graph_for(name)
+    X0 = configs.positions_for(name, g.n, 1)
+    if dim == 3:
+        X0 = np.concatenate([X0, configs.positions_for(name, g.n, 2)[:, :1]], axis=1)
+    out = {}
+    for bits in (4, 8, 16):
+        p = fdl.make_params(dim=dim, k=cfg.k_for(g.n), omega=1.5, tol=cfg.tol, max_iter=cfg.max_iter,
+                            hop_bits=bits)
+        with fdl.Layout.from_graph(g, params=p, init_pos=X0) as L:
+            got = L.info.hop_bits
+            assert got == max(bits, 4 if L.info.diameter <= 15 else (8 if L.info.diameter <= 255 else 16))
+            R, A, f = L.eval_forces()
+            info = L.step()
+            out[got] = (R, A, f, L.get_positions(), info.f_after)
+    widths = sorted(out)
+    R0, A0, f0, X1, fa = out[widths[-1]]
+    for w in widths:
+        R, A, f, X, fw = out[w]
+        assert np.array_equal(R, R0) and f == f0
+        assert relL2(A, A0) <= 1e-6
+    if 4 in out and 8 in out:
+        assert all(np.array_equal(a, b) for a, b in zip(out[4][:4], out[8][:4])) and out[4][4] == out[8][4]
