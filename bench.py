@@ -217,7 +217,8 @@ def run_gpu(args):
     n = g.n
     k = cfg.k_for(n)
     X0 = configs.positions_for(args.config, n, args.seed)
-    p = fdl.make_params(dim=cfg.dim, k=k, omega=cfg.omega, tol=cfg.tol, max_iter=100000, device=local_rank)
+    p = fdl.make_params(dim=cfg.dim, k=k, omega=cfg.omega, tol=cfg.tol, max_iter=100000, device=local_rank,
+                        cg_extrap=int(os.environ.get("FDL_CG_EXTRAP", "1")))
     if world > 1:
         from paper_1711_01228_b200 import dist as fdist
         L = fdist.sharded_layout(g, p, X0)      # NCCL id broadcast over the process group

@@ -94,6 +94,9 @@ typedef struct {
     int32_t hop_bits;     /* minimum stored hop width: 0 = auto (narrowest that holds the diameter:
                              4 bits if diam <= 15, 8 if <= 255, else 16), or 4, 8, 16. The decoded
                              hop, hence every result, is the same for every width   */
+    int32_t cg_extrap;    /* 1 (default): start PCG from X^k + rho (X^k - X^{k-1}) with rho the
+                             previous step's least-squares ratio of successive corrections
+                             (DESIGN R23); 0: start from X^k. Same minimiser either way */
 } fdl_params;
 
 typedef struct {

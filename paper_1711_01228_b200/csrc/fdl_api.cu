@@ -83,6 +83,13 @@ inline uint64_t splitmix64(uint64_t& s)
 }
 inline double u01(uint64_t& s) { return (double)(splitmix64(s) >> 11) * (1.0 / 9007199254740992.0); }
 
+// work-item length in tiles (FDL_KSEG overrides kSeg: tuning experiments only)
+int seg_len()
+{
+    static const int v = getenv("FDL_KSEG") ? std::max(1, atoi(getenv("FDL_KSEG"))) : kSeg;
+    return v;
+}
+
 // (I, J) of triangle index t (row-major upper triangle over nb blocks)
 void tri_coords(int64_t t, int64_t nb, int64_t& I, int64_t& J)
 {
@@ -129,7 +136,9 @@ struct fdl_ctx {
            *R2 = nullptr;
     double *cr = nullptr, *cz = nullptr, *cp = nullptr, *cy = nullptr;
     double *Ak = nullptr, *An = nullptr, *At = nullptr;  // carried L^W X^k, L^W X^{k+1}, L^W Xt
+    double *Xprev = nullptr, *Aprev = nullptr;           // X^{k-1}, L^W X^{k-1} (PCG start extrapolation)
     bool a_valid = false;
+    bool ext_ok = false;  // Xprev/Aprev hold the previous accepted iterate
     int a_age = 0;  // steps since Ak was last computed by a full pass
     float *posf = nullptr, *pvec = nullptr;
     double *blk_max = nullptr, *blk_cg = nullptr;
@@ -445,6 +454,7 @@ fdl_status eval_current(fdl_ctx* ctx)
 fdl_status upload_positions(fdl_ctx* ctx, const double* X)
 {
     ctx->a_valid = false;
+    ctx->ext_ok = false;
     std::vector<double> loc((size_t)ctx->n * ctx->dim);
     for (int i = 0; i < ctx->n; ++i)
         for (int q = 0; q < ctx->dim; ++q) {
@@ -619,7 +629,7 @@ void build_items(fdl_ctx* ctx, std::vector<int4>& items, std::vector<int>& lo, s
         int64_t I, J;
         tri_coords(t, nb, I, J);
         const int64_t strip_end = tri_index(I, nb - 1, nb) + 1;
-        const int64_t nt = std::min<int64_t>({(int64_t)kSeg, strip_end - t, ctx->t1 - t});
+        const int64_t nt = std::min<int64_t>({(int64_t)seg_len(), strip_end - t, ctx->t1 - t});
         if (!seen[I]) {
             seen[I] = 1;
             lo[I] = (int)items.size();
@@ -725,6 +735,8 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     FDL_ALLOC(ctx->Ak, vn);
     FDL_ALLOC(ctx->An, vn);
     FDL_ALLOC(ctx->At, vn);
+    FDL_ALLOC(ctx->Xprev, vn);
+    FDL_ALLOC(ctx->Aprev, vn);
     FDL_ALLOC(ctx->posf, (size_t)ctx->npad * 8);
     FDL_ALLOC(ctx->pvec, (size_t)ctx->npad * 4);
     FDL_ALLOC(ctx->blk_max, (size_t)ctx->nblk);
@@ -733,6 +745,8 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     FDL_CUDA(cudaMemsetAsync(ctx->posf, 0, (size_t)ctx->npad * 8 * sizeof(float), ctx->stream));
     FDL_CUDA(cudaMemsetAsync(ctx->pvec, 0, (size_t)ctx->npad * 4 * sizeof(float), ctx->stream));
     FDL_CUDA(cudaMemsetAsync(ctx->Xk, 0, vn * sizeof(double), ctx->stream));
+    FDL_CUDA(cudaMemsetAsync(ctx->Xprev, 0, vn * sizeof(double), ctx->stream));
+    FDL_CUDA(cudaMemsetAsync(ctx->Aprev, 0, vn * sizeof(double), ctx->stream));
     FDL_CUDA(cudaMemsetAsync(ctx->blk_cg, 0, (size_t)16 * ctx->nblk * sizeof(double), ctx->stream));
     if (ctx->nitems > 0)
         FDL_CUDA(cudaMemcpyAsync(ctx->items, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice,
@@ -800,7 +814,13 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
     } else {
         ctx->a_age++;
     }
-    FDL_LAUNCH(launch_cg_init(ctx->Ak, ctx->Rk, ctx->diag, ctx->cr, ctx->cz, ctx->cp, ctx->pvec, ctx->blk_cg, ctx->nblk,
+    const double* y0 = ctx->Ak;
+    if (ctx->p.cg_extrap) {  // extrapolated start (R23): x0 into Xn, L^W x0 into cy
+        FDL_LAUNCH(launch_extrap(ctx->Xk, ctx->Xprev, ctx->Ak, ctx->Aprev, ctx->Xn, ctx->cy, ctx->sc, n, dim,
+                                 ctx->ext_ok ? 1 : 0, s));
+        y0 = ctx->cy;
+    }
+    FDL_LAUNCH(launch_cg_init(y0, ctx->Rk, ctx->diag, ctx->cr, ctx->cz, ctx->cp, ctx->pvec, ctx->blk_cg, ctx->nblk,
                               n, dim, pq, s));
     FDL_LAUNCH(launch_cg_finalize(ctx->blk_cg, ctx->nblk, dim, 0, ctx->p.cg_rtol, ctx->sc, ctx->hs_dev, s));
     FDL_CUDA(cudaStreamSynchronize(s));
@@ -826,12 +846,16 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
     FDL_LAUNCH(launch_get_pin(ctx->Xn, ctx->pin_slots, 0, dim, 1, s));
     FDL_LAUNCH(launch_combine(ctx->Xk, ctx->Xn, ctx->Xt, ctx->posf, ctx->blk_max, ctx->pin_slots, n, 0, dim, omega,
                               ctx->cap, nsets, ps, s));
+    if (ctx->p.cg_extrap)  // ratio of successive corrections for the next start; X^{k-1} <- X^k
+        FDL_LAUNCH(launch_rho(ctx->Xn, ctx->Xk, ctx->Xprev, ctx->Ak, ctx->Aprev, ctx->blk_cg, n, dim,
+                              ctx->ext_ok ? 1 : 0, ctx->sc, s));
     // ---- line 6: f(Xt), f(X^{k+1}) and the next right-hand side, one fused pass
     FDL_TRY(run_sym(ctx, kSymP1, nsets, ctx->posf, ctx->R1, ctx->R2, 0));
     // ---- lines 6-8: guard
     FDL_LAUNCH(launch_select(ctx->Xk, ctx->Rk, ctx->Xn, ctx->Xt, ctx->R1, ctx->R2, ctx->blk_max, n, dim, nsets,
                              ctx->sc, ctx->Ak, ctx->An, ctx->At, s));
     ctx->a_valid = true;
+    ctx->ext_ok = ctx->p.cg_extrap != 0;
     mark_end(ctx, mstep);
     FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, s));
     FDL_CUDA(cudaStreamSynchronize(s));
@@ -906,6 +930,7 @@ void fdl_params_default(fdl_params* p)
     p->device = 0;
     p->a_refresh = 10;
     p->hop_bits = 0;
+    p->cg_extrap = 1;
 }
 
 const char* fdl_status_str(fdl_status s)
@@ -992,8 +1017,8 @@ fdl_status fdl_shard_tiles(int32_t n, int32_t world, int32_t rank, int64_t* t0, 
             const int64_t s0 = tri_index(I, I, nb), len = nb - I;
             if (s0 + len < target) continue;  // strip entirely before the target
             // segment starts inside strip I: s0, s0 + kSeg, ...
-            const int64_t k = (target - s0 + kSeg / 2) / kSeg;
-            best = std::min(s0 + k * kSeg, s0 + len);
+            const int64_t k = (target - s0 + seg_len() / 2) / seg_len();
+            best = std::min(s0 + k * seg_len(), s0 + len);
             break;
         }
         return best;

@@ -35,6 +35,7 @@ struct DevScalars {
     double rz[4], bb[4], rr[4], alpha[4], beta[4], pap[4];
     double S[4];           // sum_i p_i per column (rank-one term of the regularised operator)
     double Sd[4];          // sum_i d_i of the PCG correction d = x - x0 (for the carried L^W X)
+    double rho;            // PCG start extrapolation ratio (k_rho)
     double sigma;          // regularisation weight: (L + sigma 1 1^T), sigma = mean(diag)/n
     int active[4];
     int done;
@@ -62,6 +63,10 @@ cudaError_t launch_combine(const double* Xk, double* Xn, double* Xt, float* posf
 // carried A = L^W X: An = Rk - r_cg - sigma Sd 1 (for X^{k+1}), At = (1+w) An - w Ak (for Xt)
 cudaError_t launch_carry_a(const double* Rk, const double* rcg, const double* Ak, double* An, double* At,
                            const DevScalars* sc, int n, int dim, double omega, cudaStream_t s);
+cudaError_t launch_extrap(const double* Xk, const double* Xprev, const double* Ak, const double* Aprev, double* x,
+                          double* y0, const DevScalars* sc, int n, int dim, int valid, cudaStream_t s);
+cudaError_t launch_rho(const double* Xn, const double* Xk, double* Xprev, const double* Ak, double* Aprev,
+                       double* blk, int n, int dim, int valid, DevScalars* sc, cudaStream_t s);
 cudaError_t launch_get_pin(const double* x, double* slots, int rank, int dim, int owns_row0, cudaStream_t s);
 cudaError_t launch_select(double* Xk, double* Rk, const double* Xn, const double* Xt, const double* R1,
                           const double* R2, const double* blk_max, int nloc, int dim, int nsets,

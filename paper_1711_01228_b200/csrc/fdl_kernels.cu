@@ -227,6 +227,85 @@ cudaError_t launch_select(double* Xk, double* Rk, const double* Xn, const double
 // L d = r0 and the rank-one term only makes the operator nonsingular (fp32
 // rounding leaves sum_i r_i != 0 otherwise, an unreachable residual floor).
 // sum_i p_i is carried by the recurrence S <- sum z + beta S.
+// Extrapolated PCG start (DESIGN R23): x0 = X^k + rho (X^k - X^{k-1}),
+// L^W x0 = A^k + rho (A^k - A^{k-1}) from the carried products (L linear), so
+// no extra pass.  rho is the previous step's least-squares ratio of successive
+// corrections (k_rho); valid = 0 -> x0 = X^k.  The solve's result is the same
+// minimiser (Eq. 4) to the CG tolerance; only the start changes.
+__global__ void k_extrap(const double* __restrict__ Xk, const double* __restrict__ Xprev,
+                         const double* __restrict__ Ak, const double* __restrict__ Aprev, double* x, double* y0,
+                         const DevScalars* __restrict__ sc, int n, int dim, int valid)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double rho = valid ? sc->rho : 0.0;
+    for (int q = 0; q < dim; ++q) {
+        const size_t k = (size_t)i * dim + q;
+        x[k] = Xk[k] + rho * (Xk[k] - Xprev[k]);
+        y0[k] = Ak[k] + rho * (Ak[k] - Aprev[k]);
+    }
+}
+
+cudaError_t launch_extrap(const double* Xk, const double* Xprev, const double* Ak, const double* Aprev, double* x,
+                          double* y0, const DevScalars* sc, int n, int dim, int valid, cudaStream_t s)
+{
+    k_extrap<<<(n + 255) / 256, 256, 0, s>>>(Xk, Xprev, Ak, Aprev, x, y0, sc, n, dim, valid);
+    return cudaGetLastError();
+}
+
+// Block partials of a = <X^{k+1} - X^k, X^k - X^{k-1}>, b = |X^k - X^{k-1}|^2
+// (pinned gauge), then X^{k-1} <- X^k, A^{k-1} <- A^k for the next step.
+__global__ void __launch_bounds__(kRB) k_rho(const double* __restrict__ Xn, const double* __restrict__ Xk,
+                                             double* Xprev, const double* __restrict__ Ak, double* Aprev,
+                                             double* blk, int n, int dim, int nblk, int valid)
+{
+    __shared__ double red[8];
+    const int i = blockIdx.x * kRB + threadIdx.x;
+    double a = 0.0, b = 0.0;
+    if (i < n) {
+        for (int q = 0; q < dim; ++q) {
+            const size_t k = (size_t)i * dim + q;
+            const double xk = Xk[k], dp = xk - Xprev[k];
+            a += (Xn[k] - xk) * dp;
+            b += dp * dp;
+            Xprev[k] = xk;
+            Aprev[k] = Ak[k];
+        }
+    }
+    if (!valid) a = b = 0.0;
+    double t = block_sum_256(a, red);
+    if (threadIdx.x == 0) blk[blockIdx.x] = t;
+    t = block_sum_256(b, red);
+    if (threadIdx.x == 0) blk[nblk + blockIdx.x] = t;
+}
+
+__global__ void k_rho_finalize(const double* __restrict__ blk, int nblk, DevScalars* sc)
+{
+    const int lane = threadIdx.x;
+    double a = 0.0, b = 0.0;
+    for (int k = lane; k < nblk; k += 32) {
+        a += blk[k];
+        b += blk[nblk + k];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (lane == 0) sc->rho = b > 0.0 ? fmin(fmax(a / b, 0.0), 1.0) : 0.0;
+}
+
+cudaError_t launch_rho(const double* Xn, const double* Xk, double* Xprev, const double* Ak, double* Aprev,
+                       double* blk, int n, int dim, int valid, DevScalars* sc, cudaStream_t s)
+{
+    const int nblk = (n + kRB - 1) / kRB;
+    k_rho<<<nblk, kRB, 0, s>>>(Xn, Xk, Xprev, Ak, Aprev, blk, n, dim, nblk, valid);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_rho_finalize<<<1, 32, 0, s>>>(blk, nblk, sc);
+    return cudaGetLastError();
+}
+
 __global__ void k_cg_begin(const double* __restrict__ Xk, double* x, float* pvec, int nloc, int row0, int dim,
                            int pq)
 {

@@ -320,9 +320,16 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
         // 4-bit tiles: one byte = hops of rows (2p, 2p+1) of a column, one 8-byte
         // LUT entry per byte gives both decoded values (h^2 for P1/DIAG, w' = 1/h^2
         // for P2): 2 ALU ops + 1 LDS.64 per two pairs, no FP32-pipe decode work.
-#pragma unroll 1
+        // Both chunks are loaded up front and the 8 columns fully unrolled, so the
+        // LUT loads of the next column overlap the FP work of this one; the
+        // j-side sum of a column is split over even/odd rows (two 4-long FFMA
+        // chains instead of one 8-long chain).
+        uint4 chs[NCH];
+#pragma unroll
+        for (int kc = 0; kc < NCH; ++kc) chs[kc] = *reinterpret_cast<const uint4*>(sD + ((size_t)kc * 256 + tid) * 16);
+#pragma unroll
         for (int kc = 0; kc < NCH; ++kc) {
-            const uint4 ch = *reinterpret_cast<const uint4*>(sD + ((size_t)kc * 256 + tid) * 16);
+            const uint4 ch = chs[kc];
 #pragma unroll
             for (int cc = 0; cc < CPC; ++cc) {
                 const int c = kc * CPC + cc;
@@ -339,25 +346,29 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
                         xj[4 * q] = t.x; xj[4 * q + 1] = t.y; xj[4 * q + 2] = t.z; xj[4 * q + 3] = t.w;
                     }
                 }
-                float aj[C];
+                float aj[2][C];
 #pragma unroll
-                for (int v = 0; v < C; ++v) aj[v] = 0.0f;
+                for (int v = 0; v < C; ++v) aj[0][v] = aj[1][v] = 0.0f;
                 const uint32_t w = word_of(ch, cc);
+                float2 e[4];
 #pragma unroll
                 for (int rp = 0; rp < 4; ++rp) {
                     const uint32_t off = rp == 0 ? ((w << 3) & 0x7f8u) : ((w >> (8 * rp - 3)) & 0x7f8u);
-                    const float2 e = *reinterpret_cast<const float2*>(reinterpret_cast<const char*>(lut2) + off);
+                    e[rp] = *reinterpret_cast<const float2*>(reinterpret_cast<const char*>(lut2) + off);
+                }
+#pragma unroll
+                for (int rp = 0; rp < 4; ++rp) {
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh) {
                         const int r = 2 * rp + hh;
-                        const float v = hh ? e.y : e.x;
+                        const float v = hh ? e[rp].y : e[rp].x;
                         bool valid = true;
                         if (SAFE) valid = (v > 0.0f) && (!diag || (ty * 8 + r < jl));
-                        sym_pair<MODE, DIM, NSETS, SAFE>(&xi[r][0], xj, v, v, valid, &ai[r][0], &aj[0], sf);
+                        sym_pair<MODE, DIM, NSETS, SAFE>(&xi[r][0], xj, v, v, valid, &ai[r][0], &aj[hh][0], sf);
                     }
                 }
 #pragma unroll
-                for (int v = 0; v < C; ++v) myred[c * C + v] = aj[v];
+                for (int v = 0; v < C; ++v) myred[c * C + v] = aj[0][v] + aj[1][v];
             }
         }
         return;
@@ -381,9 +392,9 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
                     xj[4 * q] = t.x; xj[4 * q + 1] = t.y; xj[4 * q + 2] = t.z; xj[4 * q + 3] = t.w;
                 }
             }
-            float aj[C];
+            float aj[2][C];  // even / odd rows (same split and order as the 4-bit path)
 #pragma unroll
-            for (int v = 0; v < C; ++v) aj[v] = 0.0f;
+            for (int v = 0; v < C; ++v) aj[0][v] = aj[1][v] = 0.0f;
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
                 float hf, h2, wl = 0.0f;
@@ -399,10 +410,10 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
                 }
                 bool valid = true;
                 if (SAFE) valid = (h2 > 0.0f) && (!diag || (ty * 8 + r < jl));
-                sym_pair<MODE, DIM, NSETS, SAFE>(&xi[r][0], xj, h2, wl, valid, &ai[r][0], &aj[0], sf);
+                sym_pair<MODE, DIM, NSETS, SAFE>(&xi[r][0], xj, h2, wl, valid, &ai[r][0], &aj[r & 1][0], sf);
             }
 #pragma unroll
-            for (int v = 0; v < C; ++v) myred[c * C + v] = aj[v];
+            for (int v = 0; v < C; ++v) myred[c * C + v] = aj[0][v] + aj[1][v];
         }
     }
 }

@@ -48,6 +48,7 @@ class Params(ctypes.Structure):
         ("max_iter", ctypes.c_int32), ("weight_exp", ctypes.c_double), ("cg_rtol", ctypes.c_double),
         ("cg_max_iter", ctypes.c_int32), ("strategy", ctypes.c_int32), ("seed", ctypes.c_uint64),
         ("device", ctypes.c_int32), ("a_refresh", ctypes.c_int32), ("hop_bits", ctypes.c_int32),
+        ("cg_extrap", ctypes.c_int32),
     ]
 
 
@@ -144,12 +145,13 @@ def params_default() -> Params:
 
 
 def make_params(dim=2, k=0.0, omega=1.5, step=math.inf, tol=1e-4, max_iter=500, cg_rtol=0.0,
-                cg_max_iter=0, strategy=STRAT_FIXED, seed=1, device=0, a_refresh=0, hop_bits=0) -> Params:
+                cg_max_iter=0, strategy=STRAT_FIXED, seed=1, device=0, a_refresh=0, hop_bits=0, cg_extrap=1) -> Params:
     p = params_default()
     p.dim, p.k, p.omega, p.step, p.tol, p.max_iter = dim, k, omega, step, tol, max_iter
     p.cg_rtol, p.cg_max_iter, p.strategy, p.seed, p.device = cg_rtol, cg_max_iter, strategy, seed, device
     p.a_refresh = a_refresh
     p.hop_bits = hop_bits
+    p.cg_extrap = cg_extrap
     return p
 
 

@@ -331,3 +331,24 @@ def test_hop_width_invariance(name, dim):
         assert relL2(A, A0) <= 1e-6
     if 4 in out and 8 in out:
         assert all(np.array_equal(a, b) for a, b in zip(out[4][:4], out[8][:4])) and out[4][4] == out[8][4]
+
+
+@pytest.mark.parametrize("name,omega", [("C2", 1.6), ("C3", 1.5)])
+def test_extrapolated_cg_start(name, omega):
+    """PCG started from X^k + rho (X^k - X^{k-1}) (DESIGN R23) reaches the same
+    minimiser (Eq. 4) as the plain warm start X^k to the CG tolerance:
+    the same trajectory (iterations within 1, final f within 1e-5)."""
+    runs = []
+    for ext in (0, 1):
+        cfg = configs.CONFIGS[name]
+        g = configs.graph_for(name)
+        X0 = configs.positions_for(name, g.n, 1)
+        p = fdl.make_params(dim=2, k=cfg.k_for(g.n), omega=omega, tol=cfg.tol, max_iter=cfg.max_iter,
+                            cg_extrap=ext)
+        L = fdl.Layout.from_graph(g, params=p, init_pos=X0)
+        r = L.run_until_converged()
+        runs.append((r.iterations, r.f_final, r.cg_iters))
+    (it0, f0, cg0), (it1, f1, cg1) = runs
+    print(name, runs)
+    assert abs(it0 - it1) <= 1
+    assert abs(f0 - f1) / f0 <= 1e-5
