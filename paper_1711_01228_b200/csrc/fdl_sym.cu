@@ -140,11 +140,6 @@ __host__ __device__ constexpr int sym_ps()
                           : (MODE == kSymP2 ? (DIM == 2 ? 2 : 4) : 4);
 }
 
-template <int MODE, int HB>
-__host__ __device__ constexpr int sym_stages()  // TMA ring depth (bounded by 2 CTAs per SM for the 2-D passes)
-{
-    return MODE == kSymP1 ? (HB == 2 ? 2 : 3) : (HB == 2 ? 3 : 4);
-}
 
 template <int MODE, int DIM, int NSETS, int HB>
 __host__ __device__ constexpr int sym_stage_bytes()
@@ -174,10 +169,29 @@ __host__ __device__ constexpr size_t sym_red_floats()  // j-side warp buffers an
                : (size_t)256 * sym_red_pitch<MODE, DIM, NSETS>();
 }
 
+// CTAs per SM the pass is built for (register budget of __launch_bounds__)
+template <int MODE, int DIM>
+__host__ __device__ constexpr int sym_ctas_per_sm()
+{
+    return (DIM == 2 || MODE != kSymP1) ? 2 : 1;
+}
+
+// TMA ring depth: as many stages (2..4) as the shared memory left by the
+// reduction buffers allows at sym_ctas_per_sm CTAs per SM (228 KB per SM,
+// ~1 KB per CTA reserved, ~4 KB static).
+template <int MODE, int DIM, int NSETS, int HB>
+__host__ __device__ constexpr int sym_stages()
+{
+    constexpr int budget = 228 * 1024 / sym_ctas_per_sm<MODE, DIM>() - 5 * 1024 -
+                           (int)sym_red_floats<MODE, DIM, NSETS>() * 4;
+    constexpr int st = budget / sym_stage_bytes<MODE, DIM, NSETS, HB>();
+    return st < 2 ? 2 : (st > 4 ? 4 : st);
+}
+
 template <int MODE, int DIM, int NSETS, int HB>
 __host__ __device__ constexpr size_t sym_smem_bytes()
 {
-    return (size_t)sym_stages<MODE, HB>() * sym_stage_bytes<MODE, DIM, NSETS, HB>() +
+    return (size_t)sym_stages<MODE, DIM, NSETS, HB>() * sym_stage_bytes<MODE, DIM, NSETS, HB>() +
            sym_red_floats<MODE, DIM, NSETS>() * 4;
 }
 
@@ -452,7 +466,7 @@ __device__ __forceinline__ void sym_flush_warp(const float* wbuf, float* jpart_w
 }
 
 template <int MODE, int DIM, int NSETS, int HB>
-__global__ void __launch_bounds__(256, (DIM == 2 || MODE != kSymP1) ? 2 : 1) k_sym(const SymArgs a)
+__global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const SymArgs a)
 {
     constexpr int C = sym_ncomp<MODE, DIM, NSETS>();
     constexpr int PS = sym_ps<MODE, DIM, NSETS>();
@@ -460,7 +474,7 @@ __global__ void __launch_bounds__(256, (DIM == 2 || MODE != kSymP1) ? 2 : 1) k_s
     constexpr int DT = (int)tile_bytes(HB);
     constexpr int PITCH = sym_red_pitch<MODE, DIM, NSETS>();
     constexpr int JP = sym_jpitch<MODE, DIM, NSETS>();
-    constexpr int NST = sym_stages<MODE, HB>();
+    constexpr int NST = sym_stages<MODE, DIM, NSETS, HB>();
     constexpr int NW = 8;  // warps
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t full[NST];
