@@ -224,6 +224,15 @@ fdl_status fdl_get_positions(fdl_ctx* ctx, double* out, size_t count);
  * L^X X, clears the stop flag (checkpoint resume / parity). */
 fdl_status fdl_set_positions(fdl_ctx* ctx, const double* in, size_t count);
 
+/* Per-vertex relax factors omega_i >= 0 (§6 (1), line 410:
+ * x~_i = x_i^{k+1} + omega_i (x_i^{k+1} - x_i^k)), count = n, replacing the
+ * scalar omega of Eq. 10 in every later step until cleared with omega = NULL.
+ * The guard (lines 6-8) still compares f(X~) with f(X^{k+1}).  Requires the
+ * fixed strategy (FDL_E_UNSUPPORTED otherwise); X~ is then not a scalar
+ * combination of X^{k+1} and X^k, so L^W X^k is recomputed by a full pass
+ * each step instead of being carried.  The array is copied. */
+fdl_status fdl_set_omega_vertex(fdl_ctx* ctx, const double* omega, size_t count);
+
 /* Forces at the current placement, original units (each n*dim, may be NULL):
  * R = L^X X ("repulsion"), A = L^W X ("attraction"); *stress = f(X). */
 fdl_status fdl_eval_forces(fdl_ctx* ctx, double* R, double* A, double* stress);

@@ -155,8 +155,13 @@ def pin(X: np.ndarray) -> np.ndarray:
     return X - X[0]
 
 
-def sor_combine(X_next: np.ndarray, X_prev: np.ndarray, omega: float) -> np.ndarray:
-    """Eq. 10: (1 + w) X^{k+1} - w X^k."""
+def sor_combine(X_next: np.ndarray, X_prev: np.ndarray, omega) -> np.ndarray:
+    """Eq. 10: (1 + w) X^{k+1} - w X^k.  A vector omega
+    (one factor per vertex) is §6 (1), line 410:
+    x~_i = x_i^{k+1} + w_i (x_i^{k+1} - x_i^k)."""
+    if np.ndim(omega) == 1:
+        w = np.asarray(omega, dtype=np.float64)[:, None]
+        return X_next + w * (X_next - X_prev)
     return (1.0 + omega) * X_next - omega * X_prev
 
 
@@ -183,7 +188,7 @@ def run_algorithm2(prob: Problem, X0: np.ndarray, omega: float, tol: float, max_
     f = prob.f(X)
     res = LayoutResult(X=X, f=f, iterations=0, reason="max_iter", f_initial=f)
     for it in range(1, max_iter + 1):
-        w = omega if omega_fn is None else float(omega_fn(it))
+        w = omega if omega_fn is None else omega_fn(it)
         Xn = prob.H(X)                                   # line 4
         fn = prob.f(Xn)
         Xt = cap_step(sor_combine(Xn, X, w), Xn, step)   # line 5 (Eq. 10)

@@ -137,6 +137,8 @@ struct fdl_ctx {
     double *cr = nullptr, *cz = nullptr, *cp = nullptr, *cy = nullptr;
     double *Ak = nullptr, *An = nullptr, *At = nullptr;  // carried L^W X^k, L^W X^{k+1}, L^W Xt
     double *Xprev = nullptr, *Aprev = nullptr;           // X^{k-1}, L^W X^{k-1} (PCG start extrapolation)
+    double* omega_v = nullptr;   // per-vertex relax factors (fdl_set_omega_vertex), device
+    double omega_v_max = 0.0;
     bool a_valid = false;
     bool ext_ok = false;  // Xprev/Aprev hold the previous accepted iterate
     int a_age = 0;  // steps since Ak was last computed by a full pass
@@ -797,7 +799,7 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
     if (ctx->emulated) return set_err(ctx, FDL_E_UNSUPPORTED, "emulated rank: only fdl_eval_partial is available");
     if (ctx->broken) return set_err(ctx, FDL_E_STATE, ctx->err.empty() ? "context is broken" : ctx->err);
     if (ctx->stopped) return set_err(ctx, FDL_E_STATE, "the run has stopped; call fdl_set_positions to restart");
-    const double omega = pick_omega(ctx);
+    const double omega = ctx->omega_v ? ctx->omega_v_max : pick_omega(ctx);
     const int nsets = omega > 0.0 ? 2 : 1;
     const int dim = ctx->dim, n = ctx->n;
     const int pq = ps_p2(dim), ps = ps_p1(dim, nsets);
@@ -806,7 +808,8 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
     // ---- line 4: X^{k+1} = H(X^k): PCG on Eq. 5 (zero-mean gauge, R7), warm start X^k.
     // The warm-start residual needs L^W X^k: carried from the previous solve, or a full
     // P2 pass every a_refresh steps (bounds the fp32 drift of the carried value).
-    const bool refresh = !ctx->a_valid || ctx->a_age + 1 >= ctx->p.a_refresh;
+    // per-vertex omega: Xt is not a scalar combination, At cannot be carried
+    const bool refresh = !ctx->a_valid || ctx->a_age + 1 >= ctx->p.a_refresh || ctx->omega_v;
     FDL_LAUNCH(launch_cg_begin(ctx->Xk, ctx->Xn, ctx->pvec, n, 0, dim, pq, s));
     if (refresh) {
         FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->Ak, nullptr, 0));
@@ -844,7 +847,7 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
     FDL_LAUNCH(launch_carry_a(ctx->Rk, ctx->cr, ctx->Ak, ctx->An, ctx->At, ctx->sc, n, dim, omega, s));
     // ---- pin x_0 = 0, then line 5: Xt = (1+w) X^{k+1} - w X^k (Eq. 10)
     FDL_LAUNCH(launch_get_pin(ctx->Xn, ctx->pin_slots, 0, dim, 1, s));
-    FDL_LAUNCH(launch_combine(ctx->Xk, ctx->Xn, ctx->Xt, ctx->posf, ctx->blk_max, ctx->pin_slots, n, 0, dim, omega,
+    FDL_LAUNCH(launch_combine(ctx->Xk, ctx->Xn, ctx->Xt, ctx->posf, ctx->blk_max, ctx->pin_slots, n, 0, dim, omega, ctx->omega_v,
                               ctx->cap, nsets, ps, s));
     if (ctx->p.cg_extrap)  // ratio of successive corrections for the next start; X^{k-1} <- X^k
         FDL_LAUNCH(launch_rho(ctx->Xn, ctx->Xk, ctx->Xprev, ctx->Ak, ctx->Aprev, ctx->blk_cg, n, dim,
@@ -1044,6 +1047,35 @@ fdl_status fdl_set_stream(fdl_ctx* ctx, void* cuda_stream)
     if (!ctx) return FDL_E_INVALID_ARG;
     cudaStreamSynchronize(ctx->stream);
     ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
+    return FDL_OK;
+}
+
+fdl_status fdl_set_omega_vertex(fdl_ctx* ctx, const double* omega, size_t count)
+{
+    if (!ctx) return FDL_E_INVALID_ARG;
+    if (ctx->broken) return set_err(ctx, FDL_E_STATE, ctx->err);
+    if (!omega) {
+        if (ctx->omega_v) {
+            cudaFree(ctx->omega_v);
+            ctx->allocs.erase(std::find(ctx->allocs.begin(), ctx->allocs.end(), (void*)ctx->omega_v));
+            ctx->omega_v = nullptr;
+        }
+        return FDL_OK;
+    }
+    if (count != (size_t)ctx->n) return set_err(ctx, FDL_E_INVALID_ARG, "omega count must be n");
+    if (ctx->p.strategy != FDL_STRAT_FIXED)
+        return set_err(ctx, FDL_E_UNSUPPORTED, "per-vertex omega requires the fixed strategy");
+    double mx = 0.0;
+    for (size_t i = 0; i < count; ++i) {
+        if (!(omega[i] >= 0.0) || !std::isfinite(omega[i]))
+            return set_err(ctx, FDL_E_INVALID_ARG, "omega_i must be finite and >= 0");
+        mx = std::max(mx, omega[i]);
+    }
+    FDL_CUDA(cudaSetDevice(ctx->device));
+    if (!ctx->omega_v) FDL_ALLOC(ctx->omega_v, (size_t)ctx->n);
+    FDL_CUDA(cudaMemcpyAsync(ctx->omega_v, omega, sizeof(double) * count, cudaMemcpyHostToDevice, ctx->stream));
+    FDL_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->omega_v_max = mx;
     return FDL_OK;
 }
 

@@ -58,8 +58,8 @@ cudaError_t launch_bfs_init(uint32_t* frontier, uint32_t* visited, int n, int s0
 cudaError_t launch_stage_pos1(const double* X, float* posf, int nloc, int row0, int dim, int ps,
                               cudaStream_t s);
 cudaError_t launch_combine(const double* Xk, double* Xn, double* Xt, float* posf, double* blk_max,
-                           const double* xpin, int nloc, int row0, int dim, double omega, double cap,
-                           int nsets, int ps, cudaStream_t s);
+                           const double* xpin, int nloc, int row0, int dim, double omega, const double* omega_v,
+                           double cap, int nsets, int ps, cudaStream_t s);
 // carried A = L^W X: An = Rk - r_cg - sigma Sd 1 (for X^{k+1}), At = (1+w) An - w Ak (for Xt)
 cudaError_t launch_carry_a(const double* Rk, const double* rcg, const double* Ak, double* An, double* At,
                            const DevScalars* sc, int n, int dim, double omega, cudaStream_t s);

@@ -84,13 +84,15 @@ cudaError_t launch_stage_pos1(const double* X, float* posf, int nloc, int row0, 
 __global__ void __launch_bounds__(kRB) k_combine(const double* __restrict__ Xk, double* __restrict__ Xn,
                                                  double* __restrict__ Xt, float* posf, double* blk_max,
                                                  const double* __restrict__ xpin, int nloc, int row0, int dim,
-                                                 double omega, double cap, int nsets, int ps)
+                                                 double omega, const double* __restrict__ omega_v, double cap,
+                                                 int nsets, int ps)
 {
     __shared__ double red[8];
     const int lr = blockIdx.x * kRB + threadIdx.x;
     double disp2 = 0.0;
     if (lr < nloc) {
         const int64_t g = stage_slot((int64_t)row0 + lr);
+        if (omega_v) omega = omega_v[row0 + lr];  // per-vertex relax factor
         double v[3], xn[3], n2 = 0.0;
         for (int q = 0; q < dim; ++q) {
             xn[q] = Xn[(size_t)lr * dim + q] - xpin[q];
@@ -121,11 +123,11 @@ __global__ void __launch_bounds__(kRB) k_combine(const double* __restrict__ Xk, 
 }
 
 cudaError_t launch_combine(const double* Xk, double* Xn, double* Xt, float* posf, double* blk_max,
-                           const double* xpin, int nloc, int row0, int dim, double omega, double cap, int nsets,
-                           int ps, cudaStream_t s)
+                           const double* xpin, int nloc, int row0, int dim, double omega, const double* omega_v,
+                           double cap, int nsets, int ps, cudaStream_t s)
 {
-    k_combine<<<(nloc + kRB - 1) / kRB, kRB, 0, s>>>(Xk, Xn, Xt, posf, blk_max, xpin, nloc, row0, dim, omega, cap,
-                                                     nsets, ps);
+    k_combine<<<(nloc + kRB - 1) / kRB, kRB, 0, s>>>(Xk, Xn, Xt, posf, blk_max, xpin, nloc, row0, dim, omega,
+                                                     omega_v, cap, nsets, ps);
     return cudaGetLastError();
 }
 

@@ -30,7 +30,7 @@ EXPORTS = [
     "fdl_nccl_unique_id", "fdl_set_stream", "fdl_step", "fdl_run_until_converged", "fdl_get_positions",
     "fdl_set_positions", "fdl_eval_forces", "fdl_get_hop_rows", "fdl_get_diag", "fdl_get_info",
     "fdl_set_timing", "fdl_get_stats", "fdl_reset_stats", "fdl_bench_ffma", "fdl_status_str",
-    "fdl_last_error", "fdl_destroy", "fdl_eval_partial",
+    "fdl_last_error", "fdl_destroy", "fdl_eval_partial", "fdl_set_omega_vertex",
 ]
 
 
@@ -112,6 +112,7 @@ def _load():
         "fdl_get_positions": (i32, [P, P, sz]),
         "fdl_set_positions": (i32, [P, P, sz]),
         "fdl_eval_forces": (i32, [P, P, P, P]),
+        "fdl_set_omega_vertex": (i32, [P, P, sz]),
         "fdl_get_hop_rows": (i32, [P, i32, i32, P]),
         "fdl_get_diag": (i32, [P, P, sz]),
         "fdl_get_info": (i32, [P, ctypes.POINTER(CtxInfo)]),
@@ -249,6 +250,14 @@ class Layout:
     def set_positions(self, X) -> None:
         X = np.ascontiguousarray(X, dtype=np.float64)
         _check(self._h, lib.fdl_set_positions(self._h, _ptr(X), X.size))
+
+    def set_omega_vertex(self, omega) -> None:
+        """Per-vertex relax factors; None restores the scalar omega."""
+        if omega is None:
+            _check(self._h, lib.fdl_set_omega_vertex(self._h, None, 0))
+            return
+        w = np.ascontiguousarray(omega, dtype=np.float64)
+        _check(self._h, lib.fdl_set_omega_vertex(self._h, _ptr(w), w.size))
 
     def eval_forces(self):
         R = np.empty((self.n, self.dim))

@@ -352,3 +352,46 @@ def test_extrapolated_cg_start(name, omega):
     print(name, runs)
     assert abs(it0 - it1) <= 1
     assert abs(f0 - f1) / f0 <= 1e-5
+
+
+# ------------------------------------------------- NEXT-1: probabilistic strategy
+@pytest.mark.parametrize("name,seed", [("C1", 5), ("C1", 6), ("C2", 7)])
+def test_probabilistic_strategy(name, seed):
+    """Roulette strategy: the library's SplitMix64 stream gives the
+    oracle's omega sequence exactly (both implement the generator, R24), and
+    the run meets the end-to-end gates against the fp64 oracle."""
+    from oracle import strategies
+    cfg = configs.CONFIGS[name]
+    g = configs.graph_for(name)
+    k = cfg.k_for(g.n)
+    X0 = configs.positions_for(name, g.n, 1)
+    p = fdl.make_params(dim=2, k=k, tol=cfg.tol, max_iter=cfg.max_iter, strategy=fdl.STRAT_PROB, seed=seed)
+    L = fdl.Layout.from_graph(g, params=p, init_pos=X0)
+    omegas, fs = [], []
+    while True:
+        info = L.step()
+        omegas.append(info.omega)
+        fs.append(info.f_after)
+        if info.stop:
+            break
+    o = layout.run_algorithm2(layout.Problem(g, 2, k), X0, None, cfg.tol, cfg.max_iter,
+                              omega_fn=strategies.probabilistic_omega_fn(seed))
+    m = min(len(omegas), o.iterations)
+    assert omegas[:m] == [t.omega for t in o.trace[:m]]
+    _gates(len(fs), fs[-1], o)
+    assert all(b <= a * (1 + 1e-9) for a, b in zip([L.info.f] + fs, fs))
+
+
+# ----------------------------------------------------- NEXT-4: per-vertex omega
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_per_vertex_omega(name):
+    """x~_i = x_i^{k+1} + w_i (x_i^{k+1} - x_i^k), w_i
+    uniform in [0, 2] from a seeded generator: end-to-end gates against the
+    fp64 oracle with the same vector."""
+    cfg = configs.CONFIGS[name]
+    g, k, X0, L = make(name, omega=1.0)
+    w = np.random.default_rng(99).uniform(0.0, 2.0, g.n)
+    L.set_omega_vertex(w)
+    r = L.run_until_converged()
+    o = layout.run_algorithm2(layout.Problem(g, 2, k), X0, w, cfg.tol, cfg.max_iter)
+    _gates(r.iterations, r.f_final, o)

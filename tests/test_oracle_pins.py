@@ -365,3 +365,84 @@ def test_convergence_rate_theorem_3_2():
     observed = math.exp(slope)
     assert observed == pytest.approx(predicted, abs=0.01)
     assert 0.0 < predicted < 1.0
+
+
+# ------------------------------------------------ relax-factor strategies (§5.2)
+def test_splitmix64_published_vectors():
+    """The oracle's SplitMix64 reproduces the generator's published outputs
+    (tests/golden/splitmix64.json, cited there)."""
+    import json
+    import os
+    from oracle.strategies import SplitMix64
+    d = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "splitmix64.json")))
+    for v in d["vectors"]:
+        r = SplitMix64(v["seed"])
+        if "outputs_hex" in v:
+            assert [f"{r.next_u64():016x}" for _ in v["outputs_hex"]] == v["outputs_hex"]
+        else:
+            assert [str(r.next_u64()) for _ in v["outputs_dec"]] == v["outputs_dec"]
+
+
+def test_roulette_distribution():
+    """P(0.5) = P(1.0) = 0.3, P(1.5) = P(2.0) = 0.2, one draw per iteration."""
+    from oracle.strategies import probabilistic_omega_fn
+    fn = probabilistic_omega_fn(7)
+    draws = np.array([fn(i) for i in range(200000)])
+    for w, p in ((0.5, 0.3), (1.0, 0.3), (1.5, 0.2), (2.0, 0.2)):
+        assert abs(np.mean(draws == w) - p) < 0.004
+    assert set(np.unique(draws)) == {0.5, 1.0, 1.5, 2.0}
+
+
+def test_probabilistic_strategy_monotone_and_faster():
+    """With the roulette the guard keeps f non-increasing
+    and the run needs fewer iterations than Algorithm 1 (Table 1 "auto" column,
+    P:366-392, ~45-60% of the omega = 0 count)."""
+    from oracle.strategies import probabilistic_omega_fn
+    g = graphs.grid_graph(6, 6)
+    prob = layout.Problem(g, 2, 0.2)
+    X0 = graphs.init_positions(g.n, 2, 3)
+    a = layout.run_algorithm2(prob, X0, 0.0, 1e-7, 2000, omega_fn=probabilistic_omega_fn(11))
+    b = layout.run_algorithm1(prob, X0, 1e-7, 2000)
+    fs = [a.f_initial] + [t.f_after for t in a.trace]
+    assert all(y <= x for x, y in zip(fs, fs[1:]))
+    assert a.iterations < b.iterations
+    assert abs(a.f - b.f) / b.f < 1e-3
+
+
+def test_enumerating_strategy_picks_min_and_dominates():
+    """Lines 288-291: omega* = argmin over {0, 0.5, ..., 9}; omega = 0 is a
+    candidate so f(X~(omega*)) <= f(X^{k+1}); ties go to the smaller omega."""
+    from oracle.strategies import ENUM_OMEGAS, enumerate_omega
+    g = graphs.grid_graph(5, 5)
+    prob = layout.Problem(g, 2, 0.25)
+    X = graphs.init_positions(g.n, 2, 5).astype(np.float64)
+    Xn = prob.H(X)
+    w, f, fs = enumerate_omega(prob, Xn, X)
+    assert len(fs) == 19 and ENUM_OMEGAS[0] == 0.0 and ENUM_OMEGAS[-1] == 9.0
+    assert f == min(fs) and f <= prob.f(Xn)
+    assert w == ENUM_OMEGAS[fs.index(min(fs))]
+    # ties go to the smaller omega (S:306): a stress that is flat from omega = 1 on
+    class Flat:
+        @staticmethod
+        def f(Y):
+            return float(max(np.max(np.abs(Y - 2 * Xn + X)), 1.0))  # = 1 for omega <= 1, grows after
+    w1, _, fs1 = enumerate_omega(Flat, Xn, X)
+    assert fs1[0] == fs1[1] == fs1[2] == 1.0 and w1 == 0.0
+
+
+def test_per_vertex_omega_reduces_to_eq10():
+    """§6 (1), line 410: x~_i = x_i^{k+1} + w_i (x_i^{k+1} - x_i^k).  A constant
+    vector is Eq. 10 exactly (same trajectory as the scalar); a random one
+    keeps f non-increasing through the guard (lines 6-8)."""
+    g = graphs.grid_graph(5, 6)
+    prob = layout.Problem(g, 2, 0.3)
+    X0 = graphs.init_positions(g.n, 2, 4)
+    a = layout.run_algorithm2(prob, X0, 1.5, 1e-8, 300)
+    b = layout.run_algorithm2(prob, X0, np.full(g.n, 1.5), 1e-8, 300)
+    assert a.iterations == b.iterations
+    np.testing.assert_allclose(a.X, b.X, rtol=0, atol=1e-12)
+    w = np.random.default_rng(2).uniform(0.0, 2.0, g.n)
+    c = layout.run_algorithm2(prob, X0, w, 1e-8, 300)
+    fs = [c.f_initial] + [t.f_after for t in c.trace]
+    assert all(y <= x for x, y in zip(fs, fs[1:]))
+    assert abs(c.f - a.f) / a.f < 1e-2
