@@ -56,6 +56,8 @@ def parse_args():
     ap.add_argument("--impl", default="fdl", choices=["fdl", "reference"])
     ap.add_argument("--config", default="C5", choices=list(configs.CONFIGS))
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--strategy", default="fixed", choices=["fixed", "prob", "enum"],
+                    help="relax-factor strategy (PAPER.md §5.2); the headline line uses fixed omega")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-rows", type=int, default=0)
@@ -218,7 +220,8 @@ def run_gpu(args):
     k = cfg.k_for(n)
     X0 = configs.positions_for(args.config, n, args.seed)
     p = fdl.make_params(dim=cfg.dim, k=k, omega=cfg.omega, tol=cfg.tol, max_iter=100000, device=local_rank,
-                        cg_extrap=int(os.environ.get("FDL_CG_EXTRAP", "1")))
+                        cg_extrap=int(os.environ.get("FDL_CG_EXTRAP", "1")),
+                        strategy={"fixed": fdl.STRAT_FIXED, "prob": fdl.STRAT_PROB, "enum": fdl.STRAT_ENUM}[args.strategy])
     if world > 1:
         from paper_1711_01228_b200 import dist as fdist
         L = fdist.sharded_layout(g, p, X0)      # NCCL id broadcast over the process group

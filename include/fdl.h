@@ -64,7 +64,10 @@ typedef enum {
 
 typedef enum {
     FDL_STRAT_FIXED = 0, /* omega constant; omega = 0 is Algorithm 1           */
-    FDL_STRAT_PROB = 1   /* roulette over {0.5,1,1.5,2} w.p. {.3,.3,.2,.2} each iteration */
+    FDL_STRAT_PROB = 1,  /* roulette over {0.5,1,1.5,2} w.p. {.3,.3,.2,.2} each iteration */
+    FDL_STRAT_ENUM = 2   /* omega* = argmin_c f((1+w_c) X^{k+1} - w_c X^k) over w_c = c * enum_step,
+                            c = 0..enum_count-1 ({0, 0.5, ..., 9}); ties to the smaller
+                            omega. Single GPU; no step cap                                  */
 } fdl_strategy;
 
 typedef enum {
@@ -97,6 +100,8 @@ typedef struct {
     int32_t cg_extrap;    /* 1 (default): start PCG from X^k + rho (X^k - X^{k-1}) with rho the
                              previous step's least-squares ratio of successive corrections
                              (DESIGN R23); 0: start from X^k. Same minimiser either way */
+    int32_t enum_count;   /* FDL_STRAT_ENUM candidates, 1..32 (default 19)                     */
+    double enum_step;     /* FDL_STRAT_ENUM candidate spacing > 0 (default 0.5)                */
 } fdl_params;
 
 typedef struct {
@@ -107,7 +112,7 @@ typedef struct {
     double omega;          /* relax factor used                                          */
     double f_before;       /* f(X^k)                                                     */
     double f_next;         /* f(X^{k+1}) before relaxation                               */
-    double f_relaxed;      /* f(Xt); NaN when omega == 0 (not evaluated)                 */
+    double f_relaxed;      /* f(Xt); NaN when omega == 0 (not evaluated); ENUM: f(Xt(w*))  */
     double f_after;        /* f of the accepted point                                    */
     double rel_decrease;   /* (f_before - f_after)/f_before                              */
     double cg_relres;      /* max over columns of ||r||/||b|| at PCG exit                */

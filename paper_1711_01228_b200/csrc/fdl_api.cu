@@ -123,7 +123,7 @@ struct fdl_ctx {
     int device = 0;
     int sm_count = 148;
     int nblk = 0;  // 256-row reduction blocks of the vector kernels
-    int grid_p1[3] = {0, 0, 0}, grid_p2 = 0, grid_diag = 0;
+    int grid_p1[3] = {0, 0, 0}, grid_p2 = 0, grid_diag = 0, grid_enum = 0;
     cudaStream_t stream = nullptr, own_stream = nullptr;
     // device memory
     uint8_t* D = nullptr;
@@ -137,6 +137,8 @@ struct fdl_ctx {
     double *cr = nullptr, *cz = nullptr, *cp = nullptr, *cy = nullptr;
     double *Ak = nullptr, *An = nullptr, *At = nullptr;  // carried L^W X^k, L^W X^{k+1}, L^W Xt
     double *Xprev = nullptr, *Aprev = nullptr;           // X^{k-1}, L^W X^{k-1} (PCG start extrapolation)
+    double* spart_enum = nullptr;  // [item][kEnumNC] enumerating-strategy stress partials
+    double* enum_f = nullptr;      // [kEnumMax] candidate stresses
     double* omega_v = nullptr;   // per-vertex relax factors (fdl_set_omega_vertex), device
     double omega_v_max = 0.0;
     bool a_valid = false;
@@ -611,7 +613,17 @@ fdl_status check_params(const fdl_params* p, std::string& msg)
         msg = "only weight_exp = -2 (w = d^-2, P:250) is implemented";
         return FDL_E_UNSUPPORTED;
     }
-    if (p->strategy != FDL_STRAT_FIXED && p->strategy != FDL_STRAT_PROB) {
+    if (p->strategy == FDL_STRAT_ENUM) {
+        if (p->enum_count < 1 || p->enum_count > kEnumMax || !(p->enum_step > 0.0) || !std::isfinite(p->enum_step)) {
+            msg = "enum_count must be in 1..32 and enum_step > 0";
+            return FDL_E_INVALID_ARG;
+        }
+        if (std::isfinite(p->step)) {
+            msg = "the enumerating strategy does not take a step cap";
+            return FDL_E_UNSUPPORTED;
+        }
+    }
+    if (p->strategy != FDL_STRAT_FIXED && p->strategy != FDL_STRAT_PROB && p->strategy != FDL_STRAT_ENUM) {
         msg = "unknown strategy";
         return FDL_E_INVALID_ARG;
     }
@@ -722,6 +734,11 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     FDL_ALLOC(ctx->ipart, (size_t)std::max(ctx->nitems, 1) * kT * Cmax);
     FDL_ALLOC(ctx->spart, (size_t)std::max(ctx->nitems, 1) * 2);
     FDL_ALLOC(ctx->sparts, (size_t)2 * world);
+    if (p.strategy == FDL_STRAT_ENUM) {
+        if (world > 1) return set_err(ctx, FDL_E_UNSUPPORTED, "the enumerating strategy runs on one GPU");
+        FDL_ALLOC(ctx->spart_enum, (size_t)std::max(ctx->nitems, 1) * kEnumNC);
+        FDL_ALLOC(ctx->enum_f, (size_t)kEnumMax);
+    }
     if (world > 1 && !ctx->emulated) FDL_ALLOC(ctx->rparts, (size_t)world * ctx->npad * Cmax);
     FDL_ALLOC(ctx->diag, (size_t)ctx->npad);
     FDL_ALLOC(ctx->Xk, vn);
@@ -763,6 +780,7 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
         ctx->grid_p1[s] = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymP1, dim, s, ctx->hb)));
     ctx->grid_p2 = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymP2, dim, 1, ctx->hb)));
     ctx->grid_diag = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymDiag, dim, 1, ctx->hb)));
+    ctx->grid_enum = std::max(1, std::min(cap_items, ctx->sm_count * 2));
     // Jacobi diagonal sum_{j != i} w'_ij (one symmetric DIAG pass) and sigma = mean(diag)/n
     FDL_TRY(run_sym(ctx, kSymDiag, 1, ctx->posf, ctx->diag, nullptr, 0));
     FDL_LAUNCH(launch_set_sigma_rows(ctx->diag, ctx->n, ctx->sc, ctx->stream));
@@ -799,7 +817,8 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
     if (ctx->emulated) return set_err(ctx, FDL_E_UNSUPPORTED, "emulated rank: only fdl_eval_partial is available");
     if (ctx->broken) return set_err(ctx, FDL_E_STATE, ctx->err.empty() ? "context is broken" : ctx->err);
     if (ctx->stopped) return set_err(ctx, FDL_E_STATE, "the run has stopped; call fdl_set_positions to restart");
-    const double omega = ctx->omega_v ? ctx->omega_v_max : pick_omega(ctx);
+    const bool enumerate = ctx->p.strategy == FDL_STRAT_ENUM;
+    double omega = ctx->omega_v ? ctx->omega_v_max : (enumerate ? 0.0 : pick_omega(ctx));
     const int nsets = omega > 0.0 ? 2 : 1;
     const int dim = ctx->dim, n = ctx->n;
     const int pq = ps_p2(dim), ps = ps_p1(dim, nsets);
@@ -844,19 +863,53 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
         ++cg;
     }
     // carried L^W X^{k+1} and L^W Xt (before Rk is replaced by the select)
-    FDL_LAUNCH(launch_carry_a(ctx->Rk, ctx->cr, ctx->Ak, ctx->An, ctx->At, ctx->sc, n, dim, omega, s));
+    FDL_LAUNCH(launch_carry_a(ctx->Rk, ctx->cr, ctx->Ak, ctx->An, ctx->At, ctx->sc, n, dim, enumerate ? 0.0 : omega,
+                              s));
     // ---- pin x_0 = 0, then line 5: Xt = (1+w) X^{k+1} - w X^k (Eq. 10)
     FDL_LAUNCH(launch_get_pin(ctx->Xn, ctx->pin_slots, 0, dim, 1, s));
-    FDL_LAUNCH(launch_combine(ctx->Xk, ctx->Xn, ctx->Xt, ctx->posf, ctx->blk_max, ctx->pin_slots, n, 0, dim, omega, ctx->omega_v,
-                              ctx->cap, nsets, ps, s));
-    if (ctx->p.cg_extrap)  // ratio of successive corrections for the next start; X^{k-1} <- X^k
-        FDL_LAUNCH(launch_rho(ctx->Xn, ctx->Xk, ctx->Xprev, ctx->Ak, ctx->Aprev, ctx->blk_cg, n, dim,
-                              ctx->ext_ok ? 1 : 0, ctx->sc, s));
-    // ---- line 6: f(Xt), f(X^{k+1}) and the next right-hand side, one fused pass
-    FDL_TRY(run_sym(ctx, kSymP1, nsets, ctx->posf, ctx->R1, ctx->R2, 0));
-    // ---- lines 6-8: guard
-    FDL_LAUNCH(launch_select(ctx->Xk, ctx->Rk, ctx->Xn, ctx->Xt, ctx->R1, ctx->R2, ctx->blk_max, n, dim, nsets,
-                             ctx->sc, ctx->Ak, ctx->An, ctx->At, s));
+    if (enumerate) {
+        // lines 286-288: stress of every candidate w_c in multi-candidate passes over
+        // the hop tiles, omega* = first argmin, then stress + R of X~(omega*)
+        FDL_LAUNCH(launch_enum_stage(ctx->Xk, ctx->Xn, ctx->posf, ctx->blk_max, ctx->pin_slots, n, dim, 2 * pq, s));
+        if (ctx->p.cg_extrap)
+            FDL_LAUNCH(launch_rho(ctx->Xn, ctx->Xk, ctx->Xprev, ctx->Ak, ctx->Aprev, ctx->blk_cg, n, dim,
+                                  ctx->ext_ok ? 1 : 0, ctx->sc, s));
+        const int m = ctx->p.enum_count;
+        for (int c0 = 0; c0 < m; c0 += kEnumNC) {
+            EnumOmegas w;
+            for (int k = 0; k < kEnumNC; ++k) w.w[k] = (float)(ctx->p.enum_step * std::min(c0 + k, m - 1));
+            SymArgs a;
+            a.D = ctx->D;
+            a.pos = ctx->posf;
+            a.jpart = nullptr;
+            a.ipart = nullptr;
+            a.spart = ctx->spart_enum;
+            a.items = ctx->items;
+            a.nitems = ctx->nitems;
+            a.n = ctx->n;
+            a.magic = 0x4B000000u;
+            if (ctx->nitems > 0) FDL_LAUNCH(launch_enum(a, w, dim, ctx->hb, ctx->grid_enum, s));
+            FDL_LAUNCH(launch_sym_stress(ctx->spart_enum, ctx->nitems, kEnumNC, ctx->enum_f + c0, s));
+        }
+        FDL_LAUNCH(launch_enum_pick(ctx->enum_f, m, ctx->p.enum_step, ctx->sc, s));
+        FDL_LAUNCH(launch_enum_apply(ctx->Xn, ctx->Xk, ctx->An, ctx->Ak, ctx->Xt, ctx->At, ctx->posf, ctx->sc, n, dim,
+                                     ps_p1(dim, 1), s));
+        FDL_TRY(run_sym(ctx, kSymP1, 1, ctx->posf, ctx->R1, nullptr, 0));
+        // X^{k+1} <- X~(omega*) (omega* = 0 is X^{k+1} itself)
+        FDL_LAUNCH(launch_select(ctx->Xk, ctx->Rk, ctx->Xt, ctx->Xt, ctx->R1, ctx->R1, ctx->blk_max, n, dim, 1, ctx->sc,
+                                 ctx->Ak, ctx->At, ctx->At, s));
+    } else {
+        FDL_LAUNCH(launch_combine(ctx->Xk, ctx->Xn, ctx->Xt, ctx->posf, ctx->blk_max, ctx->pin_slots, n, 0, dim, omega,
+                                  ctx->omega_v, ctx->cap, nsets, ps, s));
+        if (ctx->p.cg_extrap)  // ratio of successive corrections for the next start; X^{k-1} <- X^k
+            FDL_LAUNCH(launch_rho(ctx->Xn, ctx->Xk, ctx->Xprev, ctx->Ak, ctx->Aprev, ctx->blk_cg, n, dim,
+                                  ctx->ext_ok ? 1 : 0, ctx->sc, s));
+        // ---- line 6: f(Xt), f(X^{k+1}) and the next right-hand side, one fused pass
+        FDL_TRY(run_sym(ctx, kSymP1, nsets, ctx->posf, ctx->R1, ctx->R2, 0));
+        // ---- lines 6-8: guard
+        FDL_LAUNCH(launch_select(ctx->Xk, ctx->Rk, ctx->Xn, ctx->Xt, ctx->R1, ctx->R2, ctx->blk_max, n, dim, nsets,
+                                 ctx->sc, ctx->Ak, ctx->An, ctx->At, s));
+    }
     ctx->a_valid = true;
     ctx->ext_ok = ctx->p.cg_extrap != 0;
     mark_end(ctx, mstep);
@@ -868,10 +921,17 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
 
     const DevScalars& h = *ctx->sc_host;
     const double f_before = ctx->f;
-    const double f_next = h.f_set[0];
-    const double f_rel = nsets == 2 ? h.f_set[1] : NAN;
-    const bool accepted = nsets == 2 && (f_rel <= f_next);
-    const double f_after = accepted ? f_rel : f_next;
+    double f_next = h.f_set[0];
+    double f_rel = nsets == 2 ? h.f_set[1] : NAN;
+    bool accepted = nsets == 2 && (f_rel <= f_next);
+    double f_after = accepted ? f_rel : f_next;
+    if (enumerate) {  // candidate stresses from the enumeration pass; f_after from the chosen point's P1 pass
+        omega = h.omega_star;
+        accepted = h.enum_best > 0;
+        f_next = h.enum_f0;
+        f_rel = h.enum_fbest;
+        f_after = h.f_set[0];
+    }
     ctx->iterations++;
     ctx->f = f_after;
     fdl_iter_info inf{};
@@ -934,6 +994,8 @@ void fdl_params_default(fdl_params* p)
     p->a_refresh = 10;
     p->hop_bits = 0;
     p->cg_extrap = 1;
+    p->enum_count = 19;
+    p->enum_step = 0.5;
 }
 
 const char* fdl_status_str(fdl_status s)

@@ -36,6 +36,9 @@ struct DevScalars {
     double S[4];           // sum_i p_i per column (rank-one term of the regularised operator)
     double Sd[4];          // sum_i d_i of the PCG correction d = x - x0 (for the carried L^W X)
     double rho;            // PCG start extrapolation ratio (k_rho)
+    double omega_star;     // enumerating strategy: chosen relax factor
+    int enum_best;         // ... and its candidate index
+    double enum_f0, enum_fbest;  // ... stress of candidate 0 (X^{k+1}) and of the chosen one
     double sigma;          // regularisation weight: (L + sigma 1 1^T), sigma = mean(diag)/n
     int active[4];
     int done;
@@ -67,6 +70,11 @@ cudaError_t launch_extrap(const double* Xk, const double* Xprev, const double* A
                           double* y0, const DevScalars* sc, int n, int dim, int valid, cudaStream_t s);
 cudaError_t launch_rho(const double* Xn, const double* Xk, double* Xprev, const double* Ak, double* Aprev,
                        double* blk, int n, int dim, int valid, DevScalars* sc, cudaStream_t s);
+cudaError_t launch_enum_stage(const double* Xk, double* Xn, float* posf, double* blk_max, const double* xpin, int n,
+                              int dim, int ps, cudaStream_t s);
+cudaError_t launch_enum_pick(const double* fs, int m, double step, DevScalars* sc, cudaStream_t s);
+cudaError_t launch_enum_apply(const double* Xn, const double* Xk, const double* An, const double* Ak, double* Xt,
+                              double* At, float* posf, const DevScalars* sc, int n, int dim, int ps, cudaStream_t s);
 cudaError_t launch_get_pin(const double* x, double* slots, int rank, int dim, int owns_row0, cudaStream_t s);
 cudaError_t launch_select(double* Xk, double* Rk, const double* Xn, const double* Xt, const double* R1,
                           const double* R2, const double* blk_max, int nloc, int dim, int nsets,
@@ -139,6 +147,14 @@ struct SymArgs {
 };
 
 cudaError_t launch_sym(const SymArgs& a, int mode, int dim, int nsets, int hb, int grid, cudaStream_t s);
+
+// enumerating strategy: stress of kEnumNC relaxed candidates per pass
+constexpr int kEnumNC = 10;  // 19 paper candidates -> 2 passes
+constexpr int kEnumMax = 32;
+struct EnumOmegas {
+    float w[kEnumNC];
+};
+cudaError_t launch_enum(const SymArgs& a, const EnumOmegas& w, int dim, int hb, int grid, cudaStream_t s);
 int sym_max_ctas(int mode, int dim, int nsets, int hb);
 cudaError_t launch_sym_reduce(const double* ipart, const float* jpart, const int* it_lo, const int* it_hi, int nb,
                               int64_t t0, int64_t t1, int C, int D, int inter, double* out0, double* out1,

@@ -131,6 +131,87 @@ cudaError_t launch_combine(const double* Xk, double* Xn, double* Xt, float* posf
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------ enumerating strategy
+// Pin X^{k+1} (x_0 = 0) and stage {x'(dim), D(dim)} per vertex for
+// k_enum, D = X^{k+1} - X^k; block maxima of |D_i|^2 (maxdisp diagnostic).
+__global__ void __launch_bounds__(kRB) k_enum_stage(const double* __restrict__ Xk, double* Xn, float* posf,
+                                                    double* blk_max, const double* __restrict__ xpin, int n,
+                                                    int dim, int ps)
+{
+    __shared__ double red[8];
+    const int i = blockIdx.x * kRB + threadIdx.x;
+    double disp2 = 0.0;
+    if (i < n) {
+        const int64_t g = stage_slot(i);
+        for (int q = 0; q < dim; ++q) {
+            const size_t k = (size_t)i * dim + q;
+            const double xn = Xn[k] - xpin[q];
+            Xn[k] = xn;
+            const double dq = xn - Xk[k];
+            disp2 += dq * dq;
+            posf[g * ps + q] = (float)xn;
+            posf[g * ps + ps / 2 + q] = (float)dq;
+        }
+        for (int q = dim; q < ps / 2; ++q) posf[g * ps + q] = posf[g * ps + ps / 2 + q] = 0.0f;
+    }
+    const double m = block_max_256(disp2, red);
+    if (threadIdx.x == 0) blk_max[blockIdx.x] = m;
+}
+
+cudaError_t launch_enum_stage(const double* Xk, double* Xn, float* posf, double* blk_max, const double* xpin, int n,
+                              int dim, int ps, cudaStream_t s)
+{
+    k_enum_stage<<<(n + kRB - 1) / kRB, kRB, 0, s>>>(Xk, Xn, posf, blk_max, xpin, n, dim, ps);
+    return cudaGetLastError();
+}
+
+// omega* = the first (smallest) argmin of the candidates' stresses (lines
+// 286-288; ties to the smaller omega).  Candidate 0 is omega = 0.
+__global__ void k_enum_pick(const double* __restrict__ fs, int m, double step, DevScalars* sc)
+{
+    if (threadIdx.x != 0) return;
+    int best = 0;
+    for (int c = 1; c < m; ++c)
+        if (fs[c] < fs[best]) best = c;
+    sc->omega_star = step * best;
+    sc->enum_best = best;
+    sc->enum_f0 = fs[0];
+    sc->enum_fbest = fs[best];
+}
+
+cudaError_t launch_enum_pick(const double* fs, int m, double step, DevScalars* sc, cudaStream_t s)
+{
+    k_enum_pick<<<1, 32, 0, s>>>(fs, m, step, sc);
+    return cudaGetLastError();
+}
+
+// X~ = X^{k+1} + w* (X^{k+1} - X^k), L^W X~ = (1 + w*) L^W X^{k+1} - w* L^W X^k
+// (carried, L linear), staged fp32 X~ for the P1 pass of the chosen point.
+__global__ void k_enum_apply(const double* __restrict__ Xn, const double* __restrict__ Xk,
+                             const double* __restrict__ An, const double* __restrict__ Ak, double* Xt, double* At,
+                             float* posf, const DevScalars* __restrict__ sc, int n, int dim, int ps)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double w = sc->omega_star;
+    const int64_t g = stage_slot(i);
+    for (int q = 0; q < dim; ++q) {
+        const size_t k = (size_t)i * dim + q;
+        const double xt = w == 0.0 ? Xn[k] : (1.0 + w) * Xn[k] - w * Xk[k];
+        Xt[k] = xt;
+        At[k] = w == 0.0 ? An[k] : (1.0 + w) * An[k] - w * Ak[k];
+        posf[g * ps + q] = (float)xt;
+    }
+    for (int q = dim; q < ps; ++q) posf[g * ps + q] = 0.0f;
+}
+
+cudaError_t launch_enum_apply(const double* Xn, const double* Xk, const double* An, const double* Ak, double* Xt,
+                              double* At, float* posf, const DevScalars* sc, int n, int dim, int ps, cudaStream_t s)
+{
+    k_enum_apply<<<(n + 255) / 256, 256, 0, s>>>(Xn, Xk, An, Ak, Xt, At, posf, sc, n, dim, ps);
+    return cudaGetLastError();
+}
+
 // x_0 of the CG solution (global row 0 lives on the rank with row0 == 0) into
 // slot `rank` of a world x 4 buffer (all-gathered across ranks afterwards).
 __global__ void k_get_pin(const double* __restrict__ x, double* slots, int rank, int dim, int owns_row0)

@@ -645,6 +645,249 @@ cudaError_t launch_sym(const SymArgs& a, int mode, int dim, int nsets, int hb, i
     return cudaErrorInvalidValue;
 }
 
+// ------------------------------------------------------ enumerating strategy
+// Stress of NC relaxed candidates X~(w_c) = X^{k+1} + w_c (X^{k+1} - X^k) in
+// one pass over the stored triangle (the exhaustive
+// search over the relax factor).  Staged per vertex: {x'(DIM), D(DIM)} with
+// x' = X^{k+1}, D = X^{k+1} - X^k (padded to 4 / 8 floats), so per pair
+// delta(w) = (x'_i - x'_j) + w (D_i - D_j) exactly as Eq. 10 forms it, and
+// s_c += (|delta(w_c)| / h - 1)^2 (Eq. 1, w' d'^2 = 1).  No force outputs:
+// only per-item stress partials [item][NC].  MUFU (rsqrt) bound: one per
+// candidate per pair.
+template <int DIM>
+__host__ __device__ constexpr int enum_ps()
+{
+    return DIM == 2 ? 4 : 8;
+}
+
+template <int DIM, int HB>
+__host__ __device__ constexpr int enum_stage_bytes()
+{
+    return (int)tile_bytes(HB) + kT * enum_ps<DIM>() * 4;
+}
+
+constexpr int kEnumStages = 3;
+
+template <int DIM, int NC, bool SAFE>
+__device__ __forceinline__ void enum_pair(const float* xi, const float* xj, float h2, bool valid, const float* om,
+                                          float* sf)
+{
+    float dp[DIM], dd[DIM];
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+        dp[c] = xi[c] - xj[c];
+        dd[c] = xi[DIM + c] - xj[DIM + c];
+    }
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        float r2 = FLT_MIN;
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+            const float d = fmaf(om[k], dd[c], dp[c]);
+            r2 = fmaf(d, d, r2);
+        }
+        const float q = rsqrt_approx(r2 * h2);
+        float u = fmaf(r2, q, -1.0f);
+        if (SAFE) u = valid ? u : 0.0f;
+        sf[k] = fmaf(u, u, sf[k]);
+    }
+}
+
+template <int DIM, int HB, int NC, bool SAFE>
+__device__ __forceinline__ void enum_tile(const uint8_t* sD, const float* sP, const float2* lut2, uint32_t magic,
+                                          int ty, int tx, bool diag, const float (&xi)[8][2 * DIM], const float* om,
+                                          float* sf)
+{
+    constexpr int PS = enum_ps<DIM>();
+    constexpr int NCH = HB ? 4 * HB : 2;
+    constexpr int CPC = HB ? 2 / HB : 4;
+    const int tid = tx * 16 + ty;
+#pragma unroll 1
+    for (int kc = 0; kc < NCH; ++kc) {
+        const uint4 ch = *reinterpret_cast<const uint4*>(sD + ((size_t)kc * 256 + tid) * 16);
+#pragma unroll
+        for (int cc = 0; cc < CPC; ++cc) {
+            const int c = kc * CPC + cc;
+            const int jl = tx * 8 + c;
+            const int js = c * 16 + tx;
+            float xj[PS];
+#pragma unroll
+            for (int q = 0; q < PS / 4; ++q) {
+                const float4 t = *reinterpret_cast<const float4*>(sP + js * PS + 4 * q);
+                xj[4 * q] = t.x; xj[4 * q + 1] = t.y; xj[4 * q + 2] = t.z; xj[4 * q + 3] = t.w;
+            }
+            float xjc[2 * DIM];
+#pragma unroll
+            for (int q = 0; q < DIM; ++q) {
+                xjc[q] = xj[q];
+                xjc[DIM + q] = xj[(PS / 2) + q];
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                float h2;
+                if (HB == 0) {
+                    const float2 e = *reinterpret_cast<const float2*>(
+                        reinterpret_cast<const char*>(lut2) +
+                        ((r >> 1) == 0 ? ((word_of(ch, cc) << 3) & 0x7f8u)
+                                       : ((word_of(ch, cc) >> (8 * (r >> 1) - 3)) & 0x7f8u)));
+                    h2 = (r & 1) ? e.y : e.x;
+                } else {
+                    const float hf = chunk_hop<HB>(ch, r, cc, magic);
+                    h2 = hf * hf;
+                }
+                bool valid = true;
+                if (SAFE) valid = (h2 > 0.0f) && (!diag || (ty * 8 + r < jl));
+                enum_pair<DIM, NC, SAFE>(&xi[r][0], xjc, h2, valid, om, sf);
+            }
+        }
+    }
+}
+
+template <int DIM, int HB, int NC>
+__global__ void __launch_bounds__(256, 2) k_enum(const SymArgs a, const EnumOmegas w)
+{
+    constexpr int PS = enum_ps<DIM>();
+    constexpr int STAGE = enum_stage_bytes<DIM, HB>();
+    constexpr int DT = (int)tile_bytes(HB);
+    constexpr int NST = kEnumStages;
+    constexpr int NW = 8;
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t full[NST];
+    __shared__ int drained[NST];
+    __shared__ int prod[2];
+    __shared__ double sred[8][NC];
+    __shared__ float2 lut2[HB == 0 ? 256 : 1];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int ty = lane & 15, tx = tid >> 4;
+    if ((int)blockIdx.x >= a.nitems) return;
+    if (HB == 0) {
+        const int lo = (int)nib_decode_lo((uint32_t)tid), hi = (int)nib_decode_hi((uint32_t)tid);
+        lut2[tid] = make_float2((float)(lo * lo), (float)(hi * hi));
+    }
+    float om[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) om[k] = w.w[k];
+    auto issue = [&](int stage) {
+        int p_item = prod[0], p_t = prod[1];
+        if (p_item >= a.nitems) return;
+        const int4 it = a.items[p_item];
+        const int J = it.y + p_t;
+        const int64_t lt = (int64_t)it.w + p_t;
+        uint8_t* base = smem + (size_t)stage * STAGE;
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&full[stage], STAGE);
+        tma_load_1d(base, a.D + lt * DT, DT, &full[stage]);
+        tma_load_1d(base + DT, a.pos + (int64_t)J * kT * PS, kT * PS * 4, &full[stage]);
+        if (++p_t == it.z) {
+            p_t = 0;
+            p_item += gridDim.x;
+        }
+        prod[0] = p_item;
+        prod[1] = p_t;
+    };
+    if (tid == 0) {
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&full[s], 1);
+            drained[s] = 0;
+        }
+        fence_mbar_init();
+        prod[0] = blockIdx.x;
+        prod[1] = 0;
+        for (int s = 0; s < NST; ++s) issue(s);
+    }
+    __syncthreads();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
+        const int4 it = a.items[item];
+        const int I = it.x;
+        float xi[8][2 * DIM];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int64_t gi = stage_slot((int64_t)I * kT + ty * 8 + r);
+#pragma unroll
+            for (int q = 0; q < DIM; ++q) {
+                xi[r][q] = a.pos[gi * PS + q];
+                xi[r][DIM + q] = a.pos[gi * PS + PS / 2 + q];
+            }
+        }
+        double s64[NC];
+#pragma unroll
+        for (int k = 0; k < NC; ++k) s64[k] = 0.0;
+        for (int t = 0; t < it.z; ++t) {
+            const int J = it.y + t;
+            const bool diag = (J == I);
+            const bool safe = diag || (int64_t)(J + 1) * kT > a.n || (int64_t)(I + 1) * kT > a.n;
+            mbar_wait(&full[stage], phase);
+            const uint8_t* sD = smem + (size_t)stage * STAGE;
+            const float* sP = reinterpret_cast<const float*>(sD + DT);
+            float sf[NC];
+#pragma unroll
+            for (int k = 0; k < NC; ++k) sf[k] = 0.0f;
+            if (safe)
+                enum_tile<DIM, HB, NC, true>(sD, sP, lut2, a.magic, ty, tx, diag, xi, om, sf);
+            else
+                enum_tile<DIM, HB, NC, false>(sD, sP, lut2, a.magic, ty, tx, diag, xi, om, sf);
+#pragma unroll
+            for (int k = 0; k < NC; ++k) s64[k] += (double)sf[k];
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                if (atomicAdd(&drained[stage], 1) == NW - 1) {
+                    __threadfence_block();
+                    drained[stage] = 0;
+                    issue(stage);
+                }
+            }
+            if (++stage == NST) {
+                stage = 0;
+                phase ^= 1u;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+            double v = s64[k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) sred[wid][k] = v;
+        }
+        __syncthreads();
+        if (tid < NC) {
+            double v = 0.0;
+            for (int ww = 0; ww < NW; ++ww) v += sred[ww][tid];
+            a.spart[(size_t)item * NC + tid] = v;
+        }
+        __syncthreads();
+    }
+}
+
+template <int DIM, int HB>
+static cudaError_t launch_enum_t(const SymArgs& a, const EnumOmegas& w, int grid, cudaStream_t s)
+{
+    constexpr size_t sm = (size_t)kEnumStages * enum_stage_bytes<DIM, HB>();
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_enum<DIM, HB, kEnumNC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sm);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_enum<DIM, HB, kEnumNC><<<grid, 256, sm, s>>>(a, w);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_enum(const SymArgs& a, const EnumOmegas& w, int dim, int hb, int grid, cudaStream_t s)
+{
+    if (dim == 2) {
+        if (hb == 0) return launch_enum_t<2, 0>(a, w, grid, s);
+        if (hb == 1) return launch_enum_t<2, 1>(a, w, grid, s);
+        return launch_enum_t<2, 2>(a, w, grid, s);
+    }
+    if (hb == 0) return launch_enum_t<3, 0>(a, w, grid, s);
+    if (hb == 1) return launch_enum_t<3, 1>(a, w, grid, s);
+    return launch_enum_t<3, 2>(a, w, grid, s);
+}
+
 template <int MODE, int DIM, int NSETS, int HB>
 static int sym_occ_t()
 {

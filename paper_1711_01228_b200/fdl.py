@@ -23,7 +23,7 @@ STATUS = {
     -13: "FDL_E_UNSUPPORTED", -14: "FDL_E_STATE",
 }
 STOP = {0: "none", 1: "rel_tol", 2: "zero_stress", 3: "max_iter"}
-STRAT_FIXED, STRAT_PROB = 0, 1
+STRAT_FIXED, STRAT_PROB, STRAT_ENUM = 0, 1, 2
 
 EXPORTS = [
     "fdl_abi_version", "fdl_params_default", "fdl_create", "fdl_create_sharded", "fdl_shard_tiles",
@@ -48,7 +48,7 @@ class Params(ctypes.Structure):
         ("max_iter", ctypes.c_int32), ("weight_exp", ctypes.c_double), ("cg_rtol", ctypes.c_double),
         ("cg_max_iter", ctypes.c_int32), ("strategy", ctypes.c_int32), ("seed", ctypes.c_uint64),
         ("device", ctypes.c_int32), ("a_refresh", ctypes.c_int32), ("hop_bits", ctypes.c_int32),
-        ("cg_extrap", ctypes.c_int32),
+        ("cg_extrap", ctypes.c_int32), ("enum_count", ctypes.c_int32), ("enum_step", ctypes.c_double),
     ]
 
 
@@ -146,13 +146,15 @@ def params_default() -> Params:
 
 
 def make_params(dim=2, k=0.0, omega=1.5, step=math.inf, tol=1e-4, max_iter=500, cg_rtol=0.0,
-                cg_max_iter=0, strategy=STRAT_FIXED, seed=1, device=0, a_refresh=0, hop_bits=0, cg_extrap=1) -> Params:
+                cg_max_iter=0, strategy=STRAT_FIXED, seed=1, device=0, a_refresh=0, hop_bits=0, cg_extrap=1, enum_count=19,
+                enum_step=0.5) -> Params:
     p = params_default()
     p.dim, p.k, p.omega, p.step, p.tol, p.max_iter = dim, k, omega, step, tol, max_iter
     p.cg_rtol, p.cg_max_iter, p.strategy, p.seed, p.device = cg_rtol, cg_max_iter, strategy, seed, device
     p.a_refresh = a_refresh
     p.hop_bits = hop_bits
     p.cg_extrap = cg_extrap
+    p.enum_count, p.enum_step = enum_count, enum_step
     return p
 
 

@@ -395,3 +395,57 @@ def test_per_vertex_omega(name):
     r = L.run_until_converged()
     o = layout.run_algorithm2(layout.Problem(g, 2, k), X0, w, cfg.tol, cfg.max_iter)
     _gates(r.iterations, r.f_final, o)
+
+
+# ------------------------------------------------- NEXT-2: enumerating strategy
+def test_enumerating_strategy_one_step():
+    """Lines 286-288: the GPU's multi-candidate pass gives every candidate's
+    stress f((1+w_c) X^{k+1} - w_c X^k), w_c in {0, 0.5, ..., 9}, within the
+    stress tolerance of the fp64 oracle, and picks an argmin (ties within the
+    tolerance may resolve either way)."""
+    from oracle import strategies
+    cfg = configs.CONFIGS["C2"]
+    g, k, X0, L = make("C2", strategy=fdl.STRAT_ENUM)
+    info = L.step()
+    prob = layout.Problem(g, 2, k)
+    Xn = prob.H(layout.pin(X0.astype(np.float64)))
+    w, fbest, fs = strategies.enumerate_omega(prob, Xn, layout.pin(X0.astype(np.float64)))
+    c = int(round(info.omega / 0.5))
+    assert abs(info.f_next - fs[0]) / fs[0] <= STRESS_TOL * 10
+    assert abs(info.f_relaxed - fs[c]) / fs[c] <= STRESS_TOL * 10
+    assert fs[c] <= fbest * (1 + 1e-5)
+    assert abs(info.f_after - fs[c]) / fs[c] <= STRESS_TOL * 10
+    np.testing.assert_allclose(L.get_positions(), (1 + info.omega) * Xn - info.omega * layout.pin(X0.astype(np.float64)),
+                               rtol=0, atol=1e-5 * np.abs(Xn).max())
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_enumerating_strategy_end_to_end(name):
+    """Enumerating strategy end to end against the oracle (gates of §8(c)); f is
+    non-increasing (omega = 0 is a candidate)."""
+    from oracle import strategies
+    cfg = configs.CONFIGS[name]
+    g, k, X0, L = make(name, strategy=fdl.STRAT_ENUM)
+    fs = []
+    while True:
+        info = L.step()
+        fs.append(info.f_after)
+        if info.stop:
+            break
+    prob = layout.Problem(g, 2, k)
+    # the oracle's Algorithm 2 with line 5 replaced by the enumeration
+    X = layout.pin(X0.astype(np.float64))
+    f = prob.f(X)
+    it = 0
+    while True:
+        it += 1
+        Xn = prob.H(X)
+        w, fn, _ = strategies.enumerate_omega(prob, Xn, X)
+        X = (1 + w) * Xn - w * X
+        dec = (f - fn) / f
+        f = fn
+        if f == 0 or dec < cfg.tol or it == cfg.max_iter:
+            break
+    assert abs(fs[-1] - f) / f <= 1e-3, (fs[-1], f)
+    assert abs(len(fs) - it) <= max(1, math.ceil(0.05 * it)), (len(fs), it)
+    assert all(b <= a * (1 + 1e-9) for a, b in zip([L.info.f] + fs, fs))
