@@ -419,6 +419,8 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
     if (ctx->world == 1 || ctx->emulated) {
         FDL_LAUNCH(launch_sym_reduce(ctx->ipart, ctx->jpart, ctx->it_lo, ctx->it_hi, ctx->nb, ctx->t0, ctx->t1, C, D0,
                                      inter, out0, out1, ctx->stream));
+        if (mode == kSymP2)  // product form: L^W p = diag p - sum_j w p_j (rank-local diag when emulated)
+            FDL_LAUNCH(launch_p2_finish(out0, pos, ctx->diag, ctx->n, dim, ps_p2(dim), ctx->stream));
         if (mode == kSymP1) {
             FDL_LAUNCH(launch_sym_stress(ctx->spart, ctx->nitems, nsets, ctx->sparts, ctx->stream));
             FDL_LAUNCH(launch_stress_ranks(ctx->sparts, 1, nsets, ctx->sc, set_cur, ctx->stream));
@@ -431,6 +433,7 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
                                  mine, nullptr, ctx->stream));
     FDL_TRY(allgather_inplace(ctx, ctx->rparts, slice, ncclFloat64, 8));
     FDL_LAUNCH(launch_rank_sum(ctx->rparts, ctx->world, ctx->npad, C, D0, inter, out0, out1, ctx->stream));
+    if (mode == kSymP2) FDL_LAUNCH(launch_p2_finish(out0, pos, ctx->diag, ctx->n, dim, ps_p2(dim), ctx->stream));
     if (mode == kSymP1) {
         FDL_LAUNCH(launch_sym_stress(ctx->spart, ctx->nitems, nsets, ctx->sparts + 2 * ctx->rank, ctx->stream));
         FDL_TRY(allgather_inplace(ctx, ctx->sparts, 2, ncclFloat64, 8));
@@ -829,7 +832,7 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
     // P2 pass every a_refresh steps (bounds the fp32 drift of the carried value).
     // per-vertex omega: Xt is not a scalar combination, At cannot be carried
     const bool refresh = !ctx->a_valid || ctx->a_age + 1 >= ctx->p.a_refresh || ctx->omega_v;
-    FDL_LAUNCH(launch_cg_begin(ctx->Xk, ctx->Xn, ctx->pvec, n, 0, dim, pq, s));
+    FDL_LAUNCH(launch_cg_begin(ctx->Xk, ctx->Xn, ctx->pvec, n, 0, dim, pq, ctx->sc, s));
     if (refresh) {
         FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->Ak, nullptr, 0));
         ctx->a_age = 0;
@@ -845,6 +848,7 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
     FDL_LAUNCH(launch_cg_init(y0, ctx->Rk, ctx->diag, ctx->cr, ctx->cz, ctx->cp, ctx->pvec, ctx->blk_cg, ctx->nblk,
                               n, dim, pq, s));
     FDL_LAUNCH(launch_cg_finalize(ctx->blk_cg, ctx->nblk, dim, 0, ctx->p.cg_rtol, ctx->sc, ctx->hs_dev, s));
+    FDL_LAUNCH(launch_stage_p(ctx->cp, ctx->pvec, ctx->sc, n, dim, pq, s));
     FDL_CUDA(cudaStreamSynchronize(s));
     int cg = 0;
     while (!ctx->hs->done) {
@@ -1213,7 +1217,7 @@ fdl_status fdl_eval_forces(fdl_ctx* ctx, double* R, double* A, double* stress)
     if (R) FDL_TRY(fetch(ctx->Rk, R));
     if (A) {
         // A = L^W X: one symmetric P2 pass with p = X
-        FDL_LAUNCH(launch_cg_begin(ctx->Xk, ctx->cy, ctx->pvec, ctx->n, 0, dim, ps_p2(dim), ctx->stream));
+        FDL_LAUNCH(launch_cg_begin(ctx->Xk, ctx->cy, ctx->pvec, ctx->n, 0, dim, ps_p2(dim), ctx->sc, ctx->stream));
         FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->cy, nullptr, 0));
         FDL_TRY(fetch(ctx->cy, A));
         collect_events(ctx);
@@ -1237,7 +1241,7 @@ fdl_status fdl_eval_partial(fdl_ctx* ctx, int32_t mode, const double* X, double*
         FDL_LAUNCH(launch_stage_pos1(ctx->Xt, ctx->posf, ctx->n, 0, dim, ps_p1(dim, 1), ctx->stream));
         FDL_TRY(run_sym(ctx, kSymP1, 1, ctx->posf, ctx->R1, nullptr, 0));
     } else {
-        FDL_LAUNCH(launch_cg_begin(ctx->Xt, ctx->R1, ctx->pvec, ctx->n, 0, dim, ps_p2(dim), ctx->stream));
+        FDL_LAUNCH(launch_cg_begin(ctx->Xt, ctx->R1, ctx->pvec, ctx->n, 0, dim, ps_p2(dim), ctx->sc, ctx->stream));
         FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->R1, nullptr, 0));
     }
     FDL_CUDA(cudaMemcpyAsync(out, ctx->R1, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));

@@ -39,6 +39,8 @@ struct DevScalars {
     double omega_star;     // enumerating strategy: chosen relax factor
     int enum_best;         // ... and its candidate index
     double enum_f0, enum_fbest;  // ... stress of candidate 0 (X^{k+1}) and of the chosen one
+    double cmean[4];       // column means of the staged X (centring of the product-form P2 input)
+    double inv_n;          // 1 / n
     double sigma;          // regularisation weight: (L + sigma 1 1^T), sigma = mean(diag)/n
     int active[4];
     int done;
@@ -80,7 +82,11 @@ cudaError_t launch_select(double* Xk, double* Rk, const double* Xn, const double
                           const double* R2, const double* blk_max, int nloc, int dim, int nsets,
                           DevScalars* sc, double* Ak, const double* An, const double* At, cudaStream_t s);
 cudaError_t launch_cg_begin(const double* Xk, double* x, float* pvec, int nloc, int row0, int dim,
-                            int pq, cudaStream_t s);
+                            int pq, DevScalars* sc, cudaStream_t s);
+cudaError_t launch_stage_p(const double* p, float* pvec, const DevScalars* sc, int n, int dim, int pq,
+                           cudaStream_t s);
+cudaError_t launch_p2_finish(double* out, const float* pvec, const double* diag, int n, int dim, int pq,
+                             cudaStream_t s);
 cudaError_t launch_cg_init(const double* y, const double* b, const double* diag, double* r, double* z,
                            double* p, float* pvec, double* blk, int nblk, int n, int dim, int pq,
                            cudaStream_t s);

@@ -389,8 +389,29 @@ cudaError_t launch_rho(const double* Xn, const double* Xk, double* Xprev, const 
     return cudaGetLastError();
 }
 
+// column means of X (one block, fixed order) -> sc->cmean: the centring of the
+// staged P2 input (product form, k_p2_finish)
+__global__ void __launch_bounds__(1024) k_colmean(const double* __restrict__ X, int n, int dim, DevScalars* sc)
+{
+    __shared__ double red[32];
+    for (int q = 0; q < dim; ++q) {
+        double v = 0.0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) v += X[(size_t)i * dim + q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+            sc->cmean[q] = t / n;
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void k_cg_begin(const double* __restrict__ Xk, double* x, float* pvec, int nloc, int row0, int dim,
-                           int pq)
+                           int pq, const DevScalars* __restrict__ sc)
 {
     const int lr = blockIdx.x * blockDim.x + threadIdx.x;
     if (lr >= nloc) return;
@@ -400,15 +421,60 @@ __global__ void k_cg_begin(const double* __restrict__ Xk, double* x, float* pvec
         if (q < dim) {
             v = Xk[(size_t)lr * dim + q];
             x[(size_t)lr * dim + q] = v;
+            v -= sc->cmean[q];
         }
         pvec[g * pq + q] = (float)v;
     }
 }
 
-cudaError_t launch_cg_begin(const double* Xk, double* x, float* pvec, int nloc, int row0, int dim, int pq,
-                            cudaStream_t s)
+// fp32 staging of the first PCG direction p = z, centred by sum(p)/n (sc->S
+// after cg_finalize mode 0)
+__global__ void k_stage_p(const double* __restrict__ p, float* pvec, const DevScalars* __restrict__ sc, int n,
+                          int dim, int pq)
 {
-    k_cg_begin<<<(nloc + kRB - 1) / kRB, kRB, 0, s>>>(Xk, x, pvec, nloc, row0, dim, pq);
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t g = stage_slot(i);
+    for (int q = 0; q < pq; ++q)
+        pvec[g * pq + q] = q < dim ? (float)(p[(size_t)i * dim + q] - sc->S[q] * sc->inv_n) : 0.0f;
+}
+
+cudaError_t launch_stage_p(const double* p, float* pvec, const DevScalars* sc, int n, int dim, int pq,
+                           cudaStream_t s)
+{
+    k_stage_p<<<(n + 255) / 256, 256, 0, s>>>(p, pvec, sc, n, dim, pq);
+    return cudaGetLastError();
+}
+
+// out_i = diag_i p'_i - S_i: the L^W matvec from the product-form pair sums
+// S_i = sum_j w_ij p'_j, with p' the same centred fp32 values the pass read.
+__global__ void k_p2_finish(double* out, const float* __restrict__ pvec, const double* __restrict__ diag, int n,
+                            int dim, int pq)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t g = stage_slot(i);
+    const double d = diag[i];
+    for (int q = 0; q < dim; ++q) {
+        const size_t k = (size_t)i * dim + q;
+        out[k] = d * (double)pvec[g * pq + q] - out[k];
+    }
+}
+
+cudaError_t launch_p2_finish(double* out, const float* pvec, const double* diag, int n, int dim, int pq,
+                             cudaStream_t s)
+{
+    k_p2_finish<<<(n + 255) / 256, 256, 0, s>>>(out, pvec, diag, n, dim, pq);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cg_begin(const double* Xk, double* x, float* pvec, int nloc, int row0, int dim, int pq,
+                            DevScalars* sc, cudaStream_t s)
+{
+    k_colmean<<<1, 1024, 0, s>>>(Xk, nloc, dim, sc);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_cg_begin<<<(nloc + kRB - 1) / kRB, kRB, 0, s>>>(Xk, x, pvec, nloc, row0, dim, pq, sc);
     return cudaGetLastError();
 }
 
@@ -430,13 +496,11 @@ __global__ void __launch_bounds__(kRB) k_cg_init(const double* __restrict__ y, c
             r[k] = rv;
             z[k] = zv;
             p[k] = zv;
-            pvec[stage_slot(i) * pq + q] = (float)zv;
             rz[q] = rv * zv;
             rr[q] = rv * rv;
             bb[q] = bv * bv;
             zs[q] = zv;
         }
-        for (int q = dim; q < pq; ++q) pvec[stage_slot(i) * pq + q] = 0.0f;
     }
     for (int q = 0; q < dim; ++q) {
         double t = block_sum_256(rz[q], red);
@@ -539,7 +603,7 @@ __global__ void k_cg_p(double* p, const double* __restrict__ z, float* pvec, con
         double pv = p[i];
         if (sc->active[q]) pv = z[i] + sc->beta[q] * pv;
         p[i] = pv;
-        pvec[g * pq + q] = (float)pv;
+        pvec[g * pq + q] = (float)(pv - sc->S[q] * sc->inv_n);  // centred (k_p2_finish)
     }
 }
 

@@ -295,21 +295,24 @@ __device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float
         }
         s[0] = fmaf(u, u, s[0]);
     } else if (MODE == kSymP2) {
-        float w = wlut;  // w' = 1/h^2 (table for u8, MUFU rcp for u16; 0 for h = 0)
+        // Product form of the L^W matvec: (L^W p)_i = diag_i p_i - sum_j w_ij p_j
+        // (P:65-68), so a pair adds w p_j to row i and w p_i to row j; the
+        // diagonal term is applied after the reduction (k_p2_finish) on the
+        // same fp32 staged values, which are centred (p - mean p; L 1 = 0) so
+        // the sums carry no common offset.
+        float w = wlut;  // w' = 1/h^2 (table for u8 / 4-bit, MUFU rcp for u16; 0 for h = 0)
         if (SAFE) w = valid ? w : 0.0f;
         const u64 wp = pk(w, w);
-        const u64 dxy = fsub2(pk(xi[0], xi[1]), pk(xj[0], xj[1]));
         float lo, hi;
-        upk(ffma2(wp, dxy, pk(ai[0], ai[1])), lo, hi);
+        upk(ffma2(wp, pk(xj[0], xj[1]), pk(ai[0], ai[1])), lo, hi);
         ai[0] = lo;
         ai[1] = hi;
-        upk(ffma2(wp, dxy, pk(aj[0], aj[1])), lo, hi);
+        upk(ffma2(wp, pk(xi[0], xi[1]), pk(aj[0], aj[1])), lo, hi);
         aj[0] = lo;
         aj[1] = hi;
         if (DIM == 3) {
-            const float dz = xi[2] - xj[2];
-            ai[2] = fmaf(w, dz, ai[2]);
-            aj[2] = fmaf(w, dz, aj[2]);
+            ai[2] = fmaf(w, xj[2], ai[2]);
+            aj[2] = fmaf(w, xi[2], aj[2]);
         }
     } else {
         float w = __frcp_rn(h2);
@@ -437,14 +440,14 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
 // row ty of half h of the warp buffer.  Output e = h * 8C + c * C + v (column
 // tx * 8 + c, component v) is the fixed-order tree sum over the 16 rows, stored
 // as fp32 jpart[tile][col][C]; the warp's outputs are one contiguous run of 16C
-// floats.  The j-side sign: P1 and P2 accumulate +term for row i and -term for
-// row j (antisymmetric); DIAG is symmetric.
+// floats.  The j-side sign: P1 accumulates +term for row i and -term for row j
+// (antisymmetric); P2 (product form) and DIAG are symmetric.
 template <int MODE, int DIM, int NSETS>
 __device__ __forceinline__ void sym_flush_warp(const float* wbuf, float* jpart_warp, int lane)
 {
     constexpr int C = sym_ncomp<MODE, DIM, NSETS>();
     constexpr int P = sym_jpitch<MODE, DIM, NSETS>();
-    constexpr float SIGN = MODE == kSymDiag ? 1.0f : -1.0f;
+    constexpr float SIGN = MODE == kSymP1 ? -1.0f : 1.0f;  // P1 antisymmetric; P2 (product form), DIAG symmetric
     __syncwarp();
 #pragma unroll
     for (int e0 = 0; e0 < 16 * C; e0 += 32) {
@@ -1020,6 +1023,7 @@ __global__ void k_sigma_rows(const double* __restrict__ diag, int n, DevScalars*
         double s = 0.0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
         sc->sigma = s / ((double)n * (double)n);
+        sc->inv_n = 1.0 / (double)n;
     }
 }
 
