@@ -45,6 +45,8 @@ FP32_LANES_PER_SM = 128
 # + R_j -= q delta (2d) + u = r^2 q - 1 (2) + s += u^2 (2); per pair the hop
 # decode h^2 (1), shared by the two sets.  rsqrt counted as 0 flops.
 P1_FLOPS_PER_PAIR_SET = {2: 18, 3: 25}
+# of which the R_i/R_j updates (2d + 2d): not done for the stress-only set of the split pass
+P1_FLOPS_R_PER_PAIR_SET = {2: 8, 3: 12}
 P1_FLOPS_PER_PAIR_DECODE = 1
 
 
@@ -219,8 +221,10 @@ def run_gpu(args):
     n = g.n
     k = cfg.k_for(n)
     X0 = configs.positions_for(args.config, n, args.seed)
-    p = fdl.make_params(dim=cfg.dim, k=k, omega=cfg.omega, tol=cfg.tol, max_iter=100000, device=local_rank,
+    p = fdl.make_params(dim=cfg.dim, k=k, omega=cfg.omega, tol=1e-12, max_iter=100000, device=local_rank,
+                        cg_rtol=max(1e-2 * cfg.tol, 1e-9),  # the config's solve tolerance (R8); tol only keeps the timed steps running
                         cg_extrap=int(os.environ.get("FDL_CG_EXTRAP", "1")),
+                        p1_split=int(os.environ.get("FDL_P1_SPLIT", "-1")),
                         strategy={"fixed": fdl.STRAT_FIXED, "prob": fdl.STRAT_PROB, "enum": fdl.STRAT_ENUM}[args.strategy])
     if world > 1:
         from paper_1711_01228_b200 import dist as fdist
@@ -246,8 +250,9 @@ def run_gpu(args):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    accepted = 0
     for _ in range(args.steps):
-        L.step()
+        accepted += L.step().accepted
     e1.record(stream)
     barrier()
     clk = clocks.stop()
@@ -264,7 +269,8 @@ def run_gpu(args):
     # roofline of the dominant kernel (P1 at C5): algorithmic flops / event time
     dim = cfg.dim
     unique_p1_pairs = (st.p1_pairs - st.p1_pairs_x2) + st.p1_pairs_x2 / 2
-    p1_flops = st.p1_pairs * P1_FLOPS_PER_PAIR_SET[dim] + unique_p1_pairs * P1_FLOPS_PER_PAIR_DECODE
+    p1_flops = (st.p1_pairs * P1_FLOPS_PER_PAIR_SET[dim] - st.p1_pairs_nor * P1_FLOPS_R_PER_PAIR_SET[dim]
+                + unique_p1_pairs * P1_FLOPS_PER_PAIR_DECODE)
     peaks = load_peaks()
     peak_tf = fp32_peak_tflops(peaks)
     p1_tf = p1_flops / (st.p1_ms * 1e-3) / 1e12 if st.p1_ms > 0 else 0.0
@@ -333,6 +339,7 @@ def run_gpu(args):
                        "l2": "inputs larger than L2 (hop matrix %.1f GB per GPU)" % (info.hop_matrix_bytes / 1e9)},
             "iterations_per_sec": its_per_s,
             "pcg_iters_per_step": st.cg_iters / max(st.steps, 1),
+            "sor_accept_rate": accepted / max(args.steps, 1), "p1_rejected_passes": st.p1_rejected,
             "kernel_share": {"p1": p1_share, "p2": p2_share, "other": max(0.0, 1 - p1_share - p2_share)},
             "p1_tflops": p1_tf, "p2_hop_gbs": p2_gbs,
             "fp32_ffma_microbench_tflops": ffma_tf,

@@ -102,6 +102,10 @@ typedef struct {
                              (DESIGN R23); 0: start from X^k. Same minimiser either way */
     int32_t enum_count;   /* FDL_STRAT_ENUM candidates, 1..32 (default 19)                     */
     double enum_step;     /* FDL_STRAT_ENUM candidate spacing > 0 (default 0.5)                */
+    int32_t p1_split;     /* line 6 pass over {X^{k+1}, Xt}: 1 = stresses of both + R(Xt) only, with a
+                             1-set pass for R(X^{k+1}) when the guard rejects Xt (one host sync per
+                             step); 0 = stresses and R of both in one pass; -1 (default) = 1 when
+                             n^2 >= 2^30. Same results either way (bitwise)                       */
 } fdl_params;
 
 typedef struct {
@@ -155,6 +159,8 @@ typedef struct {
     double other_ms;          /* CUDA-event time of everything else in fdl_step       */
     uint64_t steps;           /* fdl_step calls                                      */
     uint64_t cg_iters;        /* PCG iterations                                      */
+    uint64_t p1_pairs_nor;    /* P1 pair x set evaluations of stress only (no R)     */
+    uint64_t p1_rejected;     /* split P1 steps whose guard rejected Xt (extra 1-set pass) */
 } fdl_stats;
 
 /* Fill *p with defaults: dim 2, k auto, omega 1.5, step +INF, tol 1e-4,

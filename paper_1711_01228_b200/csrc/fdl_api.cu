@@ -123,7 +123,8 @@ struct fdl_ctx {
     int device = 0;
     int sm_count = 148;
     int nblk = 0;  // 256-row reduction blocks of the vector kernels
-    int grid_p1[3] = {0, 0, 0}, grid_p2 = 0, grid_diag = 0, grid_enum = 0;
+    int grid_p1[3] = {0, 0, 0}, grid_p2 = 0, grid_diag = 0, grid_enum = 0, grid_p1s = 0;
+    bool p1_split = false;  // P1 over {X^{k+1}, Xt} computes R of Xt only (R(X^{k+1}) on rejection)
     cudaStream_t stream = nullptr, own_stream = nullptr;
     // device memory
     uint8_t* D = nullptr;
@@ -391,7 +392,8 @@ fdl_status allgather_inplace(fdl_ctx* ctx, void* buf, size_t slice_elems, int nc
 fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* out0, double* out1, int set_cur)
 {
     const int dim = ctx->dim;
-    const int C = mode == kSymP1 ? nsets * dim : (mode == kSymP2 ? dim : 1);
+    const bool p1 = mode == kSymP1 || mode == kSymP1S;
+    const int C = mode == kSymP1 ? nsets * dim : ((mode == kSymP2 || mode == kSymP1S) ? dim : 1);
     const int D0 = mode == kSymP1 ? dim : C;
     const int inter = (mode == kSymP1 && nsets == 2) ? 1 : 0;  // P1 two sets: components interleaved by set
     SymArgs a;
@@ -404,13 +406,15 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
     a.nitems = ctx->nitems;
     a.n = ctx->n;
     a.magic = 0x4B000000u;
-    const int grid = mode == kSymP1 ? ctx->grid_p1[nsets] : (mode == kSymP2 ? ctx->grid_p2 : ctx->grid_diag);
-    const int mk = mark_begin(ctx, mode == kSymP1 ? 1 : (mode == kSymP2 ? 2 : 3));
+    const int grid = mode == kSymP1S ? ctx->grid_p1s
+                                     : (mode == kSymP1 ? ctx->grid_p1[nsets] : (mode == kSymP2 ? ctx->grid_p2 : ctx->grid_diag));
+    const int mk = mark_begin(ctx, p1 ? 1 : (mode == kSymP2 ? 2 : 3));
     if (ctx->nitems > 0) FDL_LAUNCH(launch_sym(a, mode, dim, nsets, ctx->hb, grid, ctx->stream));
     mark_end(ctx, mk);
-    if (mode == kSymP1) {
+    if (p1) {
         ctx->stats.p1_launches++;
         ctx->stats.p1_pairs += ctx->local_pairs * (uint64_t)nsets;
+        if (mode == kSymP1S) ctx->stats.p1_pairs_nor += ctx->local_pairs;
         if (nsets == 2) ctx->stats.p1_pairs_x2 += ctx->local_pairs * 2;
     } else if (mode == kSymP2) {
         ctx->stats.p2_launches++;
@@ -421,7 +425,7 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
                                      inter, out0, out1, ctx->stream));
         if (mode == kSymP2)  // product form: L^W p = diag p - sum_j w p_j (rank-local diag when emulated)
             FDL_LAUNCH(launch_p2_finish(out0, pos, ctx->diag, ctx->n, dim, ps_p2(dim), ctx->stream));
-        if (mode == kSymP1) {
+        if (p1) {
             FDL_LAUNCH(launch_sym_stress(ctx->spart, ctx->nitems, nsets, ctx->sparts, ctx->stream));
             FDL_LAUNCH(launch_stress_ranks(ctx->sparts, 1, nsets, ctx->sc, set_cur, ctx->stream));
         }
@@ -434,7 +438,7 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
     FDL_TRY(allgather_inplace(ctx, ctx->rparts, slice, ncclFloat64, 8));
     FDL_LAUNCH(launch_rank_sum(ctx->rparts, ctx->world, ctx->npad, C, D0, inter, out0, out1, ctx->stream));
     if (mode == kSymP2) FDL_LAUNCH(launch_p2_finish(out0, pos, ctx->diag, ctx->n, dim, ps_p2(dim), ctx->stream));
-    if (mode == kSymP1) {
+    if (p1) {
         FDL_LAUNCH(launch_sym_stress(ctx->spart, ctx->nitems, nsets, ctx->sparts + 2 * ctx->rank, ctx->stream));
         FDL_TRY(allgather_inplace(ctx, ctx->sparts, 2, ncclFloat64, 8));
         FDL_LAUNCH(launch_stress_ranks(ctx->sparts, ctx->world, nsets, ctx->sc, set_cur, ctx->stream));
@@ -784,6 +788,9 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     ctx->grid_p2 = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymP2, dim, 1, ctx->hb)));
     ctx->grid_diag = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymDiag, dim, 1, ctx->hb)));
     ctx->grid_enum = std::max(1, std::min(cap_items, ctx->sm_count * 2));
+    ctx->grid_p1s = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymP1S, dim, 2, ctx->hb)));
+    // large problems: the extra host sync of the split P1 is negligible against the pass
+    ctx->p1_split = ctx->p.p1_split == 1 || (ctx->p.p1_split < 0 && (int64_t)n * n >= (int64_t)1 << 30);
     // Jacobi diagonal sum_{j != i} w'_ij (one symmetric DIAG pass) and sigma = mean(diag)/n
     FDL_TRY(run_sym(ctx, kSymDiag, 1, ctx->posf, ctx->diag, nullptr, 0));
     FDL_LAUNCH(launch_set_sigma_rows(ctx->diag, ctx->n, ctx->sc, ctx->stream));
@@ -909,7 +916,19 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
             FDL_LAUNCH(launch_rho(ctx->Xn, ctx->Xk, ctx->Xprev, ctx->Ak, ctx->Aprev, ctx->blk_cg, n, dim,
                                   ctx->ext_ok ? 1 : 0, ctx->sc, s));
         // ---- line 6: f(Xt), f(X^{k+1}) and the next right-hand side, one fused pass
-        FDL_TRY(run_sym(ctx, kSymP1, nsets, ctx->posf, ctx->R1, ctx->R2, 0));
+        if (nsets == 2 && ctx->p1_split) {
+            // stress of both candidates + R(Xt); R(X^{k+1}) only if the guard rejects Xt
+            FDL_TRY(run_sym(ctx, kSymP1S, 2, ctx->posf, ctx->R2, nullptr, 0));
+            FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, s));
+            FDL_CUDA(cudaStreamSynchronize(s));
+            if (!(ctx->sc_host->f_set[1] <= ctx->sc_host->f_set[0])) {
+                FDL_LAUNCH(launch_stage_pos1(ctx->Xn, ctx->posf, n, 0, dim, ps_p1(dim, 1), s));
+                FDL_TRY(run_sym(ctx, kSymP1, 1, ctx->posf, ctx->R1, nullptr, 0));
+                ctx->stats.p1_rejected++;
+            }
+        } else {
+            FDL_TRY(run_sym(ctx, kSymP1, nsets, ctx->posf, ctx->R1, ctx->R2, 0));
+        }
         // ---- lines 6-8: guard
         FDL_LAUNCH(launch_select(ctx->Xk, ctx->Rk, ctx->Xn, ctx->Xt, ctx->R1, ctx->R2, ctx->blk_max, n, dim, nsets,
                                  ctx->sc, ctx->Ak, ctx->An, ctx->At, s));
@@ -1000,6 +1019,7 @@ void fdl_params_default(fdl_params* p)
     p->cg_extrap = 1;
     p->enum_count = 19;
     p->enum_step = 0.5;
+    p->p1_split = -1;
 }
 
 const char* fdl_status_str(fdl_status s)

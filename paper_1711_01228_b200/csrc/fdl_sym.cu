@@ -129,14 +129,14 @@ __device__ __forceinline__ float chunk_hop(const uint4& ch, int r, int cc, uint3
 template <int MODE, int DIM, int NSETS>
 __host__ __device__ constexpr int sym_ncomp()
 {
-    return MODE == kSymP1 ? NSETS * DIM : (MODE == kSymP2 ? DIM : 1);
+    return MODE == kSymP1 ? NSETS * DIM : ((MODE == kSymP2 || MODE == kSymP1S) ? DIM : 1);
 }
 
 // floats per vertex in the staged position vector
 template <int MODE, int DIM, int NSETS>
 __host__ __device__ constexpr int sym_ps()
 {
-    return MODE == kSymP1 ? (DIM == 2 ? (NSETS == 1 ? 2 : 4) : (NSETS == 1 ? 4 : 8))
+    return (MODE == kSymP1 || MODE == kSymP1S) ? (DIM == 2 ? (NSETS == 1 ? 2 : 4) : (NSETS == 1 ? 4 : 8))
                           : (MODE == kSymP2 ? (DIM == 2 ? 2 : 4) : 4);
 }
 
@@ -173,7 +173,7 @@ __host__ __device__ constexpr size_t sym_red_floats()  // j-side warp buffers an
 template <int MODE, int DIM>
 __host__ __device__ constexpr int sym_ctas_per_sm()
 {
-    return (DIM == 2 || MODE != kSymP1) ? 2 : 1;
+    return (DIM == 2 || (MODE != kSymP1 && MODE != kSymP1S)) ? 2 : 1;
 }
 
 // TMA ring depth: as many stages (2..4) as the shared memory left by the
@@ -237,7 +237,42 @@ template <int MODE, int DIM, int NSETS, bool SAFE>
 __device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float h2, float wlut, bool valid,
                                          float* ai, float* aj, float* s)
 {
-    if (MODE == kSymP1 && NSETS == 2) {
+    if (MODE == kSymP1S) {
+        // two sets, stress of both, R of set 1 only (Xt; R(X^{k+1}) is needed only
+        // when the guard rejects, and is then computed by a 1-set pass): the
+        // stress arithmetic is the packed 2-set code, R the scalar FMAs of set 1
+        u64 d[DIM];
+        u64 r2 = pk(FLT_MIN, FLT_MIN);
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+            d[c] = fsub2(pk(xi[2 * c], xi[2 * c + 1]), pk(xj[2 * c], xj[2 * c + 1]));
+            r2 = ffma2(d[c], d[c], r2);
+        }
+        float t0, t1;
+        upk(fmul2(r2, pk(h2, h2)), t0, t1);
+        float q0 = rsqrt_approx(t0), q1 = rsqrt_approx(t1);
+        if (SAFE) {
+            q0 = valid ? q0 : 0.0f;
+            q1 = valid ? q1 : 0.0f;
+        }
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+            float dlo, dhi;
+            upk(d[c], dlo, dhi);
+            ai[c] = fmaf(q1, dhi, ai[c]);
+            aj[c] = fmaf(q1, dhi, aj[c]);
+        }
+        float u0, u1;
+        upk(ffma2(r2, pk(q0, q1), pk(-1.0f, -1.0f)), u0, u1);
+        if (SAFE) {
+            u0 = valid ? u0 : 0.0f;
+            u1 = valid ? u1 : 0.0f;
+        }
+        float s0, s1;
+        upk(ffma2(pk(u0, u1), pk(u0, u1), pk(s[0], s[1])), s0, s1);
+        s[0] = s0;
+        s[1] = s1;
+    } else if (MODE == kSymP1 && NSETS == 2) {
         u64 d[DIM];
         u64 r2 = pk(FLT_MIN, FLT_MIN);  // r^2 > 0 for coincident points: zero R term
 #pragma unroll
@@ -447,7 +482,7 @@ __device__ __forceinline__ void sym_flush_warp(const float* wbuf, float* jpart_w
 {
     constexpr int C = sym_ncomp<MODE, DIM, NSETS>();
     constexpr int P = sym_jpitch<MODE, DIM, NSETS>();
-    constexpr float SIGN = MODE == kSymP1 ? -1.0f : 1.0f;  // P1 antisymmetric; P2 (product form), DIAG symmetric
+    constexpr float SIGN = (MODE == kSymP1 || MODE == kSymP1S) ? -1.0f : 1.0f;  // P1 antisymmetric; P2, DIAG symmetric
     __syncwarp();
 #pragma unroll
     for (int e0 = 0; e0 < 16 * C; e0 += 32) {
@@ -600,7 +635,7 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
             for (int tx2 = 0; tx2 < 16; ++tx2) s += (double)red[(size_t)(tx2 * 16 + ty2) * PITCH + rem];
             a.ipart[(size_t)item * kT * C + ty2 * 8 * C + rem] = s;
         }
-        if (MODE == kSymP1) {
+        if (MODE == kSymP1 || MODE == kSymP1S) {
             // stress of the segment: fixed-order block reduction of the fp64 thread sums
 #pragma unroll
             for (int s = 0; s < NSETS; ++s) {
@@ -611,7 +646,7 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
             }
         }
         __syncthreads();
-        if (MODE == kSymP1 && tid == 0) {
+        if ((MODE == kSymP1 || MODE == kSymP1S) && tid == 0) {
             for (int s = 0; s < NSETS; ++s) {
                 double v = 0.0;
                 for (int w = 0; w < 8; ++w) v += sred[w][s];
@@ -643,6 +678,7 @@ static cudaError_t launch_sym_t(const SymArgs& a, int grid, cudaStream_t s)
 cudaError_t launch_sym(const SymArgs& a, int mode, int dim, int nsets, int hb, int grid, cudaStream_t s)
 {
     FDL_SYM_ALLHB(kSymP1, 2, 1) FDL_SYM_ALLHB(kSymP1, 2, 2) FDL_SYM_ALLHB(kSymP1, 3, 1) FDL_SYM_ALLHB(kSymP1, 3, 2)
+    FDL_SYM_ALLHB(kSymP1S, 2, 2) FDL_SYM_ALLHB(kSymP1S, 3, 2)
     FDL_SYM_ALLHB(kSymP2, 2, 1) FDL_SYM_ALLHB(kSymP2, 3, 1)
     FDL_SYM_ALLHB(kSymDiag, 2, 1) FDL_SYM_ALLHB(kSymDiag, 3, 1)
     return cudaErrorInvalidValue;
@@ -907,6 +943,7 @@ int sym_max_ctas(int mode, int dim, int nsets, int hb)
 {
 #define FDL_SYM_OCC3(M_, D_, S_) FDL_SYM_OCC(M_, D_, S_, 0) FDL_SYM_OCC(M_, D_, S_, 1) FDL_SYM_OCC(M_, D_, S_, 2)
     FDL_SYM_OCC3(kSymP1, 2, 1) FDL_SYM_OCC3(kSymP1, 2, 2) FDL_SYM_OCC3(kSymP1, 3, 1) FDL_SYM_OCC3(kSymP1, 3, 2)
+    FDL_SYM_OCC3(kSymP1S, 2, 2) FDL_SYM_OCC3(kSymP1S, 3, 2)
     FDL_SYM_OCC3(kSymP2, 2, 1) FDL_SYM_OCC3(kSymP2, 3, 1)
     FDL_SYM_OCC3(kSymDiag, 2, 1) FDL_SYM_OCC3(kSymDiag, 3, 1)
     return 1;

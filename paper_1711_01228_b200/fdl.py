@@ -49,6 +49,7 @@ class Params(ctypes.Structure):
         ("cg_max_iter", ctypes.c_int32), ("strategy", ctypes.c_int32), ("seed", ctypes.c_uint64),
         ("device", ctypes.c_int32), ("a_refresh", ctypes.c_int32), ("hop_bits", ctypes.c_int32),
         ("cg_extrap", ctypes.c_int32), ("enum_count", ctypes.c_int32), ("enum_step", ctypes.c_double),
+        ("p1_split", ctypes.c_int32),
     ]
 
 
@@ -86,7 +87,8 @@ class Stats(ctypes.Structure):
         ("launches", ctypes.c_uint64), ("p1_launches", ctypes.c_uint64), ("p2_launches", ctypes.c_uint64),
         ("p1_pairs", ctypes.c_uint64), ("p2_pairs", ctypes.c_uint64), ("p1_pairs_x2", ctypes.c_uint64),
         ("p1_ms", ctypes.c_double), ("p2_ms", ctypes.c_double), ("other_ms", ctypes.c_double),
-        ("steps", ctypes.c_uint64), ("cg_iters", ctypes.c_uint64),
+        ("steps", ctypes.c_uint64), ("cg_iters", ctypes.c_uint64), ("p1_pairs_nor", ctypes.c_uint64),
+        ("p1_rejected", ctypes.c_uint64),
     ]
 
     def as_dict(self):
@@ -147,7 +149,7 @@ def params_default() -> Params:
 
 def make_params(dim=2, k=0.0, omega=1.5, step=math.inf, tol=1e-4, max_iter=500, cg_rtol=0.0,
                 cg_max_iter=0, strategy=STRAT_FIXED, seed=1, device=0, a_refresh=0, hop_bits=0, cg_extrap=1, enum_count=19,
-                enum_step=0.5) -> Params:
+                enum_step=0.5, p1_split=-1) -> Params:
     p = params_default()
     p.dim, p.k, p.omega, p.step, p.tol, p.max_iter = dim, k, omega, step, tol, max_iter
     p.cg_rtol, p.cg_max_iter, p.strategy, p.seed, p.device = cg_rtol, cg_max_iter, strategy, seed, device
@@ -155,6 +157,7 @@ def make_params(dim=2, k=0.0, omega=1.5, step=math.inf, tol=1e-4, max_iter=500, 
     p.hop_bits = hop_bits
     p.cg_extrap = cg_extrap
     p.enum_count, p.enum_step = enum_count, enum_step
+    p.p1_split = p1_split
     return p
 
 

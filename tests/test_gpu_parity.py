@@ -449,3 +449,28 @@ def test_enumerating_strategy_end_to_end(name):
     assert abs(fs[-1] - f) / f <= 1e-3, (fs[-1], f)
     assert abs(len(fs) - it) <= max(1, math.ceil(0.05 * it)), (len(fs), it)
     assert all(b <= a * (1 + 1e-9) for a, b in zip([L.info.f] + fs, fs))
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_split_p1_bitwise(name):
+    """The split line-6 pass (stresses of both candidates, R of Xt only, and a
+    1-set pass for R(X^{k+1}) when the guard rejects) gives bitwise the same
+    trajectory as the fused two-set pass (same per-pair fp32 arithmetic and
+    the same fixed summation orders)."""
+    cfg = configs.CONFIGS[name]
+    g = configs.graph_for(name)
+    X0 = configs.positions_for(name, g.n, 1)
+    out = []
+    for split in (0, 1):
+        p = fdl.make_params(dim=2, k=cfg.k_for(g.n), omega=1.9, tol=cfg.tol, max_iter=60, p1_split=split)
+        with fdl.Layout.from_graph(g, params=p, init_pos=X0) as L:
+            fs = []
+            for _ in range(40):
+                info = L.step()
+                fs.append((info.f_next, info.f_relaxed, info.accepted))
+                if info.stop:
+                    break
+            out.append((fs, L.get_positions(), L.get_stats().p1_rejected))
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1])
+    assert out[1][2] == sum(1 for a in out[1][0] if not a[2])
