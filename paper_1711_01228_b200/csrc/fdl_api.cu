@@ -131,7 +131,8 @@ struct fdl_ctx {
     int4* items = nullptr;
     int *it_lo = nullptr, *it_hi = nullptr;
     float* jpart = nullptr;
-    double *ipart = nullptr, *spart = nullptr;
+    float* ipart = nullptr;
+    double* spart = nullptr;
     double *rparts = nullptr, *sparts = nullptr;  // world x partials
     double *diag = nullptr, *Xk = nullptr, *Xn = nullptr, *Xt = nullptr, *Rk = nullptr, *R1 = nullptr,
            *R2 = nullptr;
@@ -426,7 +427,7 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
         if (mode == kSymP2)  // product form: L^W p = diag p - sum_j w p_j (rank-local diag when emulated)
             FDL_LAUNCH(launch_p2_finish(out0, pos, ctx->diag, ctx->n, dim, ps_p2(dim), ctx->stream));
         if (p1) {
-            FDL_LAUNCH(launch_sym_stress(ctx->spart, ctx->nitems, nsets, ctx->sparts, ctx->stream));
+            FDL_LAUNCH(launch_sym_stress(ctx->spart, ctx->nitems * 8, nsets, ctx->sparts, ctx->stream));
             FDL_LAUNCH(launch_stress_ranks(ctx->sparts, 1, nsets, ctx->sc, set_cur, ctx->stream));
         }
         return FDL_OK;
@@ -439,7 +440,7 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
     FDL_LAUNCH(launch_rank_sum(ctx->rparts, ctx->world, ctx->npad, C, D0, inter, out0, out1, ctx->stream));
     if (mode == kSymP2) FDL_LAUNCH(launch_p2_finish(out0, pos, ctx->diag, ctx->n, dim, ps_p2(dim), ctx->stream));
     if (p1) {
-        FDL_LAUNCH(launch_sym_stress(ctx->spart, ctx->nitems, nsets, ctx->sparts + 2 * ctx->rank, ctx->stream));
+        FDL_LAUNCH(launch_sym_stress(ctx->spart, ctx->nitems * 8, nsets, ctx->sparts + 2 * ctx->rank, ctx->stream));
         FDL_TRY(allgather_inplace(ctx, ctx->sparts, 2, ncclFloat64, 8));
         FDL_LAUNCH(launch_stress_ranks(ctx->sparts, ctx->world, nsets, ctx->sc, set_cur, ctx->stream));
     }
@@ -738,8 +739,8 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     FDL_ALLOC(ctx->it_lo, ctx->nb);
     FDL_ALLOC(ctx->it_hi, ctx->nb);
     FDL_ALLOC(ctx->jpart, (size_t)std::max<int64_t>(ntiles, 1) * kT * Cmax);
-    FDL_ALLOC(ctx->ipart, (size_t)std::max(ctx->nitems, 1) * kT * Cmax);
-    FDL_ALLOC(ctx->spart, (size_t)std::max(ctx->nitems, 1) * 2);
+    FDL_ALLOC(ctx->ipart, (size_t)std::max(ctx->nitems, 1) * 8 * kT * Cmax);
+    FDL_ALLOC(ctx->spart, (size_t)std::max(ctx->nitems, 1) * 8 * 2);
     FDL_ALLOC(ctx->sparts, (size_t)2 * world);
     if (p.strategy == FDL_STRAT_ENUM) {
         if (world > 1) return set_err(ctx, FDL_E_UNSUPPORTED, "the enumerating strategy runs on one GPU");

@@ -143,8 +143,8 @@ struct SymArgs {
     const uint8_t* D;      // local tiles, triangle order
     const float* pos;      // staged positions / p vector, stride sym_ps floats, nb*kT vertices
     float* jpart;          // [local tile][kT][C] fp32 j-side partials
-    double* ipart;         // [item][kT][C] fp64 i-side partials
-    double* spart;         // [item][nsets] fp64 stress partials (P1)
+    float* ipart;          // [item][warp][kT][C] fp32 i-side partials
+    double* spart;         // [item][warp][nsets] fp64 stress partials (P1); k_enum: [item][kEnumNC]
     const int4* items;     // {I, J0, ntiles, first local tile}
     int nitems;
     int n;
@@ -162,7 +162,7 @@ struct EnumOmegas {
 };
 cudaError_t launch_enum(const SymArgs& a, const EnumOmegas& w, int dim, int hb, int grid, cudaStream_t s);
 int sym_max_ctas(int mode, int dim, int nsets, int hb);
-cudaError_t launch_sym_reduce(const double* ipart, const float* jpart, const int* it_lo, const int* it_hi, int nb,
+cudaError_t launch_sym_reduce(const float* ipart, const float* jpart, const int* it_lo, const int* it_hi, int nb,
                               int64_t t0, int64_t t1, int C, int D, int inter, double* out0, double* out1,
                               cudaStream_t s);
 cudaError_t launch_sym_stress(const double* spart, int nitems, int nsets, double* out, cudaStream_t s);

@@ -147,12 +147,6 @@ __host__ __device__ constexpr int sym_stage_bytes()
     return (int)tile_bytes(HB) + kT * sym_ps<MODE, DIM, NSETS>() * 4;
 }
 
-template <int MODE, int DIM, int NSETS>
-__host__ __device__ constexpr int sym_red_pitch()  // floats per (ty, tx) cell of the i-side reduction
-{
-    return 8 * sym_ncomp<MODE, DIM, NSETS>() + 4;
-}
-
 // floats per lane row of a warp's j-side buffer: 9C keeps the 16 rows of a
 // half-warp on distinct banks for the C-wide vector stores
 template <int MODE, int DIM, int NSETS>
@@ -162,11 +156,9 @@ __host__ __device__ constexpr int sym_jpitch()
 }
 
 template <int MODE, int DIM, int NSETS>
-__host__ __device__ constexpr size_t sym_red_floats()  // j-side warp buffers and the i-side buffer share it
+__host__ __device__ constexpr size_t sym_red_floats()  // the j-side warp buffers
 {
-    return (size_t)8 * 2 * (16 * sym_jpitch<MODE, DIM, NSETS>() + 16) > (size_t)256 * sym_red_pitch<MODE, DIM, NSETS>()
-               ? (size_t)8 * 2 * (16 * sym_jpitch<MODE, DIM, NSETS>() + 16)
-               : (size_t)256 * sym_red_pitch<MODE, DIM, NSETS>();
+    return (size_t)8 * 2 * (16 * sym_jpitch<MODE, DIM, NSETS>() + 16);
 }
 
 // CTAs per SM the pass is built for (register budget of __launch_bounds__)
@@ -510,7 +502,6 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
     constexpr int PS = sym_ps<MODE, DIM, NSETS>();
     constexpr int STAGE = sym_stage_bytes<MODE, DIM, NSETS, HB>();
     constexpr int DT = (int)tile_bytes(HB);
-    constexpr int PITCH = sym_red_pitch<MODE, DIM, NSETS>();
     constexpr int JP = sym_jpitch<MODE, DIM, NSETS>();
     constexpr int NST = sym_stages<MODE, DIM, NSETS, HB>();
     constexpr int NW = 8;  // warps
@@ -518,7 +509,6 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
     __shared__ uint64_t full[NST];
     __shared__ int drained[NST];  // warps done with the stage's current tile
     __shared__ int prod[2];       // producer cursor {item, tile in item}
-    __shared__ double sred[8][NSETS > 0 ? NSETS : 1];
     __shared__ float lut[256];
     __shared__ float2 lut2[HB == 0 ? 256 : 1];
     float* red = reinterpret_cast<float*>(smem + (size_t)NST * STAGE);
@@ -620,37 +610,30 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
                 phase ^= 1u;
             }
         }
-        // i-side: reduce over the 16 thread columns (fixed order, fp64)
-        __syncthreads();  // every warp finished its last j flush (the buffer is shared below)
-        float* myred = red + (size_t)(tx * 16 + ty) * PITCH;  // [tx][ty] layout
+        // i-side, per warp (no CTA barrier): the warp's two thread columns (lanes
+        // ty and ty + 16) are summed by one xor-shuffle, and lane (ty, h) writes
+        // rows ty*8 + 4h .. +3 of the warp's partial [item][warp][row][C] (fp32;
+        // k_sym_reduce sums items and warps in a fixed order, in fp64).
+        {
+            float* ip = a.ipart + ((size_t)item * 8 + wid) * kT * C + (size_t)ty * 8 * C;
+            const int h = lane >> 4;
 #pragma unroll
-        for (int r = 0; r < 8; ++r)
+            for (int r = 0; r < 8; ++r)
 #pragma unroll
-            for (int v = 0; v < C; ++v) myred[r * C + v] = ai[r][v];
-        __syncthreads();
-        for (int e = tid; e < kT * C; e += 256) {
-            const int ty2 = e / (8 * C), rem = e % (8 * C);  // rem = r*C + v, row = ty2*8 + r
-            double s = 0.0;
-#pragma unroll 4
-            for (int tx2 = 0; tx2 < 16; ++tx2) s += (double)red[(size_t)(tx2 * 16 + ty2) * PITCH + rem];
-            a.ipart[(size_t)item * kT * C + ty2 * 8 * C + rem] = s;
+                for (int v = 0; v < C; ++v) {
+                    const float tot = ai[r][v] + __shfl_xor_sync(0xffffffffu, ai[r][v], 16);
+                    if ((r >> 2) == h) ip[r * C + v] = tot;
+                }
         }
         if (MODE == kSymP1 || MODE == kSymP1S) {
-            // stress of the segment: fixed-order block reduction of the fp64 thread sums
+            // stress of the warp's share of the segment: fixed-order warp butterfly of
+            // the fp64 thread sums -> spart[item][warp][set]
 #pragma unroll
             for (int s = 0; s < NSETS; ++s) {
                 double v = s64[s];
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                if (lane == 0) sred[wid][s] = v;
-            }
-        }
-        __syncthreads();
-        if ((MODE == kSymP1 || MODE == kSymP1S) && tid == 0) {
-            for (int s = 0; s < NSETS; ++s) {
-                double v = 0.0;
-                for (int w = 0; w < 8; ++w) v += sred[w][s];
-                a.spart[(size_t)item * NSETS + s] = v;
+                if (lane == 0) a.spart[((size_t)item * 8 + wid) * NSETS + s] = v;
             }
         }
     }
@@ -950,35 +933,55 @@ int sym_max_ctas(int mode, int dim, int nsets, int hb)
 }
 
 // ---------------------------------------------------------------- reduction
-// Per row of block B: sum, in a fixed order, the i-side segment partials of
-// strip B (items it_lo[B]..it_hi[B]) and the j-side tile partials of the local
-// tiles (I, B), I = 0..B.  4 groups of 128 threads split the I loop (I = g mod
-// 4); the group sums are combined in group order.  Blocks run largest B first.
+// Per row of block B: sum, in a fixed order, the j-side tile partials of the
+// local tiles (I, B), I = 0..B, and the i-side per-warp partials of strip B
+// (items it_lo[B]..it_hi[B], 8 warps each).  8 groups of 128 threads: group g
+// takes tiles I = g mod 8 and items it_lo + g mod 8; the group sums are
+// combined in group order (fp64).  Blocks run largest B first.
 // Output: dense fp64 rank partial, components [0, D) -> out0, [D, C) -> out1.
-__global__ void __launch_bounds__(4 * kT) k_sym_reduce(const double* __restrict__ ipart, const float* __restrict__ jpart,
-                                                       const int* __restrict__ it_lo, const int* __restrict__ it_hi,
-                                                       int nb, int64_t t0, int64_t t1, int C, int D, int inter,
-                                                       double* out0, double* out1)
+constexpr int kRedGroups = 8;
+
+template <int C>
+__global__ void __launch_bounds__(kRedGroups * kT) k_sym_reduce(const float* __restrict__ ipart,
+                                                                const float* __restrict__ jpart,
+                                                                const int* __restrict__ it_lo,
+                                                                const int* __restrict__ it_hi, int nb, int64_t t0,
+                                                                int64_t t1, int D, int inter, double* out0,
+                                                                double* out1)
 {
-    __shared__ double gsum[4][kT][8];
+    __shared__ double gsum[kRedGroups][kT][C];
     const int B = nb - 1 - (int)blockIdx.x;
     const int g = threadIdx.x / kT, r = threadIdx.x % kT;
-    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int I = g; I <= B; I += 4) {
+    double acc[C];
+#pragma unroll
+    for (int v = 0; v < C; ++v) acc[v] = 0.0;
+#pragma unroll 4
+    for (int I = g; I <= B; I += kRedGroups) {
         const int64_t t = tri_index(I, B, nb);
         if (t < t0 || t >= t1) continue;
         const float* src = jpart + ((size_t)(t - t0) * kT + r) * C;
+#pragma unroll
         for (int v = 0; v < C; ++v) acc[v] += (double)src[v];
     }
+    for (int item = it_lo[B] + g; item < it_hi[B]; item += kRedGroups)
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            const float* src = ipart + (((size_t)item * 8 + w) * kT + r) * C;
+#pragma unroll
+            for (int v = 0; v < C; ++v) acc[v] += (double)src[v];
+        }
+#pragma unroll
     for (int v = 0; v < C; ++v) gsum[g][r][v] = acc[v];
     __syncthreads();
     if (g != 0) return;
-    double tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int item = it_lo[B]; item < it_hi[B]; ++item)
-        for (int v = 0; v < C; ++v) tot[v] += ipart[((size_t)item * kT + r) * C + v];
-    for (int gg = 0; gg < 4; ++gg)
+    double tot[C];
+#pragma unroll
+    for (int v = 0; v < C; ++v) tot[v] = 0.0;
+    for (int gg = 0; gg < kRedGroups; ++gg)
+#pragma unroll
         for (int v = 0; v < C; ++v) tot[v] += gsum[gg][r][v];
     const size_t row = (size_t)B * kT + r;
+#pragma unroll
     for (int v = 0; v < C; ++v) {
         if (inter)  // two sets interleaved per component: set v&1, component v>>1
             ((v & 1) ? out1 : out0)[row * D + (v >> 1)] = tot[v];
@@ -989,12 +992,19 @@ __global__ void __launch_bounds__(4 * kT) k_sym_reduce(const double* __restrict_
     }
 }
 
-cudaError_t launch_sym_reduce(const double* ipart, const float* jpart, const int* it_lo, const int* it_hi, int nb,
+cudaError_t launch_sym_reduce(const float* ipart, const float* jpart, const int* it_lo, const int* it_hi, int nb,
                               int64_t t0, int64_t t1, int C, int D, int inter, double* out0, double* out1,
                               cudaStream_t s)
 {
-    k_sym_reduce<<<nb, 4 * kT, 0, s>>>(ipart, jpart, it_lo, it_hi, nb, t0, t1, C, D, inter, out0, out1);
-    return cudaGetLastError();
+#define FDL_RED_CASE(C_)                                                                                        \
+    if (C == C_) {                                                                                              \
+        k_sym_reduce<C_><<<nb, kRedGroups * kT, 0, s>>>(ipart, jpart, it_lo, it_hi, nb, t0, t1, D, inter, out0, \
+                                                        out1);                                                 \
+        return cudaGetLastError();                                                                              \
+    }
+    FDL_RED_CASE(1) FDL_RED_CASE(2) FDL_RED_CASE(3) FDL_RED_CASE(4) FDL_RED_CASE(6)
+#undef FDL_RED_CASE
+    return cudaErrorInvalidValue;
 }
 
 // sum of rank partials in rank order (multi-GPU): parts[world][rows][C]
