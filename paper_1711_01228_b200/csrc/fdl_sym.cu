@@ -165,7 +165,7 @@ __host__ __device__ constexpr size_t sym_red_floats()  // the j-side warp buffer
 template <int MODE, int DIM>
 __host__ __device__ constexpr int sym_ctas_per_sm()
 {
-    return (DIM == 2 || (MODE != kSymP1 && MODE != kSymP1S)) ? 2 : 1;
+    return (MODE == kSymP2 && DIM == 2) ? 3 : ((DIM == 2 || (MODE != kSymP1 && MODE != kSymP1S)) ? 2 : 1);
 }
 
 // TMA ring depth: as many stages (2..4) as the shared memory left by the

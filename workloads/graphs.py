@@ -233,3 +233,58 @@ def init_positions(n: int, dim: int, seed: int) -> np.ndarray:
     x = rng.random((n, dim), dtype=np.float32)
     x = (x - x[0]).astype(np.float32)
     return x.astype(np.float64)
+
+
+# ------------------------------------------------------------ weighted inputs
+# NEXT-3: graphs whose edges carry a length (the paper's
+# weighted "China railway" network).  Lengths are
+# inputs, aligned with ``col`` (one per stored direction, equal for both).
+
+def edge_lengths_uniform(g: Graph, lo: float, hi: float, seed: int) -> np.ndarray:
+    """Seeded lengths uniform in [lo, hi), one per undirected edge."""
+    rng = np.random.default_rng(seed)
+    e = g.edges()
+    lens = rng.uniform(lo, hi, len(e))
+    return _lengths_on_csr(g, e, lens)
+
+
+def random_geometric_graph_weighted(n: int, mean_degree: float, seed: int):
+    """RGG as in random_geometric_graph (largest component) with each edge's
+    length = the Euclidean distance of its endpoints' generating points (a
+    railway-like planar network).  Returns (graph, lengths aligned with col)."""
+    from scipy.spatial import cKDTree
+
+    rng = np.random.default_rng(seed)
+    pts = rng.random((n, 2))
+    r = math.sqrt(mean_degree / (math.pi * (n - 1)))
+    pairs = cKDTree(pts).query_pairs(r, output_type="ndarray")
+    g0 = csr_from_edges(n, pairs, name=f"wrgg{n}")
+    g = largest_component(g0)
+    # recover the kept vertices' points (largest_component relabels by increasing id)
+    keep = _largest_component_ids(g0)
+    p = pts[keep]
+    e = g.edges()
+    lens = np.sqrt(((p[e[:, 0]] - p[e[:, 1]]) ** 2).sum(axis=1))
+    return g, _lengths_on_csr(g, e, lens)
+
+
+def _largest_component_ids(g: Graph) -> np.ndarray:
+    from scipy.sparse import csr_matrix
+    from scipy.sparse.csgraph import connected_components
+
+    A = csr_matrix((np.ones(len(g.col)), g.col, g.row_ptr), shape=(g.n, g.n))
+    _, lab = connected_components(A, directed=False)
+    big = np.argmax(np.bincount(lab))
+    return np.flatnonzero(lab == big)
+
+
+def _lengths_on_csr(g: Graph, e: np.ndarray, lens: np.ndarray) -> np.ndarray:
+    out = np.empty(len(g.col), dtype=np.float64)
+    key = {}
+    for (a, b), w in zip(e.tolist(), lens.tolist()):
+        key[(a, b)] = w
+        key[(b, a)] = w
+    for v in range(g.n):
+        for k in range(int(g.row_ptr[v]), int(g.row_ptr[v + 1])):
+            out[k] = key[(v, int(g.col[k]))]
+    return out
