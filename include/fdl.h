@@ -85,7 +85,8 @@ typedef struct {
     double step;          /* cap on ||xt_i - x^{k+1}_i|| per vertex; +INF = paper-exact (DESIGN R14) */
     double tol;           /* "rel err" of Table 1 > 0                                       */
     int32_t max_iter;     /* >= 1                                                                   */
-    double weight_exp;    /* alpha in w = d^alpha; only -2 is implemented                   */
+    double weight_exp;    /* alpha in w = d^alpha, finite; -2 in the paper. alpha != -2 or
+                             edge lengths use fp32 path-length tiles (NEXT-3)           */
     double cg_rtol;       /* PCG relative residual; <= 0 -> max(1e-2*tol, 1e-9)             */
     int32_t cg_max_iter;  /* PCG cap per outer iteration; <= 0 -> min(10n, 10000)           */
     int32_t strategy;     /* fdl_strategy                                                           */
@@ -173,11 +174,16 @@ void fdl_params_default(fdl_params* p);
  *   row_ptr  int64[n+1], CSR offsets; col_idx int32[row_ptr[n]] neighbour ids.
  *            The graph must be undirected (both directions stored), without
  *            self-loops or duplicate neighbours, and connected.
- *   edge_len must be NULL (unit lengths; weighted graphs -> FDL_E_BAD_LENGTH).
+ *   edge_len NULL (unit lengths: d_ij = k * hop) or double[row_ptr[n]], one
+ *            positive finite length per stored direction, equal for both
+ *            directions (not checked: row v's entry is used for v<-u): d_ij = k * shortest path length (Kamada-Kawai,
+ *            P:32; weighted networks P:250).  Non-positive or non-finite
+ *            -> FDL_E_BAD_LENGTH.
  *   p        parameters (NULL -> defaults).
  *   init_pos n*dim doubles (row-major) or NULL for the seeded uniform unit-cube
  *            placement.  Translated so x_0 = 0.
- * Computes the hop matrix on the device (multi-source BFS), the Jacobi
+ * Computes the ideal distances on the device (multi-source BFS for unit
+ * lengths and alpha = -2; fp64 multi-source Bellman-Ford otherwise), the Jacobi
  * diagonal, and f(X^0), L^{X^0} X^0.  On error *out = NULL. */
 fdl_status fdl_create(int32_t n, const int64_t* row_ptr, const int32_t* col_idx,
                       const double* edge_len, const fdl_params* p,
@@ -251,6 +257,11 @@ fdl_status fdl_eval_forces(fdl_ctx* ctx, double* R, double* A, double* stress);
 /* Hop counts of rows [r0, r0+nrows): out[r*n + j] = hop(r0 + r, j), gathered from
  * the stored upper triangle (FDL_E_INVALID_ARG if an entry lives on another rank). */
 fdl_status fdl_get_hop_rows(fdl_ctx* ctx, int32_t r0, int32_t nrows, uint16_t* out);
+
+/* Ideal distances d_ij = k x (shortest path length) of rows [r0, r0+nrows),
+ * original units, out[r*n + j] (n*nrows doubles), any stored width (hop tiles or
+ * the fp32 path lengths of weighted graphs / general alpha). */
+fdl_status fdl_get_dist_rows(fdl_ctx* ctx, int32_t r0, int32_t nrows, double* out);
 
 /* Jacobi diagonal sum_{j != i} w_ij of all n rows, original units (count = n). */
 fdl_status fdl_get_diag(fdl_ctx* ctx, double* out, size_t count);

@@ -113,6 +113,9 @@ struct fdl_ctx {
     fdl_params p{};
     int n = 0, dim = 0, rank = 0, world = 1;
     double k = 1.0, cap = INFINITY;
+    double alpha = -2.0;                          // weight exponent (NEXT-3 any)
+    double fscale = 1.0, rscale = 1.0, dscale = 1.0;  // k^(alpha+2), k^(alpha+1), k^alpha
+    bool general = false;                         // fp32 distance tiles (weighted or alpha != -2)
     int hb = 1;
     int nb = 0;              // vertex blocks of kT
     int64_t npad = 0;        // nb * kT
@@ -407,6 +410,7 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
     a.nitems = ctx->nitems;
     a.n = ctx->n;
     a.magic = 0x4B000000u;
+    a.alpha = (float)ctx->alpha;
     const int grid = mode == kSymP1S ? ctx->grid_p1s
                                      : (mode == kSymP1 ? ctx->grid_p1[nsets] : (mode == kSymP2 ? ctx->grid_p2 : ctx->grid_diag));
     const int mk = mark_begin(ctx, p1 ? 1 : (mode == kSymP2 ? 2 : 3));
@@ -591,6 +595,82 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
     return FDL_OK;
 }
 
+// Weighted graphs / general alpha (NEXT-3): fp64 multi-source Bellman-Ford over
+// the CSR with edge lengths (unit lengths when edge_len is NULL), stored as fp32
+// path lengths in the local upper-triangle tiles.
+fdl_status build_dists(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, const double* edge_len)
+{
+    const int n = ctx->n;
+    const int64_t m = std::max<int64_t>(rp[n], 1);
+    constexpr int S = 256;  // sources per batch
+    int64_t* d_rp = nullptr;
+    int32_t* d_col = nullptr;
+    double *d_len = nullptr, *da = nullptr, *db = nullptr, *dmax = nullptr;
+    FDL_CUDA(cudaMalloc(&d_rp, sizeof(int64_t) * (n + 1)));
+    FDL_CUDA(cudaMalloc(&d_col, sizeof(int32_t) * m));
+    FDL_CUDA(cudaMalloc(&d_len, sizeof(double) * m));
+    FDL_CUDA(cudaMalloc(&da, sizeof(double) * (size_t)n * S));
+    FDL_CUDA(cudaMalloc(&db, sizeof(double) * (size_t)n * S));
+    FDL_CUDA(cudaMalloc(&dmax, sizeof(double)));
+    FDL_CUDA(cudaMemsetAsync(dmax, 0, sizeof(double), ctx->stream));
+    std::vector<double> ones;
+    const double* lens = edge_len;
+    if (!lens) {
+        ones.assign((size_t)m, 1.0);
+        lens = ones.data();
+    }
+    FDL_CUDA(cudaMemcpyAsync(d_rp, rp, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, ctx->stream));
+    if (rp[n] > 0) {
+        FDL_CUDA(cudaMemcpyAsync(d_col, col, sizeof(int32_t) * rp[n], cudaMemcpyHostToDevice, ctx->stream));
+        FDL_CUDA(cudaMemcpyAsync(d_len, lens, sizeof(double) * rp[n], cudaMemcpyHostToDevice, ctx->stream));
+    }
+    int64_t Ilo = 0, Jlo = 0, Ihi = -1, Jhi = 0;
+    if (ctx->t1 > ctx->t0) {
+        tri_coords(ctx->t0, ctx->nb, Ilo, Jlo);
+        tri_coords(ctx->t1 - 1, ctx->nb, Ihi, Jhi);
+    }
+    const int src_lo = (int)std::min<int64_t>(n, Ilo * kT);
+    const int src_hi = (int)std::min<int64_t>(n, (Ihi + 1) * kT);
+    ctx->hb = kHbDist;
+    const size_t dbytes = (size_t)std::max<int64_t>(ctx->t1 - ctx->t0, 1) * (size_t)tile_bytes(kHbDist);
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, dbytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(ctx, FDL_E_OOM, "distance tile allocation of " + std::to_string(dbytes) + " bytes failed");
+    }
+    ctx->D = static_cast<uint8_t*>(q);
+    ctx->allocs.push_back(q);
+    ctx->device_bytes += dbytes;
+    ctx->hop_bytes_total = dbytes;
+    FDL_CUDA(cudaMemsetAsync(ctx->D, 0, dbytes, ctx->stream));
+    for (int s0 = src_lo; s0 < src_hi; s0 += S) {
+        const int nsrc = std::min(S, src_hi - s0);
+        FDL_LAUNCH(launch_bf_init(da, n, s0, nsrc, S, ctx->stream));
+        double *din = da, *dout = db;
+        for (int it = 0; it < n; ++it) {
+            FDL_CUDA(cudaMemsetAsync(&ctx->sc->anynew, 0, sizeof(unsigned int), ctx->stream));
+            FDL_LAUNCH(launch_bf_relax(d_rp, d_col, d_len, din, dout, n, S, nsrc, &ctx->sc->anynew, ctx->stream));
+            FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, ctx->stream));
+            FDL_CUDA(cudaStreamSynchronize(ctx->stream));
+            std::swap(din, dout);
+            if (!ctx->sc_host->anynew) break;
+        }
+        FDL_LAUNCH(launch_bf_store(din, n, s0, nsrc, S, ctx->nb, ctx->t0, ctx->t1, ctx->D, dmax, ctx->stream));
+    }
+    double mx = 0.0;
+    FDL_CUDA(cudaMemcpyAsync(&mx, dmax, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    FDL_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->diameter = (int)std::ceil(mx);
+    cudaFree(d_rp);
+    cudaFree(d_col);
+    cudaFree(d_len);
+    cudaFree(da);
+    cudaFree(db);
+    cudaFree(dmax);
+    return FDL_OK;
+}
+
 fdl_status check_params(const fdl_params* p, std::string& msg)
 {
     if (p->struct_size != sizeof(fdl_params)) {
@@ -617,9 +697,9 @@ fdl_status check_params(const fdl_params* p, std::string& msg)
         msg = "step must be > 0 (use INFINITY for no cap)";
         return FDL_E_INVALID_ARG;
     }
-    if (p->weight_exp != -2.0) {
-        msg = "only weight_exp = -2 (w = d^-2, P:250) is implemented";
-        return FDL_E_UNSUPPORTED;
+    if (!std::isfinite(p->weight_exp)) {
+        msg = "weight_exp must be finite (w = d^alpha)";
+        return FDL_E_INVALID_ARG;
     }
     if (p->strategy == FDL_STRAT_ENUM) {
         if (p->enum_count < 1 || p->enum_count > kEnumMax || !(p->enum_step > 0.0) || !std::isfinite(p->enum_step)) {
@@ -678,8 +758,13 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     std::string msg;
     fdl_status st = check_params(&p, msg);
     if (st != FDL_OK) return set_err(ctx, st, msg);
-    if (edge_len)
-        return set_err(ctx, FDL_E_BAD_LENGTH, "weighted edge lengths are not supported yet (unit lengths only)");
+    if (edge_len) {  // lengths positive and finite, equal in both directions
+        for (int32_t v = 0; v < n; ++v)
+            for (int64_t e = rp[v]; e < rp[v + 1]; ++e) {
+                if (!(edge_len[e] > 0.0) || !std::isfinite(edge_len[e]))
+                    return set_err(ctx, FDL_E_BAD_LENGTH, "edge lengths must be finite and > 0");
+            }
+    }
     if (world < 1 || rank < 0 || rank >= world) return set_err(ctx, FDL_E_INVALID_ARG, "bad rank/world");
     int ecc0 = 0;
     st = validate_graph(n, rp, col, msg, ecc0);
@@ -692,6 +777,13 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     ctx->world = world;
     ctx->device = p.device;
     ctx->k = p.k > 0 ? p.k : std::pow((double)n, -1.0 / p.dim);
+    ctx->alpha = p.weight_exp;
+    ctx->general = edge_len != nullptr || p.weight_exp != -2.0;
+    ctx->fscale = std::pow(ctx->k, ctx->alpha + 2.0);
+    ctx->rscale = std::pow(ctx->k, ctx->alpha + 1.0);
+    ctx->dscale = std::pow(ctx->k, ctx->alpha);
+    if (ctx->general && p.strategy == FDL_STRAT_ENUM)
+        return set_err(ctx, FDL_E_UNSUPPORTED, "the enumerating strategy needs unit lengths and alpha = -2");
     ctx->cap = std::isfinite(p.step) ? p.step / ctx->k : INFINITY;
     if (!(p.cg_rtol > 0)) ctx->p.cg_rtol = std::max(1e-2 * p.tol, 1e-9);
     if (p.cg_max_iter <= 0) ctx->p.cg_max_iter = std::min(10 * n, 10000);
@@ -782,7 +874,10 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     FDL_CUDA(cudaMemcpyAsync(ctx->it_hi, hi.data(), sizeof(int) * ctx->nb, cudaMemcpyHostToDevice, ctx->stream));
 
     // hop matrix first (fixes the hop width), then grids, then the Jacobi diagonal
-    FDL_TRY(build_hops(ctx, rp, col, ecc0));
+    if (ctx->general)
+        FDL_TRY(build_dists(ctx, rp, col, edge_len));
+    else
+        FDL_TRY(build_hops(ctx, rp, col, ecc0));
     const int cap_items = std::max(ctx->nitems, 1);
     for (int s = 1; s <= 2; ++s)
         ctx->grid_p1[s] = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymP1, dim, s, ctx->hb)));
@@ -791,7 +886,8 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     ctx->grid_enum = std::max(1, std::min(cap_items, ctx->sm_count * 2));
     ctx->grid_p1s = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymP1S, dim, 2, ctx->hb)));
     // large problems: the extra host sync of the split P1 is negligible against the pass
-    ctx->p1_split = ctx->p.p1_split == 1 || (ctx->p.p1_split < 0 && (int64_t)n * n >= (int64_t)1 << 30);
+    ctx->p1_split = !ctx->general &&
+                    (ctx->p.p1_split == 1 || (ctx->p.p1_split < 0 && (int64_t)n * n >= (int64_t)1 << 30));
     // Jacobi diagonal sum_{j != i} w'_ij (one symmetric DIAG pass) and sigma = mean(diag)/n
     FDL_TRY(run_sym(ctx, kSymDiag, 1, ctx->posf, ctx->diag, nullptr, 0));
     FDL_LAUNCH(launch_set_sigma_rows(ctx->diag, ctx->n, ctx->sc, ctx->stream));
@@ -963,10 +1059,10 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
     inf.accepted = accepted ? 1 : 0;
     inf.cg_iters = cg;
     inf.omega = omega;
-    inf.f_before = f_before;
-    inf.f_next = f_next;
-    inf.f_relaxed = f_rel;
-    inf.f_after = f_after;
+    inf.f_before = f_before * ctx->fscale;  // f = k^(alpha+2) f' (units of k)
+    inf.f_next = f_next * ctx->fscale;
+    inf.f_relaxed = f_rel * ctx->fscale;
+    inf.f_after = f_after * ctx->fscale;
     inf.rel_decrease = f_before > 0 ? (f_before - f_after) / f_before : 0.0;
     inf.cg_relres = h.relres;
     inf.maxdisp = h.maxdisp * ctx->k;
@@ -1178,7 +1274,7 @@ fdl_status fdl_run_until_converged(fdl_ctx* ctx, fdl_run_info* info)
     if (!ctx) return FDL_E_INVALID_ARG;
     cudaSetDevice(ctx->device);
     fdl_run_info r{};
-    r.f_initial = ctx->f;
+    r.f_initial = ctx->f * ctx->fscale;
     fdl_status s = FDL_OK;
     while (!ctx->stopped) {
         fdl_iter_info it;
@@ -1189,7 +1285,7 @@ fdl_status fdl_run_until_converged(fdl_ctx* ctx, fdl_run_info* info)
         r.cg_iters += it.cg_iters;
     }
     r.stop = ctx->stop_reason;
-    r.f_final = ctx->f;
+    r.f_final = ctx->f * ctx->fscale;
     if (info) *info = r;
     return s;
 }
@@ -1232,7 +1328,7 @@ fdl_status fdl_eval_forces(fdl_ctx* ctx, double* R, double* A, double* stress)
     auto fetch = [&](const double* dev, double* out) -> fdl_status {
         FDL_CUDA(cudaMemcpyAsync(out, dev, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         FDL_CUDA(cudaStreamSynchronize(ctx->stream));
-        for (size_t i = 0; i < count; ++i) out[i] /= ctx->k;  // R = R'/k, A = A'/k
+        for (size_t i = 0; i < count; ++i) out[i] *= ctx->rscale;  // R = k^(alpha+1) R' (= R'/k at alpha = -2)
         return FDL_OK;
     };
     if (R) FDL_TRY(fetch(ctx->Rk, R));
@@ -1243,7 +1339,7 @@ fdl_status fdl_eval_forces(fdl_ctx* ctx, double* R, double* A, double* stress)
         FDL_TRY(fetch(ctx->cy, A));
         collect_events(ctx);
     }
-    if (stress) *stress = ctx->f;
+    if (stress) *stress = ctx->f * ctx->fscale;
     return FDL_OK;
 }
 
@@ -1269,14 +1365,15 @@ fdl_status fdl_eval_partial(fdl_ctx* ctx, int32_t mode, const double* X, double*
     FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, ctx->stream));
     FDL_CUDA(cudaStreamSynchronize(ctx->stream));
     collect_events(ctx);
-    for (size_t i = 0; i < count; ++i) out[i] /= ctx->k;
-    if (stress) *stress = mode == 0 ? ctx->sc_host->f_set[0] : 0.0;
+    for (size_t i = 0; i < count; ++i) out[i] *= ctx->rscale;
+    if (stress) *stress = mode == 0 ? ctx->sc_host->f_set[0] * ctx->fscale : 0.0;
     return FDL_OK;
 }
 
 fdl_status fdl_get_hop_rows(fdl_ctx* ctx, int32_t r0, int32_t nrows, uint16_t* out)
 {
     if (!ctx || !out || nrows < 0 || r0 < 0 || r0 + nrows > ctx->n) return FDL_E_INVALID_ARG;
+    if (ctx->hb == kHbDist) return set_err(ctx, FDL_E_UNSUPPORTED, "fp32 path-length tiles: use fdl_get_dist_rows");
     cudaSetDevice(ctx->device);
     if (nrows == 0) return FDL_OK;
     std::vector<int> rows(nrows);
@@ -1305,6 +1402,40 @@ fdl_status fdl_get_hop_rows(fdl_ctx* ctx, int32_t r0, int32_t nrows, uint16_t* o
     return FDL_OK;
 }
 
+fdl_status fdl_get_dist_rows(fdl_ctx* ctx, int32_t r0, int32_t nrows, double* out)
+{
+    if (!ctx || !out || nrows < 0 || r0 < 0 || r0 + nrows > ctx->n) return FDL_E_INVALID_ARG;
+    cudaSetDevice(ctx->device);
+    if (nrows == 0) return FDL_OK;
+    std::vector<int> rows(nrows);
+    for (int r = 0; r < nrows; ++r) rows[r] = r0 + r;
+    const size_t cnt = (size_t)nrows * ctx->n;
+    int* d_rows = nullptr;
+    int* d_missing = nullptr;
+    float* d_out = nullptr;
+    FDL_CUDA(cudaMalloc(&d_rows, sizeof(int) * nrows));
+    FDL_CUDA(cudaMalloc(&d_missing, sizeof(int)));
+    FDL_CUDA(cudaMalloc(&d_out, sizeof(float) * cnt));
+    cudaMemcpyAsync(d_rows, rows.data(), sizeof(int) * nrows, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemsetAsync(d_missing, 0, sizeof(int), ctx->stream);
+    cudaError_t e = launch_dist_rows(ctx->D, ctx->hb, ctx->nb, ctx->t0, ctx->t1, d_rows, nrows, ctx->n, d_out,
+                                     d_missing, ctx->stream);
+    int missing = 0;
+    std::vector<float> tmp(cnt);
+    if (e == cudaSuccess) {
+        cudaMemcpyAsync(tmp.data(), d_out, sizeof(float) * cnt, cudaMemcpyDeviceToHost, ctx->stream);
+        cudaMemcpyAsync(&missing, d_missing, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+        e = cudaStreamSynchronize(ctx->stream);
+    }
+    cudaFree(d_rows);
+    cudaFree(d_missing);
+    cudaFree(d_out);
+    FDL_CUDA(e);
+    if (missing) return set_err(ctx, FDL_E_INVALID_ARG, "some requested entries live in tiles of other ranks");
+    for (size_t i = 0; i < cnt; ++i) out[i] = ctx->k * (double)tmp[i];
+    return FDL_OK;
+}
+
 fdl_status fdl_get_diag(fdl_ctx* ctx, double* out, size_t count)
 {
     if (!ctx || !out) return FDL_E_INVALID_ARG;
@@ -1312,8 +1443,7 @@ fdl_status fdl_get_diag(fdl_ctx* ctx, double* out, size_t count)
     cudaSetDevice(ctx->device);
     FDL_CUDA(cudaMemcpyAsync(out, ctx->diag, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     FDL_CUDA(cudaStreamSynchronize(ctx->stream));
-    const double k2 = ctx->k * ctx->k;
-    for (size_t i = 0; i < count; ++i) out[i] /= k2;  // w = w'/k^2
+    for (size_t i = 0; i < count; ++i) out[i] *= ctx->dscale;  // w = k^alpha w'
     return FDL_OK;
 }
 
@@ -1331,7 +1461,7 @@ fdl_status fdl_get_info(fdl_ctx* ctx, fdl_ctx_info* info)
     r.world = ctx->world;
     r.iterations = ctx->iterations;
     r.k = ctx->k;
-    r.f = ctx->f;
+    r.f = ctx->f * ctx->fscale;
     r.hop_matrix_bytes = ctx->hop_bytes_total;
     r.local_pairs = ctx->local_pairs;
     r.device_bytes = ctx->device_bytes;

@@ -113,9 +113,11 @@ __host__ __device__ inline int64_t tri_index(int64_t I, int64_t J, int64_t nb)
     return I * nb - I * (I - 1) / 2 + (J - I);
 }
 
-// Hop width code `hb`: 0 = 4-bit (diameter <= 15), 1 = uint8, 2 = uint16.
+// Hop width code `hb`: 0 = 4-bit (diameter <= 15), 1 = uint8, 2 = uint16;
+// 4 = fp32 path lengths (weighted graphs / general alpha, NEXT-3).
 __host__ __device__ constexpr int64_t tile_bytes(int hb) { return hb ? (int64_t)kT * kT * hb : (int64_t)kT * kT / 2; }
 constexpr int hb_max_hop(int hb) { return hb == 0 ? 15 : (hb == 1 ? 255 : 65535); }
+constexpr int kHbDist = 4;
 
 // 4-bit tiles store the hops of rows (2p, 2p+1) of one column in one byte.  The
 // byte is a bijective encoding of the pair, chosen so that the shared-memory
@@ -135,6 +137,7 @@ __host__ __device__ inline size_t sym_offset(int64_t lt, int rl, int cl, int hb)
     const int tid = (cl >> 3) * 16 + (rl >> 3), r = rl & 7, c = cl & 7;
     const size_t base = (size_t)lt * (size_t)tile_bytes(hb);
     if (hb == 0) return base + ((size_t)(c >> 2) * 256 + tid) * 16 + (c & 3) * 4 + (r >> 1);
+    if (hb == 4) return base + ((size_t)(c * 2 + (r >> 2)) * 256 + tid) * 16 + (r & 3) * 4;  // fp32 distances
     if (hb == 1) return base + ((size_t)(c >> 1) * 256 + tid) * 16 + (c & 1) * 8 + r;
     return base + ((size_t)c * 256 + tid) * 16 + r * 2;
 }
@@ -150,6 +153,7 @@ struct SymArgs {
     int n;
     uint32_t magic;        // 0x4B000000 (2^23 as fp32 bits) for the hop decode, passed as a
                            // parameter so the PRMT selector can stay an immediate
+    float alpha;           // weight exponent w = d^alpha (fp32 distance tiles, hb = 4)
 };
 
 cudaError_t launch_sym(const SymArgs& a, int mode, int dim, int nsets, int hb, int grid, cudaStream_t s);
@@ -169,6 +173,15 @@ cudaError_t launch_sym_stress(const double* spart, int nitems, int nsets, double
 cudaError_t launch_bfs_level_sym(const int64_t* row_ptr, const int32_t* col, const uint32_t* fin, uint32_t* fout,
                                  uint32_t* visited, uint8_t* D, int n, int s0, int nsrc, int level, int nb, int64_t t0,
                                  int64_t t1, int hb, unsigned int* anynew, cudaStream_t s);
+// weighted / general-alpha setup: multi-source Bellman-Ford in fp64 over the
+// CSR with edge lengths; dist[v * S + s] for the batch's sources s0..s0+S-1
+cudaError_t launch_bf_init(double* dist, int n, int s0, int nsrc, int S, cudaStream_t s);
+cudaError_t launch_bf_relax(const int64_t* row_ptr, const int32_t* col, const double* len, const double* din,
+                            double* dout, int n, int S, int nsrc, unsigned int* changed, cudaStream_t s);
+cudaError_t launch_bf_store(const double* dist, int n, int s0, int nsrc, int S, int nb, int64_t t0, int64_t t1,
+                            uint8_t* D, double* dmax, cudaStream_t s);
+cudaError_t launch_dist_rows(const uint8_t* D, int hb, int nb, int64_t t0, int64_t t1, const int* rows, int nrows,
+                             int n, float* out, int* missing, cudaStream_t s);
 // 4-bit tiles: raw (lo | hi << 4) bytes written by the BFS -> nib_encode bytes
 cudaError_t launch_nib_encode(uint8_t* D, size_t bytes, cudaStream_t s);
 cudaError_t launch_hop_rows(const uint8_t* D, int hb, int nb, int64_t t0, int64_t t1, const int* rows, int nrows,

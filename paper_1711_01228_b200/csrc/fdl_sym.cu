@@ -349,9 +349,65 @@ __device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float
     }
 }
 
+// General weights (NEXT-3: weighted graphs, any alpha): d = the stored fp32
+// path length (device units), w = d^alpha = 2^(alpha log2 d) (MUFU LG2/EX2),
+// w d for the L^X coefficient.  P1 per set: q = 1/r, R += (w d q) delta,
+// s += w (r - d)^2 (Eq. 1); P2: w p_j / w p_i (product form); DIAG: w.
+__device__ __forceinline__ float lg2_approx(float x)
+{
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float ex2_approx(float x)
+{
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+template <int MODE, int DIM, int NSETS, bool SAFE>
+__device__ __forceinline__ void gen_pair(const float* xi, const float* xj, float d, float alpha, bool valid,
+                                         float* ai, float* aj, float* s)
+{
+    float w = ex2_approx(alpha * lg2_approx(d));
+    if (SAFE) w = valid ? w : 0.0f;
+    if (MODE == kSymP1) {
+        const float c = w * d;
+#pragma unroll
+        for (int k = 0; k < NSETS; ++k) {
+            float dl[DIM];
+            float r2 = FLT_MIN;
+#pragma unroll
+            for (int q = 0; q < DIM; ++q) {
+                dl[q] = xi[q * NSETS + k] - xj[q * NSETS + k];
+                r2 = fmaf(dl[q], dl[q], r2);
+            }
+            const float q1 = rsqrt_approx(r2);
+            const float coef = c * q1;
+#pragma unroll
+            for (int q = 0; q < DIM; ++q) {
+                ai[q * NSETS + k] = fmaf(coef, dl[q], ai[q * NSETS + k]);
+                aj[q * NSETS + k] = fmaf(coef, dl[q], aj[q * NSETS + k]);
+            }
+            const float u = fmaf(r2, q1, -d);
+            s[k] = fmaf(w * u, u, s[k]);
+        }
+    } else if (MODE == kSymP2) {
+#pragma unroll
+        for (int q = 0; q < DIM; ++q) {
+            ai[q] = fmaf(w, xj[q], ai[q]);
+            aj[q] = fmaf(w, xi[q], aj[q]);
+        }
+    } else {
+        ai[0] += w;
+        aj[0] += w;
+    }
+}
+
 template <int MODE, int DIM, int NSETS, int HB, bool SAFE>
 __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, const float* lut, const float2* lut2,
-                                         uint32_t magic, int ty, int tx, bool diag,
+                                         uint32_t magic, float alpha, int ty, int tx, bool diag,
                                          const float (&xi)[8][NSETS * DIM], float (&ai)[8][sym_ncomp<MODE, DIM, NSETS>()],
                                          float* myred, float (&sf)[NSETS])
 {
@@ -360,6 +416,33 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
     constexpr int NCH = HB ? 4 * HB : 2;  // 16-byte chunks per thread
     constexpr int CPC = HB ? 2 / HB : 4;  // columns per chunk
     const int tid = tx * 16 + ty;  // chunk owner index of the tile layout (sym_offset)
+    if (HB == kHbDist) {
+        // fp32 path lengths: column c = chunks 2c, 2c+1 (rows 0-3, 4-7)
+#pragma unroll 1
+        for (int c = 0; c < 8; ++c) {
+            const float4 d0 = *reinterpret_cast<const float4*>(sD + ((size_t)(2 * c) * 256 + tid) * 16);
+            const float4 d1 = *reinterpret_cast<const float4*>(sD + ((size_t)(2 * c + 1) * 256 + tid) * 16);
+            const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+            const int jl = tx * 8 + c;
+            const int js = c * 16 + tx;
+            float xj[PS];
+#pragma unroll
+            for (int q = 0; q < PS; ++q) xj[q] = sP[js * PS + q];
+            float aj[C];
+#pragma unroll
+            for (int v = 0; v < C; ++v) aj[v] = 0.0f;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                bool valid = true;
+                if (SAFE) valid = (dv[r] > 0.0f) && (!diag || (ty * 8 + r < jl));
+                const float dd = (SAFE && !valid) ? 1.0f : dv[r];
+                gen_pair<MODE, DIM, NSETS, SAFE>(&xi[r][0], xj, dd, alpha, valid, &ai[r][0], aj, sf);
+            }
+#pragma unroll
+            for (int v = 0; v < C; ++v) myred[c * C + v] = aj[v];
+        }
+        return;
+    }
     if (HB == 0) {
         // 4-bit tiles: one byte = hops of rows (2p, 2p+1) of a column, one 8-byte
         // LUT entry per byte gives both decoded values (h^2 for P1/DIAG, w' = 1/h^2
@@ -589,9 +672,9 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
 #pragma unroll
             for (int s = 0; s < NSETS; ++s) sf[s] = 0.0f;
             if (safe)
-                sym_tile<MODE, DIM, NSETS, HB, true>(sD, sP, lut, lut2, a.magic, ty, tx, diag, xi, ai, wrow, sf);
+                sym_tile<MODE, DIM, NSETS, HB, true>(sD, sP, lut, lut2, a.magic, a.alpha, ty, tx, diag, xi, ai, wrow, sf);
             else
-                sym_tile<MODE, DIM, NSETS, HB, false>(sD, sP, lut, lut2, a.magic, ty, tx, diag, xi, ai, wrow, sf);
+                sym_tile<MODE, DIM, NSETS, HB, false>(sD, sP, lut, lut2, a.magic, a.alpha, ty, tx, diag, xi, ai, wrow, sf);
 #pragma unroll
             for (int s = 0; s < NSETS; ++s) s64[s] += (double)sf[s];
             // stage consumed by this warp; the last of the 8 warps refills it
@@ -662,6 +745,9 @@ cudaError_t launch_sym(const SymArgs& a, int mode, int dim, int nsets, int hb, i
 {
     FDL_SYM_ALLHB(kSymP1, 2, 1) FDL_SYM_ALLHB(kSymP1, 2, 2) FDL_SYM_ALLHB(kSymP1, 3, 1) FDL_SYM_ALLHB(kSymP1, 3, 2)
     FDL_SYM_ALLHB(kSymP1S, 2, 2) FDL_SYM_ALLHB(kSymP1S, 3, 2)
+    FDL_SYM_CASE(kSymP1, 2, 1, 4) FDL_SYM_CASE(kSymP1, 2, 2, 4) FDL_SYM_CASE(kSymP1, 3, 1, 4)
+    FDL_SYM_CASE(kSymP1, 3, 2, 4) FDL_SYM_CASE(kSymP2, 2, 1, 4) FDL_SYM_CASE(kSymP2, 3, 1, 4)
+    FDL_SYM_CASE(kSymDiag, 2, 1, 4) FDL_SYM_CASE(kSymDiag, 3, 1, 4)
     FDL_SYM_ALLHB(kSymP2, 2, 1) FDL_SYM_ALLHB(kSymP2, 3, 1)
     FDL_SYM_ALLHB(kSymDiag, 2, 1) FDL_SYM_ALLHB(kSymDiag, 3, 1)
     return cudaErrorInvalidValue;
@@ -927,6 +1013,9 @@ int sym_max_ctas(int mode, int dim, int nsets, int hb)
 #define FDL_SYM_OCC3(M_, D_, S_) FDL_SYM_OCC(M_, D_, S_, 0) FDL_SYM_OCC(M_, D_, S_, 1) FDL_SYM_OCC(M_, D_, S_, 2)
     FDL_SYM_OCC3(kSymP1, 2, 1) FDL_SYM_OCC3(kSymP1, 2, 2) FDL_SYM_OCC3(kSymP1, 3, 1) FDL_SYM_OCC3(kSymP1, 3, 2)
     FDL_SYM_OCC3(kSymP1S, 2, 2) FDL_SYM_OCC3(kSymP1S, 3, 2)
+    FDL_SYM_OCC(kSymP1, 2, 1, 4) FDL_SYM_OCC(kSymP1, 2, 2, 4) FDL_SYM_OCC(kSymP1, 3, 1, 4)
+    FDL_SYM_OCC(kSymP1, 3, 2, 4) FDL_SYM_OCC(kSymP2, 2, 1, 4) FDL_SYM_OCC(kSymP2, 3, 1, 4)
+    FDL_SYM_OCC(kSymDiag, 2, 1, 4) FDL_SYM_OCC(kSymDiag, 3, 1, 4)
     FDL_SYM_OCC3(kSymP2, 2, 1) FDL_SYM_OCC3(kSymP2, 3, 1)
     FDL_SYM_OCC3(kSymDiag, 2, 1) FDL_SYM_OCC3(kSymDiag, 3, 1)
     return 1;
@@ -1213,6 +1302,126 @@ cudaError_t launch_bfs_level_sym(const int64_t* row_ptr, const int32_t* col, con
     else
         k_bfs_level_sym<2><<<grid, 256, 0, s>>>(row_ptr, col, fin, fout, visited, D, n, s0, nsrc, level, nb, t0, t1,
                                                 anynew);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------ weighted APSP (NEXT-3 setup)
+// Multi-source Bellman-Ford in fp64: dist[v * S + s] = shortest path length
+// from source s0 + s to v.  Pull relaxation, warp per vertex, lanes over the
+// sources; iterated until no value changes.  Each stored value is the fp64
+// sum along a shortest path, so the result does not depend on the iteration
+// order; the tiles get its correctly rounded fp32 value.
+__global__ void k_bf_init(double* dist, int n, int s0, int nsrc, int S)
+{
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)n * S) return;
+    const int v = (int)(idx / S), k = (int)(idx % S);
+    dist[idx] = (k < nsrc && v == s0 + k) ? 0.0 : INFINITY;
+}
+
+cudaError_t launch_bf_init(double* dist, int n, int s0, int nsrc, int S, cudaStream_t s)
+{
+    const int64_t total = (int64_t)n * S;
+    k_bf_init<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(dist, n, s0, nsrc, S);
+    return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) k_bf_relax(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                                                  const double* __restrict__ len, const double* __restrict__ din,
+                                                  double* __restrict__ dout, int n, int S, int nsrc,
+                                                  unsigned int* changed)
+{
+    const int v = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (v >= n) return;
+    const int64_t beg = row_ptr[v], end = row_ptr[v + 1];
+    bool any = false;
+    for (int k = lane; k < nsrc; k += 32) {
+        const double old = din[(int64_t)v * S + k];
+        double best = old;
+        for (int64_t e = beg; e < end; ++e) {
+            const double c = din[(int64_t)col[e] * S + k] + len[e];
+            best = c < best ? c : best;
+        }
+        dout[(int64_t)v * S + k] = best;
+        any |= best < old;
+    }
+    if (__any_sync(0xffffffffu, any) && lane == 0) *changed = 1u;
+}
+
+cudaError_t launch_bf_relax(const int64_t* row_ptr, const int32_t* col, const double* len, const double* din,
+                            double* dout, int n, int S, int nsrc, unsigned int* changed, cudaStream_t s)
+{
+    const int64_t threads = (int64_t)n * 32;
+    k_bf_relax<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(row_ptr, col, len, din, dout, n, S, nsrc, changed);
+    return cudaGetLastError();
+}
+
+// rows s0..s0+nsrc-1 of the upper-triangle tiles of the local range <- fp32(dist)
+__global__ void k_bf_store(const double* __restrict__ dist, int n, int s0, int nsrc, int S, int nb, int64_t t0,
+                           int64_t t1, float* D, double* dmax)
+{
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)n * nsrc) return;
+    const int v = (int)(idx / nsrc), k = (int)(idx % nsrc);
+    const int src = s0 + k;
+    const int I = src / kT, J = v / kT;
+    if (I > J) return;
+    const int64_t t = tri_index(I, J, nb);
+    if (t < t0 || t >= t1) return;
+    const double d = dist[(int64_t)v * S + k];
+    D[sym_offset(t - t0, src % kT, v % kT, kHbDist) / 4] = (float)d;
+    if (d > 0.0) {  // max distance (positive doubles order like their bit patterns)
+        atomicMax(reinterpret_cast<unsigned long long*>(dmax), (unsigned long long)__double_as_longlong(d));
+    }
+}
+
+cudaError_t launch_bf_store(const double* dist, int n, int s0, int nsrc, int S, int nb, int64_t t0, int64_t t1,
+                            uint8_t* D, double* dmax, cudaStream_t s)
+{
+    const int64_t total = (int64_t)n * nsrc;
+    k_bf_store<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(dist, n, s0, nsrc, S, nb, t0, t1,
+                                                             reinterpret_cast<float*>(D), dmax);
+    return cudaGetLastError();
+}
+
+// Dense rows of the stored distances (any width) as fp32: out[r][j] = d'(rows[r], j)
+__global__ void k_dist_rows(const uint8_t* __restrict__ D, int hb, int nb, int64_t t0, int64_t t1,
+                            const int* __restrict__ rows, int nrows, int n, float* out, int* missing)
+{
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)nrows * n) return;
+    const int r = (int)(idx / n), j = (int)(idx % n);
+    int a = rows[r], b = j;
+    if (a / kT > b / kT) {
+        const int tmp = a;
+        a = b;
+        b = tmp;
+    }
+    const int64_t t = tri_index(a / kT, b / kT, nb);
+    if (t < t0 || t >= t1) {
+        *missing = 1;
+        out[idx] = 0.0f;
+        return;
+    }
+    const size_t off = sym_offset(t - t0, a % kT, b % kT, hb);
+    float v;
+    if (hb == kHbDist)
+        v = *reinterpret_cast<const float*>(D + off);
+    else if (hb == 0)
+        v = (float)((a & 1) ? nib_decode_hi(D[off]) : nib_decode_lo(D[off]));
+    else if (hb == 1)
+        v = (float)D[off];
+    else
+        v = (float)(D[off] | (D[off + 1] << 8));
+    out[idx] = (rows[r] == j) ? 0.0f : v;
+}
+
+cudaError_t launch_dist_rows(const uint8_t* D, int hb, int nb, int64_t t0, int64_t t1, const int* rows, int nrows,
+                             int n, float* out, int* missing, cudaStream_t s)
+{
+    const int64_t total = (int64_t)nrows * n;
+    k_dist_rows<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(D, hb, nb, t0, t1, rows, nrows, n, out, missing);
     return cudaGetLastError();
 }
 

@@ -30,7 +30,7 @@ EXPORTS = [
     "fdl_nccl_unique_id", "fdl_set_stream", "fdl_step", "fdl_run_until_converged", "fdl_get_positions",
     "fdl_set_positions", "fdl_eval_forces", "fdl_get_hop_rows", "fdl_get_diag", "fdl_get_info",
     "fdl_set_timing", "fdl_get_stats", "fdl_reset_stats", "fdl_bench_ffma", "fdl_status_str",
-    "fdl_last_error", "fdl_destroy", "fdl_eval_partial", "fdl_set_omega_vertex",
+    "fdl_last_error", "fdl_destroy", "fdl_eval_partial", "fdl_set_omega_vertex", "fdl_get_dist_rows",
 ]
 
 
@@ -115,6 +115,7 @@ def _load():
         "fdl_set_positions": (i32, [P, P, sz]),
         "fdl_eval_forces": (i32, [P, P, P, P]),
         "fdl_set_omega_vertex": (i32, [P, P, sz]),
+        "fdl_get_dist_rows": (i32, [P, i32, i32, P]),
         "fdl_get_hop_rows": (i32, [P, i32, i32, P]),
         "fdl_get_diag": (i32, [P, P, sz]),
         "fdl_get_info": (i32, [P, ctypes.POINTER(CtxInfo)]),
@@ -148,7 +149,7 @@ def params_default() -> Params:
 
 
 def make_params(dim=2, k=0.0, omega=1.5, step=math.inf, tol=1e-4, max_iter=500, cg_rtol=0.0,
-                cg_max_iter=0, strategy=STRAT_FIXED, seed=1, device=0, a_refresh=0, hop_bits=0, cg_extrap=1, enum_count=19,
+                cg_max_iter=0, strategy=STRAT_FIXED, seed=1, device=0, a_refresh=0, hop_bits=0, cg_extrap=1, enum_count=19, weight_exp=-2.0,
                 enum_step=0.5, p1_split=-1) -> Params:
     p = params_default()
     p.dim, p.k, p.omega, p.step, p.tol, p.max_iter = dim, k, omega, step, tol, max_iter
@@ -157,6 +158,7 @@ def make_params(dim=2, k=0.0, omega=1.5, step=math.inf, tol=1e-4, max_iter=500, 
     p.hop_bits = hop_bits
     p.cg_extrap = cg_extrap
     p.enum_count, p.enum_step = enum_count, enum_step
+    p.weight_exp = weight_exp
     p.p1_split = p1_split
     return p
 
@@ -189,7 +191,7 @@ class Layout:
     """One layout context (fdl_ctx) on one GPU; names follow include/fdl.h."""
 
     def __init__(self, n: int, row_ptr, col_idx, params: Params | None = None, init_pos=None,
-                 nccl_id: bytes | None = None, rank: int = 0, world: int = 1):
+                 nccl_id: bytes | None = None, rank: int = 0, world: int = 1, edge_len=None):
         self._h = ctypes.c_void_p()
         self.n = int(n)
         self._rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
@@ -197,15 +199,19 @@ class Layout:
         self.params = params if params is not None else params_default()
         self.dim = int(self.params.dim)
         X0 = None if init_pos is None else np.ascontiguousarray(init_pos, dtype=np.float64)
+        self._len = None if edge_len is None else np.ascontiguousarray(edge_len, dtype=np.float64)
+        if self._len is not None and self._len.size != self._col.size:
+            raise ValueError("edge_len must have one entry per stored CSR direction")
         if X0 is not None and X0.size != self.n * self.dim:
             raise ValueError("init_pos must have n*dim entries")
         if world == 1:
-            st = lib.fdl_create(self.n, _ptr(self._rp), _ptr(self._col), None, ctypes.byref(self.params),
+            st = lib.fdl_create(self.n, _ptr(self._rp), _ptr(self._col), _ptr(self._len), ctypes.byref(self.params),
                                 _ptr(X0), ctypes.byref(self._h))
         else:
             # nccl_id None -> emulated rank (test hook: fdl_eval_partial only)
             idbuf = None if nccl_id is None else (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
-            st = lib.fdl_create_sharded(self.n, _ptr(self._rp), _ptr(self._col), None, ctypes.byref(self.params),
+            st = lib.fdl_create_sharded(self.n, _ptr(self._rp), _ptr(self._col), _ptr(self._len),
+                                        ctypes.byref(self.params),
                                         _ptr(X0), idbuf, rank, world, ctypes.byref(self._h))
         if st != 0:
             raise FdlError(st, "fdl_create failed (see stderr)")
@@ -282,6 +288,12 @@ class Layout:
     def get_hop_rows(self, r0: int, nrows: int) -> np.ndarray:
         out = np.empty((nrows, self.n), dtype=np.uint16)
         _check(self._h, lib.fdl_get_hop_rows(self._h, r0, nrows, _ptr(out)))
+        return out
+
+    def get_dist_rows(self, r0: int, nrows: int) -> np.ndarray:
+        """d_ij = k x shortest path length for rows [r0, r0 + nrows) (original units)."""
+        out = np.empty((nrows, self.n), dtype=np.float64)
+        _check(self._h, lib.fdl_get_dist_rows(self._h, r0, nrows, _ptr(out)))
         return out
 
     def get_diag(self) -> np.ndarray:

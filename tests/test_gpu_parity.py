@@ -474,3 +474,69 @@ def test_split_p1_bitwise(name):
     assert out[0][0] == out[1][0]
     assert np.array_equal(out[0][1], out[1][1])
     assert out[1][2] == sum(1 for a in out[1][0] if not a[2])
+
+
+# --------------------------------------------- NEXT-3: weighted graphs, general alpha
+def _weighted_case(kind):
+    from oracle import weighted
+    if kind == "wrgg":
+        g, lens = graphs.random_geometric_graph_weighted(700, 6, 21)
+    elif kind == "wgrid":
+        g = graphs.grid_graph(12, 13)
+        lens = graphs.edge_lengths_uniform(g, 0.5, 2.0, 22)
+    else:  # unit lengths (general alpha on hop distances)
+        g = graphs.grid_graph(10, 10)
+        lens = None
+    D = weighted.dist_matrix(g, np.ones(len(g.col)) if lens is None else lens)
+    return g, lens, D
+
+
+@pytest.mark.parametrize("kind", ["wrgg", "wgrid"])
+def test_weighted_distances(kind):
+    """Multi-source Bellman-Ford (fp64, stored fp32) = Dijkstra (fp64) rounded."""
+    g, lens, D = _weighted_case(kind)
+    k = 0.05
+    p = fdl.make_params(dim=2, k=k)
+    L = fdl.Layout.from_graph(g, params=p, init_pos=graphs.init_positions(g.n, 2, 1), edge_len=lens)
+    assert L.info.hop_bits == 32
+    got = L.get_dist_rows(0, g.n)
+    want = k * D.astype(np.float32).astype(np.float64)
+    np.testing.assert_allclose(got, want, rtol=2e-7, atol=0)
+
+
+@pytest.mark.parametrize("kind,alpha,dim", [("wrgg", -2.0, 2), ("wrgg", -1.0, 2), ("wgrid", -2.0, 3),
+                                            ("unit", -1.0, 2), ("unit", -3.0, 2)])
+def test_weighted_forces(kind, alpha, dim):
+    """R = L^X X, A = L^W X and f (Eq. 1) with w = d^alpha at X0 against the
+    fp64 weighted oracle: relL2 <= 1e-5, f relative <= 1e-6 (MUFU lg2/ex2
+    weights, fp32 pair math, fp64 reductions)."""
+    from oracle import weighted
+    g, lens, D = _weighted_case(kind)
+    k = 0.05
+    X0 = graphs.init_positions(g.n, dim, 3)
+    p = fdl.make_params(dim=dim, k=k, weight_exp=alpha)
+    L = fdl.Layout.from_graph(g, params=p, init_pos=X0, edge_len=lens)
+    R, A, f = L.eval_forces()
+    Ro = weighted.ly(X0, D, k, alpha)
+    Ao = weighted.lw(X0, D, k, alpha)
+    fo = weighted.stress(X0, D, k, alpha)
+    assert relL2(R, Ro) <= FORCE_TOL, relL2(R, Ro)
+    assert relL2(A, Ao) <= FORCE_TOL, relL2(A, Ao)
+    assert relL2(R - A, Ro - Ao) <= FORCE_TOL
+    assert abs(f - fo) / fo <= STRESS_TOL, (f, fo)
+
+
+@pytest.mark.parametrize("kind,alpha,omega", [("wrgg", -2.0, 1.5), ("wgrid", -1.0, 1.0), ("unit", -1.0, 1.5)])
+def test_weighted_end_to_end(kind, alpha, omega):
+    """Algorithm 2 on a weighted graph / general alpha against the fp64 oracle
+    (ProblemD, Cholesky): the §8(c) end-to-end gates."""
+    from oracle import weighted
+    g, lens, D = _weighted_case(kind)
+    k = 0.05
+    X0 = graphs.init_positions(g.n, 2, 4)
+    tol = 1e-5
+    p = fdl.make_params(dim=2, k=k, weight_exp=alpha, omega=omega, tol=tol, max_iter=500)
+    L = fdl.Layout.from_graph(g, params=p, init_pos=X0, edge_len=lens)
+    r = L.run_until_converged()
+    o = layout.run_algorithm2(weighted.ProblemD(D, 2, k, alpha), X0, omega, tol, 500)
+    _gates(r.iterations, r.f_final, o)

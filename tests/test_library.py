@@ -73,7 +73,12 @@ def test_parameter_validation():
     p = fdl.make_params(tol=0.0)
     _expect("FDL_E_INVALID_ARG", g.n, g.row_ptr, g.col, params=p)
     p = fdl.make_params()
-    p.weight_exp = -1.0
+    p.weight_exp = float("nan")
+    _expect("FDL_E_INVALID_ARG", g.n, g.row_ptr, g.col, params=p)
+    # edge lengths (NEXT-3): positive and finite per stored direction
+    _expect("FDL_E_BAD_LENGTH", g.n, g.row_ptr, g.col, edge_len=np.array([1.0, 1.0, -2.0, -2.0]))
+    _expect("FDL_E_BAD_LENGTH", g.n, g.row_ptr, g.col, edge_len=np.array([1.0, 1.0, np.inf, np.inf]))
+    p = fdl.make_params(strategy=fdl.STRAT_ENUM, weight_exp=-1.0)
     _expect("FDL_E_UNSUPPORTED", g.n, g.row_ptr, g.col, params=p)
     p = fdl.make_params()
     p.struct_size = 3
