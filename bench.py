@@ -149,14 +149,28 @@ def cpu_oracle_sample(name: str, seed: int, rows_target: int = 0):
     X1 = X0 * 1.01
     nrows = rows_target or max(64, min(g.n, int(6e8 // g.n)))
     rows = np.linspace(0, g.n - 1, nrows).astype(np.int32)
-    t0 = time.perf_counter()
-    hr = core.hop_rows(g, rows)
-    t1 = time.perf_counter()
-    core.stress_rows(X0, rows, hr, k)
-    core.stress_rows(X1, rows, hr, k)
-    core.ly_rows(X1, rows, hr, k)
-    core.lw_rows(X1, rows, hr, k)
-    t2 = time.perf_counter()
+    lens = configs.edge_lengths_for(name)
+    if lens is not None:  # weighted input (NEXT-3): Dijkstra rows + the dense numpy oracle by rows
+        from oracle import weighted
+        nrows = min(nrows, max(16, int(2e7 // g.n)))  # numpy temporaries are rows x n x dim
+        rows = np.linspace(0, g.n - 1, nrows).astype(np.int32)
+        t0 = time.perf_counter()
+        Dr = weighted.dist_rows(g, lens, rows)
+        t1 = time.perf_counter()
+        weighted.stress_rows(X0, rows, Dr, k)
+        weighted.stress_rows(X1, rows, Dr, k)
+        weighted.ly_rows(X1, rows, Dr, k)
+        weighted.lw_rows(X1, rows, Dr, k)
+        t2 = time.perf_counter()
+    else:
+        t0 = time.perf_counter()
+        hr = core.hop_rows(g, rows)
+        t1 = time.perf_counter()
+        core.stress_rows(X0, rows, hr, k)
+        core.stress_rows(X1, rows, hr, k)
+        core.ly_rows(X1, rows, hr, k)
+        core.lw_rows(X1, rows, hr, k)
+        t2 = time.perf_counter()
     ordered = 4 * nrows * (g.n - 1)
     return {
         "value": (ordered / 2) / (t2 - t1),
@@ -164,7 +178,7 @@ def cpu_oracle_sample(name: str, seed: int, rows_target: int = 0):
         "cores": core.num_threads(),
         "kind": "oracle",
         "sample": f"{nrows} of {g.n} rows of {name}: 2 stress + L^X X + L^W X row passes (fp64); "
-                  f"BFS of the sampled sources {t1 - t0:.2f}s excluded",
+                  f"{'Dijkstra' if lens is not None else 'BFS'} of the sampled sources {t1 - t0:.2f}s excluded",
         "seconds": t2 - t1,
     }
 
@@ -228,9 +242,9 @@ def run_gpu(args):
                         strategy={"fixed": fdl.STRAT_FIXED, "prob": fdl.STRAT_PROB, "enum": fdl.STRAT_ENUM}[args.strategy])
     if world > 1:
         from paper_1711_01228_b200 import dist as fdist
-        L = fdist.sharded_layout(g, p, X0)      # NCCL id broadcast over the process group
+        L = fdist.sharded_layout(g, p, X0, edge_len=configs.edge_lengths_for(args.config))
     else:
-        L = fdl.Layout.from_graph(g, params=p, init_pos=X0)
+        L = fdl.Layout.from_graph(g, params=p, init_pos=X0, edge_len=configs.edge_lengths_for(args.config))
     stream = torch.cuda.current_stream()
     L.set_stream(stream.cuda_stream)
     L.set_timing(True)

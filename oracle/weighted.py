@@ -124,3 +124,44 @@ def floyd_warshall(n: int, edges, lengths) -> np.ndarray:
                 if D[i][m] + D[m][j] < D[i][j]:
                     D[i][j] = D[i][m] + D[m][j]
     return np.array(D)
+
+
+# ------------------------------------------- row-sampled evaluations (bench CPU leg)
+def dist_rows(g, lengths: np.ndarray, rows) -> np.ndarray:
+    """Shortest path lengths from the listed sources (Dijkstra, fp64)."""
+    A = csr_matrix((np.asarray(lengths, dtype=np.float64), g.col, g.row_ptr), shape=(g.n, g.n))
+    return dijkstra(A, directed=False, indices=np.asarray(rows))
+
+
+def _row_terms(X, rows, Drows, k, alpha):
+    X = np.asarray(X, dtype=np.float64)
+    rows = np.asarray(rows)
+    diff = X[rows][:, None, :] - X[None, :, :]
+    r = np.sqrt((diff * diff).sum(axis=2))
+    d = k * np.asarray(Drows, dtype=np.float64)
+    mask = np.ones_like(d, dtype=bool)
+    mask[np.arange(len(rows)), rows] = False
+    w = np.zeros_like(d)
+    w[mask] = d[mask] ** alpha
+    return diff, r, d, w
+
+
+def stress_rows(X, rows, Drows, k, alpha=-2.0):
+    """s_i = sum_{j != i} w_ij (r_ij - d_ij)^2 (Eq. 1 by rows; f = sum s_i / 2)."""
+    _, r, d, w = _row_terms(X, rows, Drows, k, alpha)
+    return (w * (r - d) ** 2).sum(axis=1)
+
+
+def ly_rows(X, rows, Drows, k, alpha=-2.0):
+    """(L^X X)_i for the listed rows (lines 69-73)."""
+    diff, r, d, w = _row_terms(X, rows, Drows, k, alpha)
+    c = np.zeros_like(r)
+    m = r > 0
+    c[m] = w[m] * d[m] / r[m]
+    return (c[:, :, None] * diff).sum(axis=1)
+
+
+def lw_rows(X, rows, Drows, k, alpha=-2.0):
+    """(L^W X)_i for the listed rows (lines 63-68)."""
+    diff, _, _, w = _row_terms(X, rows, Drows, k, alpha)
+    return (w[:, :, None] * diff).sum(axis=1)

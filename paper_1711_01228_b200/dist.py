@@ -45,11 +45,12 @@ def sum_in_rank_order(values) -> float:
     return s
 
 
-def sharded_layout(g, params, init_pos):
+def sharded_layout(g, params, init_pos, edge_len=None):
     """Build this rank's context of a world-size layout (NCCL over NVLink)."""
     from . import fdl
 
     rank, world = dist.get_rank(), dist.get_world_size()
     nid = fdl.nccl_unique_id() if rank == 0 else None
     nid = broadcast_bytes(nid, 128, 0)
-    return fdl.Layout.from_graph(g, params=params, init_pos=init_pos, nccl_id=nid, rank=rank, world=world)
+    return fdl.Layout.from_graph(g, params=params, init_pos=init_pos, nccl_id=nid, rank=rank, world=world,
+                                 edge_len=edge_len)

@@ -43,9 +43,14 @@ CONFIGS = {
     "C3": LayoutConfig("C3", dim=2, omega=1.5, tol=1e-4, max_iter=500, k_rule="n_pow_inv_d"),
     "C4": LayoutConfig("C4", dim=3, omega=1.5, tol=1e-4, max_iter=500, k_rule="n_pow_inv_d"),
     "C5": LayoutConfig("C5", dim=2, omega=1.5, tol=1e-4, max_iter=500, k_rule="n_pow_inv_d"),
+    # NEXT-3 measurement input (not a BASELINE config): a railway-like weighted
+    # network: RGG n=50000, mean degree 6, edge length
+    # = Euclidean distance of the generating points / radius, floored at 0.25,
+    # largest component.
+    "W4": LayoutConfig("W4", dim=2, omega=1.5, tol=1e-4, max_iter=500, k_rule="n_pow_inv_d"),
 }
 
-CONFIG_INDEX = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5}
+CONFIG_INDEX = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5, "W4": 6}
 
 
 @functools.lru_cache(maxsize=8)
@@ -61,7 +66,21 @@ def graph_for(name: str) -> graphs.Graph:
         return graphs.random_geometric_graph(50000, 6.0, seed=4)
     if name == "C5":
         return graphs.barabasi_albert(200000, 3, seed=5)
+    if name == "W4":
+        return _weighted_for(name)[0]
     raise KeyError(name)
+
+
+@functools.lru_cache(maxsize=2)
+def _weighted_for(name: str):
+    if name == "W4":
+        return graphs.random_geometric_graph_weighted(50000, 6.0, seed=46)
+    raise KeyError(name)
+
+
+def edge_lengths_for(name: str):
+    """Per-direction edge lengths of a weighted configuration (None: unit lengths)."""
+    return _weighted_for(name)[1] if name.startswith("W") else None
 
 
 def positions_for(name: str, n: int, seed: int) -> np.ndarray:

@@ -248,10 +248,13 @@ def edge_lengths_uniform(g: Graph, lo: float, hi: float, seed: int) -> np.ndarra
     return _lengths_on_csr(g, e, lens)
 
 
-def random_geometric_graph_weighted(n: int, mean_degree: float, seed: int):
+def random_geometric_graph_weighted(n: int, mean_degree: float, seed: int, min_frac: float = 0.25):
     """RGG as in random_geometric_graph (largest component) with each edge's
-    length = the Euclidean distance of its endpoints' generating points (a
-    railway-like planar network).  Returns (graph, lengths aligned with col)."""
+    length = the Euclidean distance of its endpoints' generating points in
+    units of the connection radius r, floored at ``min_frac`` (a railway-like
+    planar network: segment lengths between min_frac and 1; the floor keeps
+    near-coincident points from making w = d^-2 arbitrarily large).  Returns
+    (graph, lengths aligned with col)."""
     from scipy.spatial import cKDTree
 
     rng = np.random.default_rng(seed)
@@ -264,7 +267,7 @@ def random_geometric_graph_weighted(n: int, mean_degree: float, seed: int):
     keep = _largest_component_ids(g0)
     p = pts[keep]
     e = g.edges()
-    lens = np.sqrt(((p[e[:, 0]] - p[e[:, 1]]) ** 2).sum(axis=1))
+    lens = np.maximum(np.sqrt(((p[e[:, 0]] - p[e[:, 1]]) ** 2).sum(axis=1)) / r, min_frac)
     return g, _lengths_on_csr(g, e, lens)
 
 
