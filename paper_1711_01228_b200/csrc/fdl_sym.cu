@@ -409,7 +409,7 @@ template <int MODE, int DIM, int NSETS, int HB, bool SAFE>
 __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, const float* lut, const float2* lut2,
                                          uint32_t magic, float alpha, int ty, int tx, bool diag,
                                          const float (&xi)[8][NSETS * DIM], float (&ai)[8][sym_ncomp<MODE, DIM, NSETS>()],
-                                         float* myred, float (&sf)[NSETS])
+                                         float* myred, float (&sf)[2][NSETS])
 {
     constexpr int C = sym_ncomp<MODE, DIM, NSETS>();
     constexpr int PS = sym_ps<MODE, DIM, NSETS>();
@@ -436,7 +436,7 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
                 bool valid = true;
                 if (SAFE) valid = (dv[r] > 0.0f) && (!diag || (ty * 8 + r < jl));
                 const float dd = (SAFE && !valid) ? 1.0f : dv[r];
-                gen_pair<MODE, DIM, NSETS, SAFE>(&xi[r][0], xj, dd, alpha, valid, &ai[r][0], aj, sf);
+                gen_pair<MODE, DIM, NSETS, SAFE>(&xi[r][0], xj, dd, alpha, valid, &ai[r][0], aj, &sf[r & 1][0]);
             }
 #pragma unroll
             for (int v = 0; v < C; ++v) myred[c * C + v] = aj[v];
@@ -491,7 +491,7 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
                         const float v = hh ? e[rp].y : e[rp].x;
                         bool valid = true;
                         if (SAFE) valid = (v > 0.0f) && (!diag || (ty * 8 + r < jl));
-                        sym_pair<MODE, DIM, NSETS, SAFE>(&xi[r][0], xj, v, v, valid, &ai[r][0], &aj[hh][0], sf);
+                        sym_pair<MODE, DIM, NSETS, SAFE>(&xi[r][0], xj, v, v, valid, &ai[r][0], &aj[hh][0], &sf[hh][0]);
                     }
                 }
 #pragma unroll
@@ -537,7 +537,7 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
                 }
                 bool valid = true;
                 if (SAFE) valid = (h2 > 0.0f) && (!diag || (ty * 8 + r < jl));
-                sym_pair<MODE, DIM, NSETS, SAFE>(&xi[r][0], xj, h2, wl, valid, &ai[r][0], &aj[r & 1][0], sf);
+                sym_pair<MODE, DIM, NSETS, SAFE>(&xi[r][0], xj, h2, wl, valid, &ai[r][0], &aj[r & 1][0], &sf[r & 1][0]);
             }
 #pragma unroll
             for (int v = 0; v < C; ++v) myred[c * C + v] = aj[0][v] + aj[1][v];
@@ -668,15 +668,15 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
             mbar_wait(&full[stage], phase);
             const uint8_t* sD = smem + (size_t)stage * STAGE;
             const float* sP = reinterpret_cast<const float*>(sD + DT);
-            float sf[NSETS];
+            float sf[2][NSETS];  // stress of the tile, even / odd rows (two independent FMA chains)
 #pragma unroll
-            for (int s = 0; s < NSETS; ++s) sf[s] = 0.0f;
+            for (int s = 0; s < NSETS; ++s) sf[0][s] = sf[1][s] = 0.0f;
             if (safe)
                 sym_tile<MODE, DIM, NSETS, HB, true>(sD, sP, lut, lut2, a.magic, a.alpha, ty, tx, diag, xi, ai, wrow, sf);
             else
                 sym_tile<MODE, DIM, NSETS, HB, false>(sD, sP, lut, lut2, a.magic, a.alpha, ty, tx, diag, xi, ai, wrow, sf);
 #pragma unroll
-            for (int s = 0; s < NSETS; ++s) s64[s] += (double)sf[s];
+            for (int s = 0; s < NSETS; ++s) s64[s] += (double)sf[0][s] + (double)sf[1][s];
             // stage consumed by this warp; the last of the 8 warps refills it
             __syncwarp();
             if (lane == 0) {
