@@ -203,6 +203,21 @@ fdl_status fdl_create_sharded(int32_t n, const int64_t* row_ptr, const int32_t* 
                               const double* init_pos, const uint8_t* nccl_unique_id,
                               int32_t rank, int32_t world, fdl_ctx** out);
 
+/* In-process loopback group (test hook of the multi-GPU path): `world` contexts
+ * created with fdl_create_loopback in one process, each driven from its own host
+ * thread, exchange their partial sums through a host buffer and a host barrier
+ * instead of NCCL (every all-gather of fdl_create_sharded becomes a stream sync,
+ * a device->host copy of the rank's slice, a barrier and a host->device copy).
+ * No kernel waits for another rank, so the ranks may share one GPU; the results
+ * are those of the NCCL path (same data movement).  The group outlives its
+ * contexts; fdl_group_destroy frees it. */
+typedef struct fdl_group fdl_group;
+fdl_status fdl_group_create(int32_t world, fdl_group** out);
+void fdl_group_destroy(fdl_group* group);
+fdl_status fdl_create_loopback(int32_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                               const double* edge_len, const fdl_params* p, const double* init_pos,
+                               fdl_group* group, int32_t rank, fdl_ctx** out);
+
 /* Test hook of the sharded path on one GPU.  fdl_create_sharded with
  * nccl_unique_id == NULL and world > 1 builds an EMULATED rank: it stores and
  * evaluates only its own tiles and has no communicator, so it accepts only

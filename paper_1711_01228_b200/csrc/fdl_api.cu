@@ -21,6 +21,8 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <mutex>
+#include <condition_variable>
 
 #include "fdl.h"
 #include "fdl_internal.h"
@@ -109,6 +111,33 @@ void tri_coords(int64_t t, int64_t nb, int64_t& I, int64_t& J)
 
 extern "C" fdl_status fdl_shard_tiles(int32_t n, int32_t world, int32_t rank, int64_t* t0, int64_t* t1);
 
+// In-process loopback transport (test hook): the ranks of one group are contexts
+// in one process, driven from separate host threads.  An all-gather syncs the
+// rank's stream, copies its slice to a shared host buffer, waits on a host
+// barrier for every rank, and copies the gathered buffer back; no kernel ever
+// waits for another rank (the exchange is host-side), so all ranks may share
+// one GPU.  Same data movement as the NCCL all-gather, hence the same results.
+struct fdl_group {
+    int world = 0;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t gen = 0;
+    std::vector<char> buf;
+    void barrier()
+    {
+        std::unique_lock<std::mutex> lk(m);
+        const uint64_t g = gen;
+        if (++arrived == world) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+
 struct fdl_ctx {
     fdl_params p{};
     int n = 0, dim = 0, rank = 0, world = 1;
@@ -182,6 +211,7 @@ struct fdl_ctx {
     bool broken = false;
     // NCCL
     ncclComm_t comm = nullptr;
+    fdl_group* group = nullptr;  // loopback transport instead of NCCL (test hook)
     bool emulated = false;  // world > 1 without communicator (fdl_eval_partial only)
 };
 
@@ -379,6 +409,26 @@ fdl_status allgather_inplace(fdl_ctx* ctx, void* buf, size_t slice_elems, int nc
 {
     if (ctx->world == 1 || ctx->emulated) return FDL_OK;
     char* base = static_cast<char*>(buf);
+    if (ctx->group) {
+        fdl_group& G = *ctx->group;
+        const size_t sb = slice_elems * esize;
+        FDL_CUDA(cudaStreamSynchronize(ctx->stream));
+        {
+            std::lock_guard<std::mutex> lk(G.m);
+            if (G.buf.size() < sb * G.world) G.buf.resize(sb * G.world);
+        }
+        G.barrier();  // every rank sized the buffer
+        // copies on the context's (non-blocking) stream: a plain cudaMemcpy from pageable
+        // memory may return before the data lands and is not ordered with that stream
+        FDL_CUDA(cudaMemcpyAsync(G.buf.data() + (size_t)ctx->rank * sb, base + (size_t)ctx->rank * sb, sb,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+        FDL_CUDA(cudaStreamSynchronize(ctx->stream));
+        G.barrier();  // every slice is in
+        FDL_CUDA(cudaMemcpyAsync(base, G.buf.data(), sb * G.world, cudaMemcpyHostToDevice, ctx->stream));
+        FDL_CUDA(cudaStreamSynchronize(ctx->stream));
+        G.barrier();  // every rank read the buffer before it is reused
+        return FDL_OK;
+    }
     ncclResult_t r = g_nccl.AllGather(base + (size_t)ctx->rank * slice_elems * esize, base, slice_elems, nccl_type,
                                       ctx->comm, ctx->stream);
     if (r != 0) {
@@ -796,8 +846,8 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     FDL_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
 
-    ctx->emulated = world > 1 && nccl_id == nullptr;
-    if (world > 1 && !ctx->emulated) {
+    ctx->emulated = world > 1 && nccl_id == nullptr && ctx->group == nullptr;
+    if (world > 1 && !ctx->emulated && !ctx->group) {
         if (!g_nccl.load(msg)) return set_err(ctx, FDL_E_NCCL, msg);
         ncclUniqueId id;
         memcpy(id.internal, nccl_id, 128);
@@ -1159,11 +1209,12 @@ void fdl_destroy(fdl_ctx* ctx)
 
 static fdl_status create_common(int32_t n, const int64_t* row_ptr, const int32_t* col_idx, const double* edge_len,
                                 const fdl_params* p, const double* init_pos, const uint8_t* id, int32_t rank,
-                                int32_t world, fdl_ctx** out)
+                                int32_t world, fdl_ctx** out, fdl_group* group = nullptr)
 {
     if (!out) return FDL_E_INVALID_ARG;
     *out = nullptr;
     fdl_ctx* ctx = new fdl_ctx();
+    ctx->group = group;
     fdl_status s = create_impl(n, row_ptr, col_idx, edge_len, p, init_pos, id, rank, world, ctx);
     if (s != FDL_OK) {
         fprintf(stderr, "fdl_create: %s: %s\n", fdl_status_str(s), ctx->err.c_str());
@@ -1185,6 +1236,24 @@ fdl_status fdl_create_sharded(int32_t n, const int64_t* row_ptr, const int32_t* 
                               int32_t rank, int32_t world, fdl_ctx** out)
 {
     return create_common(n, row_ptr, col_idx, edge_len, p, init_pos, nccl_unique_id, rank, world, out);
+}
+
+fdl_status fdl_group_create(int32_t world, fdl_group** out)
+{
+    if (!out || world < 1) return FDL_E_INVALID_ARG;
+    *out = new fdl_group();
+    (*out)->world = world;
+    return FDL_OK;
+}
+
+void fdl_group_destroy(fdl_group* g) { delete g; }
+
+fdl_status fdl_create_loopback(int32_t n, const int64_t* row_ptr, const int32_t* col_idx, const double* edge_len,
+                               const fdl_params* p, const double* init_pos, fdl_group* group, int32_t rank,
+                               fdl_ctx** out)
+{
+    if (!group) return FDL_E_INVALID_ARG;
+    return create_common(n, row_ptr, col_idx, edge_len, p, init_pos, nullptr, rank, group->world, out, group);
 }
 
 fdl_status fdl_shard_tiles(int32_t n, int32_t world, int32_t rank, int64_t* t0, int64_t* t1)

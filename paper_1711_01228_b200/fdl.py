@@ -31,6 +31,7 @@ EXPORTS = [
     "fdl_set_positions", "fdl_eval_forces", "fdl_get_hop_rows", "fdl_get_diag", "fdl_get_info",
     "fdl_set_timing", "fdl_get_stats", "fdl_reset_stats", "fdl_bench_ffma", "fdl_status_str",
     "fdl_last_error", "fdl_destroy", "fdl_eval_partial", "fdl_set_omega_vertex", "fdl_get_dist_rows",
+    "fdl_group_create", "fdl_group_destroy", "fdl_create_loopback",
 ]
 
 
@@ -116,6 +117,9 @@ def _load():
         "fdl_eval_forces": (i32, [P, P, P, P]),
         "fdl_set_omega_vertex": (i32, [P, P, sz]),
         "fdl_get_dist_rows": (i32, [P, i32, i32, P]),
+        "fdl_group_create": (i32, [i32, ctypes.POINTER(P)]),
+        "fdl_group_destroy": (None, [P]),
+        "fdl_create_loopback": (i32, [i32, P, P, P, ctypes.POINTER(Params), P, P, i32, ctypes.POINTER(P)]),
         "fdl_get_hop_rows": (i32, [P, i32, i32, P]),
         "fdl_get_diag": (i32, [P, P, sz]),
         "fdl_get_info": (i32, [P, ctypes.POINTER(CtxInfo)]),
@@ -187,11 +191,26 @@ def _check(ctx, status):
         raise FdlError(status, msg)
 
 
+class LoopbackGroup:
+    """In-process loopback transport of `world` ranks (include/fdl.h test hook)."""
+
+    def __init__(self, world: int):
+        self.world = int(world)
+        self._h = ctypes.c_void_p()
+        _check(None, lib.fdl_group_create(self.world, ctypes.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            lib.fdl_group_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+
 class Layout:
     """One layout context (fdl_ctx) on one GPU; names follow include/fdl.h."""
 
     def __init__(self, n: int, row_ptr, col_idx, params: Params | None = None, init_pos=None,
-                 nccl_id: bytes | None = None, rank: int = 0, world: int = 1, edge_len=None):
+                 nccl_id: bytes | None = None, rank: int = 0, world: int = 1, edge_len=None,
+                 group: "LoopbackGroup | None" = None):
         self._h = ctypes.c_void_p()
         self.n = int(n)
         self._rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
@@ -204,7 +223,10 @@ class Layout:
             raise ValueError("edge_len must have one entry per stored CSR direction")
         if X0 is not None and X0.size != self.n * self.dim:
             raise ValueError("init_pos must have n*dim entries")
-        if world == 1:
+        if group is not None:
+            st = lib.fdl_create_loopback(self.n, _ptr(self._rp), _ptr(self._col), _ptr(self._len),
+                                         ctypes.byref(self.params), _ptr(X0), group._h, rank, ctypes.byref(self._h))
+        elif world == 1:
             st = lib.fdl_create(self.n, _ptr(self._rp), _ptr(self._col), _ptr(self._len), ctypes.byref(self.params),
                                 _ptr(X0), ctypes.byref(self._h))
         else:

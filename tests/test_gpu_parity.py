@@ -540,3 +540,54 @@ def test_weighted_end_to_end(kind, alpha, omega):
     r = L.run_until_converged()
     o = layout.run_algorithm2(weighted.ProblemD(D, 2, k, alpha), X0, omega, tol, 500)
     _gates(r.iterations, r.f_final, o)
+
+
+# ------------------------------------------------ a7: the multi-rank step, on one GPU
+@pytest.mark.parametrize("name,world,omega", [("C2", 2, 1.6), ("C3", 3, 1.5), ("C3", 2, 0.0)])
+def test_loopback_ranks_bitwise(name, world, omega):
+    """The whole tile-sharded iteration (every rank evaluates its share of the
+    triangle; partial sums all-gathered and summed in rank order) through the
+    in-process loopback transport: every rank holds bitwise the single-GPU
+    trajectory (per-row sums never depend on the tile ownership)."""
+    import threading
+    cfg = configs.CONFIGS[name]
+    g = configs.graph_for(name)
+    X0 = configs.positions_for(name, g.n, 1)
+    p = fdl.make_params(dim=2, k=cfg.k_for(g.n), omega=omega, tol=cfg.tol, max_iter=cfg.max_iter)
+    steps = 12
+
+    def run(L, out):
+        fs = []
+        for _ in range(steps):
+            info = L.step()
+            fs.append((info.f_after, info.accepted, info.cg_iters))
+            if info.stop:
+                break
+        out.append((fs, L.get_positions()))
+
+    ref = []
+    with fdl.Layout.from_graph(g, params=p, init_pos=X0) as L1:
+        run(L1, ref)
+    grp = fdl.LoopbackGroup(world)
+    ctxs, outs, errs = [None] * world, [[] for _ in range(world)], []
+
+    def rank_main(r):
+        try:
+            ctxs[r] = fdl.Layout.from_graph(g, params=p, init_pos=X0, group=grp, rank=r, world=world)
+            run(ctxs[r], outs[r])
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for c in ctxs:
+        if c is not None:
+            c.close()
+    grp.close()
+    assert not errs, errs
+    for r in range(world):
+        assert outs[r][0][0] == ref[0][0], r
+        assert np.array_equal(outs[r][0][1], ref[0][1]), r
