@@ -591,3 +591,11 @@ def test_loopback_ranks_bitwise(name, world, omega):
     for r in range(world):
         assert outs[r][0][0] == ref[0][0], r
         assert np.array_equal(outs[r][0][1], ref[0][1]), r
+
+
+def test_nccl_loads_and_makes_unique_id():
+    """The NCCL transport of fdl_create_sharded: libnccl.so.2 resolves (the copy
+    torch loaded, else the system one) and yields a 128-byte unique id."""
+    import torch  # noqa: F401  (loads torch's NCCL into the process, as bench.py does)
+    uid = fdl.nccl_unique_id()
+    assert len(uid) == 128 and any(uid)
