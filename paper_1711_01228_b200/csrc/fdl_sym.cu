@@ -301,6 +301,28 @@ __device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float
         upk(ffma2(u, u, pk(s[0], s[1])), s0, s1);
         s[0] = s0;
         s[1] = s1;
+    } else if (MODE == kSymP1 && DIM == 2) {
+        // one set, 2-D: (x, y) as a packed pair for delta and the R updates (same
+        // per-element IEEE operations and order as the scalar code below)
+        const u64 d = fsub2(pk(xi[0], xi[1]), pk(xj[0], xj[1]));
+        float dx, dy;
+        upk(d, dx, dy);
+        const float r2 = fmaf(dy, dy, fmaf(dx, dx, FLT_MIN));
+        float q = rsqrt_approx(r2 * h2);
+        float u = fmaf(r2, q, -1.0f);
+        if (SAFE) {
+            q = valid ? q : 0.0f;
+            u = valid ? u : 0.0f;
+        }
+        const u64 qq = pk(q, q);
+        float lo, hi;
+        upk(ffma2(qq, d, pk(ai[0], ai[1])), lo, hi);
+        ai[0] = lo;
+        ai[1] = hi;
+        upk(ffma2(qq, d, pk(aj[0], aj[1])), lo, hi);
+        aj[0] = lo;
+        aj[1] = hi;
+        s[0] = fmaf(u, u, s[0]);
     } else if (MODE == kSymP1) {
         float d[DIM];
         float r2 = FLT_MIN;
