@@ -107,6 +107,11 @@ typedef struct {
                              1-set pass for R(X^{k+1}) when the guard rejects Xt (one host sync per
                              step); 0 = stresses and R of both in one pass; -1 (default) = 1 when
                              n^2 >= 2^30. Same results either way (bitwise)                       */
+    int32_t use_graphs;   /* 1: each step is one CUDA-graph launch (the PCG loop a device-side WHILE
+                             node), one host sync per step; 0: kernels launched eagerly with a host
+                             sync per PCG iteration; -1 (default): 1 on one GPU when the split
+                             line-6 pass is off (n^2 < 2^30). Same results either way (bitwise).
+                             With graphs the stats time whole steps only (p1_ms = p2_ms = 0)     */
 } fdl_params;
 
 typedef struct {

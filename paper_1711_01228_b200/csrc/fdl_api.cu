@@ -21,6 +21,8 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <map>
+#include <tuple>
 #include <mutex>
 #include <condition_variable>
 
@@ -138,6 +140,14 @@ struct fdl_group {
     }
 };
 
+struct StepGraphCounts {
+    uint64_t launches, p1_launches, p2_launches, p1_pairs, p2_pairs, p1_pairs_x2, p1_pairs_nor;
+};
+struct StepGraph {
+    cudaGraphExec_t exec = nullptr;
+    StepGraphCounts once{}, body{};
+};
+
 struct fdl_ctx {
     fdl_params p{};
     int n = 0, dim = 0, rank = 0, world = 1;
@@ -212,6 +222,12 @@ struct fdl_ctx {
     // NCCL
     ncclComm_t comm = nullptr;
     fdl_group* group = nullptr;  // loopback transport instead of NCCL (test hook)
+    // CUDA-graph steps (fdl_params.use_graphs): one captured graph per step shape
+    bool use_graphs = false;
+    bool capturing = false;
+    uint64_t steps_eager = 0;  // the first step runs eagerly (kernel attributes set, lazy allocations done)
+    cudaStream_t aux_stream = nullptr;
+    std::map<std::tuple<int, int, int, double>, StepGraph> graphs;
     bool emulated = false;  // world > 1 without communicator (fdl_eval_partial only)
 };
 
@@ -371,7 +387,7 @@ cudaEvent_t next_event(fdl_ctx* ctx)
 
 int mark_begin(fdl_ctx* ctx, int kind)
 {
-    if (!ctx->timing) return -1;
+    if (!ctx->timing || ctx->capturing) return -1;
     ctx->ev_marks.push_back({ctx->ev_used, kind, (size_t)-1});
     cudaEventRecord(next_event(ctx), ctx->stream);
     return (int)ctx->ev_marks.size() - 1;
@@ -936,6 +952,7 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     ctx->grid_enum = std::max(1, std::min(cap_items, ctx->sm_count * 2));
     ctx->grid_p1s = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymP1S, dim, 2, ctx->hb)));
     // large problems: the extra host sync of the split P1 is negligible against the pass
+    ctx->use_graphs = ctx->p.use_graphs == 1 || (ctx->p.use_graphs < 0 && world == 1 && (int64_t)n * n < (int64_t)1 << 30);
     ctx->p1_split = !ctx->general &&
                     (ctx->p.p1_split == 1 || (ctx->p.p1_split < 0 && (int64_t)n * n >= (int64_t)1 << 30));
     // Jacobi diagonal sum_{j != i} w'_ij (one symmetric DIAG pass) and sigma = mean(diag)/n
@@ -969,30 +986,23 @@ double pick_omega(fdl_ctx* ctx)
 }
 
 // One Algorithm-2 iteration.
-fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
+// ---- the three phases of one Algorithm-2 iteration (enqueue only; the eager
+// step syncs between them, the graph step captures them once).
+struct StepShape {
+    bool refresh;
+    bool enumerate;
+    int nsets;
+    double omega;
+};
+
+// line 4, start: L^W X^k (carried or a refresh pass), PCG start and first residual
+fdl_status enqueue_prologue(fdl_ctx* ctx, const StepShape& sh, unsigned long long cond)
 {
-    if (ctx->emulated) return set_err(ctx, FDL_E_UNSUPPORTED, "emulated rank: only fdl_eval_partial is available");
-    if (ctx->broken) return set_err(ctx, FDL_E_STATE, ctx->err.empty() ? "context is broken" : ctx->err);
-    if (ctx->stopped) return set_err(ctx, FDL_E_STATE, "the run has stopped; call fdl_set_positions to restart");
-    const bool enumerate = ctx->p.strategy == FDL_STRAT_ENUM;
-    double omega = ctx->omega_v ? ctx->omega_v_max : (enumerate ? 0.0 : pick_omega(ctx));
-    const int nsets = omega > 0.0 ? 2 : 1;
-    const int dim = ctx->dim, n = ctx->n;
-    const int pq = ps_p2(dim), ps = ps_p1(dim, nsets);
+    const int dim = ctx->dim, n = ctx->n, pq = ps_p2(dim);
+    const bool refresh = sh.refresh;
     cudaStream_t s = ctx->stream;
-    const int mstep = mark_begin(ctx, 0);
-    // ---- line 4: X^{k+1} = H(X^k): PCG on Eq. 5 (zero-mean gauge, R7), warm start X^k (S:222).
-    // The warm-start residual needs L^W X^k: carried from the previous solve, or a full
-    // P2 pass every a_refresh steps (bounds the fp32 drift of the carried value).
-    // per-vertex omega: Xt is not a scalar combination, At cannot be carried
-    const bool refresh = !ctx->a_valid || ctx->a_age + 1 >= ctx->p.a_refresh || ctx->omega_v;
     FDL_LAUNCH(launch_cg_begin(ctx->Xk, ctx->Xn, ctx->pvec, n, 0, dim, pq, ctx->sc, s));
-    if (refresh) {
-        FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->Ak, nullptr, 0));
-        ctx->a_age = 0;
-    } else {
-        ctx->a_age++;
-    }
+    if (refresh) FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->Ak, nullptr, 0));
     const double* y0 = ctx->Ak;
     if (ctx->p.cg_extrap) {  // extrapolated start (R23): x0 into Xn, L^W x0 into cy
         FDL_LAUNCH(launch_extrap(ctx->Xk, ctx->Xprev, ctx->Ak, ctx->Aprev, ctx->Xn, ctx->cy, ctx->sc, n, dim,
@@ -1001,25 +1011,37 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
     }
     FDL_LAUNCH(launch_cg_init(y0, ctx->Rk, ctx->diag, ctx->cr, ctx->cz, ctx->cp, ctx->pvec, ctx->blk_cg, ctx->nblk,
                               n, dim, pq, s));
-    FDL_LAUNCH(launch_cg_finalize(ctx->blk_cg, ctx->nblk, dim, 0, ctx->p.cg_rtol, ctx->sc, ctx->hs_dev, s));
+    FDL_LAUNCH(launch_cg_finalize(ctx->blk_cg, ctx->nblk, dim, 0, ctx->p.cg_rtol, ctx->sc, ctx->hs_dev, s, cond,
+                                  cond != 0, ctx->p.cg_max_iter));
     FDL_LAUNCH(launch_stage_p(ctx->cp, ctx->pvec, ctx->sc, n, dim, pq, s));
-    FDL_CUDA(cudaStreamSynchronize(s));
-    int cg = 0;
-    while (!ctx->hs->done) {
-        if (cg >= ctx->p.cg_max_iter) {
-            collect_events(ctx);
-            return set_err(ctx, FDL_E_SOLVER, "PCG reached cg_max_iter before cg_rtol (S:223)");
-        }
-        FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->cy, nullptr, 0));
-        FDL_LAUNCH(launch_cg_ap(ctx->cp, ctx->cy, ctx->blk_cg, ctx->nblk, n, dim, ctx->sc, s));
-        FDL_LAUNCH(launch_cg_finalize(ctx->blk_cg, ctx->nblk, dim, 1, ctx->p.cg_rtol, ctx->sc, ctx->hs_dev, s));
-        FDL_LAUNCH(launch_cg_update(ctx->Xn, ctx->cr, ctx->cz, ctx->cp, ctx->cy, ctx->diag, ctx->blk_cg, ctx->nblk,
-                                    ctx->sc, n, 0, dim, s));
-        FDL_LAUNCH(launch_cg_finalize(ctx->blk_cg, ctx->nblk, dim, 2, ctx->p.cg_rtol, ctx->sc, ctx->hs_dev, s));
-        FDL_LAUNCH(launch_cg_p(ctx->cp, ctx->cz, ctx->pvec, ctx->sc, n, 0, dim, pq, s));
-        FDL_CUDA(cudaStreamSynchronize(s));
-        ++cg;
-    }
+    return FDL_OK;
+}
+
+// one PCG iteration: a P2 pass (L^W p) and the fp64 vector updates
+fdl_status enqueue_cg_body(fdl_ctx* ctx, unsigned long long cond)
+{
+    const int dim = ctx->dim, n = ctx->n, pq = ps_p2(dim);
+    cudaStream_t s = ctx->stream;
+    FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->cy, nullptr, 0));
+    FDL_LAUNCH(launch_cg_ap(ctx->cp, ctx->cy, ctx->blk_cg, ctx->nblk, n, dim, ctx->sc, s));
+    FDL_LAUNCH(launch_cg_finalize(ctx->blk_cg, ctx->nblk, dim, 1, ctx->p.cg_rtol, ctx->sc, ctx->hs_dev, s));
+    FDL_LAUNCH(launch_cg_update(ctx->Xn, ctx->cr, ctx->cz, ctx->cp, ctx->cy, ctx->diag, ctx->blk_cg, ctx->nblk,
+                                ctx->sc, n, 0, dim, s));
+    FDL_LAUNCH(launch_cg_finalize(ctx->blk_cg, ctx->nblk, dim, 2, ctx->p.cg_rtol, ctx->sc, ctx->hs_dev, s, cond,
+                                  cond != 0, ctx->p.cg_max_iter));
+    FDL_LAUNCH(launch_cg_p(ctx->cp, ctx->cz, ctx->pvec, ctx->sc, n, 0, dim, pq, s));
+    return FDL_OK;
+}
+
+// lines 5-8: pin, combine (Eq. 10), the line-6 pass and the guard
+fdl_status enqueue_epilogue(fdl_ctx* ctx, const StepShape& sh)
+{
+    const int dim = ctx->dim, n = ctx->n, pq = ps_p2(dim);
+    const bool enumerate = sh.enumerate;
+    const int nsets = sh.nsets;
+    const double omega = sh.omega;
+    const int ps = ps_p1(dim, nsets);
+    cudaStream_t s = ctx->stream;
     // carried L^W X^{k+1} and L^W Xt (before Rk is replaced by the select)
     FDL_LAUNCH(launch_carry_a(ctx->Rk, ctx->cr, ctx->Ak, ctx->An, ctx->At, ctx->sc, n, dim, enumerate ? 0.0 : omega,
                               s));
@@ -1080,11 +1102,183 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
         FDL_LAUNCH(launch_select(ctx->Xk, ctx->Rk, ctx->Xn, ctx->Xt, ctx->R1, ctx->R2, ctx->blk_max, n, dim, nsets,
                                  ctx->sc, ctx->Ak, ctx->An, ctx->At, s));
     }
+    return FDL_OK;
+}
+
+// Stats increments of the captured phases: once per launch, and per PCG iteration.
+using StatDelta = StepGraphCounts;
+StatDelta stat_snapshot(const fdl_ctx* ctx)
+{
+    const fdl_stats& t = ctx->stats;
+    return {t.launches, t.p1_launches, t.p2_launches, t.p1_pairs, t.p2_pairs, t.p1_pairs_x2, t.p1_pairs_nor};
+}
+StatDelta stat_diff(const StatDelta& a, const StatDelta& b)
+{
+    return {b.launches - a.launches, b.p1_launches - a.p1_launches, b.p2_launches - a.p2_launches,
+            b.p1_pairs - a.p1_pairs, b.p2_pairs - a.p2_pairs, b.p1_pairs_x2 - a.p1_pairs_x2,
+            b.p1_pairs_nor - a.p1_pairs_nor};
+}
+void stat_add(fdl_ctx* ctx, const StatDelta& d, uint64_t times)
+{
+    fdl_stats& t = ctx->stats;
+    t.launches += d.launches * times;
+    t.p1_launches += d.p1_launches * times;
+    t.p2_launches += d.p2_launches * times;
+    t.p1_pairs += d.p1_pairs * times;
+    t.p2_pairs += d.p2_pairs * times;
+    t.p1_pairs_x2 += d.p1_pairs_x2 * times;
+    t.p1_pairs_nor += d.p1_pairs_nor * times;
+}
+
+// Capture one iteration as a CUDA graph: prologue -> WHILE(PCG not converged and
+// cg_iters < cg_max) { PCG iteration } -> epilogue -> D2H of the device scalars.
+// The WHILE condition is set on the device by k_cg_finalize, so a whole step is
+// one graph launch and one host sync (instead of one sync per PCG iteration).
+fdl_status build_step_graph(fdl_ctx* ctx, const StepShape& sh, StepGraph& out)
+{
+    cudaStream_t s = ctx->stream;
+    if (!ctx->aux_stream) FDL_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
+    ctx->capturing = true;
+    const StatDelta s0 = stat_snapshot(ctx);
+    cudaGraph_t g = nullptr;
+    auto fail = [&](fdl_status st) {
+        ctx->capturing = false;
+        ctx->stream = s;
+        cudaGraph_t tmp = nullptr;
+        cudaStreamEndCapture(s, &tmp);
+        if (tmp) cudaGraphDestroy(tmp);
+        cudaGetLastError();
+        return st;
+    };
+    FDL_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    cudaStreamCaptureStatus cst;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    if (cudaStreamGetCaptureInfo(s, &cst, nullptr, &g, &deps, &ndeps) != cudaSuccess) return fail(FDL_E_CUDA);
+    cudaGraphConditionalHandle h;
+    if (cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault) != cudaSuccess) return fail(FDL_E_CUDA);
+    fdl_status st = enqueue_prologue(ctx, sh, (unsigned long long)h);
+    if (st != FDL_OK) return fail(st);
+    const StatDelta s1 = stat_snapshot(ctx);
+    if (cudaStreamGetCaptureInfo(s, &cst, nullptr, &g, &deps, &ndeps) != cudaSuccess) return fail(FDL_E_CUDA);
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    if (cudaGraphAddNode(&cnode, g, deps, ndeps, &cp) != cudaSuccess) return fail(FDL_E_CUDA);
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    // body: captured on the auxiliary stream into the WHILE node's graph
+    if (cudaStreamBeginCaptureToGraph(ctx->aux_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
+        cudaSuccess)
+        return fail(FDL_E_CUDA);
+    ctx->stream = ctx->aux_stream;
+    st = enqueue_cg_body(ctx, (unsigned long long)h);
+    ctx->stream = s;
+    cudaGraph_t body_out = nullptr;
+    const cudaError_t eb = cudaStreamEndCapture(ctx->aux_stream, &body_out);
+    if (st != FDL_OK) return fail(st);
+    if (eb != cudaSuccess) return fail(FDL_E_CUDA);
+    const StatDelta s2 = stat_snapshot(ctx);
+    if (cudaStreamUpdateCaptureDependencies(s, &cnode, 1, cudaStreamSetCaptureDependencies) != cudaSuccess)
+        return fail(FDL_E_CUDA);
+    st = enqueue_epilogue(ctx, sh);
+    if (st != FDL_OK) return fail(st);
+    if (cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return fail(FDL_E_CUDA);
+    const StatDelta s3 = stat_snapshot(ctx);
+    ctx->capturing = false;
+    cudaGraph_t gout = nullptr;
+    FDL_CUDA(cudaStreamEndCapture(s, &gout));
+    const cudaError_t ei = cudaGraphInstantiate(&out.exec, gout, 0);
+    cudaGraphDestroy(gout);
+    FDL_CUDA(ei);
+    // counters: the captured launches ran once at capture time; undo, keep the deltas
+    out.once = stat_diff(s0, s1);
+    const StatDelta e = stat_diff(s2, s3);
+    out.once.launches += e.launches;
+    out.once.p1_launches += e.p1_launches;
+    out.once.p2_launches += e.p2_launches;
+    out.once.p1_pairs += e.p1_pairs;
+    out.once.p2_pairs += e.p2_pairs;
+    out.once.p1_pairs_x2 += e.p1_pairs_x2;
+    out.once.p1_pairs_nor += e.p1_pairs_nor;
+    out.body = stat_diff(s1, s2);
+    fdl_stats& t = ctx->stats;
+    t.launches = s0.launches;
+    t.p1_launches = s0.p1_launches;
+    t.p2_launches = s0.p2_launches;
+    t.p1_pairs = s0.p1_pairs;
+    t.p2_pairs = s0.p2_pairs;
+    t.p1_pairs_x2 = s0.p1_pairs_x2;
+    t.p1_pairs_nor = s0.p1_pairs_nor;
+    return FDL_OK;
+}
+
+fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
+{
+    if (ctx->emulated) return set_err(ctx, FDL_E_UNSUPPORTED, "emulated rank: only fdl_eval_partial is available");
+    if (ctx->broken) return set_err(ctx, FDL_E_STATE, ctx->err.empty() ? "context is broken" : ctx->err);
+    if (ctx->stopped) return set_err(ctx, FDL_E_STATE, "the run has stopped; call fdl_set_positions to restart");
+    const bool enumerate = ctx->p.strategy == FDL_STRAT_ENUM;
+    double omega = ctx->omega_v ? ctx->omega_v_max : (enumerate ? 0.0 : pick_omega(ctx));
+    const int nsets = omega > 0.0 ? 2 : 1;
+    cudaStream_t s = ctx->stream;
+    // ---- line 4: X^{k+1} = H(X^k): PCG on Eq. 5 (zero-mean gauge, R7), warm start X^k (S:222).
+    // The warm-start residual needs L^W X^k: carried from the previous solve, or a full
+    // P2 pass every a_refresh steps (bounds the fp32 drift of the carried value).
+    // per-vertex omega: Xt is not a scalar combination, At cannot be carried
+    const bool refresh = !ctx->a_valid || ctx->a_age + 1 >= ctx->p.a_refresh || ctx->omega_v;
+    const StepShape sh{refresh, enumerate, nsets, omega};
+    int cg = 0;
+    // graph mode: one launch per step; not with a host decision inside the step
+    // (split line 6, enumeration) or host-side exchanges (several ranks)
+    const bool graph = ctx->use_graphs && !enumerate && !(nsets == 2 && ctx->p1_split) && ctx->world == 1 &&
+                       ctx->steps_eager > 0;
+    const int mstep = mark_begin(ctx, 0);
+    if (graph) {
+        const auto key = std::make_tuple((int)refresh, nsets, (int)ctx->ext_ok, omega);
+        auto it = ctx->graphs.find(key);
+        if (it == ctx->graphs.end()) {
+            StepGraph sg;
+            FDL_TRY(build_step_graph(ctx, sh, sg));
+            it = ctx->graphs.emplace(key, sg).first;
+        }
+        FDL_CUDA(cudaGraphLaunch(it->second.exec, s));
+        mark_end(ctx, mstep);
+        FDL_CUDA(cudaStreamSynchronize(s));
+        cg = ctx->sc_host->cg_iters;
+        stat_add(ctx, it->second.once, 1);
+        stat_add(ctx, it->second.body, (uint64_t)cg);
+        if (!ctx->sc_host->done) {
+            collect_events(ctx);
+            return set_err(ctx, FDL_E_SOLVER, "PCG reached cg_max_iter before cg_rtol (S:223)");
+        }
+    } else {
+        FDL_TRY(enqueue_prologue(ctx, sh, 0));
+        FDL_CUDA(cudaStreamSynchronize(s));
+        while (!ctx->hs->done) {
+            if (cg >= ctx->p.cg_max_iter) {
+                collect_events(ctx);
+                return set_err(ctx, FDL_E_SOLVER, "PCG reached cg_max_iter before cg_rtol (S:223)");
+            }
+            FDL_TRY(enqueue_cg_body(ctx, 0));
+            FDL_CUDA(cudaStreamSynchronize(s));
+            ++cg;
+        }
+        FDL_TRY(enqueue_epilogue(ctx, sh));
+        mark_end(ctx, mstep);
+        FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, s));
+        FDL_CUDA(cudaStreamSynchronize(s));
+        ctx->steps_eager++;
+    }
+    if (refresh)
+        ctx->a_age = 0;
+    else
+        ctx->a_age++;
     ctx->a_valid = true;
     ctx->ext_ok = ctx->p.cg_extrap != 0;
-    mark_end(ctx, mstep);
-    FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, s));
-    FDL_CUDA(cudaStreamSynchronize(s));
     collect_events(ctx);
     ctx->stats.steps++;
     ctx->stats.cg_iters += cg;
@@ -1167,6 +1361,7 @@ void fdl_params_default(fdl_params* p)
     p->enum_count = 19;
     p->enum_step = 0.5;
     p->p1_split = -1;
+    p->use_graphs = -1;
 }
 
 const char* fdl_status_str(fdl_status s)
@@ -1195,6 +1390,13 @@ const char* fdl_last_error(const fdl_ctx* ctx) { return ctx ? ctx->err.c_str() :
 
 void fdl_destroy(fdl_ctx* ctx)
 {
+    if (ctx) {
+        for (auto& kv : ctx->graphs)
+            if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+        ctx->graphs.clear();
+        if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
+        ctx->aux_stream = nullptr;
+    }
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
@@ -1306,6 +1508,8 @@ fdl_status fdl_set_omega_vertex(fdl_ctx* ctx, const double* omega, size_t count)
 {
     if (!ctx) return FDL_E_INVALID_ARG;
     if (ctx->broken) return set_err(ctx, FDL_E_STATE, ctx->err);
+    for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second.exec);
+    ctx->graphs.clear();
     if (!omega) {
         if (ctx->omega_v) {
             cudaFree(ctx->omega_v);
@@ -1328,6 +1532,8 @@ fdl_status fdl_set_omega_vertex(fdl_ctx* ctx, const double* omega, size_t count)
     FDL_CUDA(cudaMemcpyAsync(ctx->omega_v, omega, sizeof(double) * count, cudaMemcpyHostToDevice, ctx->stream));
     FDL_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx->omega_v_max = mx;
+    for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second.exec);  // they baked the old omega_v
+    ctx->graphs.clear();
     return FDL_OK;
 }
 

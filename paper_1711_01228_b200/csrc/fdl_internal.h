@@ -98,8 +98,11 @@ cudaError_t launch_cg_update(double* x, double* r, double* z, const double* p, c
 cudaError_t launch_cg_p(double* p, const double* z, float* pvec, const DevScalars* sc, int nloc, int row0,
                         int dim, int pq, cudaStream_t s);
 // mode 0: after init (rz, rr, bb, sum z); 1: alpha from pAp; 2: beta + convergence
+// cond/use_cond: the WHILE-node handle of a captured step graph (continue = PCG not done
+// and cg_iters < cg_max); use_cond = 0 outside graphs
 cudaError_t launch_cg_finalize(const double* blk, int nblk, int dim, int mode, double rtol,
-                               DevScalars* sc, HostScalars* hs, cudaStream_t s);
+                               DevScalars* sc, HostScalars* hs, cudaStream_t s, unsigned long long cond = 0,
+                               int use_cond = 0, int cg_max = 0);
 cudaError_t launch_ffma_bench(float* out, int iters, int blocks, int threads, cudaStream_t s);
 
 // ------------------------------------------------------- symmetric (triangle) passes

@@ -618,7 +618,8 @@ cudaError_t launch_cg_p(double* p, const double* z, float* pvec, const DevScalar
 // one warp, fixed butterfly).  Slots: 0 r.z | p.y (mode 1), 1 r.r, 2 b.b,
 // 3 sum z.  mode 0: init; 1: alpha; 2: beta + stop test.
 __global__ void k_cg_finalize(const double* __restrict__ blk, int nblk, int dim, int mode, double rtol,
-                              DevScalars* sc, HostScalars* hs)
+                              DevScalars* sc, HostScalars* hs, cudaGraphConditionalHandle cond, int use_cond,
+                              int cg_max)
 {
     const int lane = threadIdx.x;
     double sums[4][3];
@@ -654,6 +655,7 @@ __global__ void k_cg_finalize(const double* __restrict__ blk, int nblk, int dim,
         sc->cg_iters = 0;
         sc->relres = rel;
         hs->done = !any;
+        if (use_cond) cudaGraphSetConditional(cond, (any && cg_max > 0) ? 1u : 0u);  // WHILE node of the step graph
     } else if (mode == 1) {
         for (int c = 0; c < dim; ++c) {
             sc->pap[c] = sums[0][c];
@@ -680,13 +682,15 @@ __global__ void k_cg_finalize(const double* __restrict__ blk, int nblk, int dim,
         sc->done = !any;
         sc->relres = rel;
         hs->done = !any;
+        if (use_cond) cudaGraphSetConditional(cond, (any && sc->cg_iters < cg_max) ? 1u : 0u);
     }
 }
 
 cudaError_t launch_cg_finalize(const double* blk, int nblk, int dim, int mode, double rtol, DevScalars* sc,
-                               HostScalars* hs, cudaStream_t s)
+                               HostScalars* hs, cudaStream_t s, unsigned long long cond, int use_cond, int cg_max)
 {
-    k_cg_finalize<<<1, 32, 0, s>>>(blk, nblk, dim, mode, rtol, sc, hs);
+    k_cg_finalize<<<1, 32, 0, s>>>(blk, nblk, dim, mode, rtol, sc, hs, (cudaGraphConditionalHandle)cond, use_cond,
+                                   cg_max);
     return cudaGetLastError();
 }
 

@@ -599,3 +599,24 @@ def test_nccl_loads_and_makes_unique_id():
     import torch  # noqa: F401  (loads torch's NCCL into the process, as bench.py does)
     uid = fdl.nccl_unique_id()
     assert len(uid) == 128 and any(uid)
+
+
+@pytest.mark.parametrize("name,omega,strategy", [("C1", 1.5, 0), ("C2", 1.9, 0), ("C3", 1.5, 0), ("C1", 0.0, 0),
+                                                 ("C2", 1.5, 1)])
+def test_graph_steps_bitwise(name, omega, strategy):
+    """A step as one CUDA-graph launch (PCG loop = device-side WHILE node) gives
+    bitwise the eager step's trajectory (same kernels, same arguments)."""
+    cfg = configs.CONFIGS[name]
+    g = configs.graph_for(name)
+    X0 = configs.positions_for(name, g.n, 2)
+    out = []
+    for graphs_on in (0, 1):
+        p = fdl.make_params(dim=2, k=cfg.k_for(g.n), omega=omega, tol=cfg.tol, max_iter=cfg.max_iter,
+                            use_graphs=graphs_on, strategy=strategy, seed=3)
+        with fdl.Layout.from_graph(g, params=p, init_pos=X0) as L:
+            r = L.run_until_converged()
+            st = L.get_stats()
+            out.append((r.iterations, r.f_final, r.cg_iters, L.get_positions(), st.p2_launches, st.p1_launches))
+    a, b = out
+    assert a[:3] == b[:3] and np.array_equal(a[3], b[3])
+    assert a[4:] == b[4:]  # launch accounting of the captured phases
