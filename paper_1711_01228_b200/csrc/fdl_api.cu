@@ -175,6 +175,7 @@ struct fdl_ctx {
     float* jpart = nullptr;
     float* ipart = nullptr;
     double* spart = nullptr;
+    double* stress_scratch = nullptr;  // chunk sums of the two-stage stress reduction
     double *rparts = nullptr, *sparts = nullptr;  // world x partials
     double *diag = nullptr, *Xk = nullptr, *Xn = nullptr, *Xt = nullptr, *Rk = nullptr, *R1 = nullptr,
            *R2 = nullptr;
@@ -261,6 +262,13 @@ fdl_status cuda_fail(fdl_ctx* c, cudaError_t e, const char* what)
         cudaError_t e_ = (call);                                 \
         ctx->stats.launches++;                                   \
         if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
+    } while (0)
+
+// launchers that enqueue two kernels (count both in the launch statistics)
+#define FDL_LAUNCH2(call)      \
+    do {                       \
+        FDL_LAUNCH(call);      \
+        ctx->stats.launches++; \
     } while (0)
 
 #define FDL_TRY(x)                     \
@@ -497,7 +505,7 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
         if (mode == kSymP2)  // product form: L^W p = diag p - sum_j w p_j (rank-local diag when emulated)
             FDL_LAUNCH(launch_p2_finish(out0, pos, ctx->diag, ctx->n, dim, ps_p2(dim), ctx->stream));
         if (p1) {
-            FDL_LAUNCH(launch_sym_stress(ctx->spart, ctx->nitems * 8, nsets, ctx->sparts, ctx->stream));
+            FDL_LAUNCH2(launch_sym_stress(ctx->spart, ctx->nitems * 8, nsets, ctx->sparts, ctx->stress_scratch, ctx->stream));
             FDL_LAUNCH(launch_stress_ranks(ctx->sparts, 1, nsets, ctx->sc, set_cur, ctx->stream));
         }
         return FDL_OK;
@@ -510,7 +518,8 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
     FDL_LAUNCH(launch_rank_sum(ctx->rparts, ctx->world, ctx->npad, C, D0, inter, out0, out1, ctx->stream));
     if (mode == kSymP2) FDL_LAUNCH(launch_p2_finish(out0, pos, ctx->diag, ctx->n, dim, ps_p2(dim), ctx->stream));
     if (p1) {
-        FDL_LAUNCH(launch_sym_stress(ctx->spart, ctx->nitems * 8, nsets, ctx->sparts + 2 * ctx->rank, ctx->stream));
+        FDL_LAUNCH2(launch_sym_stress(ctx->spart, ctx->nitems * 8, nsets, ctx->sparts + 2 * ctx->rank, ctx->stress_scratch,
+                                     ctx->stream));
         FDL_TRY(allgather_inplace(ctx, ctx->sparts, 2, ncclFloat64, 8));
         FDL_LAUNCH(launch_stress_ranks(ctx->sparts, ctx->world, nsets, ctx->sc, set_cur, ctx->stream));
     }
@@ -900,6 +909,7 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     FDL_ALLOC(ctx->ipart, (size_t)std::max(ctx->nitems, 1) * 8 * kT * Cmax);
     FDL_ALLOC(ctx->spart, (size_t)std::max(ctx->nitems, 1) * 8 * 2);
     FDL_ALLOC(ctx->sparts, (size_t)2 * world);
+    FDL_ALLOC(ctx->stress_scratch, (size_t)sym_stress_chunks(std::max(ctx->nitems, 1) * 8) * kEnumNC);
     if (p.strategy == FDL_STRAT_ENUM) {
         if (world > 1) return set_err(ctx, FDL_E_UNSUPPORTED, "the enumerating strategy runs on one GPU");
         FDL_ALLOC(ctx->spart_enum, (size_t)std::max(ctx->nitems, 1) * kEnumNC);
@@ -1001,7 +1011,7 @@ fdl_status enqueue_prologue(fdl_ctx* ctx, const StepShape& sh, unsigned long lon
     const int dim = ctx->dim, n = ctx->n, pq = ps_p2(dim);
     const bool refresh = sh.refresh;
     cudaStream_t s = ctx->stream;
-    FDL_LAUNCH(launch_cg_begin(ctx->Xk, ctx->Xn, ctx->pvec, n, 0, dim, pq, ctx->sc, s));
+    FDL_LAUNCH2(launch_cg_begin(ctx->Xk, ctx->Xn, ctx->pvec, n, 0, dim, pq, ctx->sc, s));
     if (refresh) FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->Ak, nullptr, 0));
     const double* y0 = ctx->Ak;
     if (ctx->p.cg_extrap) {  // extrapolated start (R23): x0 into Xn, L^W x0 into cy
@@ -1052,7 +1062,7 @@ fdl_status enqueue_epilogue(fdl_ctx* ctx, const StepShape& sh)
         // the hop tiles, omega* = first argmin, then stress + R of X~(omega*)
         FDL_LAUNCH(launch_enum_stage(ctx->Xk, ctx->Xn, ctx->posf, ctx->blk_max, ctx->pin_slots, n, dim, 2 * pq, s));
         if (ctx->p.cg_extrap)
-            FDL_LAUNCH(launch_rho(ctx->Xn, ctx->Xk, ctx->Xprev, ctx->Ak, ctx->Aprev, ctx->blk_cg, n, dim,
+            FDL_LAUNCH2(launch_rho(ctx->Xn, ctx->Xk, ctx->Xprev, ctx->Ak, ctx->Aprev, ctx->blk_cg, n, dim,
                                   ctx->ext_ok ? 1 : 0, ctx->sc, s));
         const int m = ctx->p.enum_count;
         for (int c0 = 0; c0 < m; c0 += kEnumNC) {
@@ -1069,7 +1079,7 @@ fdl_status enqueue_epilogue(fdl_ctx* ctx, const StepShape& sh)
             a.n = ctx->n;
             a.magic = 0x4B000000u;
             if (ctx->nitems > 0) FDL_LAUNCH(launch_enum(a, w, dim, ctx->hb, ctx->grid_enum, s));
-            FDL_LAUNCH(launch_sym_stress(ctx->spart_enum, ctx->nitems, kEnumNC, ctx->enum_f + c0, s));
+            FDL_LAUNCH2(launch_sym_stress(ctx->spart_enum, ctx->nitems, kEnumNC, ctx->enum_f + c0, ctx->stress_scratch, s));
         }
         FDL_LAUNCH(launch_enum_pick(ctx->enum_f, m, ctx->p.enum_step, ctx->sc, s));
         FDL_LAUNCH(launch_enum_apply(ctx->Xn, ctx->Xk, ctx->An, ctx->Ak, ctx->Xt, ctx->At, ctx->posf, ctx->sc, n, dim,
@@ -1082,7 +1092,7 @@ fdl_status enqueue_epilogue(fdl_ctx* ctx, const StepShape& sh)
         FDL_LAUNCH(launch_combine(ctx->Xk, ctx->Xn, ctx->Xt, ctx->posf, ctx->blk_max, ctx->pin_slots, n, 0, dim, omega,
                                   ctx->omega_v, ctx->cap, nsets, ps, s));
         if (ctx->p.cg_extrap)  // ratio of successive corrections for the next start; X^{k-1} <- X^k
-            FDL_LAUNCH(launch_rho(ctx->Xn, ctx->Xk, ctx->Xprev, ctx->Ak, ctx->Aprev, ctx->blk_cg, n, dim,
+            FDL_LAUNCH2(launch_rho(ctx->Xn, ctx->Xk, ctx->Xprev, ctx->Ak, ctx->Aprev, ctx->blk_cg, n, dim,
                                   ctx->ext_ok ? 1 : 0, ctx->sc, s));
         // ---- line 6: f(Xt), f(X^{k+1}) and the next right-hand side, one fused pass
         if (nsets == 2 && ctx->p1_split) {
@@ -1609,7 +1619,7 @@ fdl_status fdl_eval_forces(fdl_ctx* ctx, double* R, double* A, double* stress)
     if (R) FDL_TRY(fetch(ctx->Rk, R));
     if (A) {
         // A = L^W X: one symmetric P2 pass with p = X
-        FDL_LAUNCH(launch_cg_begin(ctx->Xk, ctx->cy, ctx->pvec, ctx->n, 0, dim, ps_p2(dim), ctx->sc, ctx->stream));
+        FDL_LAUNCH2(launch_cg_begin(ctx->Xk, ctx->cy, ctx->pvec, ctx->n, 0, dim, ps_p2(dim), ctx->sc, ctx->stream));
         FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->cy, nullptr, 0));
         FDL_TRY(fetch(ctx->cy, A));
         collect_events(ctx);
@@ -1633,7 +1643,7 @@ fdl_status fdl_eval_partial(fdl_ctx* ctx, int32_t mode, const double* X, double*
         FDL_LAUNCH(launch_stage_pos1(ctx->Xt, ctx->posf, ctx->n, 0, dim, ps_p1(dim, 1), ctx->stream));
         FDL_TRY(run_sym(ctx, kSymP1, 1, ctx->posf, ctx->R1, nullptr, 0));
     } else {
-        FDL_LAUNCH(launch_cg_begin(ctx->Xt, ctx->R1, ctx->pvec, ctx->n, 0, dim, ps_p2(dim), ctx->sc, ctx->stream));
+        FDL_LAUNCH2(launch_cg_begin(ctx->Xt, ctx->R1, ctx->pvec, ctx->n, 0, dim, ps_p2(dim), ctx->sc, ctx->stream));
         FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->R1, nullptr, 0));
     }
     FDL_CUDA(cudaMemcpyAsync(out, ctx->R1, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));

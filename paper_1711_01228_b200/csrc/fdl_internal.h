@@ -172,7 +172,10 @@ int sym_max_ctas(int mode, int dim, int nsets, int hb);
 cudaError_t launch_sym_reduce(const float* ipart, const float* jpart, const int* it_lo, const int* it_hi, int nb,
                               int64_t t0, int64_t t1, int C, int D, int inter, double* out0, double* out1,
                               cudaStream_t s);
-cudaError_t launch_sym_stress(const double* spart, int nitems, int nsets, double* out, cudaStream_t s);
+// scratch: sym_stress_chunks(nitems) * nsets doubles
+int sym_stress_chunks(int nitems);
+cudaError_t launch_sym_stress(const double* spart, int nitems, int nsets, double* out, double* scratch,
+                              cudaStream_t s);
 cudaError_t launch_bfs_level_sym(const int64_t* row_ptr, const int32_t* col, const uint32_t* fin, uint32_t* fout,
                                  uint32_t* visited, uint8_t* D, int n, int s0, int nsrc, int level, int nb, int64_t t0,
                                  int64_t t1, int hb, unsigned int* anynew, cudaStream_t s);

@@ -1226,30 +1226,61 @@ cudaError_t launch_hop_rows(const uint8_t* D, int hb, int nb, int64_t t0, int64_
     return cudaGetLastError();
 }
 
-// stress partial of the rank: fixed-order block reduction of the segment partials
-__global__ void __launch_bounds__(1024) k_sym_stress(const double* __restrict__ spart, int nitems, int nsets,
-                                                     double* out)
+// stress partial of the rank: fixed-order two-stage reduction of the
+// [item(x warp)][nsets] partials -- stage 1: block b sums the fixed chunk
+// [b*kStressChunk, (b+1)*kStressChunk) (thread stride, warp butterfly, warps in
+// order); stage 2: one block sums the chunk sums in the same pattern.
+constexpr int kStressChunk = 8192;
+
+__device__ __forceinline__ double block_sum_1024(double v, double* red)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    __syncthreads();
+    return t;
+}
+
+__global__ void __launch_bounds__(1024) k_sym_stress1(const double* __restrict__ spart, int nitems, int nsets,
+                                                      double* chunk_sums)
+{
+    __shared__ double red[32];
+    const int b = blockIdx.x;
+    const int lo = b * kStressChunk, hi = min(nitems, lo + kStressChunk);
+    for (int s = 0; s < nsets; ++s) {
+        double v = 0.0;
+        for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) v += spart[(size_t)i * nsets + s];
+        const double t = block_sum_1024(v, red);
+        if (threadIdx.x == 0) chunk_sums[(size_t)b * nsets + s] = t;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_sym_stress2(const double* __restrict__ chunk_sums, int nchunks, int nsets,
+                                                      double* out)
 {
     __shared__ double red[32];
     for (int s = 0; s < nsets; ++s) {
         double v = 0.0;
-        for (int i = threadIdx.x; i < nitems; i += blockDim.x) v += spart[(size_t)i * nsets + s];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0.0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-            out[s] = t;
-        }
-        __syncthreads();
+        for (int i = threadIdx.x; i < nchunks; i += blockDim.x) v += chunk_sums[(size_t)i * nsets + s];
+        const double t = block_sum_1024(v, red);
+        if (threadIdx.x == 0) out[s] = t;
     }
 }
 
-cudaError_t launch_sym_stress(const double* spart, int nitems, int nsets, double* out, cudaStream_t s)
+int sym_stress_chunks(int nitems) { return std::max(1, (nitems + kStressChunk - 1) / kStressChunk); }
+
+cudaError_t launch_sym_stress(const double* spart, int nitems, int nsets, double* out, double* scratch,
+                              cudaStream_t s)
 {
-    k_sym_stress<<<1, 1024, 0, s>>>(spart, nitems, nsets, out);
+    const int nc = sym_stress_chunks(nitems);
+    k_sym_stress1<<<nc, 1024, 0, s>>>(spart, nitems, nsets, scratch);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_sym_stress2<<<1, 1024, 0, s>>>(scratch, nc, nsets, out);
     return cudaGetLastError();
 }
 
