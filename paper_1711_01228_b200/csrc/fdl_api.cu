@@ -87,12 +87,8 @@ inline uint64_t splitmix64(uint64_t& s)
 }
 inline double u01(uint64_t& s) { return (double)(splitmix64(s) >> 11) * (1.0 / 9007199254740992.0); }
 
-// work-item length in tiles (FDL_KSEG overrides kSeg: tuning experiments only)
-int seg_len()
-{
-    static const int v = getenv("FDL_KSEG") ? std::max(1, atoi(getenv("FDL_KSEG"))) : kSeg;
-    return v;
-}
+// work-item length in tiles (strip segments)
+int seg_len() { return kSeg; }
 
 // (I, J) of triangle index t (row-major upper triangle over nb blocks)
 void tri_coords(int64_t t, int64_t nb, int64_t& I, int64_t& J)
