@@ -673,15 +673,17 @@ fdl_status build_dists(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, cons
 {
     const int n = ctx->n;
     const int64_t m = std::max<int64_t>(rp[n], 1);
-    constexpr int S = 256;  // sources per batch
+    // sources per batch: up to 1024, within ~1 GB of fp64 distance buffers
+    const int S = (int)std::max<int64_t>(32, std::min<int64_t>(1024, ((int64_t)1 << 30) / (8 * (int64_t)n) / 32 * 32));
     int64_t* d_rp = nullptr;
     int32_t* d_col = nullptr;
-    double *d_len = nullptr, *da = nullptr, *db = nullptr, *dmax = nullptr;
+    double *d_len = nullptr, *da = nullptr, *dmax = nullptr;
     FDL_CUDA(cudaMalloc(&d_rp, sizeof(int64_t) * (n + 1)));
     FDL_CUDA(cudaMalloc(&d_col, sizeof(int32_t) * m));
     FDL_CUDA(cudaMalloc(&d_len, sizeof(double) * m));
     FDL_CUDA(cudaMalloc(&da, sizeof(double) * (size_t)n * S));
-    FDL_CUDA(cudaMalloc(&db, sizeof(double) * (size_t)n * S));
+    int* stamp = nullptr;
+    FDL_CUDA(cudaMalloc(&stamp, sizeof(int) * n));
     FDL_CUDA(cudaMalloc(&dmax, sizeof(double)));
     FDL_CUDA(cudaMemsetAsync(dmax, 0, sizeof(double), ctx->stream));
     std::vector<double> ones;
@@ -718,16 +720,18 @@ fdl_status build_dists(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, cons
     for (int s0 = src_lo; s0 < src_hi; s0 += S) {
         const int nsrc = std::min(S, src_hi - s0);
         FDL_LAUNCH(launch_bf_init(da, n, s0, nsrc, S, ctx->stream));
-        double *din = da, *dout = db;
-        for (int it = 0; it < n; ++it) {
+        FDL_CUDA(cudaMemsetAsync(stamp, 0xFF, sizeof(int) * n, ctx->stream));  // -1: never changed
+        // sweeps are idempotent at the fixed point, so 8 run between host checks
+        for (int it = 0; it < 4 * n + 8; it += 8) {
             FDL_CUDA(cudaMemsetAsync(&ctx->sc->anynew, 0, sizeof(unsigned int), ctx->stream));
-            FDL_LAUNCH(launch_bf_relax(d_rp, d_col, d_len, din, dout, n, S, nsrc, &ctx->sc->anynew, ctx->stream));
+            for (int k = 0; k < 8; ++k)
+                FDL_LAUNCH(launch_bf_relax(d_rp, d_col, d_len, da, stamp, n, S, nsrc, it + k, &ctx->sc->anynew,
+                                           ctx->stream));
             FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, ctx->stream));
             FDL_CUDA(cudaStreamSynchronize(ctx->stream));
-            std::swap(din, dout);
             if (!ctx->sc_host->anynew) break;
         }
-        FDL_LAUNCH(launch_bf_store(din, n, s0, nsrc, S, ctx->nb, ctx->t0, ctx->t1, ctx->D, dmax, ctx->stream));
+        FDL_LAUNCH(launch_bf_store(da, n, s0, nsrc, S, ctx->nb, ctx->t0, ctx->t1, ctx->D, dmax, ctx->stream));
     }
     double mx = 0.0;
     FDL_CUDA(cudaMemcpyAsync(&mx, dmax, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -737,7 +741,7 @@ fdl_status build_dists(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, cons
     cudaFree(d_col);
     cudaFree(d_len);
     cudaFree(da);
-    cudaFree(db);
+    cudaFree(stamp);
     cudaFree(dmax);
     return FDL_OK;
 }

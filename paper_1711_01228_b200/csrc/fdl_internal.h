@@ -182,8 +182,8 @@ cudaError_t launch_bfs_level_sym(const int64_t* row_ptr, const int32_t* col, con
 // weighted / general-alpha setup: multi-source Bellman-Ford in fp64 over the
 // CSR with edge lengths; dist[v * S + s] for the batch's sources s0..s0+S-1
 cudaError_t launch_bf_init(double* dist, int n, int s0, int nsrc, int S, cudaStream_t s);
-cudaError_t launch_bf_relax(const int64_t* row_ptr, const int32_t* col, const double* len, const double* din,
-                            double* dout, int n, int S, int nsrc, unsigned int* changed, cudaStream_t s);
+cudaError_t launch_bf_relax(const int64_t* row_ptr, const int32_t* col, const double* len, double* dist, int* stamp,
+                            int n, int S, int nsrc, int it, unsigned int* changed, cudaStream_t s);
 cudaError_t launch_bf_store(const double* dist, int n, int s0, int nsrc, int S, int nb, int64_t t0, int64_t t1,
                             uint8_t* D, double* dmax, cudaStream_t s);
 cudaError_t launch_dist_rows(const uint8_t* D, int hb, int nb, int64_t t0, int64_t t1, const int* rows, int nrows,

@@ -1379,34 +1379,48 @@ cudaError_t launch_bf_init(double* dist, int n, int s0, int nsrc, int S, cudaStr
     return cudaGetLastError();
 }
 
+// In-place (Gauss-Seidel order) pull relaxation with a change frontier: vertex v
+// is recomputed only if a neighbour changed in this or the previous sweep
+// (stamp[u] >= it - 1).  Values only decrease and stay lengths of real paths
+// (aligned 64-bit stores are atomic), so the sweep converges to the same fixed
+// point as a Jacobi sweep, in fewer sweeps and touching only the wavefront.
 __global__ void __launch_bounds__(256) k_bf_relax(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-                                                  const double* __restrict__ len, const double* __restrict__ din,
-                                                  double* __restrict__ dout, int n, int S, int nsrc,
-                                                  unsigned int* changed)
+                                                  const double* __restrict__ len, double* dist, int* stamp, int n,
+                                                  int S, int nsrc, int it, unsigned int* changed)
 {
     const int v = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (v >= n) return;
     const int64_t beg = row_ptr[v], end = row_ptr[v + 1];
+    bool active = it == 0;
+    for (int64_t e = beg + lane; e < end && !active; e += 32) active = stamp[col[e]] >= it - 1;
+    if (!__any_sync(0xffffffffu, active)) return;
     bool any = false;
     for (int k = lane; k < nsrc; k += 32) {
-        const double old = din[(int64_t)v * S + k];
+        volatile double* dv = dist;
+        const double old = dv[(int64_t)v * S + k];
         double best = old;
         for (int64_t e = beg; e < end; ++e) {
-            const double c = din[(int64_t)col[e] * S + k] + len[e];
+            const double c = dv[(int64_t)col[e] * S + k] + len[e];
             best = c < best ? c : best;
         }
-        dout[(int64_t)v * S + k] = best;
-        any |= best < old;
+        if (best < old) {
+            dv[(int64_t)v * S + k] = best;
+            any = true;
+        }
     }
-    if (__any_sync(0xffffffffu, any) && lane == 0) *changed = 1u;
+    if (__any_sync(0xffffffffu, any) && lane == 0) {
+        stamp[v] = it;
+        *changed = 1u;
+    }
 }
 
-cudaError_t launch_bf_relax(const int64_t* row_ptr, const int32_t* col, const double* len, const double* din,
-                            double* dout, int n, int S, int nsrc, unsigned int* changed, cudaStream_t s)
+cudaError_t launch_bf_relax(const int64_t* row_ptr, const int32_t* col, const double* len, double* dist, int* stamp,
+                            int n, int S, int nsrc, int it, unsigned int* changed, cudaStream_t s)
 {
     const int64_t threads = (int64_t)n * 32;
-    k_bf_relax<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(row_ptr, col, len, din, dout, n, S, nsrc, changed);
+    k_bf_relax<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(row_ptr, col, len, dist, stamp, n, S, nsrc, it,
+                                                                 changed);
     return cudaGetLastError();
 }
 
