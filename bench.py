@@ -308,6 +308,25 @@ def run_gpu(args):
                 "bytes_per_launch": st.p2_pairs * hop_bytes / max(st.p2_launches, 1),
                 "avg_launch_ms": st.p2_ms / max(st.p2_launches, 1)}
 
+    # traffic of the dominant kernel: DRAM bytes per launch from the newest committed
+    # `ncu --set full` capture of the same kernel instantiation (profiles/*_traffic.json)
+    hb = {3: 5, 4: 0, 8: 1, 16: 2, 32: 4}.get(info.hop_bits, -1)
+    if dominant_p1:
+        mode, nsets = (3, 2) if st.p1_pairs_nor > 0 else (0, 2 if st.p1_pairs_x2 > 0 else 1)
+    else:
+        mode, nsets = 1, 1
+    kname = f"k_sym<{mode}, {dim}, {nsets}, {hb}>"
+    import glob
+    for tf in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")), reverse=True):
+        try:
+            tj = json.load(open(tf))
+        except Exception:
+            continue
+        if kname in tj.get("bytes_per_launch", {}):
+            roof["traffic"] = tj["bytes_per_launch"][kname]
+            roof["traffic_source"] = f"{os.path.basename(tf)}: {tj.get('source', '')} ({kname})"
+            break
+
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:

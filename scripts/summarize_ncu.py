@@ -54,6 +54,7 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "sm__sass_thread_inst_ex
        "gpu__time_duration.sum", "sm__inst_executed_pipe_xu.sum", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
        "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"]
+traffic = {}
 for kern in ("p1", "p2"):
     rep = os.path.join(SRC, f"{TAG}_prof_{kern}.ncu-rep")
     if not os.path.exists(rep):
@@ -73,10 +74,16 @@ for kern in ("p1", "p2"):
     rr = list(csv.reader(io.StringIO(raw)))
     if len(rr) >= 3:
         hh, units, vals = rr[0], rr[1], rr[2]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
         for k in RAW:
             if k in hh:
                 j = hh.index(k)
                 out.append(f"| raw | {k} | {vals[j]} {units[j]} |")
+        if "dram__bytes_read.sum" in hh and "dram__bytes_write.sum" in hh:
+            jr, jw = hh.index("dram__bytes_read.sum"), hh.index("dram__bytes_write.sum")
+            tb = (float(vals[jr].replace(",", "")) * scale.get(units[jr], 1)
+                  + float(vals[jw].replace(",", "")) * scale.get(units[jw], 1))
+            traffic[name.split("(")[0].replace("void ", "").strip()] = tb
         stalls = [(hh[j], vals[j]) for j in range(len(hh)) if hh[j].startswith("smsp__average_warps_issue_stalled_")
                   and hh[j].endswith("_per_issue_active.ratio")]
         stalls = sorted(stalls, key=lambda x: -float(x[1] or 0))[:6]
@@ -84,6 +91,12 @@ for kern in ("p1", "p2"):
             f"{s.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', '')}={float(v):.2f}"
             for s, v in stalls) + " |")
     out.append("")
+
+if traffic:  # per-launch DRAM bytes of the captured kernels (bench.py roofline.traffic)
+    import json
+    with open(os.path.join(DST, f"{TAG}_traffic.json"), "w") as f:
+        json.dump({"tag": TAG, "source": "ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum",
+                   "bytes_per_launch": traffic}, f, indent=1)
 
 path = os.path.join(DST, f"{TAG}_ncu_summary.md")
 with open(path, "w") as f:
