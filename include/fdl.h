@@ -167,6 +167,8 @@ typedef struct {
     uint64_t cg_iters;        /* PCG iterations                                      */
     uint64_t p1_pairs_nor;    /* P1 pair x set evaluations of stress only (no R)     */
     uint64_t p1_rejected;     /* split P1 steps whose guard rejected Xt (extra 1-set pass) */
+    uint64_t p1s_launches;    /* ... of the P1 launches: split line-6 passes (P1S)         */
+    double p1s_ms;            /* ... and their CUDA-event time (included in p1_ms)       */
 } fdl_stats;
 
 /* Fill *p with defaults: dim 2, k auto, omega 1.5, step +INF, tol 1e-4,

@@ -378,7 +378,8 @@ int ps_p2(int dim) { return dim == 2 ? 2 : 4; }
 
 // ------------------------------------------------------------ event timing
 // Intervals are (start event, end event, kind): kind 1 = P1 pass, 2 = P2
-// pass, 3 = DIAG pass, 0 = a whole fdl_step.  Recorded on the context stream.
+// pass, 3 = DIAG pass, 4 = split line-6 pass (P1S, also a P1 pass), 0 = a whole
+// fdl_step.  Recorded on the context stream.
 cudaEvent_t next_event(fdl_ctx* ctx)
 {
     if (ctx->ev_used == ctx->ev_pool.size()) {
@@ -412,7 +413,10 @@ void collect_events(fdl_ctx* ctx)
         if (m.end == (size_t)-1) continue;
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ctx->ev_pool[m.start], ctx->ev_pool[m.end]);
-        if (m.kind == 1) p1 += ms;
+        if (m.kind == 4) {  // the split line-6 pass (also counted as P1)
+            ctx->stats.p1s_ms += ms;
+            p1 += ms;
+        } else if (m.kind == 1) p1 += ms;
         else if (m.kind == 2) p2 += ms;
         else if (m.kind == 0) step += ms;
     }
@@ -483,13 +487,16 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
     a.alpha = (float)ctx->alpha;
     const int grid = mode == kSymP1S ? ctx->grid_p1s
                                      : (mode == kSymP1 ? ctx->grid_p1[nsets] : (mode == kSymP2 ? ctx->grid_p2 : ctx->grid_diag));
-    const int mk = mark_begin(ctx, p1 ? 1 : (mode == kSymP2 ? 2 : 3));
+    const int mk = mark_begin(ctx, mode == kSymP1S ? 4 : (p1 ? 1 : (mode == kSymP2 ? 2 : 3)));
     if (ctx->nitems > 0) FDL_LAUNCH(launch_sym(a, mode, dim, nsets, ctx->hb, grid, ctx->stream));
     mark_end(ctx, mk);
     if (p1) {
         ctx->stats.p1_launches++;
         ctx->stats.p1_pairs += ctx->local_pairs * (uint64_t)nsets;
-        if (mode == kSymP1S) ctx->stats.p1_pairs_nor += ctx->local_pairs;
+        if (mode == kSymP1S) {
+            ctx->stats.p1_pairs_nor += ctx->local_pairs;
+            ctx->stats.p1s_launches++;
+        }
         if (nsets == 2) ctx->stats.p1_pairs_x2 += ctx->local_pairs * 2;
     } else if (mode == kSymP2) {
         ctx->stats.p2_launches++;

@@ -89,7 +89,7 @@ class Stats(ctypes.Structure):
         ("p1_pairs", ctypes.c_uint64), ("p2_pairs", ctypes.c_uint64), ("p1_pairs_x2", ctypes.c_uint64),
         ("p1_ms", ctypes.c_double), ("p2_ms", ctypes.c_double), ("other_ms", ctypes.c_double),
         ("steps", ctypes.c_uint64), ("cg_iters", ctypes.c_uint64), ("p1_pairs_nor", ctypes.c_uint64),
-        ("p1_rejected", ctypes.c_uint64),
+        ("p1_rejected", ctypes.c_uint64), ("p1s_launches", ctypes.c_uint64), ("p1s_ms", ctypes.c_double),
     ]
 
     def as_dict(self):

@@ -543,17 +543,27 @@ def test_weighted_end_to_end(kind, alpha, omega):
 
 
 # ------------------------------------------------ a7: the multi-rank step, on one GPU
-@pytest.mark.parametrize("name,world,omega", [("C2", 2, 1.6), ("C3", 3, 1.5), ("C3", 2, 0.0)])
-def test_loopback_ranks_bitwise(name, world, omega):
+@pytest.mark.parametrize("name,world,omega,kw", [("C2", 2, 1.6, {}), ("C3", 3, 1.5, {}), ("C3", 2, 0.0, {}),
+                                                 ("C3", 2, 1.5, {"dim": 3, "hop_bits": 16}),
+                                                 ("wrgg", 2, 1.5, {"weight_exp": -1.0}),
+                                                 ("C2", 3, 1.5, {"strategy": 1, "seed": 4})])
+def test_loopback_ranks_bitwise(name, world, omega, kw):
     """The whole tile-sharded iteration (every rank evaluates its share of the
     triangle; partial sums all-gathered and summed in rank order) through the
     in-process loopback transport: every rank holds bitwise the single-GPU
     trajectory (per-row sums never depend on the tile ownership)."""
     import threading
-    cfg = configs.CONFIGS[name]
-    g = configs.graph_for(name)
-    X0 = configs.positions_for(name, g.n, 1)
-    p = fdl.make_params(dim=2, k=cfg.k_for(g.n), omega=omega, tol=cfg.tol, max_iter=cfg.max_iter)
+    kw = dict(kw)
+    dim = kw.pop("dim", 2)
+    lens = None
+    if name == "wrgg":
+        g, lens = graphs.random_geometric_graph_weighted(700, 6, 21)
+        cfg = configs.CONFIGS["C3"]
+    else:
+        cfg = configs.CONFIGS[name]
+        g = configs.graph_for(name)
+    X0 = graphs.init_positions(g.n, dim, 5)
+    p = fdl.make_params(dim=dim, k=cfg.k_for(g.n), omega=omega, tol=cfg.tol, max_iter=cfg.max_iter, **kw)
     steps = 12
 
     def run(L, out):
@@ -566,14 +576,15 @@ def test_loopback_ranks_bitwise(name, world, omega):
         out.append((fs, L.get_positions()))
 
     ref = []
-    with fdl.Layout.from_graph(g, params=p, init_pos=X0) as L1:
+    with fdl.Layout.from_graph(g, params=p, init_pos=X0, edge_len=lens) as L1:
         run(L1, ref)
     grp = fdl.LoopbackGroup(world)
     ctxs, outs, errs = [None] * world, [[] for _ in range(world)], []
 
     def rank_main(r):
         try:
-            ctxs[r] = fdl.Layout.from_graph(g, params=p, init_pos=X0, group=grp, rank=r, world=world)
+            ctxs[r] = fdl.Layout.from_graph(g, params=p, init_pos=X0, group=grp, rank=r, world=world,
+                                            edge_len=lens)
             run(ctxs[r], outs[r])
         except Exception as e:  # noqa: BLE001
             errs.append(e)
