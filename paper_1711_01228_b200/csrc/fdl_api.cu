@@ -1251,17 +1251,26 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
     int cg = 0;
     // graph mode: one launch per step; not with a host decision inside the step
     // (split line 6, enumeration) or host-side exchanges (several ranks)
-    const bool graph = ctx->use_graphs && !enumerate && !(nsets == 2 && ctx->p1_split) && ctx->world == 1 &&
-                       ctx->steps_eager > 0;
+    bool graph = ctx->use_graphs && !enumerate && !(nsets == 2 && ctx->p1_split) && ctx->world == 1 &&
+                 ctx->steps_eager > 0;
+    const auto key = std::make_tuple((int)refresh, nsets, (int)ctx->ext_ok, omega);
+    auto it = ctx->graphs.find(key);
+    if (graph && it == ctx->graphs.end()) {
+        StepGraph sg;
+        if (build_step_graph(ctx, sh, sg) == FDL_OK) {
+            it = ctx->graphs.emplace(key, sg).first;
+        } else {
+            // capture refused (driver without conditional nodes, ...): eager from now on
+            fprintf(stderr, "fdl: step graph capture failed (%s); using eager launches\n", ctx->err.c_str());
+            cudaGetLastError();
+            ctx->use_graphs = false;
+            ctx->broken = false;
+            ctx->err.clear();
+            graph = false;
+        }
+    }
     const int mstep = mark_begin(ctx, 0);
     if (graph) {
-        const auto key = std::make_tuple((int)refresh, nsets, (int)ctx->ext_ok, omega);
-        auto it = ctx->graphs.find(key);
-        if (it == ctx->graphs.end()) {
-            StepGraph sg;
-            FDL_TRY(build_step_graph(ctx, sh, sg));
-            it = ctx->graphs.emplace(key, sg).first;
-        }
         FDL_CUDA(cudaGraphLaunch(it->second.exec, s));
         mark_end(ctx, mstep);
         FDL_CUDA(cudaStreamSynchronize(s));
