@@ -467,7 +467,8 @@ fdl_status allgather_inplace(fdl_ctx* ctx, void* buf, size_t slice_elems, int nc
 // One symmetric pass over the local tiles + the per-row fixed-order
 // reduction; with several ranks the dense rank partials are all-gathered and
 // summed in rank order.  out0 gets components [0, D0), out1 the rest.
-fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* out0, double* out1, int set_cur)
+fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* out0, double* out1, int set_cur,
+                   bool p2_finish = true)
 {
     const int dim = ctx->dim;
     const bool p1 = mode == kSymP1 || mode == kSymP1S;
@@ -505,7 +506,7 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
     if (ctx->world == 1 || ctx->emulated) {
         FDL_LAUNCH(launch_sym_reduce(ctx->ipart, ctx->jpart, ctx->it_lo, ctx->it_hi, ctx->nb, ctx->t0, ctx->t1, C, D0,
                                      inter, out0, out1, ctx->stream));
-        if (mode == kSymP2)  // product form: L^W p = diag p - sum_j w p_j (rank-local diag when emulated)
+        if (mode == kSymP2 && p2_finish)  // product form: L^W p = diag p - sum_j w p_j (rank-local diag when emulated)
             FDL_LAUNCH(launch_p2_finish(out0, pos, ctx->diag, ctx->n, dim, ps_p2(dim), ctx->stream));
         if (p1) {
             FDL_LAUNCH2(launch_sym_stress(ctx->spart, ctx->nitems * 8, nsets, ctx->sparts, ctx->stress_scratch, ctx->stream));
@@ -519,7 +520,8 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
                                  mine, nullptr, ctx->stream));
     FDL_TRY(allgather_inplace(ctx, ctx->rparts, slice, ncclFloat64, 8));
     FDL_LAUNCH(launch_rank_sum(ctx->rparts, ctx->world, ctx->npad, C, D0, inter, out0, out1, ctx->stream));
-    if (mode == kSymP2) FDL_LAUNCH(launch_p2_finish(out0, pos, ctx->diag, ctx->n, dim, ps_p2(dim), ctx->stream));
+    if (mode == kSymP2 && p2_finish)
+        FDL_LAUNCH(launch_p2_finish(out0, pos, ctx->diag, ctx->n, dim, ps_p2(dim), ctx->stream));
     if (p1) {
         FDL_LAUNCH2(launch_sym_stress(ctx->spart, ctx->nitems * 8, nsets, ctx->sparts + 2 * ctx->rank, ctx->stress_scratch,
                                      ctx->stream));
@@ -1003,6 +1005,8 @@ double pick_omega(fdl_ctx* ctx)
 }
 
 // One Algorithm-2 iteration.
+constexpr int kTailBlocks = 8;  // fused PCG tail for n <= 8 * 256 rows (one block is slower beyond)
+
 // ---- the three phases of one Algorithm-2 iteration (enqueue only; the eager
 // step syncs between them, the graph step captures them once).
 struct StepShape {
@@ -1039,6 +1043,14 @@ fdl_status enqueue_cg_body(fdl_ctx* ctx, unsigned long long cond)
 {
     const int dim = ctx->dim, n = ctx->n, pq = ps_p2(dim);
     cudaStream_t s = ctx->stream;
+    if (ctx->nblk <= kTailBlocks) {
+        // small n: the vector part of the iteration in one block (bitwise the same sequence)
+        FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->cy, nullptr, 0, false));
+        FDL_LAUNCH(launch_cg_tail(ctx->cy, ctx->pvec, ctx->diag, ctx->Xn, ctx->cr, ctx->cz, ctx->cp, ctx->pvec,
+                                  ctx->blk_cg, n, dim, (n + kRB - 1) / kRB, pq, ctx->p.cg_rtol, ctx->sc, ctx->hs_dev,
+                                  s, cond, cond != 0, ctx->p.cg_max_iter));
+        return FDL_OK;
+    }
     FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->cy, nullptr, 0));
     FDL_LAUNCH(launch_cg_ap(ctx->cp, ctx->cy, ctx->blk_cg, ctx->nblk, n, dim, ctx->sc, s));
     FDL_LAUNCH(launch_cg_finalize(ctx->blk_cg, ctx->nblk, dim, 1, ctx->p.cg_rtol, ctx->sc, ctx->hs_dev, s));

@@ -103,6 +103,12 @@ cudaError_t launch_cg_p(double* p, const double* z, float* pvec, const DevScalar
 cudaError_t launch_cg_finalize(const double* blk, int nblk, int dim, int mode, double rtol,
                                DevScalars* sc, HostScalars* hs, cudaStream_t s, unsigned long long cond = 0,
                                int use_cond = 0, int cg_max = 0);
+// one PCG iteration after the P2 pass in one 1024-thread block (small n), bitwise the
+// k_p2_finish / k_cg_ap / finalize / k_cg_update / finalize / k_cg_p sequence
+cudaError_t launch_cg_tail(double* y, const float* pvec_in, const double* diag, double* x, double* r, double* z,
+                           double* p, float* pvec, double* blk, int n, int dim, int nblk, int pq, double rtol,
+                           DevScalars* sc, HostScalars* hs, cudaStream_t s, unsigned long long cond, int use_cond,
+                           int cg_max);
 cudaError_t launch_ffma_bench(float* out, int iters, int blocks, int threads, cudaStream_t s);
 
 // ------------------------------------------------------- symmetric (triangle) passes

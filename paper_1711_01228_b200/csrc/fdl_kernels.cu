@@ -617,11 +617,12 @@ cudaError_t launch_cg_p(double* p, const double* z, float* pvec, const DevScalar
 // Scalar step of PCG from block partials (summed in global block order by
 // one warp, fixed butterfly).  Slots: 0 r.z | p.y (mode 1), 1 r.r, 2 b.b,
 // 3 sum z.  mode 0: init; 1: alpha; 2: beta + stop test.
-__global__ void k_cg_finalize(const double* __restrict__ blk, int nblk, int dim, int mode, double rtol,
-                              DevScalars* sc, HostScalars* hs, cudaGraphConditionalHandle cond, int use_cond,
-                              int cg_max)
+// Scalar PCG step by one warp (lane = threadIdx.x & 31 of warp 0 of the block).
+__device__ __forceinline__ void cg_finalize_warp(const double* __restrict__ blk, int nblk, int dim, int mode,
+                                                 double rtol, DevScalars* sc, HostScalars* hs,
+                                                 cudaGraphConditionalHandle cond, int use_cond, int cg_max)
 {
-    const int lane = threadIdx.x;
+    const int lane = threadIdx.x & 31;
     double sums[4][3];
     for (int qq = 0; qq < 4; ++qq)
         for (int c = 0; c < dim; ++c) {
@@ -684,6 +685,122 @@ __global__ void k_cg_finalize(const double* __restrict__ blk, int nblk, int dim,
         hs->done = !any;
         if (use_cond) cudaGraphSetConditional(cond, (any && sc->cg_iters < cg_max) ? 1u : 0u);
     }
+}
+
+__global__ void k_cg_finalize(const double* __restrict__ blk, int nblk, int dim, int mode, double rtol,
+                              DevScalars* sc, HostScalars* hs, cudaGraphConditionalHandle cond, int use_cond,
+                              int cg_max)
+{
+    cg_finalize_warp(blk, nblk, dim, mode, rtol, sc, hs, cond, use_cond, cg_max);
+}
+
+// ---------------------------------------------------------- fused PCG tail
+// One PCG iteration after the P2 pass (k_p2_finish, k_cg_ap, finalize 1,
+// k_cg_update, finalize 2, k_cg_p) in ONE block of 1024 threads, for small n:
+// the 256-row blocks are processed four at a time by the four 256-thread
+// quarters with the same per-row arithmetic, the same warp butterflies and the
+// same warp and block orders as the separate kernels, so the results are
+// bitwise those of the multi-kernel sequence (fewer launches per iteration).
+__device__ __forceinline__ double quarter_sum(double v, double* red /* 32 */)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    if ((threadIdx.x & 255) == 0) {
+        const int w0 = (threadIdx.x >> 8) * 8;
+        for (int k = 0; k < 8; ++k) t += red[w0 + k];
+    }
+    return t;
+}
+
+__global__ void __launch_bounds__(1024) k_cg_tail(double* y, const float* __restrict__ pvec_in,
+                                                 const double* __restrict__ diag, double* x, double* r, double* z,
+                                                 double* p, float* pvec, double* blk, int n, int dim, int nblk,
+                                                 int pq, double rtol, DevScalars* sc, HostScalars* hs,
+                                                 cudaGraphConditionalHandle cond, int use_cond, int cg_max)
+{
+    __shared__ double red[32];
+    const int quarter = threadIdx.x >> 8, tq = threadIdx.x & 255;
+    // (1) y = diag p' - S (k_p2_finish), y += sigma S_p (k_cg_ap), p.y partials
+    for (int b0 = 0; b0 < nblk; b0 += 4) {
+        const int b = b0 + quarter;
+        const int i = b * kRB + tq;
+        double py[3] = {0, 0, 0};
+        if (b < nblk && i < n) {
+            const int64_t g = stage_slot(i);
+            const double d = diag[i];
+            for (int q = 0; q < dim; ++q) {
+                const size_t k = (size_t)i * dim + q;
+                double yv = d * (double)pvec_in[g * pq + q] - y[k];
+                yv = yv + sc->sigma * sc->S[q];
+                y[k] = yv;
+                py[q] = p[k] * yv;
+            }
+        }
+        for (int q = 0; q < dim; ++q) {
+            const double t = quarter_sum(py[q], red);
+            if (tq == 0 && b < nblk) blk[(size_t)q * nblk + b] = t;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) cg_finalize_warp(blk, nblk, dim, 1, rtol, sc, hs, cond, 0, cg_max);
+    __syncthreads();
+    // (2) x += alpha p, r -= alpha y, z = r / diag, dot partials (k_cg_update)
+    for (int b0 = 0; b0 < nblk; b0 += 4) {
+        const int b = b0 + quarter;
+        const int i = b * kRB + tq;
+        double rz[3] = {0, 0, 0}, rr[3] = {0, 0, 0}, zs[3] = {0, 0, 0};
+        if (b < nblk && i < n) {
+            for (int q = 0; q < dim; ++q) {
+                const size_t k = (size_t)i * dim + q;
+                const double al = sc->alpha[q];
+                const double xv = x[k] + al * p[k];
+                const double rv = r[k] - al * y[k];
+                const double zv = rv / diag[i];
+                x[k] = xv;
+                r[k] = rv;
+                z[k] = zv;
+                rz[q] = rv * zv;
+                rr[q] = rv * rv;
+                zs[q] = zv;
+            }
+        }
+        for (int q = 0; q < dim; ++q) {
+            double t = quarter_sum(rz[q], red);
+            if (tq == 0 && b < nblk) blk[(size_t)(0 * 4 + q) * nblk + b] = t;
+            t = quarter_sum(rr[q], red);
+            if (tq == 0 && b < nblk) blk[(size_t)(1 * 4 + q) * nblk + b] = t;
+            t = quarter_sum(zs[q], red);
+            if (tq == 0 && b < nblk) blk[(size_t)(3 * 4 + q) * nblk + b] = t;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) cg_finalize_warp(blk, nblk, dim, 2, rtol, sc, hs, cond, use_cond, cg_max);
+    __syncthreads();
+    // (3) p = z + beta p (active columns), fp32 staging centred by S/n (k_cg_p)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int64_t g = stage_slot(i);
+        for (int q = 0; q < dim; ++q) {
+            const size_t k = (size_t)i * dim + q;
+            double pv = p[k];
+            if (sc->active[q]) pv = z[k] + sc->beta[q] * pv;
+            p[k] = pv;
+            pvec[g * pq + q] = (float)(pv - sc->S[q] * sc->inv_n);
+        }
+    }
+}
+
+cudaError_t launch_cg_tail(double* y, const float* pvec_in, const double* diag, double* x, double* r, double* z,
+                           double* p, float* pvec, double* blk, int n, int dim, int nblk, int pq, double rtol,
+                           DevScalars* sc, HostScalars* hs, cudaStream_t s, unsigned long long cond, int use_cond,
+                           int cg_max)
+{
+    k_cg_tail<<<1, 1024, 0, s>>>(y, pvec_in, diag, x, r, z, p, pvec, blk, n, dim, nblk, pq, rtol, sc, hs,
+                                 (cudaGraphConditionalHandle)cond, use_cond, cg_max);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_cg_finalize(const double* blk, int nblk, int dim, int mode, double rtol, DevScalars* sc,

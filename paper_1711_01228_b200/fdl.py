@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libfdl.so")
+LIB_PATH = os.environ.get("FDL_LIB") or os.path.join(_PKG, "lib", "libfdl.so")  # FDL_LIB: A/B builds in tests
 
 FDL_TILE = 128
 STATUS = {
