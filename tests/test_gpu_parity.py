@@ -631,3 +631,21 @@ def test_graph_steps_bitwise(name, omega, strategy):
     a, b = out
     assert a[:3] == b[:3] and np.array_equal(a[3], b[3])
     assert a[4:] == b[4:]  # launch accounting of the captured phases
+
+
+@pytest.mark.parametrize("bits", [16, 0])
+def test_end_to_end_3d_rgg(bits):
+    """C4's family at a size the fp64 oracle runs in seconds: 3-D layout of a
+    random geometric graph (C4 generator, n = 2500), 16-bit hop tiles forced
+    (C4's width) or auto; §8(c) end-to-end gates against the Cholesky oracle."""
+    cfg = configs.CONFIGS["C4"]
+    g = graphs.random_geometric_graph(2500, 6.0, seed=44)
+    k = cfg.k_for(g.n)
+    X0 = graphs.init_positions(g.n, 3, 45)
+    p = fdl.make_params(dim=3, k=k, omega=1.5, tol=cfg.tol, max_iter=cfg.max_iter, hop_bits=bits)
+    L = fdl.Layout.from_graph(g, params=p, init_pos=X0)
+    if bits == 16:
+        assert L.info.hop_bits == 16
+    r = L.run_until_converged()
+    o = layout.run_algorithm2(layout.Problem(g, 3, k), X0, 1.5, cfg.tol, cfg.max_iter)
+    _gates(r.iterations, r.f_final, o)
