@@ -621,14 +621,18 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
         const int maxhop = hb_max_hop(hb);
         bool overflow = false;
         int diam = 0;
+        uint8_t* bbuf = nullptr;
+        const size_t bbytes = (size_t)n * bfs_row_bytes_host(hb);
+        FDL_CUDA(cudaMalloc(&bbuf, bbytes));
         for (int s0 = src_lo; s0 < src_hi && !overflow; s0 += 32 * kBFSWords) {
             const int nsrc = std::min(32 * kBFSWords, src_hi - s0);
+            FDL_CUDA(cudaMemsetAsync(bbuf, 0, bbytes, ctx->stream));
             FDL_LAUNCH(launch_bfs_init(fa, vis, n, s0, ctx->stream));
             uint32_t *fin = fa, *fout = fb;
             for (int level = 1;; ++level) {
                 FDL_CUDA(cudaMemsetAsync(&ctx->sc->anynew, 0, sizeof(unsigned int), ctx->stream));
-                FDL_LAUNCH(launch_bfs_level_sym(d_rp, d_col, fin, fout, vis, ctx->D, n, s0, nsrc, level, ctx->nb,
-                                                ctx->t0, ctx->t1, hb, &ctx->sc->anynew, ctx->stream));
+                FDL_LAUNCH(launch_bfs_level_sym(d_rp, d_col, fin, fout, vis, bbuf, n, nsrc, level, hb,
+                                                &ctx->sc->anynew, ctx->stream));
                 FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost,
                                          ctx->stream));
                 FDL_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -640,7 +644,11 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
                 diam = std::max(diam, level);
                 std::swap(fin, fout);
             }
+            if (!overflow)
+                FDL_LAUNCH(launch_bfs_retile(bbuf, ctx->D, n, s0, nsrc, ctx->nb, ctx->t0, ctx->t1, hb, ctx->stream));
         }
+        FDL_CUDA(cudaStreamSynchronize(ctx->stream));
+        cudaFree(bbuf);
         if (!overflow) {
             ctx->diameter = diam;
             if (hb == 0) FDL_LAUNCH(launch_nib_encode(ctx->D, dbytes, ctx->stream));

@@ -183,8 +183,12 @@ int sym_stress_chunks(int nitems);
 cudaError_t launch_sym_stress(const double* spart, int nitems, int nsets, double* out, double* scratch,
                               cudaStream_t s);
 cudaError_t launch_bfs_level_sym(const int64_t* row_ptr, const int32_t* col, const uint32_t* fin, uint32_t* fout,
-                                 uint32_t* visited, uint8_t* D, int n, int s0, int nsrc, int level, int nb, int64_t t0,
-                                 int64_t t1, int hb, unsigned int* anynew, cudaStream_t s);
+                                 uint32_t* visited, uint8_t* bbuf, int n, int nsrc, int level, int hb,
+                                 unsigned int* anynew, cudaStream_t s);
+// batch rows [s0, s0 + nsrc) of bbuf (cells [v][source]) -> the local triangle tiles
+cudaError_t launch_bfs_retile(const uint8_t* bbuf, uint8_t* D, int n, int s0, int nsrc, int nb, int64_t t0,
+                              int64_t t1, int hb, cudaStream_t s);
+int bfs_row_bytes_host(int hb);  // batch-buffer bytes per vertex
 // weighted / general-alpha setup: multi-source Bellman-Ford in fp64 over the
 // CSR with edge lengths; dist[v * S + s] for the batch's sources s0..s0+S-1
 cudaError_t launch_bf_init(double* dist, int n, int s0, int nsrc, int S, cudaStream_t s);

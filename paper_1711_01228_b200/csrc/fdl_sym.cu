@@ -1284,15 +1284,65 @@ cudaError_t launch_sym_stress(const double* spart, int nitems, int nsets, double
     return cudaGetLastError();
 }
 
-// MS-BFS level writing into the triangle tile layout: entry (s, v) goes to tile
-// (s/kT, v/kT) when s/kT <= v/kT and that tile is in [t0, t1).
+// MS-BFS level: vertex v ORs its neighbours' 1024-source frontier words
+// (warp per vertex, lane = 32 sources, coalesced neighbour reads), keeps the
+// new bits, and records their level in the batch buffer bbuf[v][source] (cells
+// of the stored width, each lane's 32 cells contiguous: one vector
+// read-modify-write per lane and level).  k_bfs_retile then moves the batch's
+// rows into the triangle tiles with coalesced 16-byte chunk stores.
+template <int HB>
+__device__ __forceinline__ void bfs_record(uint8_t* cells, uint32_t nw, int level)
+{
+    if (HB == 0) {  // 32 nibbles = 16 bytes
+        uint4 c = *reinterpret_cast<uint4*>(cells);
+        uint32_t w[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if ((nw >> (8 * q + k)) & 1u) w[q] |= (uint32_t)level << (4 * k);
+        *reinterpret_cast<uint4*>(cells) = make_uint4(w[0], w[1], w[2], w[3]);
+    } else if (HB == 1) {  // 32 bytes
+        uint4* p = reinterpret_cast<uint4*>(cells);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint4 c = p[h];
+            uint32_t w[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if ((nw >> (16 * h + 4 * q + k)) & 1u) w[q] |= (uint32_t)level << (8 * k);
+            p[h] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+    } else {  // 32 x uint16 = 64 bytes
+        uint4* p = reinterpret_cast<uint4*>(cells);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            uint4 c = p[h];
+            uint32_t w[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+                    if ((nw >> (8 * h + 2 * q + k)) & 1u) w[q] |= (uint32_t)level << (16 * k);
+            p[h] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+    }
+}
+
+template <int HB>
+__host__ __device__ constexpr int bfs_row_bytes()  // batch-buffer bytes per vertex (1024 sources)
+{
+    return HB == 0 ? 512 : 1024 * HB;
+}
+
 template <int HB>
 __global__ void __launch_bounds__(256) k_bfs_level_sym(const int64_t* __restrict__ row_ptr,
                                                        const int32_t* __restrict__ col,
                                                        const uint32_t* __restrict__ fin, uint32_t* __restrict__ fout,
-                                                       uint32_t* __restrict__ visited, uint8_t* __restrict__ D, int n,
-                                                       int s0, int nsrc, int level, int nb, int64_t t0, int64_t t1,
-                                                       unsigned int* anynew)
+                                                       uint32_t* __restrict__ visited, uint8_t* __restrict__ bbuf,
+                                                       int n, int nsrc, int level, unsigned int* anynew)
 {
     const int v = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
@@ -1315,48 +1365,101 @@ __global__ void __launch_bounds__(256) k_bfs_level_sym(const int64_t* __restrict
             acc |= fin[(int64_t)u * kBFSWords + lane];
         }
     }
-    uint32_t nw = acc & ~vis & full;
+    const uint32_t nw = acc & ~vis & full;
     fout[(int64_t)v * kBFSWords + lane] = nw;
-    if (nw) visited[(int64_t)v * kBFSWords + lane] = vis | nw;
+    if (nw) {
+        visited[(int64_t)v * kBFSWords + lane] = vis | nw;
+        bfs_record<HB>(bbuf + (int64_t)v * bfs_row_bytes<HB>() + lane * (bfs_row_bytes<HB>() / 32), nw, level);
+    }
     if (__any_sync(0xffffffffu, nw != 0u) && lane == 0) *anynew = 1u;
-    const int J = v / kT, cl = v % kT;
-    while (nw) {
-        const int b = __ffs(nw) - 1;
-        nw &= nw - 1u;
-        const int s = s0 + 32 * lane + b;
-        const int I = s / kT, rl = s % kT;
-        if (I > J) continue;
-        const int64_t t = tri_index(I, J, nb);
-        if (t < t0 || t >= t1) continue;
-        if (HB == 0) {
-            // raw nibble (row parity); both nibbles of a byte belong to sources
-            // s, s^1 = bits of this lane's word, so no other thread writes the byte
-            uint8_t* p = D + sym_offset(t - t0, rl, cl, 0);
-            *p = (uint8_t)(*p | (level << (4 * (rl & 1))));
-        } else {
-            D[sym_offset(t - t0, rl, cl, HB)] = (uint8_t)level;
-            if (HB == 2) D[sym_offset(t - t0, rl, cl, HB) + 1] = (uint8_t)(level >> 8);
+}
+
+// Batch rows [s0, s0 + 1024) into the local triangle tiles: CTA per tile (I, J)
+// of the batch's row blocks; thread (ty, tx) gathers the 8 x 8 cells of its
+// sub-block (rows = batch sources, columns = vertices) from bbuf (8 or 16 bytes
+// per column, contiguous) and stores its 16-byte chunks.
+template <int HB>
+__global__ void __launch_bounds__(256) k_bfs_retile(const uint8_t* __restrict__ bbuf, uint8_t* __restrict__ D, int n,
+                                                    int s0, int nb, int64_t t0, int64_t t1, int I0, int nI)
+{
+    const int tid = threadIdx.x, ty = tid & 15, tx = tid >> 4;
+    // tile index within the batch: row block I = I0 + bI, J = I .. nb-1
+    int64_t q = blockIdx.x;
+    int bI = 0;
+    while (bI < nI && q >= nb - (I0 + bI)) {
+        q -= nb - (I0 + bI);
+        ++bI;
+    }
+    if (bI >= nI) return;
+    const int I = I0 + bI, J = I + (int)q;
+    const int64_t t = tri_index(I, J, nb);
+    if (t < t0 || t >= t1) return;
+    const int k0 = I * kT + ty * 8 - s0;  // first batch source (row) of the sub-block
+    uint8_t* tile = D + (size_t)(t - t0) * (size_t)tile_bytes(HB);
+    constexpr int RB = bfs_row_bytes<HB>();
+    if (HB == 0) {
+#pragma unroll
+        for (int kc = 0; kc < 2; ++kc) {
+            uint32_t w[4];
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+                const int v = J * kT + tx * 8 + kc * 4 + cc;
+                w[cc] = v < n ? *reinterpret_cast<const uint32_t*>(bbuf + (int64_t)v * RB + k0 / 2) : 0u;
+            }
+            *reinterpret_cast<uint4*>(tile + ((size_t)kc * 256 + tid) * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+    } else if (HB == 1) {
+#pragma unroll
+        for (int kc = 0; kc < 4; ++kc) {
+            uint2 a = make_uint2(0u, 0u), b = make_uint2(0u, 0u);
+            const int v0 = J * kT + tx * 8 + kc * 2;
+            if (v0 < n) a = *reinterpret_cast<const uint2*>(bbuf + (int64_t)v0 * RB + k0);
+            if (v0 + 1 < n) b = *reinterpret_cast<const uint2*>(bbuf + (int64_t)(v0 + 1) * RB + k0);
+            *reinterpret_cast<uint4*>(tile + ((size_t)kc * 256 + tid) * 16) = make_uint4(a.x, a.y, b.x, b.y);
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const int v = J * kT + tx * 8 + c;
+            uint4 a = make_uint4(0u, 0u, 0u, 0u);
+            if (v < n) a = *reinterpret_cast<const uint4*>(bbuf + (int64_t)v * RB + 2 * k0);
+            *reinterpret_cast<uint4*>(tile + ((size_t)c * 256 + tid) * 16) = a;
         }
     }
 }
 
 cudaError_t launch_bfs_level_sym(const int64_t* row_ptr, const int32_t* col, const uint32_t* fin, uint32_t* fout,
-                                 uint32_t* visited, uint8_t* D, int n, int s0, int nsrc, int level, int nb, int64_t t0,
-                                 int64_t t1, int hb, unsigned int* anynew, cudaStream_t s)
+                                 uint32_t* visited, uint8_t* bbuf, int n, int nsrc, int level, int hb,
+                                 unsigned int* anynew, cudaStream_t s)
 {
     const int64_t threads = (int64_t)n * 32;
     const unsigned grid = (unsigned)((threads + 255) / 256);
     if (hb == 0)
-        k_bfs_level_sym<0><<<grid, 256, 0, s>>>(row_ptr, col, fin, fout, visited, D, n, s0, nsrc, level, nb, t0, t1,
-                                                anynew);
+        k_bfs_level_sym<0><<<grid, 256, 0, s>>>(row_ptr, col, fin, fout, visited, bbuf, n, nsrc, level, anynew);
     else if (hb == 1)
-        k_bfs_level_sym<1><<<grid, 256, 0, s>>>(row_ptr, col, fin, fout, visited, D, n, s0, nsrc, level, nb, t0, t1,
-                                                anynew);
+        k_bfs_level_sym<1><<<grid, 256, 0, s>>>(row_ptr, col, fin, fout, visited, bbuf, n, nsrc, level, anynew);
     else
-        k_bfs_level_sym<2><<<grid, 256, 0, s>>>(row_ptr, col, fin, fout, visited, D, n, s0, nsrc, level, nb, t0, t1,
-                                                anynew);
+        k_bfs_level_sym<2><<<grid, 256, 0, s>>>(row_ptr, col, fin, fout, visited, bbuf, n, nsrc, level, anynew);
     return cudaGetLastError();
 }
+
+cudaError_t launch_bfs_retile(const uint8_t* bbuf, uint8_t* D, int n, int s0, int nsrc, int nb, int64_t t0,
+                              int64_t t1, int hb, cudaStream_t s)
+{
+    const int I0 = s0 / kT, nI = (nsrc + kT - 1) / kT;
+    int64_t ntile = 0;
+    for (int b = 0; b < nI; ++b) ntile += nb - (I0 + b);
+    if (ntile <= 0) return cudaSuccess;
+    if (hb == 0)
+        k_bfs_retile<0><<<(unsigned)ntile, 256, 0, s>>>(bbuf, D, n, s0, nb, t0, t1, I0, nI);
+    else if (hb == 1)
+        k_bfs_retile<1><<<(unsigned)ntile, 256, 0, s>>>(bbuf, D, n, s0, nb, t0, t1, I0, nI);
+    else
+        k_bfs_retile<2><<<(unsigned)ntile, 256, 0, s>>>(bbuf, D, n, s0, nb, t0, t1, I0, nI);
+    return cudaGetLastError();
+}
+
+int bfs_row_bytes_host(int hb) { return hb == 0 ? bfs_row_bytes<0>() : (hb == 1 ? bfs_row_bytes<1>() : bfs_row_bytes<2>()); }
 
 // ------------------------------------------------ weighted APSP (NEXT-3 setup)
 // Multi-source Bellman-Ford in fp64: dist[v * S + s] = shortest path length
