@@ -155,6 +155,7 @@ struct fdl_ctx {
     int nb = 0;              // vertex blocks of kT
     int64_t npad = 0;        // nb * kT
     int64_t t0 = 0, t1 = 0;  // local tile range [t0, t1) in triangle order
+    int Ilo = 0, Ihi = -1;   // row blocks of the local tiles
     int nitems = 0;
     uint64_t local_pairs = 0;  // unordered pairs in the local tiles
     int diameter = 0;
@@ -504,7 +505,8 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
         ctx->stats.p2_pairs += ctx->local_pairs;
     }
     if (ctx->world == 1 || ctx->emulated) {
-        FDL_LAUNCH(launch_sym_reduce(ctx->ipart, ctx->jpart, ctx->it_lo, ctx->it_hi, ctx->nb, ctx->t0, ctx->t1, C, D0,
+        FDL_LAUNCH(launch_sym_reduce(ctx->ipart, ctx->jpart, ctx->it_lo, ctx->it_hi, ctx->nb, ctx->t0, ctx->t1,
+                                     ctx->Ilo, ctx->Ihi, C, D0,
                                      inter, out0, out1, ctx->stream));
         if (mode == kSymP2 && p2_finish)  // product form: L^W p = diag p - sum_j w p_j (rank-local diag when emulated)
             FDL_LAUNCH(launch_p2_finish(out0, pos, ctx->diag, ctx->n, dim, ps_p2(dim), ctx->stream));
@@ -516,7 +518,8 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
     }
     const size_t slice = (size_t)ctx->npad * C;
     double* mine = ctx->rparts + (size_t)ctx->rank * slice;
-    FDL_LAUNCH(launch_sym_reduce(ctx->ipart, ctx->jpart, ctx->it_lo, ctx->it_hi, ctx->nb, ctx->t0, ctx->t1, C, C, 0,
+    FDL_LAUNCH(launch_sym_reduce(ctx->ipart, ctx->jpart, ctx->it_lo, ctx->it_hi, ctx->nb, ctx->t0, ctx->t1, ctx->Ilo,
+                                 ctx->Ihi, C, C, 0,
                                  mine, nullptr, ctx->stream));
     FDL_TRY(allgather_inplace(ctx, ctx->rparts, slice, ncclFloat64, 8));
     FDL_LAUNCH(launch_rank_sum(ctx->rparts, ctx->world, ctx->npad, C, D0, inter, out0, out1, ctx->stream));
@@ -903,6 +906,13 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     ctx->nb = (n + kT - 1) / kT;
     ctx->npad = (int64_t)ctx->nb * kT;
     fdl_shard_tiles(n, world, rank, &ctx->t0, &ctx->t1);
+    if (ctx->t1 > ctx->t0) {
+        int64_t a, b;
+        tri_coords(ctx->t0, ctx->nb, a, b);
+        ctx->Ilo = (int)a;
+        tri_coords(ctx->t1 - 1, ctx->nb, a, b);
+        ctx->Ihi = (int)a;
+    }
     std::vector<int4> items;
     std::vector<int> lo, hi;
     build_items(ctx, items, lo, hi);

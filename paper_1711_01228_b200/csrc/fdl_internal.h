@@ -175,9 +175,10 @@ struct EnumOmegas {
 };
 cudaError_t launch_enum(const SymArgs& a, const EnumOmegas& w, int dim, int hb, int grid, cudaStream_t s);
 int sym_max_ctas(int mode, int dim, int nsets, int hb);
+// Ilo..Ihi: row blocks of the local tiles [t0, t1)
 cudaError_t launch_sym_reduce(const float* ipart, const float* jpart, const int* it_lo, const int* it_hi, int nb,
-                              int64_t t0, int64_t t1, int C, int D, int inter, double* out0, double* out1,
-                              cudaStream_t s);
+                              int64_t t0, int64_t t1, int Ilo, int Ihi, int C, int D, int inter, double* out0,
+                              double* out1, cudaStream_t s);
 // scratch: sym_stress_chunks(nitems) * nsets doubles
 int sym_stress_chunks(int nitems);
 cudaError_t launch_sym_stress(const double* spart, int nitems, int nsets, double* out, double* scratch,

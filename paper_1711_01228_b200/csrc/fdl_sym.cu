@@ -1057,8 +1057,8 @@ __global__ void __launch_bounds__(kRedGroups * kT) k_sym_reduce(const float* __r
                                                                 const float* __restrict__ jpart,
                                                                 const int* __restrict__ it_lo,
                                                                 const int* __restrict__ it_hi, int nb, int64_t t0,
-                                                                int64_t t1, int D, int inter, double* out0,
-                                                                double* out1)
+                                                                int64_t t1, int Ilo, int Ihi, int D, int inter,
+                                                                double* out0, double* out1)
 {
     __shared__ double gsum[kRedGroups][kT][C];
     const int B = nb - 1 - (int)blockIdx.x;
@@ -1066,8 +1066,11 @@ __global__ void __launch_bounds__(kRedGroups * kT) k_sym_reduce(const float* __r
     double acc[C];
 #pragma unroll
     for (int v = 0; v < C; ++v) acc[v] = 0.0;
+    // only the local row blocks [Ilo, Ihi] (the rank's tile range); group g keeps I = g mod 8
+    const int Ifirst = Ilo + ((g - Ilo) % kRedGroups + kRedGroups) % kRedGroups;
+    const int Ilast = min(B, Ihi);
 #pragma unroll 4
-    for (int I = g; I <= B; I += kRedGroups) {
+    for (int I = Ifirst; I <= Ilast; I += kRedGroups) {
         const int64_t t = tri_index(I, B, nb);
         if (t < t0 || t >= t1) continue;
         const float* src = jpart + ((size_t)(t - t0) * kT + r) * C;
@@ -1104,13 +1107,13 @@ __global__ void __launch_bounds__(kRedGroups * kT) k_sym_reduce(const float* __r
 }
 
 cudaError_t launch_sym_reduce(const float* ipart, const float* jpart, const int* it_lo, const int* it_hi, int nb,
-                              int64_t t0, int64_t t1, int C, int D, int inter, double* out0, double* out1,
-                              cudaStream_t s)
+                              int64_t t0, int64_t t1, int Ilo, int Ihi, int C, int D, int inter, double* out0,
+                              double* out1, cudaStream_t s)
 {
 #define FDL_RED_CASE(C_)                                                                                        \
     if (C == C_) {                                                                                              \
-        k_sym_reduce<C_><<<nb, kRedGroups * kT, 0, s>>>(ipart, jpart, it_lo, it_hi, nb, t0, t1, D, inter, out0, \
-                                                        out1);                                                 \
+        k_sym_reduce<C_><<<nb, kRedGroups * kT, 0, s>>>(ipart, jpart, it_lo, it_hi, nb, t0, t1, Ilo, Ihi, D, inter, \
+                                                        out0, out1);                                           \
         return cudaGetLastError();                                                                              \
     }
     FDL_RED_CASE(1) FDL_RED_CASE(2) FDL_RED_CASE(3) FDL_RED_CASE(4) FDL_RED_CASE(6)
