@@ -204,7 +204,10 @@ fdl_status fdl_create(int32_t n, const int64_t* row_ptr, const int32_t* col_idx,
  * (positions, forces, PCG vectors) replicated.  After each pair pass the
  * per-rank partial sums are all-gathered over NCCL and summed in rank order,
  * so all ranks hold identical state.  Every rank must pass identical graph,
- * parameters and init_pos. */
+ * parameters and init_pos.  world = 1 with a non-NULL id runs the same
+ * distributed path through a one-rank communicator (results identical to
+ * fdl_create's; steps are launched eagerly, not as CUDA graphs).  The
+ * enumerating strategy is single-GPU only (FDL_E_UNSUPPORTED here). */
 fdl_status fdl_create_sharded(int32_t n, const int64_t* row_ptr, const int32_t* col_idx,
                               const double* edge_len, const fdl_params* p,
                               const double* init_pos, const uint8_t* nccl_unique_id,

@@ -227,6 +227,7 @@ struct fdl_ctx {
     cudaStream_t aux_stream = nullptr;
     std::map<std::tuple<int, int, int, double>, StepGraph> graphs;
     bool emulated = false;  // world > 1 without communicator (fdl_eval_partial only)
+    bool distributed = false;  // partials exchanged through comm or group (any world, incl. 1)
 };
 
 namespace {
@@ -432,7 +433,7 @@ void collect_events(fdl_ctx* ctx)
 // rank * slice_elems) of `buf` in place.
 fdl_status allgather_inplace(fdl_ctx* ctx, void* buf, size_t slice_elems, int nccl_type, size_t esize)
 {
-    if (ctx->world == 1 || ctx->emulated) return FDL_OK;
+    if (!ctx->distributed) return FDL_OK;
     char* base = static_cast<char*>(buf);
     if (ctx->group) {
         fdl_group& G = *ctx->group;
@@ -504,7 +505,7 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
         ctx->stats.p2_launches++;
         ctx->stats.p2_pairs += ctx->local_pairs;
     }
-    if (ctx->world == 1 || ctx->emulated) {
+    if (!ctx->distributed) {
         FDL_LAUNCH(launch_sym_reduce(ctx->ipart, ctx->jpart, ctx->it_lo, ctx->it_hi, ctx->nb, ctx->t0, ctx->t1,
                                      ctx->Ilo, ctx->Ihi, C, D0,
                                      inter, out0, out1, ctx->stream));
@@ -669,7 +670,7 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
     cudaFree(fb);
     cudaFree(vis);
     if (st != FDL_OK) return st;
-    if (ctx->world > 1 && !ctx->emulated) {
+    if (ctx->distributed) {
         // every rank BFSed only its sources: agree on the diameter and hop width (max over ranks)
         int* dd = nullptr;
         FDL_CUDA(cudaMalloc(&dd, sizeof(int) * 2 * ctx->world));
@@ -892,7 +893,9 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     ctx->stream = ctx->own_stream;
 
     ctx->emulated = world > 1 && nccl_id == nullptr && ctx->group == nullptr;
-    if (world > 1 && !ctx->emulated && !ctx->group) {
+    // A communicator is made whenever an id is given, also for world = 1 (a one-rank NCCL
+    // run of the distributed path: exercises the NCCL calls on a single GPU).
+    if (nccl_id != nullptr && !ctx->group) {
         if (!g_nccl.load(msg)) return set_err(ctx, FDL_E_NCCL, msg);
         ncclUniqueId id;
         memcpy(id.internal, nccl_id, 128);
@@ -901,6 +904,7 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
             return set_err(ctx, FDL_E_NCCL, std::string("ncclCommInitRank: ") +
                                                  (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
     }
+    ctx->distributed = ctx->comm != nullptr || ctx->group != nullptr;
 
     // ---- geometry: tiles of kT x kT, this rank's share of the triangle
     ctx->nb = (n + kT - 1) / kT;
@@ -938,11 +942,12 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     FDL_ALLOC(ctx->sparts, (size_t)2 * world);
     FDL_ALLOC(ctx->stress_scratch, (size_t)sym_stress_chunks(std::max(ctx->nitems, 1) * 8) * kEnumNC);
     if (p.strategy == FDL_STRAT_ENUM) {
-        if (world > 1) return set_err(ctx, FDL_E_UNSUPPORTED, "the enumerating strategy runs on one GPU");
+        if (world > 1 || ctx->distributed)
+            return set_err(ctx, FDL_E_UNSUPPORTED, "the enumerating strategy runs on one GPU");
         FDL_ALLOC(ctx->spart_enum, (size_t)std::max(ctx->nitems, 1) * kEnumNC);
         FDL_ALLOC(ctx->enum_f, (size_t)kEnumMax);
     }
-    if (world > 1 && !ctx->emulated) FDL_ALLOC(ctx->rparts, (size_t)world * ctx->npad * Cmax);
+    if (ctx->distributed) FDL_ALLOC(ctx->rparts, (size_t)world * ctx->npad * Cmax);
     FDL_ALLOC(ctx->diag, (size_t)ctx->npad);
     FDL_ALLOC(ctx->Xk, vn);
     FDL_ALLOC(ctx->Xn, vn);
@@ -989,7 +994,7 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     ctx->grid_enum = std::max(1, std::min(cap_items, ctx->sm_count * 2));
     ctx->grid_p1s = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymP1S, dim, 2, ctx->hb)));
     // large problems: the extra host sync of the split P1 is negligible against the pass
-    ctx->use_graphs = ctx->p.use_graphs == 1 || (ctx->p.use_graphs < 0 && world == 1 && (int64_t)n * n < (int64_t)1 << 30);
+    ctx->use_graphs = ctx->p.use_graphs == 1 || (ctx->p.use_graphs < 0 && !ctx->distributed && (int64_t)n * n < (int64_t)1 << 30);
     ctx->p1_split = !ctx->general &&
                     (ctx->p.p1_split == 1 || (ctx->p.p1_split < 0 && (int64_t)n * n >= (int64_t)1 << 30));
     // Jacobi diagonal sum_{j != i} w'_ij (one symmetric DIAG pass) and sigma = mean(diag)/n
@@ -1281,7 +1286,7 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
     int cg = 0;
     // graph mode: one launch per step; not with a host decision inside the step
     // (split line 6, enumeration) or host-side exchanges (several ranks)
-    bool graph = ctx->use_graphs && !enumerate && !(nsets == 2 && ctx->p1_split) && ctx->world == 1 &&
+    bool graph = ctx->use_graphs && !enumerate && !(nsets == 2 && ctx->p1_split) && !ctx->distributed &&
                  ctx->steps_eager > 0;
     const auto key = std::make_tuple((int)refresh, nsets, (int)ctx->ext_ok, omega);
     auto it = ctx->graphs.find(key);

@@ -227,11 +227,12 @@ class Layout:
         if group is not None:
             st = lib.fdl_create_loopback(self.n, _ptr(self._rp), _ptr(self._col), _ptr(self._len),
                                          ctypes.byref(self.params), _ptr(X0), group._h, rank, ctypes.byref(self._h))
-        elif world == 1:
+        elif world == 1 and nccl_id is None:
             st = lib.fdl_create(self.n, _ptr(self._rp), _ptr(self._col), _ptr(self._len), ctypes.byref(self.params),
                                 _ptr(X0), ctypes.byref(self._h))
         else:
-            # nccl_id None -> emulated rank (test hook: fdl_eval_partial only)
+            # nccl_id None -> emulated rank (test hook: fdl_eval_partial only);
+            # world 1 with an id -> one-rank communicator
             idbuf = None if nccl_id is None else (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
             st = lib.fdl_create_sharded(self.n, _ptr(self._rp), _ptr(self._col), _ptr(self._len),
                                         ctypes.byref(self.params),

@@ -612,6 +612,31 @@ def test_nccl_loads_and_makes_unique_id():
     assert len(uid) == 128 and any(uid)
 
 
+@pytest.mark.parametrize("name,dim", [("C2", 2), ("C3", 3)])
+def test_nccl_one_rank_bitwise(name, dim):
+    """The distributed path over a real NCCL communicator with one rank
+    (ncclCommInitRank + ncclAllGather of the row and stress partials, rank-order
+    sums) on the single GPU available: bitwise the single-GPU trajectory."""
+    import torch  # noqa: F401
+    cfg = configs.CONFIGS[name]
+    g = configs.graph_for(name)
+    X0 = graphs.init_positions(g.n, dim, 6)
+    p = fdl.make_params(dim=dim, k=cfg.k_for(g.n), omega=1.5, tol=cfg.tol, max_iter=cfg.max_iter)
+    out = []
+    for nid in (None, fdl.nccl_unique_id()):
+        kw = {} if nid is None else {"nccl_id": nid, "rank": 0, "world": 1}
+        with fdl.Layout.from_graph(g, params=p, init_pos=X0, **kw) as L:
+            fs = []
+            for _ in range(10):
+                info = L.step()
+                fs.append((info.f_after, info.accepted, info.cg_iters))
+                if info.stop:
+                    break
+            out.append((fs, L.get_positions()))
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1])
+
+
 @pytest.mark.parametrize("name,omega,strategy", [("C1", 1.5, 0), ("C2", 1.9, 0), ("C3", 1.5, 0), ("C1", 0.0, 0),
                                                  ("C2", 1.5, 1)])
 def test_graph_steps_bitwise(name, omega, strategy):
