@@ -98,9 +98,12 @@ typedef struct {
     int32_t hop_bits;     /* minimum stored hop width: 0 = auto (narrowest that holds the diameter:
                              4 bits if diam <= 15, 8 if <= 255, else 16), or 4, 8, 16. The decoded
                              hop, hence every result, is the same for every width   */
-    int32_t cg_extrap;    /* 1 (default): start PCG from X^k + rho (X^k - X^{k-1}) with rho the
-                             previous step's least-squares ratio of successive corrections
-                             (DESIGN R23); 0: start from X^k. Same minimiser either way */
+    int32_t cg_extrap;    /* PCG start.  2 (default): X^k + V y, the Galerkin (A-norm optimal)
+                             correction over the last cg_history step differences V, L^W V from the
+                             carried products (DESIGN R27); 1: X^k + rho (X^k - X^{k-1}) with
+                             rho the previous step's least-squares ratio of successive
+                             corrections (R23); 0: X^k.  The solve runs to cg_rtol
+                             from any of them: same minimiser, different PCG counts */
     int32_t enum_count;   /* FDL_STRAT_ENUM candidates, 1..32 (default 19)                     */
     double enum_step;     /* FDL_STRAT_ENUM candidate spacing > 0 (default 0.5)                */
     int32_t p1_split;     /* line 6 pass over {X^{k+1}, Xt}: 1 = stresses of both + R(Xt) only, with a
@@ -112,6 +115,8 @@ typedef struct {
                              sync per PCG iteration; -1 (default): 1 on one GPU when the split
                              line-6 pass is off (n^2 < 2^30). Same results either way (bitwise).
                              With graphs the stats time whole steps only (p1_ms = p2_ms = 0)     */
+    int32_t cg_history;   /* cg_extrap = 2: step differences kept for the start, 1..8 (0 = default 2;
+                             more vectors cut PCG counts a little further, DESIGN R27)           */
 } fdl_params;
 
 typedef struct {

@@ -179,6 +179,8 @@ struct fdl_ctx {
     double *cr = nullptr, *cz = nullptr, *cp = nullptr, *cy = nullptr;
     double *Ak = nullptr, *An = nullptr, *At = nullptr;  // carried L^W X^k, L^W X^{k+1}, L^W Xt
     double *Xprev = nullptr, *Aprev = nullptr;           // X^{k-1}, L^W X^{k-1} (PCG start extrapolation)
+    double *Vh = nullptr, *AVh = nullptr;               // recycled start (R27): kGalMax step differences, L^W of them
+    double* blk_gal = nullptr;                          // ... block partials of its Gram systems
     double* spart_enum = nullptr;  // [item][kEnumNC] enumerating-strategy stress partials
     double* enum_f = nullptr;      // [kEnumMax] candidate stresses
     double* omega_v = nullptr;   // per-vertex relax factors (fdl_set_omega_vertex), device
@@ -555,6 +557,8 @@ fdl_status upload_positions(fdl_ctx* ctx, const double* X)
 {
     ctx->a_valid = false;
     ctx->ext_ok = false;
+    // the step history of the recycled start belongs to the old placement
+    FDL_CUDA(cudaMemsetAsync(&ctx->sc->gal_cnt, 0, sizeof(int), ctx->stream));
     std::vector<double> loc((size_t)ctx->n * ctx->dim);
     for (int i = 0; i < ctx->n; ++i)
         for (int q = 0; q < ctx->dim; ++q) {
@@ -807,6 +811,14 @@ fdl_status check_params(const fdl_params* p, std::string& msg)
             return FDL_E_UNSUPPORTED;
         }
     }
+    if (p->cg_extrap < 0 || p->cg_extrap > 2) {
+        msg = "cg_extrap must be 0, 1 or 2";
+        return FDL_E_INVALID_ARG;
+    }
+    if (p->cg_history < 0 || p->cg_history > kGalMax) {
+        msg = "cg_history must be in 0..8";
+        return FDL_E_INVALID_ARG;
+    }
     if (p->strategy != FDL_STRAT_FIXED && p->strategy != FDL_STRAT_PROB && p->strategy != FDL_STRAT_ENUM) {
         msg = "unknown strategy";
         return FDL_E_INVALID_ARG;
@@ -882,6 +894,7 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
         return set_err(ctx, FDL_E_UNSUPPORTED, "the enumerating strategy needs unit lengths and alpha = -2");
     ctx->cap = std::isfinite(p.step) ? p.step / ctx->k : INFINITY;
     if (!(p.cg_rtol > 0)) ctx->p.cg_rtol = std::max(1e-2 * p.tol, 1e-9);
+    if (p.cg_history == 0) ctx->p.cg_history = 2;
     if (p.cg_max_iter <= 0) ctx->p.cg_max_iter = std::min(10 * n, 10000);
     if (p.a_refresh <= 0) ctx->p.a_refresh = 10;
     if (std::isfinite(p.step)) ctx->p.a_refresh = 1;  // the cap makes Xt non-linear in X^{k+1}
@@ -964,6 +977,16 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     FDL_ALLOC(ctx->At, vn);
     FDL_ALLOC(ctx->Xprev, vn);
     FDL_ALLOC(ctx->Aprev, vn);
+    if (ctx->p.cg_extrap == 2) {
+        const int m = ctx->p.cg_history;
+        FDL_ALLOC(ctx->Vh, (size_t)m * vn);
+        FDL_ALLOC(ctx->AVh, (size_t)m * vn);
+        FDL_ALLOC(ctx->blk_gal, (size_t)3 * kGalNV * ctx->nblk);
+        FDL_CUDA(cudaMemsetAsync(ctx->Vh, 0, (size_t)m * vn * sizeof(double), ctx->stream));
+        FDL_CUDA(cudaMemsetAsync(ctx->AVh, 0, (size_t)m * vn * sizeof(double), ctx->stream));
+        FDL_CUDA(cudaMemcpyAsync(&ctx->sc->gal_m, &m, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+        FDL_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
     FDL_ALLOC(ctx->posf, (size_t)ctx->npad * 8);
     FDL_ALLOC(ctx->pvec, (size_t)ctx->npad * 4);
     FDL_ALLOC(ctx->blk_max, (size_t)ctx->nblk);
@@ -1039,6 +1062,9 @@ struct StepShape {
     double omega;
 };
 
+// every step refreshes L^W X^k: Xt is then not a scalar combination of carried products
+bool always_refresh(const fdl_ctx* ctx) { return ctx->p.a_refresh <= 1 || ctx->omega_v != nullptr; }
+
 // line 4, start: L^W X^k (carried or a refresh pass), PCG start and first residual
 fdl_status enqueue_prologue(fdl_ctx* ctx, const StepShape& sh, unsigned long long cond)
 {
@@ -1048,9 +1074,23 @@ fdl_status enqueue_prologue(fdl_ctx* ctx, const StepShape& sh, unsigned long lon
     FDL_LAUNCH2(launch_cg_begin(ctx->Xk, ctx->Xn, ctx->pvec, n, 0, dim, pq, ctx->sc, s));
     if (refresh) FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->Ak, nullptr, 0));
     const double* y0 = ctx->Ak;
-    if (ctx->p.cg_extrap) {  // extrapolated start (R23): x0 into Xn, L^W x0 into cy
+    if (ctx->p.cg_extrap == 2) {  // recycled start (R27): x0 into Xn, L^W x0 into cy
+        // history when every step refreshes A^k (per-vertex omega, step cap, a_refresh = 1):
+        // the last step's X^k - X^{k-1} with the difference of the two fresh products
+        // (Xprev/Aprev were set by k_rho at the end of the last step)
+        if (ctx->ext_ok && always_refresh(ctx))
+            FDL_LAUNCH(launch_gal_push(ctx->Xk, ctx->Xprev, ctx->Ak, ctx->Aprev, ctx->Vh, ctx->AVh, n, dim,
+                                       ctx->p.cg_history, s));
+        FDL_LAUNCH(launch_gal_start(ctx->Vh, ctx->AVh, ctx->Rk, ctx->Xk, ctx->Ak, ctx->Xn, ctx->cy, ctx->blk_gal,
+                                    ctx->nblk, ctx->sc, n, dim, s));
+        ctx->stats.launches += 2;
+        y0 = ctx->cy;
+    } else if (ctx->p.cg_extrap) {  // extrapolated start (R23): x0 into Xn, L^W x0 into cy
+        // not right after a refresh of carried products: A^k - A^{k-1} would then hold the
+        // whole accumulated drift of A^{k-1}, and the start would feed it back (x0 = X^k there)
+        const bool ok = ctx->ext_ok && (!refresh || always_refresh(ctx));
         FDL_LAUNCH(launch_extrap(ctx->Xk, ctx->Xprev, ctx->Ak, ctx->Aprev, ctx->Xn, ctx->cy, ctx->sc, n, dim,
-                                 ctx->ext_ok ? 1 : 0, s));
+                                 ok ? 1 : 0, s));
         y0 = ctx->cy;
     }
     FDL_LAUNCH(launch_cg_init(y0, ctx->Rk, ctx->diag, ctx->cr, ctx->cz, ctx->cp, ctx->pvec, ctx->blk_cg, ctx->nblk,
@@ -1154,6 +1194,13 @@ fdl_status enqueue_epilogue(fdl_ctx* ctx, const StepShape& sh)
         FDL_LAUNCH(launch_select(ctx->Xk, ctx->Rk, ctx->Xn, ctx->Xt, ctx->R1, ctx->R2, ctx->blk_max, n, dim, nsets,
                                  ctx->sc, ctx->Ak, ctx->An, ctx->At, s));
     }
+    // history with carried products: X^{k+1} - X^k and A^{k+1} - A^k, both from this step
+    // (A^{k+1} - A^k = L^W (x0 - X^k) + sum alpha L^W p algebraically, (1 + w) times that
+    // for Xt: no carried drift enters the history; a difference against a refreshed A^k
+    // would bring the whole accumulated drift in and feed it back through the start)
+    if (ctx->p.cg_extrap == 2 && !always_refresh(ctx))
+        FDL_LAUNCH(launch_gal_push(ctx->Xk, ctx->Xprev, ctx->Ak, ctx->Aprev, ctx->Vh, ctx->AVh, n, dim,
+                                       ctx->p.cg_history, s));
     return FDL_OK;
 }
 
@@ -1418,11 +1465,12 @@ void fdl_params_default(fdl_params* p)
     p->device = 0;
     p->a_refresh = 10;
     p->hop_bits = 0;
-    p->cg_extrap = 1;
+    p->cg_extrap = 2;
     p->enum_count = 19;
     p->enum_step = 0.5;
     p->p1_split = -1;
     p->use_graphs = -1;
+    p->cg_history = 0;
 }
 
 const char* fdl_status_str(fdl_status s)

@@ -21,6 +21,8 @@ __host__ __device__ inline int64_t stage_slot(int64_t v)
 
 // ------------------------------------------------------------ constants
 constexpr int kRB = 256;           // row block of all fp64 vector reductions
+constexpr int kGalMax = 8;         // history window of the recycled PCG start (R27)
+constexpr int kGalNV = kGalMax * (kGalMax + 1) / 2 + kGalMax;  // Gram entries + right-hand sides per column
 constexpr int kBFSWords = 32;      // MS-BFS source batch = 32 words x 32 bits = 1024
 
 // Device-resident scalars of the iteration (one struct per context).
@@ -47,6 +49,12 @@ struct DevScalars {
     int cg_iters;
     double relres;
     unsigned int anynew;   // MS-BFS level flag
+    // recycled PCG start (R27): y of x0 = X^k + V y per column, basis vectors in use
+    double gal_y[3][8];
+    int gal_cnt;           // valid history vectors for the next start (<= kGalMax)
+    int gal_use;           // vectors used by the current start
+    int gal_dropped;       // dependent vectors skipped by the last solve
+    int gal_m;             // window (fdl_params.cg_history, <= kGalMax)
 };
 
 // Host-mapped flag the host reads after a stream sync.
@@ -70,6 +78,14 @@ cudaError_t launch_carry_a(const double* Rk, const double* rcg, const double* Ak
                            const DevScalars* sc, int n, int dim, double omega, cudaStream_t s);
 cudaError_t launch_extrap(const double* Xk, const double* Xprev, const double* Ak, const double* Aprev, double* x,
                           double* y0, const DevScalars* sc, int n, int dim, int valid, cudaStream_t s);
+// Recycled PCG start (R27): Galerkin projection of the warm-start error onto the
+// last kGalMax step differences V (with AV = L^W V from the carried products).
+cudaError_t launch_gal_start(const double* V, const double* AV, const double* b, const double* Xk, const double* Ak,
+                             double* x, double* y0, double* blk, int nblk, DevScalars* sc, int n, int dim,
+                             cudaStream_t s);
+// V <- [X^k - X^{k-1}, V[0..m-2]], AV likewise (m = window)
+cudaError_t launch_gal_push(const double* Xk, const double* Xprev, const double* Ak, const double* Aprev, double* V,
+                            double* AV, int n, int dim, int m, cudaStream_t s);
 cudaError_t launch_rho(const double* Xn, const double* Xk, double* Xprev, const double* Ak, double* Aprev,
                        double* blk, int n, int dim, int valid, DevScalars* sc, cudaStream_t s);
 cudaError_t launch_enum_stage(const double* Xk, double* Xn, float* posf, double* blk_max, const double* xpin, int n,

@@ -389,6 +389,190 @@ cudaError_t launch_rho(const double* Xn, const double* Xk, double* Xprev, const 
     return cudaGetLastError();
 }
 
+// ------------------------------------------------ recycled PCG start (R27)
+// L^W is the same matrix at every step, so the directions the run already took
+// carry over: the start is the Galerkin (A-norm optimal) correction of X^k over
+// the span of the last m step differences v_s = X^{j+1} - X^j, whose products
+// L^W v_s are differences of the carried L^W X (no extra pair pass):
+//   x0 = X^k + V y,  L^W x0 = A^k + (AV) y,  (V^T AV) y = V^T (b - A^k),  per column.
+// The solve still runs to cg_rtol from there: only the start changes.
+constexpr int kGalNG = kGalMax * (kGalMax + 1) / 2;  // upper-triangle Gram entries (kGalNV: + right-hand sides)
+
+__device__ __forceinline__ double warp_sum_d(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// block partials of G_st = (v_s.av_t + v_t.av_s)/2 (s <= t) and v_s.r, r = b - A^k
+__global__ void __launch_bounds__(kRB) k_gal_partial(const double* __restrict__ V, const double* __restrict__ AV,
+                                                     const double* __restrict__ b, const double* __restrict__ Ak,
+                                                     double* blk, int n, int dim, int nblk,
+                                                     const DevScalars* __restrict__ sc)
+{
+    __shared__ double red[kRB / 32][3 * kGalNV];
+    const int cnt = sc->gal_cnt;
+    if (cnt == 0) return;  // k_gal_solve does not read the partials
+    const int i = blockIdx.x * kRB + threadIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const size_t nd = (size_t)n * dim;
+    for (int c = 0; c < dim; ++c) {
+        const size_t k = (size_t)i * dim + c;
+        double v[kGalMax], av[kGalMax], r = 0.0;
+#pragma unroll
+        for (int q = 0; q < kGalMax; ++q) {
+            v[q] = (i < n && q < cnt) ? V[q * nd + k] : 0.0;
+            av[q] = (i < n && q < cnt) ? AV[q * nd + k] : 0.0;
+        }
+        if (i < n) r = b[k] - Ak[k];
+        int e = c * kGalNV;
+#pragma unroll
+        for (int q = 0; q < kGalMax; ++q)
+#pragma unroll
+            for (int t = q; t < kGalMax; ++t, ++e) {
+                double g = 0.0;
+                if (t < cnt) g = warp_sum_d(0.5 * (v[q] * av[t] + v[t] * av[q]));
+                if (lane == 0) red[w][e] = g;
+            }
+#pragma unroll
+        for (int q = 0; q < kGalMax; ++q, ++e) {
+            double g = 0.0;
+            if (q < cnt) g = warp_sum_d(v[q] * r);
+            if (lane == 0) red[w][e] = g;
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < dim * kGalNV; e += kRB) {
+        double t = 0.0;
+        for (int ww = 0; ww < kRB / 32; ++ww) t += red[ww][e];
+        blk[(size_t)e * nblk + blockIdx.x] = t;
+    }
+}
+
+// one block: fixed-order sums of the partials, then per column an LDL^T solve of
+// the cnt x cnt Gram system that skips dependent vectors (pivot below 1e-6 of
+// the vector's own A-norm: it adds nothing the earlier ones do not span).
+__global__ void __launch_bounds__(256) k_gal_solve(const double* __restrict__ blk, int nblk, int dim, DevScalars* sc)
+{
+    __shared__ double tot[3 * kGalNV];
+    const int cnt = sc->gal_cnt;
+    for (int e = threadIdx.x; e < dim * kGalNV && cnt > 0; e += blockDim.x) {
+        double t = 0.0;
+        for (int q = 0; q < nblk; ++q) t += blk[(size_t)e * nblk + q];
+        tot[e] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        const int c = threadIdx.x;
+        double y[kGalMax];
+        int dropped = 0;
+        for (int q = 0; q < kGalMax; ++q) y[q] = 0.0;
+        if (c < dim && cnt > 0) {
+            double G[kGalMax][kGalMax], L[kGalMax][kGalMax], D[kGalMax], z[kGalMax];
+            bool keep[kGalMax];
+            const double* T = tot + c * kGalNV;
+            int e = 0;
+            for (int q = 0; q < kGalMax; ++q)
+                for (int t = q; t < kGalMax; ++t, ++e) G[q][t] = G[t][q] = T[e];
+            for (int q = 0; q < cnt; ++q) {
+                double d = G[q][q];
+                for (int k = 0; k < q; ++k)
+                    if (keep[k]) d -= L[q][k] * L[q][k] * D[k];
+                keep[q] = G[q][q] > 0.0 && d > 1e-6 * G[q][q];
+                if (!keep[q]) {
+                    ++dropped;
+                    continue;
+                }
+                D[q] = d;
+                for (int t = q + 1; t < cnt; ++t) {
+                    double g = G[t][q];
+                    for (int k = 0; k < q; ++k)
+                        if (keep[k]) g -= L[t][k] * L[q][k] * D[k];
+                    L[t][q] = g / d;
+                }
+            }
+            for (int q = 0; q < cnt; ++q) {
+                if (!keep[q]) continue;
+                double v = T[kGalNG + q];
+                for (int k = 0; k < q; ++k)
+                    if (keep[k]) v -= L[q][k] * z[k];
+                z[q] = v;
+            }
+            for (int q = cnt - 1; q >= 0; --q) {
+                if (!keep[q]) continue;
+                double v = z[q] / D[q];
+                for (int t = q + 1; t < cnt; ++t)
+                    if (keep[t]) v -= L[t][q] * y[t];
+                y[q] = v;
+            }
+        }
+        for (int q = 0; q < kGalMax; ++q) sc->gal_y[c][q] = y[q];
+        if (c == 0) sc->gal_dropped = dropped;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        sc->gal_use = cnt;
+        sc->gal_cnt = cnt + 1 < sc->gal_m ? cnt + 1 : sc->gal_m;  // after the next step's push
+    }
+}
+
+__global__ void k_gal_apply(const double* __restrict__ V, const double* __restrict__ AV,
+                            const double* __restrict__ Xk, const double* __restrict__ Ak, double* x, double* y0,
+                            const DevScalars* __restrict__ sc, int n, int dim)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int use = sc->gal_use;
+    const size_t nd = (size_t)n * dim;
+    for (int c = 0; c < dim; ++c) {
+        const size_t k = (size_t)i * dim + c;
+        double xv = Xk[k], yv = Ak[k];
+        for (int q = 0; q < use; ++q) {
+            const double g = sc->gal_y[c][q];
+            xv += g * V[q * nd + k];
+            yv += g * AV[q * nd + k];
+        }
+        x[k] = xv;
+        y0[k] = yv;
+    }
+}
+
+cudaError_t launch_gal_start(const double* V, const double* AV, const double* b, const double* Xk, const double* Ak,
+                             double* x, double* y0, double* blk, int nblk, DevScalars* sc, int n, int dim,
+                             cudaStream_t s)
+{
+    k_gal_partial<<<nblk, kRB, 0, s>>>(V, AV, b, Ak, blk, n, dim, nblk, sc);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_gal_solve<<<1, 256, 0, s>>>(blk, nblk, dim, sc);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_gal_apply<<<(n + 255) / 256, 256, 0, s>>>(V, AV, Xk, Ak, x, y0, sc, n, dim);
+    return cudaGetLastError();
+}
+
+__global__ void k_gal_push(const double* __restrict__ Xk, const double* __restrict__ Xprev,
+                           const double* __restrict__ Ak, const double* __restrict__ Aprev, double* V, double* AV,
+                           size_t nd, int m)
+{
+    const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nd) return;
+    for (int q = m - 1; q > 0; --q) {
+        V[q * nd + k] = V[(q - 1) * nd + k];
+        AV[q * nd + k] = AV[(q - 1) * nd + k];
+    }
+    V[k] = Xk[k] - Xprev[k];
+    AV[k] = Ak[k] - Aprev[k];
+}
+
+cudaError_t launch_gal_push(const double* Xk, const double* Xprev, const double* Ak, const double* Aprev, double* V,
+                            double* AV, int n, int dim, int m, cudaStream_t s)
+{
+    const size_t nd = (size_t)n * dim;
+    k_gal_push<<<(unsigned)((nd + 255) / 256), 256, 0, s>>>(Xk, Xprev, Ak, Aprev, V, AV, nd, m);
+    return cudaGetLastError();
+}
+
 // column means of X (one block, fixed order) -> sc->cmean: the centring of the
 // staged P2 input (product form, k_p2_finish)
 __global__ void __launch_bounds__(1024) k_colmean(const double* __restrict__ X, int n, int dim, DevScalars* sc)

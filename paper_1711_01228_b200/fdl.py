@@ -50,7 +50,7 @@ class Params(ctypes.Structure):
         ("cg_max_iter", ctypes.c_int32), ("strategy", ctypes.c_int32), ("seed", ctypes.c_uint64),
         ("device", ctypes.c_int32), ("a_refresh", ctypes.c_int32), ("hop_bits", ctypes.c_int32),
         ("cg_extrap", ctypes.c_int32), ("enum_count", ctypes.c_int32), ("enum_step", ctypes.c_double),
-        ("p1_split", ctypes.c_int32), ("use_graphs", ctypes.c_int32),
+        ("p1_split", ctypes.c_int32), ("use_graphs", ctypes.c_int32), ("cg_history", ctypes.c_int32),
     ]
 
 
@@ -153,8 +153,8 @@ def params_default() -> Params:
 
 
 def make_params(dim=2, k=0.0, omega=1.5, step=math.inf, tol=1e-4, max_iter=500, cg_rtol=0.0,
-                cg_max_iter=0, strategy=STRAT_FIXED, seed=1, device=0, a_refresh=0, hop_bits=0, cg_extrap=1, enum_count=19, weight_exp=-2.0,
-                enum_step=0.5, p1_split=-1, use_graphs=-1) -> Params:
+                cg_max_iter=0, strategy=STRAT_FIXED, seed=1, device=0, a_refresh=0, hop_bits=0, cg_extrap=2, enum_count=19, weight_exp=-2.0,
+                enum_step=0.5, p1_split=-1, use_graphs=-1, cg_history=0) -> Params:
     p = params_default()
     p.dim, p.k, p.omega, p.step, p.tol, p.max_iter = dim, k, omega, step, tol, max_iter
     p.cg_rtol, p.cg_max_iter, p.strategy, p.seed, p.device = cg_rtol, cg_max_iter, strategy, seed, device
@@ -165,6 +165,7 @@ def make_params(dim=2, k=0.0, omega=1.5, step=math.inf, tol=1e-4, max_iter=500, 
     p.weight_exp = weight_exp
     p.p1_split = p1_split
     p.use_graphs = use_graphs
+    p.cg_history = cg_history
     return p
 
 
