@@ -28,6 +28,13 @@
 
 #include "fdl_internal.h"
 
+#ifndef FDL_PACKED_FMA
+#define FDL_PACKED_FMA 1  // 0: two scalar FFMAs instead of fma.rn.f32x2 (measured slower)
+#endif
+#ifndef FDL_MAXST
+#define FDL_MAXST 4  // deepest TMA ring of the pair passes
+#endif
+
 namespace fdl {
 
 namespace {
@@ -177,7 +184,7 @@ __host__ __device__ constexpr int sym_stages()
     constexpr int budget = 228 * 1024 / sym_ctas_per_sm<MODE, DIM>() - 5 * 1024 -
                            (int)sym_red_floats<MODE, DIM, NSETS>() * 4;
     constexpr int st = budget / sym_stage_bytes<MODE, DIM, NSETS, HB>();
-    return st < 2 ? 2 : (st > 4 ? 4 : st);
+    return st < 2 ? 2 : (st > FDL_MAXST ? FDL_MAXST : st);
 }
 
 template <int MODE, int DIM, int NSETS, int HB>
@@ -209,9 +216,21 @@ __device__ __forceinline__ u64 fsub2(u64 a, u64 b)
 }
 __device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c)
 {
+#if FDL_PACKED_FMA
     u64 d;
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
     return d;
+#else
+    // two scalar FFMAs (same IEEE operation per element).  Alone, an FFMA2 with three
+    // register pairs issues at ~3.1 cycles per warp against 2 x 1.1 for the scalar pair
+    // (scripts/pipe_rates.cu), but inside k_sym the scalar form is slower (more issue
+    // slots; C5 P2 1846 -> 1681 GB/s, P1S 15.58 -> 15.70 ms)
+    float al, ah, bl, bh, cl, ch;
+    upk(a, al, ah);
+    upk(b, bl, bh);
+    upk(c, cl, ch);
+    return pk(fmaf(al, bl, cl), fmaf(ah, bh, ch));
+#endif
 }
 __device__ __forceinline__ u64 fmul2(u64 a, u64 b)
 {
