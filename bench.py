@@ -224,8 +224,16 @@ def run_gpu(args):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local_rank)
     dist = None
-    if world > 1:
+    # FDL_BENCH_FORCE_DIST=1 runs the multi-GPU code path (process group, NCCL
+    # communicator, tile-sharded context) with one rank: a one-GPU check of the
+    # launch path the scaling runs take
+    force_dist = world == 1 and os.environ.get("FDL_BENCH_FORCE_DIST") == "1"
+    if world > 1 or force_dist:
         import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     from paper_1711_01228_b200 import fdl
@@ -240,7 +248,7 @@ def run_gpu(args):
                         cg_extrap=int(os.environ.get("FDL_CG_EXTRAP", "2")),
                         p1_split=int(os.environ.get("FDL_P1_SPLIT", "-1")),
                         strategy={"fixed": fdl.STRAT_FIXED, "prob": fdl.STRAT_PROB, "enum": fdl.STRAT_ENUM}[args.strategy])
-    if world > 1:
+    if world > 1 or force_dist:
         from paper_1711_01228_b200 import dist as fdist
         L = fdist.sharded_layout(g, p, X0, edge_len=configs.edge_lengths_for(args.config))
     else:
@@ -329,6 +337,10 @@ def run_gpu(args):
         try:
             tj = json.load(open(tf))
         except Exception:
+            continue
+        # the capture's workload (prof.sh profiles C5 on one GPU): bytes per launch of another
+        # config or of a rank's share are not this launch's
+        if tj.get("config", "C5") != args.config or world != 1:
             continue
         if kname in tj.get("bytes_per_launch", {}):
             roof["traffic"] = tj["bytes_per_launch"][kname]

@@ -95,7 +95,8 @@ for kern in ("p1", "p2"):
 if traffic:  # per-launch DRAM bytes of the captured kernels (bench.py roofline.traffic)
     import json
     with open(os.path.join(DST, f"{TAG}_traffic.json"), "w") as f:
-        json.dump({"tag": TAG, "source": "ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum",
+        json.dump({"tag": TAG, "config": os.environ.get("FDL_PROF_CONFIG", "C5"),
+                   "source": "ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum",
                    "bytes_per_launch": traffic}, f, indent=1)
 
 path = os.path.join(DST, f"{TAG}_ncu_summary.md")
