@@ -374,6 +374,14 @@ def run_gpu(args):
                "iterations_per_sec": args.steps / (ms2 * 1e-3)}
 
     ffma_tf, _ = fdl.bench_ffma(local_rank)
+    # ceiling of the line-6 pass's own arithmetic (same per-tile function on a resident
+    # tile, no HBM / pipeline / reductions): how much of the gap to peak is the mix itself
+    if roof.get("kernel") == "p1_repulse_stress" and dim == 2 and info.hop_bits == 4 and roof.get("achieved"):
+        mix_tf, _ = fdl.bench_p1s_mix(local_rank)
+        roof["mix_ceiling"] = {"achieved": mix_tf, "frac_of_peak": mix_tf / roof["peak"],
+                               "kernel_frac_of_ceiling": roof["achieved"] / mix_tf,
+                               "source": "fdl_bench_p1s_mix: sym_tile<P1S> repeated on a tile resident in "
+                                         "shared memory at the pass's occupancy (DESIGN §7)"}
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:

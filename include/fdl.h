@@ -308,6 +308,13 @@ fdl_status fdl_reset_stats(fdl_ctx* ctx);
  * issues only FFMA (the measured FP32 roofline denominator). */
 fdl_status fdl_bench_ffma(int32_t device, double* tflops, double* ms);
 
+/* Ceiling of the line-6 pass (P1S) on `device`: the same per-tile function the
+ * pass runs (hop decode, pair arithmetic, j-side stores; 2-D, 4-bit hops 1..8)
+ * repeated on one tile resident in shared memory, at the pass's occupancy, with
+ * no HBM traffic, TMA pipeline or reductions.  *tflops counts the pass's 29
+ * algorithmic flops per unordered pair. */
+fdl_status fdl_bench_p1s_mix(int32_t device, double* tflops, double* ms);
+
 const char* fdl_status_str(fdl_status s);
 const char* fdl_last_error(const fdl_ctx* ctx); /* valid until the next call on ctx */
 void fdl_destroy(fdl_ctx* ctx);                 /* NULL-safe */

@@ -1906,4 +1906,44 @@ fdl_status fdl_bench_ffma(int32_t device, double* tflops, double* ms)
     return e == cudaSuccess ? FDL_OK : FDL_E_CUDA;
 }
 
+fdl_status fdl_bench_p1s_mix(int32_t device, double* tflops, double* ms)
+{
+    if (!tflops || !ms) return FDL_E_INVALID_ARG;
+    if (cudaSetDevice(device) != cudaSuccess) return FDL_E_CUDA;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int blocks = sms * p1s_mix_ctas_per_sm(), iters = 2000;
+    float *pos = nullptr, *out = nullptr;
+    if (cudaMalloc(&pos, kT * 4 * sizeof(float)) != cudaSuccess) return FDL_E_OOM;
+    if (cudaMalloc(&out, (size_t)blocks * 256 * sizeof(float)) != cudaSuccess) {
+        cudaFree(pos);
+        return FDL_E_OOM;
+    }
+    std::vector<float> h(kT * 4);
+    for (int k = 0; k < kT * 4; ++k) h[k] = (float)((k * 37 % 101) * 0.01);
+    cudaMemcpy(pos, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice);
+    cudaStream_t s;
+    cudaStreamCreate(&s);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    launch_p1s_mix(pos, out, 20, blocks, s);  // warm-up
+    cudaEventRecord(a, s);
+    launch_p1s_mix(pos, out, iters, blocks, s);
+    cudaEventRecord(b, s);
+    cudaError_t e = cudaEventSynchronize(b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, a, b);
+    // 64 pairs per thread per tile, 29 algorithmic flops per pair
+    const double flops = (double)blocks * 256 * iters * 64.0 * 29.0;
+    *ms = t;
+    *tflops = flops / (t * 1e-3) / 1e12;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaStreamDestroy(s);
+    cudaFree(pos);
+    cudaFree(out);
+    return e == cudaSuccess ? FDL_OK : FDL_E_CUDA;
+}
+
 }  // extern "C"

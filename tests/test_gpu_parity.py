@@ -725,3 +725,11 @@ def test_end_to_end_3d_rgg(bits):
     r = L.run_until_converged()
     o = layout.run_algorithm2(layout.Problem(g, 3, k), X0, 1.5, cfg.tol, cfg.max_iter)
     _gates(r.iterations, r.f_final, o)
+
+
+def test_p1s_mix_ceiling_bench():
+    """fdl_bench_p1s_mix runs the line-6 pass's per-tile function on a resident
+    tile: a positive FLOP rate below the FP32 FFMA rate of the same GPU."""
+    mix, ms = fdl.bench_p1s_mix(0)
+    ffma, _ = fdl.bench_ffma(0)
+    assert ms > 0 and 0 < mix < ffma
