@@ -374,10 +374,13 @@ def run_gpu(args):
                "iterations_per_sec": args.steps / (ms2 * 1e-3)}
 
     ffma_tf, _ = fdl.bench_ffma(local_rank)
+    extra_p2_mix = {}
     # ceiling of the line-6 pass's own arithmetic (same per-tile function on a resident
     # tile, no HBM / pipeline / reductions): how much of the gap to peak is the mix itself
     if roof.get("kernel") == "p1_repulse_stress" and dim == 2 and info.hop_bits == 4 and roof.get("achieved"):
         mix_tf, _ = fdl.bench_p1s_mix(local_rank)
+        p2_mix_gbs, _ = fdl.bench_p2_mix(local_rank)
+        extra_p2_mix = {"p2_mix_ceiling_hop_gbs": p2_mix_gbs}
         roof["mix_ceiling"] = {"achieved": mix_tf, "frac_of_peak": mix_tf / roof["peak"],
                                "kernel_frac_of_ceiling": roof["achieved"] / mix_tf,
                                "source": "fdl_bench_p1s_mix: sym_tile<P1S> repeated on a tile resident in "
@@ -406,6 +409,7 @@ def run_gpu(args):
             "kernel_share": {"p1": p1_share, "p2": p2_share, "other": max(0.0, 1 - p1_share - p2_share)},
             "p1_tflops": p1_tf, "p2_hop_gbs": p2_gbs,
             "fp32_ffma_microbench_tflops": ffma_tf,
+            **extra_p2_mix,
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -314,6 +314,9 @@ fdl_status fdl_bench_ffma(int32_t device, double* tflops, double* ms);
  * no HBM traffic, TMA pipeline or reductions.  *tflops counts the pass's 29
  * algorithmic flops per unordered pair. */
 fdl_status fdl_bench_p1s_mix(int32_t device, double* tflops, double* ms);
+/* Same for the PCG matvec pass (P2, product form): *hop_gbs = the pass's
+ * algorithmic hop bytes (0.5 B per unordered pair at 4 bits) per second. */
+fdl_status fdl_bench_p2_mix(int32_t device, double* hop_gbs, double* ms);
 
 const char* fdl_status_str(fdl_status s);
 const char* fdl_last_error(const fdl_ctx* ctx); /* valid until the next call on ctx */

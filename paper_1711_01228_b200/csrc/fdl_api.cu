@@ -1906,13 +1906,14 @@ fdl_status fdl_bench_ffma(int32_t device, double* tflops, double* ms)
     return e == cudaSuccess ? FDL_OK : FDL_E_CUDA;
 }
 
-fdl_status fdl_bench_p1s_mix(int32_t device, double* tflops, double* ms)
+// pairs/s of sym_tile<mode> on a resident tile (fdl_bench_p1s_mix, fdl_bench_p2_mix)
+static fdl_status bench_tile_mix(int32_t device, int mode, double* pairs_per_s, double* ms)
 {
-    if (!tflops || !ms) return FDL_E_INVALID_ARG;
+    if (!pairs_per_s || !ms) return FDL_E_INVALID_ARG;
     if (cudaSetDevice(device) != cudaSuccess) return FDL_E_CUDA;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    const int blocks = sms * p1s_mix_ctas_per_sm(), iters = 2000;
+    const int blocks = sms * tile_mix_ctas_per_sm(mode), iters = 2000;
     float *pos = nullptr, *out = nullptr;
     if (cudaMalloc(&pos, kT * 4 * sizeof(float)) != cudaSuccess) return FDL_E_OOM;
     if (cudaMalloc(&out, (size_t)blocks * 256 * sizeof(float)) != cudaSuccess) {
@@ -1927,23 +1928,38 @@ fdl_status fdl_bench_p1s_mix(int32_t device, double* tflops, double* ms)
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    launch_p1s_mix(pos, out, 20, blocks, s);  // warm-up
+    launch_tile_mix(mode, pos, out, 20, blocks, s);  // warm-up
     cudaEventRecord(a, s);
-    launch_p1s_mix(pos, out, iters, blocks, s);
+    launch_tile_mix(mode, pos, out, iters, blocks, s);
     cudaEventRecord(b, s);
     cudaError_t e = cudaEventSynchronize(b);
     float t = 0.f;
     cudaEventElapsedTime(&t, a, b);
-    // 64 pairs per thread per tile, 29 algorithmic flops per pair
-    const double flops = (double)blocks * 256 * iters * 64.0 * 29.0;
+    const double pairs = (double)blocks * 256 * iters * 64.0;  // 64 pairs per thread per tile
     *ms = t;
-    *tflops = flops / (t * 1e-3) / 1e12;
+    *pairs_per_s = pairs / (t * 1e-3);
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     cudaStreamDestroy(s);
     cudaFree(pos);
     cudaFree(out);
     return e == cudaSuccess ? FDL_OK : FDL_E_CUDA;
+}
+
+fdl_status fdl_bench_p1s_mix(int32_t device, double* tflops, double* ms)
+{
+    double pps = 0.0;
+    fdl_status st = bench_tile_mix(device, kSymP1S, &pps, ms);
+    if (st == FDL_OK) *tflops = pps * 29.0 / 1e12;  // 29 algorithmic flops per pair
+    return st;
+}
+
+fdl_status fdl_bench_p2_mix(int32_t device, double* hop_gbs, double* ms)
+{
+    double pps = 0.0;
+    fdl_status st = bench_tile_mix(device, kSymP2, &pps, ms);
+    if (st == FDL_OK) *hop_gbs = pps * 0.5 / 1e9;  // 4-bit hops: 0.5 B per unordered pair
+    return st;
 }
 
 }  // extern "C"

@@ -126,9 +126,9 @@ cudaError_t launch_cg_tail(double* y, const float* pvec_in, const double* diag, 
                            DevScalars* sc, HostScalars* hs, cudaStream_t s, unsigned long long cond, int use_cond,
                            int cg_max);
 cudaError_t launch_ffma_bench(float* out, int iters, int blocks, int threads, cudaStream_t s);
-// sym_tile<P1S> on a resident tile (the line-6 pass's arithmetic ceiling, 29 flops/pair)
-cudaError_t launch_p1s_mix(const float* pos, float* out, int iters, int blocks, cudaStream_t s);
-int p1s_mix_ctas_per_sm();
+// sym_tile<mode> (kSymP1S or kSymP2, 2-D, 4-bit) on a resident tile: the pass's arithmetic ceiling
+cudaError_t launch_tile_mix(int mode, const float* pos, float* out, int iters, int blocks, cudaStream_t s);
+int tile_mix_ctas_per_sm(int mode);
 
 // ------------------------------------------------------- symmetric (triangle) passes
 constexpr int kT = 128;            // tile edge: tiles (I, J), I <= J, of kT x kT pairs

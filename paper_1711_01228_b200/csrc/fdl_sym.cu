@@ -795,30 +795,32 @@ cudaError_t launch_sym(const SymArgs& a, int mode, int dim, int nsets, int hb, i
 }
 
 // ------------------------------------------- P1S arithmetic ceiling (diagnostic)
-// The line-6 pass's per-tile work alone -- sym_tile<P1S> (the same function
-// k_sym runs: hop decode from shared memory, pair arithmetic, j-side stores) on
-// one resident 4-bit tile and position block, at k_sym's occupancy -- without the
-// TMA ring, HBM, the warp flushes or the reductions.  Its FLOP rate is the
-// ceiling the instruction mix itself allows (fdl_bench_p1s_mix, bench.py).
-__global__ void __launch_bounds__(256, sym_ctas_per_sm<kSymP1S, 2>()) k_p1s_mix(const float* __restrict__ pos,
-                                                                                 float* out, int iters)
+// A pass's per-tile work alone -- sym_tile (the same function k_sym runs: hop
+// decode from shared memory, pair arithmetic, j-side stores) on one resident
+// 4-bit tile and position block, at k_sym's occupancy -- without the TMA ring,
+// HBM, the warp flushes or the reductions: the ceiling the instruction mix
+// itself allows (fdl_bench_p1s_mix for the line-6 pass, bench.py; P2 alike).
+template <int MODE, int NSETS>
+__global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, 2>()) k_tile_mix(const float* __restrict__ pos,
+                                                                              float* out, int iters)
 {
-    constexpr int C = sym_ncomp<kSymP1S, 2, 2>();
-    constexpr int PS = sym_ps<kSymP1S, 2, 2>();
-    constexpr int JP = sym_jpitch<kSymP1S, 2, 2>();
+    constexpr int C = sym_ncomp<MODE, 2, NSETS>();
+    constexpr int PS = sym_ps<MODE, 2, NSETS>();
+    constexpr int JP = sym_jpitch<MODE, 2, NSETS>();
     __shared__ __align__(128) uint8_t sD[tile_bytes(0)];
     __shared__ __align__(16) float sP[kT * PS];
     __shared__ float lut[256];
     __shared__ float2 lut2[256];
-    __shared__ float red[sym_red_floats<kSymP1S, 2, 2>()];
+    __shared__ float red[sym_red_floats<MODE, 2, NSETS>()];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int ty = lane & 15, tx = tid >> 4;
     lut[tid] = tid ? 1.0f / (float)(tid * tid) : 0.0f;
     {
         const int lo = (int)nib_decode_lo((uint32_t)tid), hi = (int)nib_decode_hi((uint32_t)tid);
-        lut2[tid] = make_float2((float)(lo * lo), (float)(hi * hi));
+        lut2[tid] = MODE == kSymP2 ? make_float2(lo ? 1.0f / (float)(lo * lo) : 0.0f, hi ? 1.0f / (float)(hi * hi) : 0.0f)
+                                   : make_float2((float)(lo * lo), (float)(hi * hi));
     }
-    for (int k = tid; k < kT * PS; k += 256) sP[k] = pos[k];
+    for (int k = tid; k < kT * PS; k += 256) sP[k] = pos[k % (kT * 4)];
     for (int k = tid; k < (int)tile_bytes(0); k += 256) {  // hops 1..8 (C5's range)
         const uint32_t z = (uint32_t)k * 2654435761u + blockIdx.x * 40503u;
         sD[k] = (uint8_t)nib_encode(1u + ((z >> 7) & 7u), 1u + ((z >> 17) & 7u));
@@ -828,32 +830,39 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<kSymP1S, 2>()) k_p1s_mix(
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
 #pragma unroll
-        for (int q = 0; q < PS; ++q) xi[r][q] = pos[(ty * 8 + r) * PS + q] + 0.37f;
+        for (int q = 0; q < PS; ++q) xi[r][q] = pos[((ty * 8 + r) * PS + q) % (kT * 4)] + 0.37f;
 #pragma unroll
         for (int v = 0; v < C; ++v) ai[r][v] = 0.0f;
     }
     float* wrow = red + wid * 2 * (16 * JP + 16) + (tx & 1) * (16 * JP + 16) + ty * JP;
     double s64 = 0.0;
     for (int it = 0; it < iters; ++it) {
-        float sf[2][2] = {{0.0f, 0.0f}, {0.0f, 0.0f}};
-        sym_tile<kSymP1S, 2, 2, 0, false>(sD, sP, lut, lut2, 0x4B000000u, -2.0f, ty, tx, false, xi, ai, wrow, sf);
-        s64 += (double)sf[0][0] + (double)sf[1][1];
+        float sf[2][NSETS];
+#pragma unroll
+        for (int q = 0; q < NSETS; ++q) sf[0][q] = sf[1][q] = 0.0f;
+        sym_tile<MODE, 2, NSETS, 0, false>(sD, sP, lut, lut2, 0x4B000000u, -2.0f, ty, tx, false, xi, ai, wrow, sf);
+        s64 += (double)sf[0][0] + (double)sf[1][NSETS - 1];
         __syncwarp();
     }
     __syncwarp();
     float t = (float)s64 + red[wid * 2 * (16 * JP + 16) + lane];  // keeps the j-side stores
 #pragma unroll
-    for (int r = 0; r < 8; ++r) t += ai[r][0] + ai[r][1];
+    for (int r = 0; r < 8; ++r) t += ai[r][0] + ai[r][C - 1];
     out[blockIdx.x * 256 + tid] = t;
 }
 
-cudaError_t launch_p1s_mix(const float* pos, float* out, int iters, int blocks, cudaStream_t s)
+cudaError_t launch_tile_mix(int mode, const float* pos, float* out, int iters, int blocks, cudaStream_t s)
 {
-    k_p1s_mix<<<blocks, 256, 0, s>>>(pos, out, iters);
+    if (mode == kSymP1S)
+        k_tile_mix<kSymP1S, 2><<<blocks, 256, 0, s>>>(pos, out, iters);
+    else if (mode == kSymP2)
+        k_tile_mix<kSymP2, 1><<<blocks, 256, 0, s>>>(pos, out, iters);
+    else
+        return cudaErrorInvalidValue;
     return cudaGetLastError();
 }
 
-int p1s_mix_ctas_per_sm() { return sym_ctas_per_sm<kSymP1S, 2>(); }
+int tile_mix_ctas_per_sm(int mode) { return mode == kSymP2 ? sym_ctas_per_sm<kSymP2, 2>() : sym_ctas_per_sm<kSymP1S, 2>(); }
 
 // ------------------------------------------------------ enumerating strategy
 // Stress of NC relaxed candidates X~(w_c) = X^{k+1} + w_c (X^{k+1} - X^k) in

@@ -29,7 +29,7 @@ EXPORTS = [
     "fdl_abi_version", "fdl_params_default", "fdl_create", "fdl_create_sharded", "fdl_shard_tiles",
     "fdl_nccl_unique_id", "fdl_set_stream", "fdl_step", "fdl_run_until_converged", "fdl_get_positions",
     "fdl_set_positions", "fdl_eval_forces", "fdl_get_hop_rows", "fdl_get_diag", "fdl_get_info",
-    "fdl_set_timing", "fdl_get_stats", "fdl_reset_stats", "fdl_bench_ffma", "fdl_bench_p1s_mix", "fdl_status_str",
+    "fdl_set_timing", "fdl_get_stats", "fdl_reset_stats", "fdl_bench_ffma", "fdl_bench_p1s_mix", "fdl_bench_p2_mix", "fdl_status_str",
     "fdl_last_error", "fdl_destroy", "fdl_eval_partial", "fdl_set_omega_vertex", "fdl_get_dist_rows",
     "fdl_group_create", "fdl_group_destroy", "fdl_create_loopback",
 ]
@@ -128,6 +128,7 @@ def _load():
         "fdl_reset_stats": (i32, [P]),
         "fdl_bench_ffma": (i32, [i32, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]),
         "fdl_bench_p1s_mix": (i32, [i32, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]),
+        "fdl_bench_p2_mix": (i32, [i32, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]),
         "fdl_status_str": (ctypes.c_char_p, [i32]),
         "fdl_last_error": (ctypes.c_char_p, [P]),
         "fdl_destroy": (None, [P]),
@@ -187,6 +188,13 @@ def bench_p1s_mix(device: int = 0):
     tf, ms = ctypes.c_double(), ctypes.c_double()
     _check(None, lib.fdl_bench_p1s_mix(device, ctypes.byref(tf), ctypes.byref(ms)))
     return tf.value, ms.value
+
+
+def bench_p2_mix(device: int = 0):
+    """(hop GB/s, ms) of the PCG matvec pass's per-tile work on a resident tile."""
+    gbs, ms = ctypes.c_double(), ctypes.c_double()
+    _check(None, lib.fdl_bench_p2_mix(device, ctypes.byref(gbs), ctypes.byref(ms)))
+    return gbs.value, ms.value
 
 
 def bench_ffma(device: int = 0):

@@ -733,3 +733,5 @@ def test_p1s_mix_ceiling_bench():
     mix, ms = fdl.bench_p1s_mix(0)
     ffma, _ = fdl.bench_ffma(0)
     assert ms > 0 and 0 < mix < ffma
+    gbs, ms2 = fdl.bench_p2_mix(0)
+    assert ms2 > 0 and gbs > 0
