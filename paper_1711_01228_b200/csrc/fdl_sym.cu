@@ -31,6 +31,15 @@
 #ifndef FDL_PACKED_FMA
 #define FDL_PACKED_FMA 1  // 0: two scalar FFMAs instead of fma.rn.f32x2 (measured slower)
 #endif
+#ifndef FDL_P2_SHFL
+#define FDL_P2_SHFL 0  // 1: P2 hop weights by warp shuffle (experiment; slower in k_sym)
+#endif
+#ifndef FDL_P1_SHFL
+#define FDL_P1_SHFL 0  // 1: P1 hop decode by warp shuffle (experiment; slower)
+#endif
+#ifndef FDL_P2_CTAS
+#define FDL_P2_CTAS 3  // CTAs per SM of the 2-D PCG matvec pass
+#endif
 #ifndef FDL_MAXST
 #define FDL_MAXST 4  // deepest TMA ring of the pair passes
 #endif
@@ -172,7 +181,7 @@ __host__ __device__ constexpr size_t sym_red_floats()  // the j-side warp buffer
 template <int MODE, int DIM>
 __host__ __device__ constexpr int sym_ctas_per_sm()
 {
-    return (MODE == kSymP2 && DIM == 2) ? 3 : ((DIM == 2 || (MODE != kSymP1 && MODE != kSymP1S)) ? 2 : 1);
+    return (MODE == kSymP2 && DIM == 2) ? FDL_P2_CTAS : ((DIM == 2 || (MODE != kSymP1 && MODE != kSymP1S)) ? 2 : 1);
 }
 
 // TMA ring depth: as many stages (2..4) as the shared memory left by the
@@ -493,6 +502,8 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
         // j-side sum of a column is split over even/odd rows (two 4-long FFMA
         // chains instead of one 8-long chain).
         uint4 chs[NCH];
+        const float wtab = MODE == kSymP2 ? lut[threadIdx.x & 15]  // w'_h for h = lane & 15 (w'_0 = 0)
+                                          : (float)((threadIdx.x & 15) * (threadIdx.x & 15));  // h^2 (shuffle experiments)
 #pragma unroll
         for (int kc = 0; kc < NCH; ++kc) chs[kc] = *reinterpret_cast<const uint4*>(sD + ((size_t)kc * 256 + tid) * 16);
 #pragma unroll
@@ -522,6 +533,20 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
 #pragma unroll
                 for (int rp = 0; rp < 4; ++rp) {
                     const uint32_t off = rp == 0 ? ((w << 3) & 0x7f8u) : ((w >> (8 * rp - 3)) & 0x7f8u);
+                    if ((FDL_P2_SHFL && MODE == kSymP2) || (FDL_P1_SHFL && (MODE == kSymP1 || MODE == kSymP1S))) {
+                        // experiment (off): weights by warp shuffle from a 16-entry register
+                        // table (lane h holds w'_h or h^2) instead of the shared-memory table.
+                        // The shuffle reads lane (index mod 32) and the table repeats every 16
+                        // lanes, so only the low 4 bits of each index matter: hi = the shifted
+                        // word, lo = ((b & 15) - 4 hi) mod 16 = x - 4 y (nib_decode_lo).  P2's
+                        // per-tile work alone gets 21% faster, but inside k_sym the pass gets
+                        // 14% slower (two SHFL per byte load the MIO queue the warp flush also
+                        // uses); P1S 7% slower
+                        const uint32_t x = rp == 0 ? w : (w >> (8 * rp)), y = w >> (8 * rp + 4);
+                        e[rp] = make_float2(__shfl_sync(0xffffffffu, wtab, (int)(x - 4u * y)),
+                                            __shfl_sync(0xffffffffu, wtab, (int)y));
+                        continue;
+                    }
                     e[rp] = *reinterpret_cast<const float2*>(reinterpret_cast<const char*>(lut2) + off);
                 }
 #pragma unroll
