@@ -35,6 +35,7 @@ def test_abi_version_and_defaults():
     assert p.struct_size == 88 or p.struct_size == __import__("ctypes").sizeof(fdl.Params)
     assert p.dim == 2 and p.omega == 1.5 and math.isinf(p.step) and p.tol == 1e-4
     assert p.max_iter == 500 and p.weight_exp == -2.0 and p.strategy == fdl.STRAT_FIXED
+    assert p.cg_extrap == 2 and p.cg_history == 0 and p.a_refresh == 10
 
 
 def test_status_strings():
@@ -80,6 +81,10 @@ def test_parameter_validation():
     _expect("FDL_E_BAD_LENGTH", g.n, g.row_ptr, g.col, edge_len=np.array([1.0, 1.0, np.inf, np.inf]))
     p = fdl.make_params(strategy=fdl.STRAT_ENUM, weight_exp=-1.0)
     _expect("FDL_E_UNSUPPORTED", g.n, g.row_ptr, g.col, params=p)
+    p = fdl.make_params(cg_history=9)  # recycled PCG start window: 0 (default 2) .. 8
+    _expect("FDL_E_INVALID_ARG", g.n, g.row_ptr, g.col, params=p)
+    p = fdl.make_params(cg_extrap=3)
+    _expect("FDL_E_INVALID_ARG", g.n, g.row_ptr, g.col, params=p)
     p = fdl.make_params()
     p.struct_size = 3
     _expect("FDL_E_INVALID_ARG", g.n, g.row_ptr, g.col, params=p)
