@@ -145,14 +145,14 @@ __device__ __forceinline__ float chunk_hop(const uint4& ch, int r, int cc, uint3
 template <int MODE, int DIM, int NSETS>
 __host__ __device__ constexpr int sym_ncomp()
 {
-    return MODE == kSymP1 ? NSETS * DIM : ((MODE == kSymP2 || MODE == kSymP1S) ? DIM : 1);
+    return MODE == kSymP1 ? NSETS * DIM : (MODE == kSymP1A ? 2 * DIM : ((MODE == kSymP2 || MODE == kSymP1S) ? DIM : 1));
 }
 
 // floats per vertex in the staged position vector
 template <int MODE, int DIM, int NSETS>
 __host__ __device__ constexpr int sym_ps()
 {
-    return (MODE == kSymP1 || MODE == kSymP1S) ? (DIM == 2 ? (NSETS == 1 ? 2 : 4) : (NSETS == 1 ? 4 : 8))
+    return (MODE == kSymP1 || MODE == kSymP1S || MODE == kSymP1A) ? (DIM == 2 ? (NSETS == 1 ? 2 : 4) : (NSETS == 1 ? 4 : 8))
                           : (MODE == kSymP2 ? (DIM == 2 ? 2 : 4) : 4);
 }
 
@@ -181,7 +181,8 @@ __host__ __device__ constexpr size_t sym_red_floats()  // the j-side warp buffer
 template <int MODE, int DIM>
 __host__ __device__ constexpr int sym_ctas_per_sm()
 {
-    return (MODE == kSymP2 && DIM == 2) ? FDL_P2_CTAS : ((DIM == 2 || (MODE != kSymP1 && MODE != kSymP1S)) ? 2 : 1);
+    return (MODE == kSymP2 && DIM == 2) ? FDL_P2_CTAS
+                                        : ((DIM == 2 || (MODE != kSymP1 && MODE != kSymP1S && MODE != kSymP1A)) ? 2 : 1);
 }
 
 // TMA ring depth: as many stages (2..4) as the shared memory left by the
@@ -371,6 +372,60 @@ __device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float
             aj[c] = fmaf(q, d[c], aj[c]);
         }
         s[0] = fmaf(u, u, s[0]);
+    } else if (MODE == kSymP1A) {
+        // one set: stress and R as the 1-set P1 pass (same operations and order, so
+        // R and f are bitwise those of kSymP1), plus (L^W X)_i = sum_j w_ij (x_i - x_j)
+        // in difference form on the same delta (w = wlut = 1/h^2, the P2 table value)
+        float d[DIM];
+        float r2 = FLT_MIN;
+        float q, u;
+        float w = wlut;
+        if (DIM == 2) {
+            const u64 dd = fsub2(pk(xi[0], xi[1]), pk(xj[0], xj[1]));
+            upk(dd, d[0], d[1]);
+            r2 = fmaf(d[1], d[1], fmaf(d[0], d[0], FLT_MIN));
+            q = rsqrt_approx(r2 * h2);
+            u = fmaf(r2, q, -1.0f);
+            if (SAFE) {
+                q = valid ? q : 0.0f;
+                u = valid ? u : 0.0f;
+                w = valid ? w : 0.0f;
+            }
+            float lo, hi;
+            upk(ffma2(pk(q, q), dd, pk(ai[0], ai[1])), lo, hi);
+            ai[0] = lo;
+            ai[1] = hi;
+            upk(ffma2(pk(q, q), dd, pk(aj[0], aj[1])), lo, hi);
+            aj[0] = lo;
+            aj[1] = hi;
+            upk(ffma2(pk(w, w), dd, pk(ai[2], ai[3])), lo, hi);
+            ai[2] = lo;
+            ai[3] = hi;
+            upk(ffma2(pk(w, w), dd, pk(aj[2], aj[3])), lo, hi);
+            aj[2] = lo;
+            aj[3] = hi;
+        } else {
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) {
+                d[c] = xi[c] - xj[c];
+                r2 = fmaf(d[c], d[c], r2);
+            }
+            q = rsqrt_approx(r2 * h2);
+            u = fmaf(r2, q, -1.0f);
+            if (SAFE) {
+                q = valid ? q : 0.0f;
+                u = valid ? u : 0.0f;
+                w = valid ? w : 0.0f;
+            }
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) {
+                ai[c] = fmaf(q, d[c], ai[c]);
+                aj[c] = fmaf(q, d[c], aj[c]);
+                ai[DIM + c] = fmaf(w, d[c], ai[DIM + c]);
+                aj[DIM + c] = fmaf(w, d[c], aj[DIM + c]);
+            }
+        }
+        s[0] = fmaf(u, u, s[0]);
     } else if (MODE == kSymP2) {
         // Product form of the L^W matvec: (L^W p)_i = diag_i p_i - sum_j w_ij p_j
         // (P:65-68), so a pair adds w p_j to row i and w p_i to row j; the
@@ -457,7 +512,7 @@ __device__ __forceinline__ void gen_pair(const float* xi, const float* xj, float
 
 template <int MODE, int DIM, int NSETS, int HB, bool SAFE>
 __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, const float* lut, const float2* lut2,
-                                         uint32_t magic, float alpha, int ty, int tx, bool diag,
+                                         const float2* lutw, uint32_t magic, float alpha, int ty, int tx, bool diag,
                                          const float (&xi)[8][NSETS * DIM], float (&ai)[8][sym_ncomp<MODE, DIM, NSETS>()],
                                          float* myred, float (&sf)[2][NSETS])
 {
@@ -529,10 +584,12 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
 #pragma unroll
                 for (int v = 0; v < C; ++v) aj[0][v] = aj[1][v] = 0.0f;
                 const uint32_t w = word_of(ch, cc);
-                float2 e[4];
+                float2 e[4], ew[4];
 #pragma unroll
                 for (int rp = 0; rp < 4; ++rp) {
                     const uint32_t off = rp == 0 ? ((w << 3) & 0x7f8u) : ((w >> (8 * rp - 3)) & 0x7f8u);
+                    if (MODE == kSymP1A)  // w' = 1/h^2 of the same byte (the P2 table values)
+                        ew[rp] = *reinterpret_cast<const float2*>(reinterpret_cast<const char*>(lutw) + off);
                     if ((FDL_P2_SHFL && MODE == kSymP2) || (FDL_P1_SHFL && (MODE == kSymP1 || MODE == kSymP1S))) {
                         // experiment (off): weights by warp shuffle from a 16-entry register
                         // table (lane h holds w'_h or h^2) instead of the shared-memory table.
@@ -555,9 +612,10 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
                     for (int hh = 0; hh < 2; ++hh) {
                         const int r = 2 * rp + hh;
                         const float v = hh ? e[rp].y : e[rp].x;
+                        const float vw = MODE == kSymP1A ? (hh ? ew[rp].y : ew[rp].x) : v;
                         bool valid = true;
                         if (SAFE) valid = (v > 0.0f) && (!diag || (ty * 8 + r < jl));
-                        sym_pair<MODE, DIM, NSETS, SAFE>(&xi[r][0], xj, v, v, valid, &ai[r][0], &aj[hh][0], &sf[hh][0]);
+                        sym_pair<MODE, DIM, NSETS, SAFE>(&xi[r][0], xj, v, vw, valid, &ai[r][0], &aj[hh][0], &sf[hh][0]);
                     }
                 }
 #pragma unroll
@@ -600,6 +658,7 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
                     hf = chunk_hop<HB>(ch, r, cc, magic);
                     h2 = hf * hf;
                     if (MODE == kSymP2) wl = rcp_approx(h2);
+                    if (MODE == kSymP1A) wl = HB == 1 ? lut[(int)hf] : rcp_approx(h2);  // as P2 at this width
                 }
                 bool valid = true;
                 if (SAFE) valid = (h2 > 0.0f) && (!diag || (ty * 8 + r < jl));
@@ -623,7 +682,7 @@ __device__ __forceinline__ void sym_flush_warp(const float* wbuf, float* jpart_w
 {
     constexpr int C = sym_ncomp<MODE, DIM, NSETS>();
     constexpr int P = sym_jpitch<MODE, DIM, NSETS>();
-    constexpr float SIGN = (MODE == kSymP1 || MODE == kSymP1S) ? -1.0f : 1.0f;  // P1 antisymmetric; P2, DIAG symmetric
+    constexpr float SIGN = (MODE == kSymP1 || MODE == kSymP1S || MODE == kSymP1A) ? -1.0f : 1.0f;  // P1 antisymmetric; P2, DIAG symmetric
     __syncwarp();
 #pragma unroll
     for (int e0 = 0; e0 < 16 * C; e0 += 32) {
@@ -660,6 +719,7 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
     __shared__ int prod[2];       // producer cursor {item, tile in item}
     __shared__ float lut[256];
     __shared__ float2 lut2[HB == 0 ? 256 : 1];
+    __shared__ float2 lutw2[(HB == 0 && MODE == kSymP1A) ? 256 : 1];
     float* red = reinterpret_cast<float*>(smem + (size_t)NST * STAGE);
 
     // Thread (ty, tx) owns rows ty*8.. and columns tx*8.. of a tile; a warp holds
@@ -674,6 +734,8 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
         lut2[tid] = MODE == kSymP2 ? make_float2(lo ? 1.0f / (float)(lo * lo) : 0.0f,
                                                  hi ? 1.0f / (float)(hi * hi) : 0.0f)
                                    : make_float2((float)(lo * lo), (float)(hi * hi));
+        if (MODE == kSymP1A)
+            lutw2[tid] = make_float2(lo ? 1.0f / (float)(lo * lo) : 0.0f, hi ? 1.0f / (float)(hi * hi) : 0.0f);
     }
     // producer: the next tile of this CTA's items (cursor in shared memory; it is
     // advanced by whichever warp frees a stage last, see below)
@@ -738,9 +800,9 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
 #pragma unroll
             for (int s = 0; s < NSETS; ++s) sf[0][s] = sf[1][s] = 0.0f;
             if (safe)
-                sym_tile<MODE, DIM, NSETS, HB, true>(sD, sP, lut, lut2, a.magic, a.alpha, ty, tx, diag, xi, ai, wrow, sf);
+                sym_tile<MODE, DIM, NSETS, HB, true>(sD, sP, lut, lut2, lutw2, a.magic, a.alpha, ty, tx, diag, xi, ai, wrow, sf);
             else
-                sym_tile<MODE, DIM, NSETS, HB, false>(sD, sP, lut, lut2, a.magic, a.alpha, ty, tx, diag, xi, ai, wrow, sf);
+                sym_tile<MODE, DIM, NSETS, HB, false>(sD, sP, lut, lut2, lutw2, a.magic, a.alpha, ty, tx, diag, xi, ai, wrow, sf);
 #pragma unroll
             for (int s = 0; s < NSETS; ++s) s64[s] += (double)sf[0][s] + (double)sf[1][s];
             // stage consumed by this warp; the last of the 8 warps refills it
@@ -774,7 +836,7 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
                     if ((r >> 2) == h) ip[r * C + v] = tot;
                 }
         }
-        if (MODE == kSymP1 || MODE == kSymP1S) {
+        if (MODE == kSymP1 || MODE == kSymP1S || MODE == kSymP1A) {
             // stress of the warp's share of the segment: fixed-order warp butterfly of
             // the fp64 thread sums -> spart[item][warp][set]
 #pragma unroll
@@ -811,6 +873,7 @@ cudaError_t launch_sym(const SymArgs& a, int mode, int dim, int nsets, int hb, i
 {
     FDL_SYM_ALLHB(kSymP1, 2, 1) FDL_SYM_ALLHB(kSymP1, 2, 2) FDL_SYM_ALLHB(kSymP1, 3, 1) FDL_SYM_ALLHB(kSymP1, 3, 2)
     FDL_SYM_ALLHB(kSymP1S, 2, 2) FDL_SYM_ALLHB(kSymP1S, 3, 2)
+    FDL_SYM_ALLHB(kSymP1A, 2, 1) FDL_SYM_ALLHB(kSymP1A, 3, 1)
     FDL_SYM_CASE(kSymP1, 2, 1, 4) FDL_SYM_CASE(kSymP1, 2, 2, 4) FDL_SYM_CASE(kSymP1, 3, 1, 4)
     FDL_SYM_CASE(kSymP1, 3, 2, 4) FDL_SYM_CASE(kSymP2, 2, 1, 4) FDL_SYM_CASE(kSymP2, 3, 1, 4)
     FDL_SYM_CASE(kSymDiag, 2, 1, 4) FDL_SYM_CASE(kSymDiag, 3, 1, 4)
@@ -865,7 +928,7 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, 2>()) k_tile_mix(co
         float sf[2][NSETS];
 #pragma unroll
         for (int q = 0; q < NSETS; ++q) sf[0][q] = sf[1][q] = 0.0f;
-        sym_tile<MODE, 2, NSETS, 0, false>(sD, sP, lut, lut2, 0x4B000000u, -2.0f, ty, tx, false, xi, ai, wrow, sf);
+        sym_tile<MODE, 2, NSETS, 0, false>(sD, sP, lut, lut2, lut2, 0x4B000000u, -2.0f, ty, tx, false, xi, ai, wrow, sf);
         s64 += (double)sf[0][0] + (double)sf[1][NSETS - 1];
         __syncwarp();
     }
@@ -1149,6 +1212,7 @@ int sym_max_ctas(int mode, int dim, int nsets, int hb)
 #define FDL_SYM_OCC3(M_, D_, S_) FDL_SYM_OCC(M_, D_, S_, 0) FDL_SYM_OCC(M_, D_, S_, 1) FDL_SYM_OCC(M_, D_, S_, 2)
     FDL_SYM_OCC3(kSymP1, 2, 1) FDL_SYM_OCC3(kSymP1, 2, 2) FDL_SYM_OCC3(kSymP1, 3, 1) FDL_SYM_OCC3(kSymP1, 3, 2)
     FDL_SYM_OCC3(kSymP1S, 2, 2) FDL_SYM_OCC3(kSymP1S, 3, 2)
+    FDL_SYM_OCC3(kSymP1A, 2, 1) FDL_SYM_OCC3(kSymP1A, 3, 1)
     FDL_SYM_OCC(kSymP1, 2, 1, 4) FDL_SYM_OCC(kSymP1, 2, 2, 4) FDL_SYM_OCC(kSymP1, 3, 1, 4)
     FDL_SYM_OCC(kSymP1, 3, 2, 4) FDL_SYM_OCC(kSymP2, 2, 1, 4) FDL_SYM_OCC(kSymP2, 3, 1, 4)
     FDL_SYM_OCC(kSymDiag, 2, 1, 4) FDL_SYM_OCC(kSymDiag, 3, 1, 4)

@@ -735,3 +735,28 @@ def test_p1s_mix_ceiling_bench():
     assert ms > 0 and 0 < mix < ffma
     gbs, ms2 = fdl.bench_p2_mix(0)
     assert ms2 > 0 and gbs > 0
+
+
+@pytest.mark.parametrize("name,dim", [("C2", 2), ("C3", 2), ("C3", 3)])
+def test_fused_evaluation_l_w_x(name, dim):
+    """The evaluation at create / fdl_set_positions is one fused pass (kSymP1A:
+    f, R = L^X X and L^W X in difference form), so the first step needs no
+    refresh pass.  Its first step equals the one started from a fresh
+    product-form P2 refresh (a_refresh = 1) within the fp32 pair arithmetic of
+    the two L^W X forms (the first-iteration gate of test_first_iteration)."""
+    cfg = configs.CONFIGS[name]
+    g = configs.graph_for(name)
+    X0 = graphs.init_positions(g.n, dim, 8)
+    out = []
+    for refresh in (10, 1):
+        p = fdl.make_params(dim=dim, k=cfg.k_for(g.n), omega=1.5, tol=cfg.tol, max_iter=cfg.max_iter,
+                            a_refresh=refresh, cg_rtol=1e-10)
+        with fdl.Layout.from_graph(g, params=p, init_pos=X0) as L:
+            st0 = L.get_stats()
+            info = L.step()
+            st1 = L.get_stats()
+            out.append((info.f_next, L.get_positions(), st1.p2_launches - st0.p2_launches, info.cg_iters))
+    (f10, X10, p2a, cga), (f1, X1, p2b, cgb) = out
+    assert p2a == cga and p2b == cgb + 1  # no refresh pass after the fused evaluation
+    assert abs(f10 - f1) / f1 <= 1e-6
+    assert relL2(X10, X1) <= FORCE_TOL
