@@ -566,8 +566,8 @@ fdl_status upload_positions(fdl_ctx* ctx, const double* X)
 {
     ctx->a_valid = false;
     ctx->ext_ok = false;
-    // the step history of the recycled start belongs to the old placement
-    FDL_CUDA(cudaMemsetAsync(&ctx->sc->gal_cnt, 0, sizeof(int), ctx->stream));
+    // (the recycled-start basis is kept: V and L^W V belong to the matrix L^W, which
+    // does not depend on the placement, so they remain a valid Galerkin subspace, R27)
     std::vector<double> loc((size_t)ctx->n * ctx->dim);
     for (int i = 0; i < ctx->n; ++i)
         for (int q = 0; q < ctx->dim; ++q) {
