@@ -760,3 +760,24 @@ def test_fused_evaluation_l_w_x(name, dim):
     assert p2a == cga and p2b == cgb + 1  # no refresh pass after the fused evaluation
     assert abs(f10 - f1) / f1 <= 1e-6
     assert relL2(X10, X1) <= FORCE_TOL
+
+
+@pytest.mark.parametrize("n", [520, 700])
+def test_long_cycle_16_bit_hops(n):
+    """A graph whose diameter exceeds 255 (cycle of n: diameter n/2) takes 16-bit
+    hop tiles on its own: hops bit-exact, forces at X0 within the gate, and the
+    run meets the end-to-end gates against the Cholesky oracle."""
+    g = graphs.cycle_graph(n)
+    k = math.sqrt(1.0 / n)
+    X0 = graphs.init_positions(n, 2, 11)
+    p = fdl.make_params(dim=2, k=k, omega=1.5, tol=1e-4, max_iter=500)
+    L = fdl.Layout.from_graph(g, params=p, init_pos=X0)
+    hop = core.hop_matrix(g)
+    assert L.info.hop_bits == 16 and L.info.diameter == n // 2
+    assert np.array_equal(L.get_hop_rows(0, n), hop)
+    R, A, f = L.eval_forces()
+    Ro, Ao, _ = core.forces(X0, hop, k)
+    assert relL2(R, Ro) <= FORCE_TOL and relL2(A, Ao) <= FORCE_TOL
+    r = L.run_until_converged()
+    o = layout.run_algorithm2(layout.Problem(g, 2, k), X0, 1.5, 1e-4, 500)
+    _gates(r.iterations, r.f_final, o)
