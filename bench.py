@@ -350,9 +350,15 @@ def run_gpu(args):
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        # pinned host buffer (page-locked: the copies run at PCIe/C2C DMA speed)
+        # pinned host buffer (page-locked: the copies run at PCIe/C2C DMA speed). The run restarts
+        # from X0 with the same warm-up, so the timed e2e steps are the same iterations of the
+        # trajectory as the device-timed ones (PCG counts depend on the phase of the run)
         Xh = torch.empty((n, dim), dtype=torch.float64, pin_memory=True).numpy()
-        L.get_positions(Xh)
+        Xh[:] = X0
+        for _ in range(args.warmup):
+            L.set_positions(Xh)
+            L.step()
+            L.get_positions(Xh)
         L.reset_stats()
         barrier()
         e2 = torch.cuda.Event(enable_timing=True)
