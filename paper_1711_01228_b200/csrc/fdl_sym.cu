@@ -37,6 +37,9 @@
 #ifndef FDL_P1_SHFL
 #define FDL_P1_SHFL 0  // 1: P1 hop decode by warp shuffle (experiment; slower)
 #endif
+#ifndef FDL_P1A_CTAS
+#define FDL_P1A_CTAS 2  // CTAs per SM of the 2-D fused evaluation pass
+#endif
 #ifndef FDL_P2_CTAS
 #define FDL_P2_CTAS 3  // CTAs per SM of the 2-D PCG matvec pass
 #endif
@@ -181,8 +184,9 @@ __host__ __device__ constexpr size_t sym_red_floats()  // the j-side warp buffer
 template <int MODE, int DIM>
 __host__ __device__ constexpr int sym_ctas_per_sm()
 {
-    return (MODE == kSymP2 && DIM == 2) ? FDL_P2_CTAS
-                                        : ((DIM == 2 || (MODE != kSymP1 && MODE != kSymP1S && MODE != kSymP1A)) ? 2 : 1);
+    return (MODE == kSymP2 && DIM == 2)    ? FDL_P2_CTAS
+           : (MODE == kSymP1A && DIM == 2) ? FDL_P1A_CTAS
+                                           : ((DIM == 2 || (MODE != kSymP1 && MODE != kSymP1S && MODE != kSymP1A)) ? 2 : 1);
 }
 
 // TMA ring depth: as many stages (2..4) as the shared memory left by the
