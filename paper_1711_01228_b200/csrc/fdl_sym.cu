@@ -37,6 +37,10 @@
 #ifndef FDL_P1_SHFL
 #define FDL_P1_SHFL 0  // 1: P1 hop decode by warp shuffle (experiment; slower)
 #endif
+#ifndef FDL_BFS_UNROLL
+#define FDL_BFS_UNROLL 4  // neighbour frontier loads in flight per warp (MS-BFS)
+#endif
+constexpr int kBfsUnroll = FDL_BFS_UNROLL;
 #ifndef FDL_P1A_CTAS
 #define FDL_P1A_CTAS 2  // CTAs per SM of the 2-D fused evaluation pass
 #endif
@@ -1544,7 +1548,7 @@ __global__ void __launch_bounds__(256) k_bfs_level_sym(const int64_t* __restrict
     for (int64_t e0 = beg; e0 < end; e0 += 32) {
         const int myu = (e0 + lane < end) ? col[e0 + lane] : 0;
         const int cnt = (int)min((int64_t)32, end - e0);
-#pragma unroll 4
+#pragma unroll kBfsUnroll
         for (int k = 0; k < cnt; ++k) {
             const int u = __shfl_sync(0xffffffffu, myu, k);
             acc |= fin[(int64_t)u * kBFSWords + lane];
