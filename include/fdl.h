@@ -8,7 +8,7 @@
  * The method (§2 and §4):
  *   stress      f(X) = sum_{i<j} w_ij (||x_i - x_j|| - d_ij)^2           Eq. 1
  *   ideal dist  d_ij = k * hop(i,j) (graph distance, DESIGN R1)
- *   weights     w_ij = d_ij^-2
+ *   weights     w_ij = d_ij^-2; d_ij^alpha for weight_exp = alpha (NEXT-3)
  *   one step    solve L^W X^{k+1} = L^{X^k} X^k with x_0 = 0              Eq. 2-5, Prop. 2.3
  *   relaxation  Xt = (1+omega) X^{k+1} - omega X^k                       Eq. 10
  *   guard       if f(Xt) <= f(X^{k+1}) then X^{k+1} <- Xt                 Algorithm 2 l.6-8
@@ -51,7 +51,7 @@ typedef enum {
     FDL_E_DUPLICATE_EDGE = -3, /* CSR row lists a neighbour twice                 */
     FDL_E_ASYMMETRIC = -4,     /* (u,v) present but (v,u) missing: graph must be undirected */
     FDL_E_DISCONNECTED = -5,   /* graph not connected: d_ij undefined        */
-    FDL_E_BAD_LENGTH = -6,     /* edge lengths given (weighted graphs are not supported yet) */
+    FDL_E_BAD_LENGTH = -6,     /* an edge length is not positive and finite       */
     FDL_E_DIAMETER = -7,       /* hop count exceeds 65535                                 */
     FDL_E_OOM = -8,            /* device allocation failed                                */
     FDL_E_CUDA = -9,           /* CUDA runtime error                                      */
