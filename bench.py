@@ -134,6 +134,16 @@ def fp32_peak_tflops(peaks):
 
 
 # ---------------------------------------------------------- CPU (oracle) leg
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_oracle_sample(name: str, seed: int, rows_target: int = 0):
     """The fp64 oracle as it stands, on a bounded row sample of the workload:
     BFS hop rows of the sampled sources, then per sampled row the quantities
@@ -176,6 +186,7 @@ def cpu_oracle_sample(name: str, seed: int, rows_target: int = 0):
         "value": (ordered / 2) / (t2 - t1),
         "unit": "pair-interactions/sec",
         "cores": core.num_threads(),
+        "cpu_model": _cpu_model(),
         "kind": "oracle",
         "sample": f"{nrows} of {g.n} rows of {name}: 2 stress + L^X X + L^W X row passes (fp64); "
                   f"{'Dijkstra' if lens is not None else 'BFS'} of the sampled sources {t1 - t0:.2f}s excluded",
@@ -206,7 +217,7 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "n": g.n, "edges": g.num_edges, "dim": cfg.dim,
                    "omega": cfg.omega, "sample": res["sample"]},
-        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "cpu_model", "kind", "sample")},
         "e2e": {"value": v, "unit": "pair-interactions/sec", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     line["cpu_baseline"]["value"] = v
@@ -396,7 +407,7 @@ def run_gpu(args):
         if world == 1 and not args.no_cpu_baseline:
             try:
                 cpu = cpu_oracle_sample(args.config, args.seed, args.cpu_sample_rows)
-                cpu = {k2: cpu[k2] for k2 in ("value", "unit", "cores", "kind", "sample")}
+                cpu = {k2: cpu[k2] for k2 in ("value", "unit", "cores", "cpu_model", "kind", "sample")}
             except Exception as ex:  # pragma: no cover
                 cpu = {"error": str(ex)}
         line = {
