@@ -213,7 +213,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "pair-interactions/sec", "value": v, "unit": "pair-interactions/sec",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * t_all / max(args.steps, 1), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * t_all / max(args.steps, 1), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "n": g.n, "edges": g.num_edges, "dim": cfg.dim,
                    "omega": cfg.omega, "sample": res["sample"]},
