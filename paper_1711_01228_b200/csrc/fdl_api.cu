@@ -568,13 +568,11 @@ fdl_status upload_positions(fdl_ctx* ctx, const double* X)
     ctx->ext_ok = false;
     // (the recycled-start basis is kept: V and L^W V belong to the matrix L^W, which
     // does not depend on the placement, so they remain a valid Galerkin subspace, R27)
-    std::vector<double> loc((size_t)ctx->n * ctx->dim);
-    for (int i = 0; i < ctx->n; ++i)
-        for (int q = 0; q < ctx->dim; ++q) {
-            const size_t g = (size_t)i * ctx->dim + q;
-            loc[g] = (X[g] - X[q]) / ctx->k;
-        }
-    FDL_CUDA(cudaMemcpyAsync(ctx->Xk, loc.data(), loc.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    // raw copy (a DMA straight from the caller's buffer when it is page-locked), then the
+    // pin x_0 = 0 and the 1/k scaling on the device: (x - x_0) / k in fp64
+    const size_t count = (size_t)ctx->n * ctx->dim;
+    FDL_CUDA(cudaMemcpyAsync(ctx->Xt, X, count * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    FDL_LAUNCH(launch_pin_scale(ctx->Xt, ctx->Xk, ctx->n, ctx->dim, ctx->k, 0, ctx->stream));
     return eval_current(ctx);
 }
 
@@ -1692,9 +1690,10 @@ fdl_status fdl_get_positions(fdl_ctx* ctx, double* out, size_t count)
     if (count != (size_t)ctx->n * ctx->dim) return set_err(ctx, FDL_E_INVALID_ARG, "count must be n*dim");
     if (ctx->broken) return FDL_E_STATE;
     cudaSetDevice(ctx->device);
-    FDL_CUDA(cudaMemcpyAsync(out, ctx->Xk, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    // x k on the device (into PCG scratch, free between steps), then one copy to the caller
+    FDL_LAUNCH(launch_pin_scale(ctx->Xk, ctx->cy, ctx->n, ctx->dim, ctx->k, 1, ctx->stream));
+    FDL_CUDA(cudaMemcpyAsync(out, ctx->cy, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     FDL_CUDA(cudaStreamSynchronize(ctx->stream));
-    for (size_t i = 0; i < count; ++i) out[i] *= ctx->k;
     return FDL_OK;
 }
 

@@ -78,6 +78,8 @@ cudaError_t launch_carry_a(const double* Rk, const double* rcg, const double* Ak
                            const DevScalars* sc, int n, int dim, double omega, cudaStream_t s);
 cudaError_t launch_extrap(const double* Xk, const double* Xprev, const double* Ak, const double* Aprev, double* x,
                           double* y0, const DevScalars* sc, int n, int dim, int valid, cudaStream_t s);
+// ABI units: mode 0 y = (x - x_0) / k (upload, pin), mode 1 y = x k (download)
+cudaError_t launch_pin_scale(const double* x, double* y, int n, int dim, double k, int mode, cudaStream_t s);
 // Recycled PCG start (R27): Galerkin projection of the warm-start error onto the
 // last kGalMax step differences V (with AV = L^W V from the carried products).
 cudaError_t launch_gal_start(const double* V, const double* AV, const double* b, const double* Xk, const double* Ak,

@@ -389,6 +389,23 @@ cudaError_t launch_rho(const double* Xn, const double* Xk, double* Xprev, const 
     return cudaGetLastError();
 }
 
+// Placement units at the ABI: mode 0 (upload) y = (x - x_0) / k, the pin
+// x_0 = 0 of P:125 (fp64 subtract, then divide: the same IEEE operations as on the
+// host); mode 1 (download) y = x * k.
+__global__ void k_pin_scale(const double* __restrict__ x, double* __restrict__ y, int n, int dim, double k, int mode)
+{
+    const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= (size_t)n * dim) return;
+    y[g] = mode == 0 ? (x[g] - x[g % dim]) / k : x[g] * k;
+}
+
+cudaError_t launch_pin_scale(const double* x, double* y, int n, int dim, double k, int mode, cudaStream_t s)
+{
+    const size_t cnt = (size_t)n * dim;
+    k_pin_scale<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(x, y, n, dim, k, mode);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------ recycled PCG start (R27)
 // L^W is the same matrix at every step, so the directions the run already took
 // carry over: the start is the Galerkin (A-norm optimal) correction of X^k over
