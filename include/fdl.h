@@ -258,17 +258,25 @@ fdl_status fdl_nccl_unique_id(uint8_t* out128);
 fdl_status fdl_set_stream(fdl_ctx* ctx, void* cuda_stream);
 
 /* One Algorithm-2 iteration on the device; info may be NULL.
- * Returns FDL_E_STATE once the run has stopped (query info->stop). */
+ * Errors: FDL_E_STATE once the run has stopped (info->stop of the last step says
+ * why; fdl_set_positions restarts) or after an earlier CUDA error;
+ * FDL_E_SOLVER if PCG reaches cg_max_iter before cg_rtol;
+ * FDL_E_NONFINITE if the stress becomes NaN/Inf. */
 fdl_status fdl_step(fdl_ctx* ctx, fdl_iter_info* info);
 
-/* Iterate until a stop rule fires (or max_iter).  info may be NULL. */
+/* Iterate until a stop rule fires (DESIGN R4: rel decrease < tol, f = 0, or
+ * max_iter).  info may be NULL.  Errors as fdl_step. */
 fdl_status fdl_run_until_converged(fdl_ctx* ctx, fdl_run_info* info);
 
-/* Current placement (count must be n*dim), original units, x_0 = 0. */
+/* Current placement into the caller's buffer (count must be n*dim, else
+ * FDL_E_INVALID_ARG), original units, x_0 = 0.  Synchronises the stream; a
+ * page-locked buffer is filled by one DMA. */
 fdl_status fdl_get_positions(fdl_ctx* ctx, double* out, size_t count);
 
-/* Replace the placement (count n*dim); re-pins x_0 = 0, recomputes f and
- * L^X X, clears the stop flag (checkpoint resume / parity). */
+/* Replace the placement (count n*dim, all finite, else FDL_E_INVALID_ARG);
+ * re-pins x_0 = 0, recomputes f, L^X X and L^W X at it (one fused pass)
+ * and clears the stop flag (checkpoint resume / interactive layouts / parity).
+ * The recycled PCG basis (DESIGN R27) belongs to L^W and is kept. */
 fdl_status fdl_set_positions(fdl_ctx* ctx, const double* in, size_t count);
 
 /* Per-vertex relax factors omega_i >= 0 (§6 (1), line 410:
@@ -296,6 +304,7 @@ fdl_status fdl_get_dist_rows(fdl_ctx* ctx, int32_t r0, int32_t nrows, double* ou
 /* Jacobi diagonal sum_{j != i} w_ij of all n rows, original units (count = n). */
 fdl_status fdl_get_diag(fdl_ctx* ctx, double* out, size_t count);
 
+/* Geometry, sizes and current state of the context (never fails on a valid ctx). */
 fdl_status fdl_get_info(fdl_ctx* ctx, fdl_ctx_info* info);
 
 /* Kernel statistics.  With timing on, every P1/P2 launch and the rest of each
