@@ -335,6 +335,13 @@ def run_gpu(args):
                 "bytes_per_launch": st.p2_pairs * hop_bytes / max(st.p2_launches, 1),
                 "avg_launch_ms": st.p2_ms / max(st.p2_launches, 1)}
 
+    if st.p1_ms == 0 and st.p2_ms == 0:
+        # CUDA-graph steps (small configs): the library times whole steps only, so no
+        # per-kernel duration exists for the roofline; say so instead of reporting 0
+        roof.update({"achieved": None, "frac": None, "avg_launch_ms": None,
+                     "note": "CUDA-graph steps: per-kernel times are not observable (launch-latency-bound "
+                             "config); see DESIGN.md §10 for the eager configs' rooflines"})
+
     # traffic of the dominant kernel: DRAM bytes per launch from the newest committed
     # `ncu --set full` capture of the same kernel instantiation (profiles/*_traffic.json)
     hb = {3: 5, 4: 0, 8: 1, 16: 2, 32: 4}.get(info.hop_bits, -1)
@@ -423,7 +430,8 @@ def run_gpu(args):
             "iterations_per_sec": its_per_s,
             "pcg_iters_per_step": st.cg_iters / max(st.steps, 1),
             "sor_accept_rate": accepted / max(args.steps, 1), "p1_rejected_passes": st.p1_rejected,
-            "kernel_share": {"p1": p1_share, "p2": p2_share, "other": max(0.0, 1 - p1_share - p2_share)},
+            "kernel_share": ({"p1": p1_share, "p2": p2_share, "other": max(0.0, 1 - p1_share - p2_share)}
+                             if (st.p1_ms > 0 or st.p2_ms > 0) else None),
             "p1_tflops": p1_tf, "p2_hop_gbs": p2_gbs,
             "fp32_ffma_microbench_tflops": ffma_tf,
             **extra_p2_mix,
