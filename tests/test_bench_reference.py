@@ -22,3 +22,28 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["config"]["workload"] == "C1" and d["steps"] == 2 and d["warmup"] == 1
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_gpu_bench_json_line():
+    """bench.py's GPU arm on a small config: one JSON line with the contract's keys
+    (value, e2e with copy bytes, roofline, cpu_baseline, clocks, gpu_launches)."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "C3", "--steps", "3",
+                        "--warmup", "3", "--cpu-sample-rows", "64"], capture_output=True, text=True, timeout=900,
+                       cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "clocks", "gpu_launches",
+                "iterations_per_sec"):
+        assert key in d, key
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["config"]["workload"].startswith("C3")
+    for key in ("bound", "peak", "unit", "frac", "traffic"):
+        assert key in d["roofline"], key
