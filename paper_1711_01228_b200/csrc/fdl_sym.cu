@@ -47,6 +47,9 @@ constexpr int kBfsUnroll = FDL_BFS_UNROLL;
 #ifndef FDL_P2_CTAS
 #define FDL_P2_CTAS 3  // CTAs per SM of the 2-D PCG matvec pass
 #endif
+#ifndef FDL_TPS_P2
+#define FDL_TPS_P2 2  // 4-bit P2: tiles of one work item per TMA stage (one mbarrier wait / refill each)
+#endif
 #ifndef FDL_MAXST
 #define FDL_MAXST 4  // deepest TMA ring of the pair passes
 #endif
@@ -164,6 +167,15 @@ __host__ __device__ constexpr int sym_ps()
 }
 
 
+// tiles per TMA stage: 2 for the 4-bit matvec pass (its per-tile work is short, so halving
+// the mbarrier waits and refills pays: C5 P2 1820 -> 1913 GB/s), 1 elsewhere (the line-6 pass
+// got slower with 2, and wider tiles would not fit two per stage)
+template <int MODE, int HB>
+__host__ __device__ constexpr int sym_tps()
+{
+    return (MODE == kSymP2 && HB == 0) ? FDL_TPS_P2 : 1;
+}
+
 template <int MODE, int DIM, int NSETS, int HB>
 __host__ __device__ constexpr int sym_stage_bytes()
 {
@@ -201,14 +213,14 @@ __host__ __device__ constexpr int sym_stages()
 {
     constexpr int budget = 228 * 1024 / sym_ctas_per_sm<MODE, DIM>() - 5 * 1024 -
                            (int)sym_red_floats<MODE, DIM, NSETS>() * 4;
-    constexpr int st = budget / sym_stage_bytes<MODE, DIM, NSETS, HB>();
+    constexpr int st = budget / (sym_tps<MODE, HB>() * sym_stage_bytes<MODE, DIM, NSETS, HB>());
     return st < 2 ? 2 : (st > FDL_MAXST ? FDL_MAXST : st);
 }
 
 template <int MODE, int DIM, int NSETS, int HB>
 __host__ __device__ constexpr size_t sym_smem_bytes()
 {
-    return (size_t)sym_stages<MODE, DIM, NSETS, HB>() * sym_stage_bytes<MODE, DIM, NSETS, HB>() +
+    return (size_t)sym_stages<MODE, DIM, NSETS, HB>() * sym_tps<MODE, HB>() * sym_stage_bytes<MODE, DIM, NSETS, HB>() +
            sym_red_floats<MODE, DIM, NSETS>() * 4;
 }
 
@@ -728,7 +740,9 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
     __shared__ float lut[256];
     __shared__ float2 lut2[HB == 0 ? 256 : 1];
     __shared__ float2 lutw2[(HB == 0 && MODE == kSymP1A) ? 256 : 1];
-    float* red = reinterpret_cast<float*>(smem + (size_t)NST * STAGE);
+    constexpr int TPS = sym_tps<MODE, HB>();
+    constexpr int SLOT = TPS * STAGE;  // one stage: up to TPS consecutive tiles of one item
+    float* red = reinterpret_cast<float*>(smem + (size_t)NST * SLOT);
 
     // Thread (ty, tx) owns rows ty*8.. and columns tx*8.. of a tile; a warp holds
     // two thread columns (tx = 2w, 2w+1) x all 16 thread rows, so the j-side sum
@@ -751,14 +765,18 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
         int p_item = prod[0], p_t = prod[1];
         if (p_item >= a.nitems) return;
         const int4 it = a.items[p_item];  // {I, J0, ntiles, first local tile}
-        const int J = it.y + p_t;
-        const int64_t lt = (int64_t)it.w + p_t;
-        uint8_t* base = smem + (size_t)stage * STAGE;
+        const int cnt = min(TPS, it.z - p_t);  // tiles of this item in the stage
         fence_proxy_async();
-        mbar_arrive_expect_tx(&full[stage], STAGE);
-        tma_load_1d(base, a.D + lt * DT, DT, &full[stage]);
-        tma_load_1d(base + DT, a.pos + (int64_t)J * kT * PS, kT * PS * 4, &full[stage]);
-        if (++p_t == it.z) {
+        mbar_arrive_expect_tx(&full[stage], cnt * STAGE);
+        for (int k = 0; k < cnt; ++k) {
+            const int J = it.y + p_t + k;
+            const int64_t lt = (int64_t)it.w + p_t + k;
+            uint8_t* base = smem + (size_t)stage * SLOT + (size_t)k * STAGE;
+            tma_load_1d(base, a.D + lt * DT, DT, &full[stage]);
+            tma_load_1d(base + DT, a.pos + (int64_t)J * kT * PS, kT * PS * 4, &full[stage]);
+        }
+        p_t += cnt;
+        if (p_t == it.z) {
             p_t = 0;
             p_item += gridDim.x;
         }
@@ -801,8 +819,10 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
             const int J = it.y + t;
             const bool diag = (J == I);
             const bool safe = diag || (int64_t)(J + 1) * kT > a.n || (int64_t)(I + 1) * kT > a.n;
-            mbar_wait(&full[stage], phase);
-            const uint8_t* sD = smem + (size_t)stage * STAGE;
+            const int k = t % TPS;                            // tile within its stage
+            const bool last = k == TPS - 1 || t == it.z - 1;  // the stage's last tile
+            if (k == 0) mbar_wait(&full[stage], phase);
+            const uint8_t* sD = smem + (size_t)stage * SLOT + (size_t)k * STAGE;
             const float* sP = reinterpret_cast<const float*>(sD + DT);
             float sf[2][NSETS];  // stress of the tile, even / odd rows (two independent FMA chains)
 #pragma unroll
@@ -814,17 +834,19 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
 #pragma unroll
             for (int s = 0; s < NSETS; ++s) s64[s] += (double)sf[0][s] + (double)sf[1][s];
             // stage consumed by this warp; the last of the 8 warps refills it
-            __syncwarp();
-            if (lane == 0) {
-                __threadfence_block();
-                if (atomicAdd(&drained[stage], 1) == NW - 1) {
+            if (last) {
+                __syncwarp();
+                if (lane == 0) {
                     __threadfence_block();
-                    drained[stage] = 0;
-                    issue(stage);
+                    if (atomicAdd(&drained[stage], 1) == NW - 1) {
+                        __threadfence_block();
+                        drained[stage] = 0;
+                        issue(stage);
+                    }
                 }
             }
             sym_flush_warp<MODE, DIM, NSETS>(wbuf, a.jpart + ((size_t)it.w + t) * kT * C + wid * 16 * C, lane);
-            if (++stage == NST) {
+            if (last && ++stage == NST) {
                 stage = 0;
                 phase ^= 1u;
             }
