@@ -47,6 +47,9 @@ constexpr int kBfsUnroll = FDL_BFS_UNROLL;
 #ifndef FDL_P2_CTAS
 #define FDL_P2_CTAS 3  // CTAs per SM of the 2-D PCG matvec pass
 #endif
+#ifndef FDL_TPS_P1
+#define FDL_TPS_P1 1  // 4-bit P1 (fused / one set) and P1A: tiles per TMA stage
+#endif
 #ifndef FDL_TPS_P2
 #define FDL_TPS_P2 2  // 4-bit P2: tiles of one work item per TMA stage (one mbarrier wait / refill each)
 #endif
@@ -173,7 +176,7 @@ __host__ __device__ constexpr int sym_ps()
 template <int MODE, int HB>
 __host__ __device__ constexpr int sym_tps()
 {
-    return (MODE == kSymP2 && HB == 0) ? FDL_TPS_P2 : 1;
+    return (MODE == kSymP2 && HB == 0) ? FDL_TPS_P2 : ((MODE == kSymP1 || MODE == kSymP1A) && HB == 0 ? FDL_TPS_P1 : 1);
 }
 
 template <int MODE, int DIM, int NSETS, int HB>
