@@ -162,7 +162,7 @@ struct fdl_ctx {
     int device = 0;
     int sm_count = 148;
     int nblk = 0;  // 256-row reduction blocks of the vector kernels
-    int grid_p1[3] = {0, 0, 0}, grid_p2 = 0, grid_diag = 0, grid_enum = 0, grid_p1s = 0, grid_p1a = 0;
+    int grid_p1[3] = {0, 0, 0}, grid_p2 = 0, grid_diag = 0, grid_enum = 0, grid_p1s = 0, grid_p1a = 0, grid_p1r = 0;
     bool p1_split = false;  // P1 over {X^{k+1}, Xt} computes R of Xt only (R(X^{k+1}) on rejection)
     cudaStream_t stream = nullptr, own_stream = nullptr;
     // device memory
@@ -477,7 +477,8 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
     const int dim = ctx->dim;
     const bool p1 = mode == kSymP1 || mode == kSymP1S || mode == kSymP1A;
     const int C = mode == kSymP1 ? nsets * dim
-                                 : (mode == kSymP1A ? 2 * dim : ((mode == kSymP2 || mode == kSymP1S) ? dim : 1));
+                                 : (mode == kSymP1A ? 2 * dim
+                                                    : ((mode == kSymP2 || mode == kSymP1S || mode == kSymP1R) ? dim : 1));
     const int D0 = (mode == kSymP1 || mode == kSymP1A) ? dim : C;  // P1A: R into out0, L^W X into out1
     const int inter = (mode == kSymP1 && nsets == 2) ? 1 : 0;  // P1 two sets: components interleaved by set
     SymArgs a;
@@ -493,10 +494,15 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
     a.alpha = (float)ctx->alpha;
     const int grid = mode == kSymP1S   ? ctx->grid_p1s
                      : mode == kSymP1A ? ctx->grid_p1a
+                     : mode == kSymP1R ? ctx->grid_p1r
                      : (mode == kSymP1 ? ctx->grid_p1[nsets] : (mode == kSymP2 ? ctx->grid_p2 : ctx->grid_diag));
-    const int mk = mark_begin(ctx, mode == kSymP1S ? 4 : (p1 ? 1 : (mode == kSymP2 ? 2 : 3)));
+    const int mk = mark_begin(ctx, mode == kSymP1S ? 4 : ((p1 || mode == kSymP1R) ? 1 : (mode == kSymP2 ? 2 : 3)));
     if (ctx->nitems > 0) FDL_LAUNCH(launch_sym(a, mode, dim, nsets, ctx->hb, grid, ctx->stream));
     mark_end(ctx, mk);
+    if (mode == kSymP1R) {  // R-only rejection pass: a P1 launch (its time is P1 time)
+        ctx->stats.p1_launches++;
+        ctx->stats.p1_pairs += ctx->local_pairs;
+    }
     if (p1) {
         ctx->stats.p1_launches++;
         ctx->stats.p1_pairs += ctx->local_pairs * (uint64_t)nsets;
@@ -1023,8 +1029,10 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     ctx->grid_diag = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymDiag, dim, 1, ctx->hb)));
     ctx->grid_enum = std::max(1, std::min(cap_items, ctx->sm_count * 2));
     ctx->grid_p1s = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymP1S, dim, 2, ctx->hb)));
-    if (!ctx->general)
+    if (!ctx->general) {
         ctx->grid_p1a = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymP1A, dim, 1, ctx->hb)));
+        ctx->grid_p1r = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymP1R, dim, 1, ctx->hb)));
+    }
     // large problems: the extra host sync of the split P1 is negligible against the pass
     ctx->use_graphs = ctx->p.use_graphs == 1 || (ctx->p.use_graphs < 0 && !ctx->distributed && (int64_t)n * n < (int64_t)1 << 30);
     ctx->p1_split = !ctx->general &&
@@ -1193,7 +1201,7 @@ fdl_status enqueue_epilogue(fdl_ctx* ctx, const StepShape& sh)
             FDL_CUDA(cudaStreamSynchronize(s));
             if (!(ctx->sc_host->f_set[1] <= ctx->sc_host->f_set[0])) {
                 FDL_LAUNCH(launch_stage_pos1(ctx->Xn, ctx->posf, n, 0, dim, ps_p1(dim, 1), s));
-                FDL_TRY(run_sym(ctx, kSymP1, 1, ctx->posf, ctx->R1, nullptr, 0));
+                FDL_TRY(run_sym(ctx, kSymP1R, 1, ctx->posf, ctx->R1, nullptr, 0));  // R only: f(X^{k+1}) is known
                 ctx->stats.p1_rejected++;
             }
         } else {

@@ -158,14 +158,16 @@ __device__ __forceinline__ float chunk_hop(const uint4& ch, int r, int cc, uint3
 template <int MODE, int DIM, int NSETS>
 __host__ __device__ constexpr int sym_ncomp()
 {
-    return MODE == kSymP1 ? NSETS * DIM : (MODE == kSymP1A ? 2 * DIM : ((MODE == kSymP2 || MODE == kSymP1S) ? DIM : 1));
+    return MODE == kSymP1 ? NSETS * DIM
+                          : (MODE == kSymP1A ? 2 * DIM : ((MODE == kSymP2 || MODE == kSymP1S || MODE == kSymP1R) ? DIM : 1));
 }
 
 // floats per vertex in the staged position vector
 template <int MODE, int DIM, int NSETS>
 __host__ __device__ constexpr int sym_ps()
 {
-    return (MODE == kSymP1 || MODE == kSymP1S || MODE == kSymP1A) ? (DIM == 2 ? (NSETS == 1 ? 2 : 4) : (NSETS == 1 ? 4 : 8))
+    return (MODE == kSymP1 || MODE == kSymP1S || MODE == kSymP1A || MODE == kSymP1R)
+               ? (DIM == 2 ? (NSETS == 1 ? 2 : 4) : (NSETS == 1 ? 4 : 8))
                           : (MODE == kSymP2 ? (DIM == 2 ? 2 : 4) : 4);
 }
 
@@ -176,7 +178,8 @@ __host__ __device__ constexpr int sym_ps()
 template <int MODE, int HB>
 __host__ __device__ constexpr int sym_tps()
 {
-    return (MODE == kSymP2 && HB == 0) ? FDL_TPS_P2 : ((MODE == kSymP1 || MODE == kSymP1A) && HB == 0 ? FDL_TPS_P1 : 1);
+    return (MODE == kSymP2 && HB == 0) ? FDL_TPS_P2
+                                       : ((MODE == kSymP1 || MODE == kSymP1A || MODE == kSymP1R) && HB == 0 ? FDL_TPS_P1 : 1);
 }
 
 template <int MODE, int DIM, int NSETS, int HB>
@@ -205,7 +208,8 @@ __host__ __device__ constexpr int sym_ctas_per_sm()
 {
     return (MODE == kSymP2 && DIM == 2)    ? FDL_P2_CTAS
            : (MODE == kSymP1A && DIM == 2) ? FDL_P1A_CTAS
-                                           : ((DIM == 2 || (MODE != kSymP1 && MODE != kSymP1S && MODE != kSymP1A)) ? 2 : 1);
+                                           : ((DIM == 2 || (MODE != kSymP1 && MODE != kSymP1S && MODE != kSymP1A &&
+                                                            MODE != kSymP1R)) ? 2 : 1);
 }
 
 // TMA ring depth: as many stages (2..4) as the shared memory left by the
@@ -353,9 +357,9 @@ __device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float
         upk(ffma2(u, u, pk(s[0], s[1])), s0, s1);
         s[0] = s0;
         s[1] = s1;
-    } else if (MODE == kSymP1 && DIM == 2) {
+    } else if ((MODE == kSymP1 || MODE == kSymP1R) && DIM == 2) {
         // one set, 2-D: (x, y) as a packed pair for delta and the R updates (same
-        // per-element IEEE operations and order as the scalar code below)
+        // per-element IEEE operations and order as the scalar code below); P1R: R only
         const u64 d = fsub2(pk(xi[0], xi[1]), pk(xj[0], xj[1]));
         float dx, dy;
         upk(d, dx, dy);
@@ -374,8 +378,8 @@ __device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float
         upk(ffma2(qq, d, pk(aj[0], aj[1])), lo, hi);
         aj[0] = lo;
         aj[1] = hi;
-        s[0] = fmaf(u, u, s[0]);
-    } else if (MODE == kSymP1) {
+        if (MODE == kSymP1) s[0] = fmaf(u, u, s[0]);
+    } else if (MODE == kSymP1 || MODE == kSymP1R) {
         float d[DIM];
         float r2 = FLT_MIN;
 #pragma unroll
@@ -394,7 +398,7 @@ __device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float
             ai[c] = fmaf(q, d[c], ai[c]);
             aj[c] = fmaf(q, d[c], aj[c]);
         }
-        s[0] = fmaf(u, u, s[0]);
+        if (MODE == kSymP1) s[0] = fmaf(u, u, s[0]);
     } else if (MODE == kSymP1A) {
         // one set: stress and R as the 1-set P1 pass (same operations and order, so
         // R and f are bitwise those of kSymP1), plus (L^W X)_i = sum_j w_ij (x_i - x_j)
@@ -705,7 +709,8 @@ __device__ __forceinline__ void sym_flush_warp(const float* wbuf, float* jpart_w
 {
     constexpr int C = sym_ncomp<MODE, DIM, NSETS>();
     constexpr int P = sym_jpitch<MODE, DIM, NSETS>();
-    constexpr float SIGN = (MODE == kSymP1 || MODE == kSymP1S || MODE == kSymP1A) ? -1.0f : 1.0f;  // P1 antisymmetric; P2, DIAG symmetric
+    constexpr float SIGN = (MODE == kSymP1 || MODE == kSymP1S || MODE == kSymP1A || MODE == kSymP1R)
+                               ? -1.0f : 1.0f;  // P1 antisymmetric; P2, DIAG symmetric
     __syncwarp();
 #pragma unroll
     for (int e0 = 0; e0 < 16 * C; e0 += 32) {
@@ -907,6 +912,7 @@ cudaError_t launch_sym(const SymArgs& a, int mode, int dim, int nsets, int hb, i
     FDL_SYM_ALLHB(kSymP1, 2, 1) FDL_SYM_ALLHB(kSymP1, 2, 2) FDL_SYM_ALLHB(kSymP1, 3, 1) FDL_SYM_ALLHB(kSymP1, 3, 2)
     FDL_SYM_ALLHB(kSymP1S, 2, 2) FDL_SYM_ALLHB(kSymP1S, 3, 2)
     FDL_SYM_ALLHB(kSymP1A, 2, 1) FDL_SYM_ALLHB(kSymP1A, 3, 1)
+    FDL_SYM_ALLHB(kSymP1R, 2, 1) FDL_SYM_ALLHB(kSymP1R, 3, 1)
     FDL_SYM_CASE(kSymP1, 2, 1, 4) FDL_SYM_CASE(kSymP1, 2, 2, 4) FDL_SYM_CASE(kSymP1, 3, 1, 4)
     FDL_SYM_CASE(kSymP1, 3, 2, 4) FDL_SYM_CASE(kSymP2, 2, 1, 4) FDL_SYM_CASE(kSymP2, 3, 1, 4)
     FDL_SYM_CASE(kSymDiag, 2, 1, 4) FDL_SYM_CASE(kSymDiag, 3, 1, 4)
@@ -1246,6 +1252,7 @@ int sym_max_ctas(int mode, int dim, int nsets, int hb)
     FDL_SYM_OCC3(kSymP1, 2, 1) FDL_SYM_OCC3(kSymP1, 2, 2) FDL_SYM_OCC3(kSymP1, 3, 1) FDL_SYM_OCC3(kSymP1, 3, 2)
     FDL_SYM_OCC3(kSymP1S, 2, 2) FDL_SYM_OCC3(kSymP1S, 3, 2)
     FDL_SYM_OCC3(kSymP1A, 2, 1) FDL_SYM_OCC3(kSymP1A, 3, 1)
+    FDL_SYM_OCC3(kSymP1R, 2, 1) FDL_SYM_OCC3(kSymP1R, 3, 1)
     FDL_SYM_OCC(kSymP1, 2, 1, 4) FDL_SYM_OCC(kSymP1, 2, 2, 4) FDL_SYM_OCC(kSymP1, 3, 1, 4)
     FDL_SYM_OCC(kSymP1, 3, 2, 4) FDL_SYM_OCC(kSymP2, 2, 1, 4) FDL_SYM_OCC(kSymP2, 3, 1, 4)
     FDL_SYM_OCC(kSymDiag, 2, 1, 4) FDL_SYM_OCC(kSymDiag, 3, 1, 4)
