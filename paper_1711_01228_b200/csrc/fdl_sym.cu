@@ -41,6 +41,9 @@
 #define FDL_BFS_UNROLL 4  // neighbour frontier loads in flight per warp (MS-BFS)
 #endif
 constexpr int kBfsUnroll = FDL_BFS_UNROLL;
+#ifndef FDL_P1S_CTAS
+#define FDL_P1S_CTAS 2  // CTAs per SM of the 2-D line-6 pass
+#endif
 #ifndef FDL_P1A_CTAS
 #define FDL_P1A_CTAS 2  // CTAs per SM of the 2-D fused evaluation pass
 #endif
@@ -208,6 +211,7 @@ __host__ __device__ constexpr int sym_ctas_per_sm()
 {
     return (MODE == kSymP2 && DIM == 2)    ? FDL_P2_CTAS
            : (MODE == kSymP1A && DIM == 2) ? FDL_P1A_CTAS
+           : (MODE == kSymP1S && DIM == 2) ? FDL_P1S_CTAS
                                            : ((DIM == 2 || (MODE != kSymP1 && MODE != kSymP1S && MODE != kSymP1A &&
                                                             MODE != kSymP1R)) ? 2 : 1);
 }
