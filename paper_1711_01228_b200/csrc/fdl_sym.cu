@@ -23,6 +23,7 @@
 // partials (j side, per tile) and fp64 segment partials (i side, stress),
 // summed per row in a fixed order by k_sym_reduce: deterministic, no atomics.
 #include <algorithm>
+#include <atomic>
 #include <cfloat>
 #include <cstdint>
 
@@ -892,17 +893,27 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
     }
 }
 
+// Opt-in dynamic shared memory of a kernel, once per device (thread-safe: contexts of
+// several ranks may launch from several host threads, e.g. the loopback group)
+template <typename K>
+static cudaError_t ensure_smem_attr(K* fn, size_t sm, std::atomic<uint32_t>& done)
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint32_t bit = 1u << (dev & 31);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+    return e;
+}
+
 template <int MODE, int DIM, int NSETS, int HB>
 static cudaError_t launch_sym_t(const SymArgs& a, int grid, cudaStream_t s)
 {
     const size_t sm = sym_smem_bytes<MODE, DIM, NSETS, HB>();
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e =
-            cudaFuncSetAttribute(k_sym<MODE, DIM, NSETS, HB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static std::atomic<uint32_t> attr{0};
+    const cudaError_t e = ensure_smem_attr(k_sym<MODE, DIM, NSETS, HB>, sm, attr);
+    if (e != cudaSuccess) return e;
     k_sym<MODE, DIM, NSETS, HB><<<grid, 256, sm, s>>>(a);
     return cudaGetLastError();
 }
@@ -1215,13 +1226,9 @@ template <int DIM, int HB>
 static cudaError_t launch_enum_t(const SymArgs& a, const EnumOmegas& w, int grid, cudaStream_t s)
 {
     constexpr size_t sm = (size_t)kEnumStages * enum_stage_bytes<DIM, HB>();
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_enum<DIM, HB, kEnumNC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)sm);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static std::atomic<uint32_t> attr{0};
+    const cudaError_t e = ensure_smem_attr(k_enum<DIM, HB, kEnumNC>, sm, attr);
+    if (e != cudaSuccess) return e;
     k_enum<DIM, HB, kEnumNC><<<grid, 256, sm, s>>>(a, w);
     return cudaGetLastError();
 }
