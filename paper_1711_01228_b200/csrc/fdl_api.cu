@@ -582,6 +582,32 @@ fdl_status upload_positions(fdl_ctx* ctx, const double* X)
     return eval_current(ctx);
 }
 
+// Temporary device buffers of one call, freed on every return path.
+struct Scratch {
+    std::vector<void*> bufs;
+    ~Scratch()
+    {
+        for (void* q : bufs) cudaFree(q);
+    }
+    template <typename T>
+    cudaError_t alloc(T** p, size_t bytes)
+    {
+        void* q = nullptr;
+        const cudaError_t e = cudaMalloc(&q, bytes);
+        if (e == cudaSuccess) bufs.push_back(q);
+        *p = static_cast<T*>(q);
+        return e;
+    }
+    void release(void* q)
+    {
+        for (auto& b : bufs)
+            if (b == q) {
+                cudaFree(b);
+                b = nullptr;
+            }
+    }
+};
+
 // ------------------------------------------------------------------ MS-BFS
 // Sources: the rows of the blocks I of the local tiles.  Writes the upper
 // triangle tiles of the local range; the Jacobi diagonal follows from one
@@ -593,11 +619,12 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
     int32_t* d_col = nullptr;
     uint32_t *fa = nullptr, *fb = nullptr, *vis = nullptr;
     const size_t masks = (size_t)n * kBFSWords;
-    FDL_CUDA(cudaMalloc(&d_rp, sizeof(int64_t) * (n + 1)));
-    FDL_CUDA(cudaMalloc(&d_col, sizeof(int32_t) * std::max<int64_t>(rp[n], 1)));
-    FDL_CUDA(cudaMalloc(&fa, masks * 4));
-    FDL_CUDA(cudaMalloc(&fb, masks * 4));
-    FDL_CUDA(cudaMalloc(&vis, masks * 4));
+    Scratch tmp;
+    FDL_CUDA(tmp.alloc(&d_rp, sizeof(int64_t) * (n + 1)));
+    FDL_CUDA(tmp.alloc(&d_col, sizeof(int32_t) * std::max<int64_t>(rp[n], 1)));
+    FDL_CUDA(tmp.alloc(&fa, masks * 4));
+    FDL_CUDA(tmp.alloc(&fb, masks * 4));
+    FDL_CUDA(tmp.alloc(&vis, masks * 4));
     FDL_CUDA(cudaMemcpyAsync(d_rp, rp, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, ctx->stream));
     if (rp[n] > 0)
         FDL_CUDA(cudaMemcpyAsync(d_col, col, sizeof(int32_t) * rp[n], cudaMemcpyHostToDevice, ctx->stream));
@@ -644,7 +671,7 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
         int diam = 0;
         uint8_t* bbuf = nullptr;
         const size_t bbytes = (size_t)n * bfs_row_bytes_host(hb);
-        FDL_CUDA(cudaMalloc(&bbuf, bbytes));
+        FDL_CUDA(tmp.alloc(&bbuf, bbytes));
         for (int s0 = src_lo; s0 < src_hi && !overflow; s0 += 32 * kBFSWords) {
             const int nsrc = std::min(32 * kBFSWords, src_hi - s0);
             FDL_CUDA(cudaMemsetAsync(bbuf, 0, bbytes, ctx->stream));
@@ -669,7 +696,7 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
                 FDL_LAUNCH(launch_bfs_retile(bbuf, ctx->D, n, s0, nsrc, ctx->nb, ctx->t0, ctx->t1, hb, ctx->stream));
         }
         FDL_CUDA(cudaStreamSynchronize(ctx->stream));
-        cudaFree(bbuf);
+        tmp.release(bbuf);
         if (!overflow) {
             ctx->diameter = diam;
             if (hb == 0) FDL_LAUNCH(launch_nib_encode(ctx->D, dbytes, ctx->stream));
@@ -681,23 +708,17 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
         }
         ++hb;
     }
-    cudaFree(d_rp);
-    cudaFree(d_col);
-    cudaFree(fa);
-    cudaFree(fb);
-    cudaFree(vis);
     if (st != FDL_OK) return st;
     if (ctx->distributed) {
         // every rank BFSed only its sources: agree on the diameter and hop width (max over ranks)
         int* dd = nullptr;
-        FDL_CUDA(cudaMalloc(&dd, sizeof(int) * 2 * ctx->world));
+        FDL_CUDA(tmp.alloc(&dd, sizeof(int) * 2 * ctx->world));
         int mine[2] = {ctx->diameter, ctx->hb};
         FDL_CUDA(cudaMemcpyAsync(dd + 2 * ctx->rank, mine, sizeof mine, cudaMemcpyHostToDevice, ctx->stream));
         fdl_status s2 = allgather_inplace(ctx, dd, 2, ncclInt32, 4);
         std::vector<int> all(2 * ctx->world);
         cudaMemcpyAsync(all.data(), dd, sizeof(int) * 2 * ctx->world, cudaMemcpyDeviceToHost, ctx->stream);
         cudaStreamSynchronize(ctx->stream);
-        cudaFree(dd);
         FDL_TRY(s2);
         for (int g = 0; g < ctx->world; ++g) ctx->diameter = std::max(ctx->diameter, all[2 * g]);
     }
@@ -713,16 +734,17 @@ fdl_status build_dists(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, cons
     const int64_t m = std::max<int64_t>(rp[n], 1);
     // sources per batch: up to 1024, within ~1 GB of fp64 distance buffers
     const int S = (int)std::max<int64_t>(32, std::min<int64_t>(1024, ((int64_t)1 << 30) / (8 * (int64_t)n) / 32 * 32));
+    Scratch tmp;
     int64_t* d_rp = nullptr;
     int32_t* d_col = nullptr;
     double *d_len = nullptr, *da = nullptr, *dmax = nullptr;
-    FDL_CUDA(cudaMalloc(&d_rp, sizeof(int64_t) * (n + 1)));
-    FDL_CUDA(cudaMalloc(&d_col, sizeof(int32_t) * m));
-    FDL_CUDA(cudaMalloc(&d_len, sizeof(double) * m));
-    FDL_CUDA(cudaMalloc(&da, sizeof(double) * (size_t)n * S));
+    FDL_CUDA(tmp.alloc(&d_rp, sizeof(int64_t) * (n + 1)));
+    FDL_CUDA(tmp.alloc(&d_col, sizeof(int32_t) * m));
+    FDL_CUDA(tmp.alloc(&d_len, sizeof(double) * m));
+    FDL_CUDA(tmp.alloc(&da, sizeof(double) * (size_t)n * S));
     int* stamp = nullptr;
-    FDL_CUDA(cudaMalloc(&stamp, sizeof(int) * n));
-    FDL_CUDA(cudaMalloc(&dmax, sizeof(double)));
+    FDL_CUDA(tmp.alloc(&stamp, sizeof(int) * n));
+    FDL_CUDA(tmp.alloc(&dmax, sizeof(double)));
     FDL_CUDA(cudaMemsetAsync(dmax, 0, sizeof(double), ctx->stream));
     std::vector<double> ones;
     const double* lens = edge_len;
@@ -775,12 +797,6 @@ fdl_status build_dists(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, cons
     FDL_CUDA(cudaMemcpyAsync(&mx, dmax, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     FDL_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx->diameter = (int)std::ceil(mx);
-    cudaFree(d_rp);
-    cudaFree(d_col);
-    cudaFree(d_len);
-    cudaFree(da);
-    cudaFree(stamp);
-    cudaFree(dmax);
     return FDL_OK;
 }
 
@@ -1783,9 +1799,10 @@ fdl_status fdl_get_hop_rows(fdl_ctx* ctx, int32_t r0, int32_t nrows, uint16_t* o
     int* d_rows = nullptr;
     int* d_missing = nullptr;
     uint16_t* d_out = nullptr;
-    FDL_CUDA(cudaMalloc(&d_rows, sizeof(int) * nrows));
-    FDL_CUDA(cudaMalloc(&d_missing, sizeof(int)));
-    FDL_CUDA(cudaMalloc(&d_out, sizeof(uint16_t) * (size_t)nrows * ctx->n));
+    Scratch tmp;
+    FDL_CUDA(tmp.alloc(&d_rows, sizeof(int) * nrows));
+    FDL_CUDA(tmp.alloc(&d_missing, sizeof(int)));
+    FDL_CUDA(tmp.alloc(&d_out, sizeof(uint16_t) * (size_t)nrows * ctx->n));
     cudaMemcpyAsync(d_rows, rows.data(), sizeof(int) * nrows, cudaMemcpyHostToDevice, ctx->stream);
     cudaMemsetAsync(d_missing, 0, sizeof(int), ctx->stream);
     cudaError_t e = launch_hop_rows(ctx->D, ctx->hb, ctx->nb, ctx->t0, ctx->t1, d_rows, nrows, ctx->n, d_out,
@@ -1796,9 +1813,6 @@ fdl_status fdl_get_hop_rows(fdl_ctx* ctx, int32_t r0, int32_t nrows, uint16_t* o
         cudaMemcpyAsync(&missing, d_missing, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
         e = cudaStreamSynchronize(ctx->stream);
     }
-    cudaFree(d_rows);
-    cudaFree(d_missing);
-    cudaFree(d_out);
     FDL_CUDA(e);
     if (missing) return set_err(ctx, FDL_E_INVALID_ARG, "some requested entries live in tiles of other ranks");
     return FDL_OK;
@@ -1815,26 +1829,24 @@ fdl_status fdl_get_dist_rows(fdl_ctx* ctx, int32_t r0, int32_t nrows, double* ou
     int* d_rows = nullptr;
     int* d_missing = nullptr;
     float* d_out = nullptr;
-    FDL_CUDA(cudaMalloc(&d_rows, sizeof(int) * nrows));
-    FDL_CUDA(cudaMalloc(&d_missing, sizeof(int)));
-    FDL_CUDA(cudaMalloc(&d_out, sizeof(float) * cnt));
+    Scratch tmp;
+    FDL_CUDA(tmp.alloc(&d_rows, sizeof(int) * nrows));
+    FDL_CUDA(tmp.alloc(&d_missing, sizeof(int)));
+    FDL_CUDA(tmp.alloc(&d_out, sizeof(float) * cnt));
     cudaMemcpyAsync(d_rows, rows.data(), sizeof(int) * nrows, cudaMemcpyHostToDevice, ctx->stream);
     cudaMemsetAsync(d_missing, 0, sizeof(int), ctx->stream);
     cudaError_t e = launch_dist_rows(ctx->D, ctx->hb, ctx->nb, ctx->t0, ctx->t1, d_rows, nrows, ctx->n, d_out,
                                      d_missing, ctx->stream);
     int missing = 0;
-    std::vector<float> tmp(cnt);
+    std::vector<float> host(cnt);
     if (e == cudaSuccess) {
-        cudaMemcpyAsync(tmp.data(), d_out, sizeof(float) * cnt, cudaMemcpyDeviceToHost, ctx->stream);
+        cudaMemcpyAsync(host.data(), d_out, sizeof(float) * cnt, cudaMemcpyDeviceToHost, ctx->stream);
         cudaMemcpyAsync(&missing, d_missing, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
         e = cudaStreamSynchronize(ctx->stream);
     }
-    cudaFree(d_rows);
-    cudaFree(d_missing);
-    cudaFree(d_out);
     FDL_CUDA(e);
     if (missing) return set_err(ctx, FDL_E_INVALID_ARG, "some requested entries live in tiles of other ranks");
-    for (size_t i = 0; i < cnt; ++i) out[i] = ctx->k * (double)tmp[i];
+    for (size_t i = 0; i < cnt; ++i) out[i] = ctx->k * (double)host[i];
     return FDL_OK;
 }
 
