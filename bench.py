@@ -399,6 +399,7 @@ def run_gpu(args):
                "iterations_per_sec": args.steps / (ms2 * 1e-3)}
 
     ffma_tf, _ = fdl.bench_ffma(local_rank)
+    l2_bytes = torch.cuda.get_device_properties(local_rank).L2_cache_size
     extra_p2_mix = {}
     # ceiling of the line-6 pass's own arithmetic (same per-tile function on a resident
     # tile, no HBM / pipeline / reductions): how much of the gap to peak is the mix itself
@@ -422,12 +423,16 @@ def run_gpu(args):
             "metric": "pair-interactions/sec", "value": value, "unit": "pair-interactions/sec",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f32 pair math / f64 reductions+state", "data": "synthetic",
+            "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{args.config}: BA n={n} m=3 |E|={g.num_edges}" if args.config == "C5"
                        else f"{args.config} n={n} |E|={g.num_edges}",
                        "dim": dim, "omega": cfg.omega, "k": k, "diameter": info.diameter,
                        "hop_bits": info.hop_bits, "parallelism": f"triangle-tile shard x{world} (NCCL all-gather of partials)",
-                       "l2": "inputs larger than L2 (hop matrix %.1f GB per GPU)" % (info.hop_matrix_bytes / 1e9)},
+                       "precision": "f32 pair arithmetic, f64 reductions, PCG state and positions",
+                       "l2": ("inputs larger than L2 (hop matrix %.1f GB per GPU, L2 %.0f MB)"
+                              % (info.hop_matrix_bytes / 1e9, l2_bytes / 1e6) if info.hop_matrix_bytes > l2_bytes else
+                              "no L2 flush: the hop matrix (%.1f MB) fits in L2 (%.0f MB), as it does in every step "
+                              "of a real run of this size" % (info.hop_matrix_bytes / 1e6, l2_bytes / 1e6))},
             "iterations_per_sec": its_per_s,
             "pcg_iters_per_step": st.cg_iters / max(st.steps, 1),
             "sor_accept_rate": accepted / max(args.steps, 1), "p1_rejected_passes": st.p1_rejected,
