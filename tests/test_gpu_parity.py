@@ -505,7 +505,7 @@ def test_enumerating_strategy_end_to_end(name):
 @pytest.mark.parametrize("name", ["C2", "C3"])
 def test_split_p1_bitwise(name):
     """The split line-6 pass (stresses of both candidates, R of Xt only, and a
-    1-set pass for R(X^{k+1}) when the guard rejects) gives bitwise the same
+    R-only 1-set pass for R(X^{k+1}) when the guard rejects) gives bitwise the same
     trajectory as the fused two-set pass (same per-pair fp32 arithmetic and
     the same fixed summation orders)."""
     cfg = configs.CONFIGS[name]
@@ -525,6 +525,7 @@ def test_split_p1_bitwise(name):
     assert out[0][0] == out[1][0]
     assert np.array_equal(out[0][1], out[1][1])
     assert out[1][2] == sum(1 for a in out[1][0] if not a[2])
+    assert out[1][2] > 0  # the R-only rejection pass (kSymP1R) ran
 
 
 # --------------------------------------------- NEXT-3: weighted graphs, general alpha
