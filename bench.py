@@ -13,8 +13,16 @@ evaluations + 1 repulsion evaluation (fused in one P1 pass) + one L^W matvec
 per P2 pass (1 + PCG iterations) -- SURVEY.md §8(d).  SOR iterations/sec is
 reported beside it.
 
-Launch: python bench.py [--gpus N --steps K --warmup W] (N>1 under torchrun,
-rows sharded over ranks, NCCL all-gathers; time = max over ranks).
+Every timed step is an iteration of a real trajectory: the runs use the
+config's own tolerance, and when the stop rule fires the layout restarts from
+X0 (fdl_set_positions) outside the timed brackets (each step is bracketed by
+CUDA events on the library's stream; restarts are not timed).  A separate leg
+times one whole fdl_run_until_converged from X0 (SURVEY §8(d)'s "SOR
+iterations/sec"; setup excluded).
+
+Launch: python bench.py [--gpus N --steps K --warmup W].  N > 1 under
+torch.distributed.run (one rank per GPU, NCCL); without it, bench.py re-launches
+itself under torch.distributed.run with N ranks.  Time = max over ranks.
 `--impl reference` times the fp64 CPU oracle (oracle/) on a bounded sample
 of the same workload.
 """
@@ -48,6 +56,12 @@ P1_FLOPS_PER_PAIR_SET = {2: 18, 3: 25}
 # of which the R_i/R_j updates (2d + 2d): not done for the stress-only set of the split pass
 P1_FLOPS_R_PER_PAIR_SET = {2: 8, 3: 12}
 P1_FLOPS_PER_PAIR_DECODE = 1
+# SURVEY.md §8(d) (lines 753-757) counts the method's own work per unordered pair of the
+# line-6 pass: 2 stress evaluations x (2d + 4) flops + R for both rows 2d FMA = 4d flops
+# (2-D: 24, 3-D: 32).  The roofline's headline `achieved` uses this count; the builder's
+# instruction-level count (above: 29 in 2-D) is reported beside it.
+def survey_flops_line6(dim: int) -> int:
+    return 2 * (2 * dim + 4) + 4 * dim
 
 
 def parse_args():
@@ -63,7 +77,48 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-rows", type=int, default=0)
+    ap.add_argument("--no-run-leg", action="store_true", help="skip the whole-run (fdl_run_until_converged) leg")
+    ap.add_argument("--plumbing-only", action="store_true",
+                    help="test hook: ranks join a gloo group and report; no GPU work (tests/test_bench_spawn.py)")
     return ap.parse_args()
+
+
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` without torch.distributed.run: re-launch this script as N ranks
+    (one process per GPU) on 127.0.0.1 and return the launcher's exit code.  Rank 0
+    prints the JSON line; NCCL's INIT log goes to stderr so the ranks can be counted
+    without mixing it into the JSON output."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def run_plumbing(args):
+    """Rank bootstrap only (gloo): what the spawned ranks do before any GPU work,
+    reported as one JSON line by rank 0 (CPU test of the spawn path)."""
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo")
+    world, rank = dist.get_world_size(), dist.get_rank()
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"plumbing": True, "n_gpus": world, "max_rank_plus_one": float(t.item()),
+                          "ranks_env": [os.environ.get("LOCAL_RANK"), os.environ.get("WORLD_SIZE")]}), flush=True)
+    dist.destroy_process_group()
 
 
 # ------------------------------------------------------------------ clocks
@@ -225,6 +280,25 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ GPU leg
+def _stats_sub(a, b):
+    """Field-wise a - b of two fdl stats records (b may be None)."""
+    if b is None:
+        return a
+    out = type(a)()
+    for f, _ in a._fields_:
+        setattr(out, f, getattr(a, f) - getattr(b, f))
+    return out
+
+
+def _stats_add(a, b):
+    if a is None:
+        return b
+    out = type(b)()
+    for f, _ in b._fields_:
+        setattr(out, f, getattr(a, f) + getattr(b, f))
+    return out
+
+
 def run_gpu(args):
     import torch
 
@@ -255,8 +329,8 @@ def run_gpu(args):
     n = g.n
     k = cfg.k_for(n)
     X0 = configs.positions_for(args.config, n, args.seed)
-    p = fdl.make_params(dim=cfg.dim, k=k, omega=cfg.omega, tol=1e-12, max_iter=100000, device=local_rank,
-                        cg_rtol=max(float(os.environ.get("FDL_CG_RTOL_F", "1e-2")) * cfg.tol, 1e-9),  # the config's solve tolerance (R8); tol only keeps the timed steps running
+    p = fdl.make_params(dim=cfg.dim, k=k, omega=cfg.omega, tol=cfg.tol, max_iter=cfg.max_iter, device=local_rank,
+                        cg_rtol=max(float(os.environ.get("FDL_CG_RTOL_F", "1e-2")) * cfg.tol, 1e-9),  # the config's solve tolerance (R8)
                         cg_extrap=int(os.environ.get("FDL_CG_EXTRAP", "2")),
                         p1_split=int(os.environ.get("FDL_P1_SPLIT", "-1")),
                         strategy={"fixed": fdl.STRAT_FIXED, "prob": fdl.STRAT_PROB, "enum": fdl.STRAT_ENUM}[args.strategy])
@@ -265,7 +339,11 @@ def run_gpu(args):
         L = fdist.sharded_layout(g, p, X0, edge_len=configs.edge_lengths_for(args.config))
     else:
         L = fdl.Layout.from_graph(g, params=p, init_pos=X0, edge_len=configs.edge_lengths_for(args.config))
-    stream = torch.cuda.current_stream()
+    # an explicit stream: the library enqueues everything on it and the timing events are
+    # recorded on it (torch's default stream has handle 0, which the library would replace
+    # by its own stream, unordered with events on the legacy stream)
+    stream = torch.cuda.Stream(device=local_rank)
+    torch.cuda.set_stream(stream)
     L.set_stream(stream.cuda_stream)
     L.set_timing(True)
     info = L.get_info()
@@ -275,23 +353,45 @@ def run_gpu(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    restarts = 0
+
+    def step_or_restart():
+        """One iteration of the trajectory; when its stop rule fires the layout
+        restarts from X0 (untimed), so every timed step is a real iteration."""
+        nonlocal restarts
+        inf = L.step()
+        if inf.stop:
+            L.set_positions(X0)
+            restarts += 1
+        return inf
+
     for _ in range(args.warmup):
-        L.step()
+        step_or_restart()
+    restarts = 0
     L.reset_stats()
     clocks = ClockSampler(local_rank)
     barrier()
     clocks.start()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
+    marks = []
     accepted = 0
+    st_excl = None  # stats of the untimed restarts (the P1A evaluation pass of set_positions)
     for _ in range(args.steps):
-        accepted += L.step().accepted
-    e1.record(stream)
+        ea = torch.cuda.Event(enable_timing=True)
+        eb = torch.cuda.Event(enable_timing=True)
+        ea.record(stream)
+        inf = L.step()
+        eb.record(stream)
+        marks.append((ea, eb))
+        accepted += inf.accepted
+        if inf.stop:
+            before = L.get_stats()
+            L.set_positions(X0)
+            restarts += 1
+            st_excl = _stats_add(st_excl, _stats_sub(L.get_stats(), before))
     barrier()
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    st = L.get_stats()
+    ms = sum(a.elapsed_time(b) for a, b in marks)
+    st = _stats_sub(L.get_stats(), st_excl) if st_excl is not None else L.get_stats()
     if dist is not None:
         ms = fdist.max_over_ranks(ms)
     pairs_unordered = n * (n - 1) / 2
@@ -316,6 +416,10 @@ def run_gpu(args):
         p1_flops_roof = st.p1_pairs_nor * (2 * P1_FLOPS_PER_PAIR_SET[dim] - P1_FLOPS_R_PER_PAIR_SET[dim]
                                            + P1_FLOPS_PER_PAIR_DECODE)
     p1_tf_roof = p1_flops_roof / (p1_ms_roof * 1e-3) / 1e12 if p1_ms_roof > 0 else 0.0
+    survey_flops_roof = None
+    if st.p1s_launches > 0 and st.p1s_ms > 0:
+        survey_flops_roof = st.p1_pairs_nor * survey_flops_line6(dim)
+        survey_tf_roof = survey_flops_roof / (p1_ms_roof * 1e-3) / 1e12
     # P2 streams the stored upper triangle: algorithmic bytes = 1 hop per unordered pair
     hop_bytes = info.hop_bits / 8.0
     p2_gbs = (st.p2_pairs * hop_bytes) / (st.p2_ms * 1e-3) / 1e9 if st.p2_ms > 0 else 0.0
@@ -329,6 +433,16 @@ def run_gpu(args):
                                "(MEASURED_PEAKS sm_max_mhz)",
                 "flops_per_launch": p1_flops_roof / max(p1_launches, 1),
                 "avg_launch_ms": p1_ms_roof / max(p1_launches, 1)}
+        if survey_flops_roof is not None:
+            roof.update({
+                "achieved": survey_tf_roof, "frac": survey_tf_roof / peak_tf,
+                "flops_per_pair": survey_flops_line6(dim),
+                "flop_count": "SURVEY §8(d): 2 stresses x (2d+4) + R of both rows 4d per unordered pair",
+                "flops_per_launch": survey_flops_roof / max(p1_launches, 1),
+                "builder_count": {"flops_per_pair": 2 * P1_FLOPS_PER_PAIR_SET[dim] - P1_FLOPS_R_PER_PAIR_SET[dim]
+                                  + P1_FLOPS_PER_PAIR_DECODE, "achieved": p1_tf_roof,
+                                  "frac": p1_tf_roof / peak_tf,
+                                  "note": "instruction-level count incl. r^2 h^2 and the h^2 decode (DESIGN §7)"}})
     else:
         hbm = peaks.get("hbm_gbs", 6650.0)
         roof = {"bound": "hbm", "kernel": "p2_lw_matvec", "achieved": p2_gbs, "peak": hbm, "unit": "GB/s",
@@ -374,9 +488,12 @@ def run_gpu(args):
         # trajectory as the device-timed ones (PCG counts depend on the phase of the run)
         Xh = torch.empty((n, dim), dtype=torch.float64, pin_memory=True).numpy()
         Xh[:] = X0
+        L.set_positions(X0)
         for _ in range(args.warmup):
             L.set_positions(Xh)
-            L.step()
+            if L.step().stop:
+                Xh[:] = X0
+                continue
             L.get_positions(Xh)
         L.reset_stats()
         barrier()
@@ -385,8 +502,10 @@ def run_gpu(args):
         e2.record(stream)
         for _ in range(args.steps):
             L.set_positions(Xh)          # H2D of the step's input; re-evaluates f, L^X X at it
-            L.step()
+            stop = L.step().stop
             L.get_positions(Xh)          # D2H of the result
+            if stop:                     # the trajectory converged: the next step restarts it
+                Xh[:] = X0
         e3.record(stream)
         barrier()
         ms2 = e2.elapsed_time(e3)
@@ -397,6 +516,29 @@ def run_gpu(args):
         e2e = {"value": sweeps2 * pairs_unordered / (ms2 * 1e-3), "unit": "pair-interactions/sec",
                "h2d_bytes_per_step": int(n * dim * 8), "d2h_bytes_per_step": int(n * dim * 8),
                "iterations_per_sec": args.steps / (ms2 * 1e-3)}
+
+    # ---- one whole run to the stop rule from X0 (SURVEY §8(d) "SOR iterations/sec":
+    # iterations / time of fdl_run_until_converged, setup excluded)
+    run_leg = None
+    if not args.no_run_leg:
+        L.set_positions(X0)
+        L.reset_stats()
+        barrier()
+        e4 = torch.cuda.Event(enable_timing=True)
+        e5 = torch.cuda.Event(enable_timing=True)
+        e4.record(stream)
+        r = L.run_until_converged()
+        e5.record(stream)
+        barrier()
+        ms4 = e4.elapsed_time(e5)
+        if dist is not None:
+            ms4 = fdist.max_over_ranks(ms4)
+        st4 = L.get_stats()
+        run_leg = {"iterations": r.iterations, "accepted": r.accepted, "stop": fdl.STOP.get(r.stop, r.stop),
+                   "pcg_iters": r.cg_iters, "ms": ms4, "iterations_per_sec": r.iterations / (ms4 * 1e-3),
+                   "pair_interactions_per_sec": (3 * st4.steps + st4.p2_launches) * n * (n - 1) / 2 / (ms4 * 1e-3),
+                   "f_initial": r.f_initial, "f_final": r.f_final, "setup_ms_excluded": info.setup_ms,
+                   "tol": cfg.tol}
 
     ffma_tf, _ = fdl.bench_ffma(local_rank)
     l2_bytes = torch.cuda.get_device_properties(local_rank).L2_cache_size
@@ -434,6 +576,11 @@ def run_gpu(args):
                               "no L2 flush: the hop matrix (%.1f MB) fits in L2 (%.0f MB), as it does in every step "
                               "of a real run of this size" % (info.hop_matrix_bytes / 1e6, l2_bytes / 1e6))},
             "iterations_per_sec": its_per_s,
+            "sor_iterations_per_sec": run_leg["iterations_per_sec"] if run_leg else None,
+            "run_to_convergence": run_leg,
+            "timing": ("sum of per-step CUDA-event intervals on the library's stream over K iterations of real "
+                       "trajectories (config tol %g); %d restart(s) from X0 at the stop rule, untimed"
+                       % (cfg.tol, restarts)),
             "pcg_iters_per_step": st.cg_iters / max(st.steps, 1),
             "sor_accept_rate": accepted / max(args.steps, 1), "p1_rejected_passes": st.p1_rejected,
             "kernel_share": ({"p1": p1_share, "p2": p2_share, "other": max(0.0, 1 - p1_share - p2_share)}
@@ -456,7 +603,11 @@ def run_gpu(args):
 
 def main():
     args = parse_args()
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(spawn_ranks(args))
+    if args.plumbing_only:
+        run_plumbing(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_gpu(args)

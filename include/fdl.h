@@ -64,10 +64,10 @@ typedef enum {
 
 typedef enum {
     FDL_STRAT_FIXED = 0, /* omega constant; omega = 0 is Algorithm 1           */
-    FDL_STRAT_PROB = 1,  /* roulette over {0.5,1,1.5,2} w.p. {.3,.3,.2,.2} each iteration */
-    FDL_STRAT_ENUM = 2   /* omega* = argmin_c f((1+w_c) X^{k+1} - w_c X^k) over w_c = c * enum_step,
+    FDL_STRAT_ENUM = 1,  /* omega* = argmin_c f((1+w_c) X^{k+1} - w_c X^k) over w_c = c * enum_step,
                             c = 0..enum_count-1 ({0, 0.5, ..., 9}); ties to the smaller
                             omega. Single GPU; no step cap                                  */
+    FDL_STRAT_PROB = 2   /* roulette over {0.5,1,1.5,2} w.p. {.3,.3,.2,.2} each iteration */
 } fdl_strategy;
 
 typedef enum {
@@ -260,7 +260,11 @@ fdl_status fdl_set_stream(fdl_ctx* ctx, void* cuda_stream);
 /* One Algorithm-2 iteration on the device; info may be NULL.
  * Errors: FDL_E_STATE once the run has stopped (info->stop of the last step says
  * why; fdl_set_positions restarts) or after an earlier CUDA error;
- * FDL_E_SOLVER if PCG reaches cg_max_iter before cg_rtol;
+ * FDL_E_SOLVER if PCG reaches cg_max_iter before cg_rtol: the step is
+ * not applied (placement, stress and iteration count stay those of X^k, in
+ * eager and CUDA-graph launches alike; the graph's lines 5-8 sit in an IF node
+ * on the solve's convergence flag), so the caller may raise cg_max_iter /
+ * cg_rtol through a new context or stop;
  * FDL_E_NONFINITE if the stress becomes NaN/Inf. */
 fdl_status fdl_step(fdl_ctx* ctx, fdl_iter_info* info);
 

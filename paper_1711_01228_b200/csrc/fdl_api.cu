@@ -906,6 +906,23 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     int ecc0 = 0;
     st = validate_graph(n, rp, col, msg, ecc0);
     if (st != FDL_OK) return set_err(ctx, st, msg);
+    if (edge_len) {  // the two stored directions of an edge carry the same length
+        for (int32_t v = 0; v < n; ++v)
+            for (int64_t e = rp[v]; e < rp[v + 1]; ++e) {
+                const int32_t u = col[e];
+                if (u < v) continue;  // each undirected edge once, from its smaller endpoint
+                int64_t r = -1;
+                for (int64_t f = rp[u]; f < rp[u + 1]; ++f)
+                    if (col[f] == v) {
+                        r = f;
+                        break;
+                    }
+                if (r < 0 || edge_len[r] != edge_len[e])
+                    return set_err(ctx, FDL_E_BAD_LENGTH,
+                                   "edge (" + std::to_string(v) + "," + std::to_string(u) +
+                                       ") has different lengths in its two directions (S:52)");
+            }
+    }
 
     ctx->p = p;
     ctx->n = n;
@@ -987,7 +1004,9 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
         if (world > 1 || ctx->distributed)
             return set_err(ctx, FDL_E_UNSUPPORTED, "the enumerating strategy runs on one GPU");
         FDL_ALLOC(ctx->spart_enum, (size_t)std::max(ctx->nitems, 1) * kEnumNC);
-        FDL_ALLOC(ctx->enum_f, (size_t)kEnumMax);
+        // candidate passes write kEnumNC stresses each at enum_f + c0 (c0 a multiple of
+        // kEnumNC), so the buffer holds kEnumMax rounded up to whole passes
+        FDL_ALLOC(ctx->enum_f, (size_t)((kEnumMax + kEnumNC - 1) / kEnumNC) * kEnumNC);
     }
     if (ctx->distributed) FDL_ALLOC(ctx->rparts, (size_t)world * ctx->npad * Cmax);
     FDL_ALLOC(ctx->diag, (size_t)ctx->npad);
@@ -1315,8 +1334,33 @@ fdl_status build_step_graph(fdl_ctx* ctx, const StepShape& sh, StepGraph& out)
     const StatDelta s2 = stat_snapshot(ctx);
     if (cudaStreamUpdateCaptureDependencies(s, &cnode, 1, cudaStreamSetCaptureDependencies) != cudaSuccess)
         return fail(FDL_E_CUDA);
+    // lines 5-8 inside an IF node on sc->done: a solve that hit cg_max_iter leaves the
+    // context as the eager step does (X^k, R^k, A^k untouched; FDL_E_SOLVER on the host)
+    cudaGraphConditionalHandle hif;
+    if (cudaGraphConditionalHandleCreate(&hif, g, 0, cudaGraphCondAssignDefault) != cudaSuccess)
+        return fail(FDL_E_CUDA);
+    if (launch_cond_done(ctx->sc, s, (unsigned long long)hif) != cudaSuccess) return fail(FDL_E_CUDA);
+    if (cudaStreamGetCaptureInfo(s, &cst, nullptr, &g, &deps, &ndeps) != cudaSuccess) return fail(FDL_E_CUDA);
+    cudaGraphNodeParams ip = {};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = hif;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    cudaGraphNode_t inode;
+    if (cudaGraphAddNode(&inode, g, deps, ndeps, &ip) != cudaSuccess) return fail(FDL_E_CUDA);
+    if (cudaStreamBeginCaptureToGraph(ctx->aux_stream, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+        return fail(FDL_E_CUDA);
+    ctx->stream = ctx->aux_stream;
     st = enqueue_epilogue(ctx, sh);
+    ctx->stream = s;
+    cudaGraph_t epi_out = nullptr;
+    const cudaError_t ee = cudaStreamEndCapture(ctx->aux_stream, &epi_out);
     if (st != FDL_OK) return fail(st);
+    if (ee != cudaSuccess) return fail(FDL_E_CUDA);
+    if (cudaStreamUpdateCaptureDependencies(s, &inode, 1, cudaStreamSetCaptureDependencies) != cudaSuccess)
+        return fail(FDL_E_CUDA);
+    ctx->stats.launches++;  // k_cond_done
     if (cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, s) != cudaSuccess)
         return fail(FDL_E_CUDA);
     const StatDelta s3 = stat_snapshot(ctx);

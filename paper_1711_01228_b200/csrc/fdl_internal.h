@@ -118,6 +118,7 @@ cudaError_t launch_cg_p(double* p, const double* z, float* pvec, const DevScalar
 // mode 0: after init (rz, rr, bb, sum z); 1: alpha from pAp; 2: beta + convergence
 // cond/use_cond: the WHILE-node handle of a captured step graph (continue = PCG not done
 // and cg_iters < cg_max); use_cond = 0 outside graphs
+cudaError_t launch_cond_done(const DevScalars* sc, cudaStream_t s, unsigned long long cond);
 cudaError_t launch_cg_finalize(const double* blk, int nblk, int dim, int mode, double rtol,
                                DevScalars* sc, HostScalars* hs, cudaStream_t s, unsigned long long cond = 0,
                                int use_cond = 0, int cg_max = 0);

@@ -1012,6 +1012,19 @@ cudaError_t launch_cg_finalize(const double* blk, int nblk, int dim, int mode, d
     return cudaGetLastError();
 }
 
+// IF node of the step graph: the epilogue (lines 5-8) runs only when the solve
+// converged, so a capped PCG leaves X^k, R^k, A^k as the eager step leaves them
+__global__ void k_cond_done(const DevScalars* sc, cudaGraphConditionalHandle cond)
+{
+    cudaGraphSetConditional(cond, sc->done ? 1u : 0u);
+}
+
+cudaError_t launch_cond_done(const DevScalars* sc, cudaStream_t s, unsigned long long cond)
+{
+    k_cond_done<<<1, 1, 0, s>>>(sc, (cudaGraphConditionalHandle)cond);
+    return cudaGetLastError();
+}
+
 // ============================================================ FFMA roofline
 // Peak FP32 microbenchmark: 8 independent FFMA chains per thread.
 __global__ void k_ffma(float* out, int iters)

@@ -900,10 +900,12 @@ static cudaError_t ensure_smem_attr(K* fn, size_t sm, std::atomic<uint32_t>& don
 {
     int dev = 0;
     cudaGetDevice(&dev);
-    const uint32_t bit = 1u << (dev & 31);
-    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    // one flag bit per ordinal 0..31; other ordinals set the attribute on every launch
+    const bool flagged = dev >= 0 && dev < 32;
+    const uint32_t bit = flagged ? 1u << dev : 0u;
+    if (flagged && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
     const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+    if (e == cudaSuccess && flagged) done.fetch_or(bit, std::memory_order_release);
     return e;
 }
 

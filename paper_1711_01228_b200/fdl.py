@@ -23,7 +23,7 @@ STATUS = {
     -13: "FDL_E_UNSUPPORTED", -14: "FDL_E_STATE",
 }
 STOP = {0: "none", 1: "rel_tol", 2: "zero_stress", 3: "max_iter"}
-STRAT_FIXED, STRAT_PROB, STRAT_ENUM = 0, 1, 2
+STRAT_FIXED, STRAT_ENUM, STRAT_PROB = 0, 1, 2  # include/fdl.h fdl_strategy
 
 EXPORTS = [
     "fdl_abi_version", "fdl_params_default", "fdl_create", "fdl_create_sharded", "fdl_shard_tiles",

@@ -143,22 +143,121 @@ def _gates(gpu_it, gpu_f, o):
     assert abs(gpu_it - o.iterations) <= max(1, math.ceil(0.02 * o.iterations)), (gpu_it, o.iterations)
 
 
-@pytest.mark.parametrize("seed", [1, 2, 3])
+def _mean_gate(gpu_its, oracle_its):
+    """the mean iteration count over the seed set within 2%
+    (the paper's numbers are 20-run means)."""
+    mg, mo = float(np.mean(gpu_its)), float(np.mean(oracle_its))
+    assert abs(mg - mo) <= 0.02 * mo, (gpu_its, oracle_its)
+
+
 @pytest.mark.parametrize("omega", [0.0, 1.5])
-def test_end_to_end_C1(seed, omega):
+def test_end_to_end_C1_seeds(omega):
+    """C1 over position seeds 1-5 (SURVEY §8(d) seed protocol): per-seed gates,
+    monotone stress, and the seed-mean iteration gate."""
     cfg = configs.CONFIGS["C1"]
-    g, k, X0, L = make("C1", seed=seed, omega=omega)
-    trace = []
-    while True:
-        info = L.step()
-        trace.append(info.f_after)
-        if info.stop:
+    its_g, its_o = [], []
+    for seed in range(1, 6):
+        g, k, X0, L = make("C1", seed=seed, omega=omega)
+        trace = []
+        while True:
+            info = L.step()
+            trace.append(info.f_after)
+            if info.stop:
+                break
+        fs = [L.info.f] + trace
+        L.close()
+        o = layout.run_algorithm2(layout.Problem(g, 2, k), X0, omega, cfg.tol, cfg.max_iter)
+        _gates(len(trace), trace[-1], o)
+        assert all(b <= a * (1 + 1e-9) for a, b in zip(fs, fs[1:]))
+        its_g.append(len(trace))
+        its_o.append(o.iterations)
+    _mean_gate(its_g, its_o)
+
+
+def test_end_to_end_C2_seeds():
+    """C2 (omega 1.6) over position seeds 1-5: per-seed and seed-mean gates."""
+    cfg = configs.CONFIGS["C2"]
+    its_g, its_o = [], []
+    for seed in range(1, 6):
+        g, k, X0, L = make("C2", seed=seed)
+        r = L.run_until_converged()
+        L.close()
+        o = layout.run_algorithm2(layout.Problem(g, 2, k), X0, cfg.omega, cfg.tol, cfg.max_iter)
+        _gates(r.iterations, r.f_final, o)
+        its_g.append(r.iterations)
+        its_o.append(o.iterations)
+    _mean_gate(its_g, its_o)
+
+
+@pytest.mark.parametrize("name,step_k", [("C1", 0.5), ("C2", 2.0)])
+def test_step_cap_and_maxdisp_vs_oracle(name, step_k):
+    """A finite cooling bound `step` (north_star; DESIGN R14: clamp
+    ||x~_i - x^{k+1}_i|| <= step before the guard) against oracle/layout.py's
+    cap_step in Algorithm 2, iteration by iteration: f(X^{k+1}), f(X~), the
+    guard decision and the max-displacement residual max_i ||x^{k+1}_i - x^k_i||
+    while the decisions agree, then the end-to-end gates.  The bound binds: the
+    first extrapolation omega * maxdisp exceeds it."""
+    cfg = configs.CONFIGS[name]
+    g = configs.graph_for(name)
+    k = cfg.k_for(g.n)
+    step = step_k * k
+    X0 = configs.positions_for(name, g.n, 1)
+    p = fdl.make_params(dim=2, k=k, omega=cfg.omega, tol=cfg.tol, max_iter=cfg.max_iter, step=step,
+                        cg_rtol=1e-10)
+    infos = []
+    with fdl.Layout.from_graph(g, params=p, init_pos=X0) as L:
+        while True:
+            info = L.step()
+            infos.append((info.f_next, info.f_relaxed, bool(info.accepted), info.f_after, info.maxdisp))
+            if info.stop:
+                break
+    o = layout.run_algorithm2(layout.Problem(g, 2, k), X0, cfg.omega, cfg.tol, cfg.max_iter, step=step)
+    assert cfg.omega * o.trace[0].maxdisp > 2 * step  # the cap changes X~ on the first step
+    # maxdisp is a difference of positions: near convergence (maxdisp ~ 1e-4 of the
+    # layout's extent) its error is the positions' own -- fp32 pair arithmetic
+    # accumulated along the trajectory (measured 1.5e-6 of the extent after 46 C2
+    # iterations) -- not a fraction of maxdisp
+    extent = float(np.abs(o.X).max())
+    checked = 0
+    for got, t in zip(infos, o.trace):
+        if got[2] != t.accepted:
             break
-    prob = layout.Problem(g, 2, k)
-    o = layout.run_algorithm2(prob, X0, omega, cfg.tol, cfg.max_iter)
-    _gates(len(trace), trace[-1], o)
-    fs = [L.info.f] + trace
-    assert all(b <= a * (1 + 1e-9) for a, b in zip(fs, fs[1:]))
+        assert abs(got[0] - t.f_next) / t.f_next <= 1e-5
+        assert abs(got[1] - t.f_relaxed) / t.f_relaxed <= 1e-5
+        assert abs(got[4] - t.maxdisp) <= 1e-4 * t.maxdisp + 1e-5 * extent, (got[4], t.maxdisp)
+        checked += 1
+    assert checked >= min(10, len(o.trace))
+    _gates(len(infos), infos[-1][3], o)
+
+
+def test_maxdisp_matches_unrelaxed_step():
+    """fdl_iter_info.maxdisp is max_i ||x^{k+1}_i - x^k_i|| of the UNRELAXED
+    solve (oracle/layout.py IterRecord.maxdisp): on C1's first steps it equals
+    the oracle's value within the solve/pair-arithmetic tolerance."""
+    cfg = configs.CONFIGS["C1"]
+    g, k, X0, L = make("C1", seed=2, cg_rtol=1e-10)
+    got = [L.step().maxdisp for _ in range(6)]
+    o = layout.run_algorithm2(layout.Problem(g, 2, k), X0, cfg.omega, 0.0, 6)
+    np.testing.assert_allclose(got, [t.maxdisp for t in o.trace], rtol=1e-5)
+
+
+def test_nonfinite_stress_is_reported():
+    """S:316 fault injection: a finite placement whose fp32 pair distances
+    overflow (coordinates 1e25) makes the stress non-finite; the step reports
+    FDL_E_NONFINITE (or the solve's FDL_E_SOLVER), never a finite stress."""
+    g, k, X0, L = make("C2", seed=1)
+    Y = X0.copy()
+    Y[17] = [1e25, -1e25]
+    with pytest.raises(fdl.FdlError) as e:
+        L.set_positions(Y)  # evaluates f at the placement: already non-finite
+        for _ in range(3):
+            L.step()
+    assert e.value.name in ("FDL_E_NONFINITE", "FDL_E_SOLVER"), e.value.name
+    # the context recovers from a finite placement
+    L.set_positions(X0)
+    info = L.step()
+    assert np.isfinite(info.f_after)
+    L.close()
 
 
 @pytest.mark.parametrize("omega", [1.0, 1.3, 1.6, 1.9])
@@ -249,36 +348,84 @@ GOLDEN = __import__("pathlib").Path(__file__).parent / "golden"
 def _golden_graph(d):
     if d["graph"] == "BA20k":
         return graphs.barabasi_albert(20000, 3, seed=5)
+    if d["graph"] == "BA40k":
+        return graphs.barabasi_albert(40000, 3, seed=5)
     return configs.graph_for(d["graph"])
 
 
-@pytest.mark.parametrize("case", ["C3", "BA20k", "C2tol5", "C4"])
-def test_end_to_end_vs_oracle_trace(case):
-    """Full runs against traces written by tests/golden/make_oracle_traces.py
-    (fp64 oracle only).  BA20k is SURVEY §8(d)'s C5 fallback (same generator,
-    20k vertices): a full fp64 C5 run costs 40-110 core-hours."""
-    path = GOLDEN / f"trace_{case}.json"
-    if not path.exists():
-        pytest.skip(f"oracle trace {path.name} not generated yet")
+TRACE_CASES = ["C3", "BA20k", "C2tol5", "C4", "BA40k"]
+# launch paths of the line-6 pass and the step: the library's default for the size
+# (fused + CUDA graph below n^2 = 2^30, split + eager above: C4, BA40k and C5), and
+# each one forced on every case
+PATHS = {"default": {}, "split_eager": {"p1_split": 1, "use_graphs": 0},
+         "fused_graph": {"p1_split": 0, "use_graphs": 1}}
+
+
+def _trace_files(case):
+    import glob
     import json
-    d = json.loads(path.read_text())
-    g = _golden_graph(d)
-    assert g.n == d["n"] and g.num_edges == d["edges"]
+    out = []
+    for f in sorted(glob.glob(str(GOLDEN / f"trace_{case}*.json"))):
+        d = json.loads(open(f).read())
+        if d.get("case") == case:
+            out.append(d)
+    return sorted(out, key=lambda d: d["seed"])
+
+
+def _run_trace(d, g, **kw):
     X0 = graphs.init_positions(g.n, d["dim"], d["position_seed"])
-    p = fdl.make_params(dim=d["dim"], k=d["k"], omega=d["omega"], tol=d["tol"], max_iter=d["max_iter"])
-    L = fdl.Layout.from_graph(g, params=p, init_pos=X0)
-    f0 = L.info.f
-    assert abs(f0 - d["f_initial"]) / d["f_initial"] <= STRESS_TOL
-    fs = [f0]
-    while True:
-        info = L.step()
-        fs.append(info.f_after)
-        if info.stop:
-            break
+    p = fdl.make_params(dim=d["dim"], k=d["k"], omega=d["omega"], tol=d["tol"], max_iter=d["max_iter"], **kw)
+    with fdl.Layout.from_graph(g, params=p, init_pos=X0) as L:
+        f0 = L.info.f
+        assert abs(f0 - d["f_initial"]) / d["f_initial"] <= STRESS_TOL
+        fs, infos = [f0], []
+        while True:
+            info = L.step()
+            fs.append(info.f_after)
+            infos.append((info.f_next, info.f_relaxed, bool(info.accepted), info.maxdisp))
+            if info.stop:
+                break
     it = len(fs) - 1
     assert abs(fs[-1] - d["f_final"]) / d["f_final"] <= 1e-3, (fs[-1], d["f_final"])
     assert abs(it - d["iterations"]) <= max(1, math.ceil(0.02 * d["iterations"])), (it, d["iterations"])
     assert all(b <= a * (1 + 1e-9) for a, b in zip(fs, fs[1:]))
+    if "trace_maxdisp" in d:  # per-iteration diagnostics while the guard decisions agree
+        # the solve stops at cg_rtol = 1e-2 tol (R8), so X^{k+1} carries a solve error of
+        # that order relative to the layout's extent; maxdisp is compared on that scale
+        extent = float(np.abs(np.load(str(GOLDEN / (f"trace_{d['case']}" + ("" if d["seed"] == 1 else f"_s{d['seed']}")
+                                                     + "_X.npy")))).max())
+        for got, fn, acc, md in zip(infos, d["trace_f_next"], d["trace_accepted"], d["trace_maxdisp"]):
+            if got[2] != bool(acc):
+                break
+            assert abs(got[0] - fn) / fn <= 1e-4
+            assert abs(got[3] - md) <= 1e-3 * md + 1e-4 * extent, (got[3], md)
+    return it
+
+
+@pytest.mark.parametrize("case", TRACE_CASES)
+def test_end_to_end_vs_oracle_traces(case):
+    """Full runs against traces written by tests/golden/make_oracle_traces.py
+    (fp64 oracle only), over every stored position seed, on the library's
+    default launch path: per-seed gates (final f within 1e-3, iterations within
+    max(1, 2%)), monotone f, and the seed-mean iteration gate.  BA20k and BA40k
+    are SURVEY §8(d)'s C5 stand-ins (same generator; a full fp64 C5 run costs
+    40-110 core-hours); BA40k is large enough (n^2 >= 2^30) for C5's launch path."""
+    ds = _trace_files(case)
+    assert ds, f"no oracle trace for {case} (tests/golden/make_oracle_traces.py {case})"
+    g = _golden_graph(ds[0])
+    assert g.n == ds[0]["n"] and g.num_edges == ds[0]["edges"]
+    its = [_run_trace(d, g) for d in ds]
+    _mean_gate(its, [d["iterations"] for d in ds])
+
+
+@pytest.mark.parametrize("path", ["split_eager", "fused_graph"])
+@pytest.mark.parametrize("case", TRACE_CASES)
+def test_end_to_end_launch_paths(case, path):
+    """Seed 1 of every stored trace through each launch path forced (the split
+    line-6 pass with eager PCG that bench.py times at C5, and the fused pass in
+    one CUDA graph per step): the same end-to-end gates."""
+    d = _trace_files(case)[0]
+    _run_trace(d, _golden_graph(d), **PATHS[path])
 
 
 def test_carried_lw_matches_full_refresh():
@@ -498,7 +645,7 @@ def test_enumerating_strategy_end_to_end(name):
         if f == 0 or dec < cfg.tol or it == cfg.max_iter:
             break
     assert abs(fs[-1] - f) / f <= 1e-3, (fs[-1], f)
-    assert abs(len(fs) - it) <= max(1, math.ceil(0.05 * it)), (len(fs), it)
+    assert abs(len(fs) - it) <= max(1, math.ceil(0.02 * it)), (len(fs), it)
     assert all(b <= a * (1 + 1e-9) for a, b in zip([L.info.f] + fs, fs))
 
 
@@ -598,7 +745,7 @@ def test_weighted_end_to_end(kind, alpha, omega):
 @pytest.mark.parametrize("name,world,omega,kw", [("C2", 2, 1.6, {}), ("C3", 3, 1.5, {}), ("C3", 2, 0.0, {}),
                                                  ("C3", 2, 1.5, {"dim": 3, "hop_bits": 16}),
                                                  ("wrgg", 2, 1.5, {"weight_exp": -1.0}),
-                                                 ("C2", 3, 1.5, {"strategy": 1, "seed": 4})])
+                                                 ("C2", 3, 1.5, {"strategy": fdl.STRAT_PROB, "seed": 4})])
 def test_loopback_ranks_bitwise(name, world, omega, kw):
     """The whole tile-sharded iteration (every rank evaluates its share of the
     triangle; partial sums all-gathered and summed in rank order) through the
@@ -690,7 +837,7 @@ def test_nccl_one_rank_bitwise(name, dim):
 
 
 @pytest.mark.parametrize("name,omega,strategy", [("C1", 1.5, 0), ("C2", 1.9, 0), ("C3", 1.5, 0), ("C1", 0.0, 0),
-                                                 ("C2", 1.5, 1)])
+                                                 ("C2", 1.5, fdl.STRAT_PROB)])
 def test_graph_steps_bitwise(name, omega, strategy):
     """A step as one CUDA-graph launch (PCG loop = device-side WHILE node) gives
     bitwise the eager step's trajectory (same kernels, same arguments)."""

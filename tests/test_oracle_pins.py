@@ -90,6 +90,19 @@ def test_weight_laplacian_p3():
     np.testing.assert_allclose(core.lw_rows(X, np.arange(3), hop, 1.0), np.array(gold("lw_p3")) @ X, atol=1e-14)
 
 
+def test_weight_laplacian_diagonal():
+    """The Jacobi diagonal sum_{j != i} w_ij (orc_lw_diag, orc_lw_diag_rows) against
+    the diagonal of S:144's worked example and a hand-computed P4 with k = 2
+    (w = (k h)^-2): a dropped term, a wrong power or a missing k fails."""
+    hop = core.hop_matrix(graphs.path_graph(3))
+    np.testing.assert_allclose(core.lw_diag(hop, 1.0), gold("lw_p3_diag"), rtol=0, atol=1e-15)
+    np.testing.assert_allclose(core.lw_diag_rows([2, 0], hop[[2, 0]], 1.0), np.array(gold("lw_p3_diag"))[[2, 0]],
+                               rtol=0, atol=1e-15)
+    hop4 = core.hop_matrix(graphs.path_graph(4))
+    np.testing.assert_allclose(core.lw_diag(hop4, 2.0), gold("lw_p4_diag_k2"), rtol=1e-15, atol=0)
+    np.testing.assert_allclose(core.lw_diag_rows(np.arange(4), hop4, 2.0), gold("lw_p4_diag_k2"), rtol=1e-15, atol=0)
+
+
 def test_iteration_laplacian_example_and_coincident_rule():
     """single edge, w = 1 (alpha = 0), d = 2, ||y_0 - y_1|| = 4 ->
     off-diagonal -0.5; coincident y_0 = y_1 -> zero matrix."""
@@ -295,6 +308,21 @@ def test_scale_equivariance_in_k():
     np.testing.assert_allclose(r2.X, 0.1 * r1.X, rtol=1e-7, atol=1e-9)
 
 
+def test_sor_combine_worked_examples():
+    """Eq. 10 against SPEC S:300-302: omega = 0 returns x_next; the
+    (1,0), (0,0), omega = 0.5 example gives (1.5, 0); x_next = x_prev is fixed."""
+    e = GOLD["sor_combine_example"]
+    got = layout.sor_combine(np.array(e["x_next"]), np.array(e["x_prev"]), e["omega"])
+    np.testing.assert_array_equal(got, np.array(e["value"]))
+    rng = np.random.default_rng(3)
+    Xn, Xp = rng.normal(size=(5, 2)), rng.normal(size=(5, 2))
+    np.testing.assert_array_equal(layout.sor_combine(Xn, Xp, 0.0), Xn)
+    np.testing.assert_allclose(layout.sor_combine(Xn, Xn, 1.7), Xn, rtol=4e-15, atol=0)  # fp64 rounding of (1+w)x - wx
+    # the per-vertex form (P:410) with a constant vector is Eq. 10
+    np.testing.assert_allclose(layout.sor_combine(Xn, Xp, np.full(5, 0.5)), layout.sor_combine(Xn, Xp, 0.5),
+                               rtol=0, atol=1e-15)
+
+
 def test_step_cap():
     """cap_step: +inf is the identity (paper-exact); a finite cap bounds every
     vertex move and the guard keeps f monotone."""
@@ -303,6 +331,13 @@ def test_step_cap():
     assert np.array_equal(layout.cap_step(Xt, Xn, math.inf), Xt)
     capped = layout.cap_step(Xt, Xn, 0.1)
     assert np.all(np.linalg.norm(capped - Xn, axis=1) <= 0.1 + 1e-15)
+    # the clamp keeps the direction of the extrapolation and leaves short moves alone
+    v, c = Xt - Xn, capped - Xn
+    long = np.linalg.norm(v, axis=1) > 0.1
+    np.testing.assert_allclose(np.linalg.norm(c[long], axis=1), 0.1, rtol=1e-14)
+    np.testing.assert_allclose(np.sum(v[long] * c[long], axis=1),
+                               np.linalg.norm(v[long], axis=1) * 0.1, rtol=1e-14)
+    assert np.array_equal(layout.cap_step(Xt, Xn, 1e9), Xt)
     g = graphs.grid_graph(4, 4)
     r = layout.run_algorithm2(layout.Problem(g, 2, 0.25), graphs.init_positions(16, 2, 1), 1.5, 1e-8, 100, step=0.01)
     fs = [r.f_initial] + [t.f_after for t in r.trace]
