@@ -594,6 +594,13 @@ def run_gpu(args):
             "clocks": clk,
             "gpu_launches": int(st.launches),
             "setup_ms": info.setup_ms,
+            "setup": {"ms": info.setup_ms, "ideal_distances_ms": info.setup_dist_ms,
+                      "bfs_gather_bytes": int(info.bfs_bytes),
+                      "bfs_gather_gbs": (info.bfs_bytes / (info.setup_dist_ms * 1e-3) / 1e9
+                                         if info.bfs_bytes and info.setup_dist_ms > 0 else None),
+                      "note": "MS-BFS level kernels' gather bytes (neighbour frontier + visited + new-frontier "
+                              "words, 128 B each per searched vertex) over the whole ideal-distance build; "
+                              "the gathers are L2-resident (frontier words n x 128 B)"},
         }
         print(json.dumps(line), flush=True)
     L.close()

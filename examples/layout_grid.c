@@ -61,7 +61,11 @@ static int check_errors(void)
 int main(int argc, char** argv)
 {
     if (argc > 1 && argv[1][0] == '-') return check_errors();
+    /* layout_grid ROWS COLS [X0_FILE OUT_FILE]: the optional files hold n*2 doubles
+       (row-major): the initial placement, and the final one written back */
     const int rows = argc > 2 ? atoi(argv[1]) : 10, cols = argc > 2 ? atoi(argv[2]) : 10;
+    const char* x0_file = argc > 4 ? argv[3] : NULL;
+    const char* out_file = argc > 4 ? argv[4] : NULL;
     const int n = rows * cols;
     int64_t* rp = malloc(sizeof(int64_t) * (n + 1));
     int32_t* col = malloc(sizeof(int32_t) * 4 * n);
@@ -75,8 +79,18 @@ int main(int argc, char** argv)
     p.tol = 1e-6;        /* Table 1's rel err for n <= 86 .. C1 (DESIGN R5) */
     p.seed = 7;          /* initial placement uniform in the unit square */
 
+    double* X0 = NULL;
+    if (x0_file) {
+        FILE* f = fopen(x0_file, "rb");
+        X0 = malloc(sizeof(double) * 2 * n);
+        if (!f || fread(X0, sizeof(double), (size_t)2 * n, f) != (size_t)2 * n) {
+            fprintf(stderr, "cannot read %s\n", x0_file);
+            return 1;
+        }
+        fclose(f);
+    }
     fdl_ctx* ctx = NULL;
-    fdl_status s = fdl_create(n, rp, col, NULL, &p, NULL, &ctx);
+    fdl_status s = fdl_create(n, rp, col, NULL, &p, X0, &ctx);
     if (s != FDL_OK) {
         fprintf(stderr, "fdl_create: %s\n", fdl_status_str(s));
         return 1;
@@ -93,9 +107,18 @@ int main(int argc, char** argv)
            info.iterations, info.accepted, info.cg_iters, info.f_initial, info.f_final);
     printf("x_0 = (%.3g, %.3g)  x_1 = (%.6f, %.6f)  |x_1 - x_0| / k = %.4f\n", X[0], X[1], X[2], X[3],
            sqrt(X[2] * X[2] + X[3] * X[3]) / p.k);
+    if (out_file) {
+        FILE* f = fopen(out_file, "wb");
+        if (!f || fwrite(X, sizeof(double), (size_t)2 * n, f) != (size_t)2 * n) {
+            fprintf(stderr, "cannot write %s\n", out_file);
+            return 1;
+        }
+        fclose(f);
+    }
     fdl_destroy(ctx);
     free(rp);
     free(col);
     free(X);
+    free(X0);
     return info.f_final < info.f_initial ? 0 : 1;
 }

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FDL_ABI_VERSION 1
+#define FDL_ABI_VERSION 2  /* 2: fdl_strategy ENUM = 1, PROB = 2; fdl_ctx_info setup breakdown */
 
 typedef struct fdl_ctx fdl_ctx; /* opaque; owned by the library */
 
@@ -156,6 +156,11 @@ typedef struct {
     uint64_t local_pairs;      /* unordered vertex pairs in this rank's tiles   */
     uint64_t device_bytes;     /* all device memory held by the context         */
     double setup_ms;       /* MS-BFS + rowsum + first stress pass at create     */
+    double setup_dist_ms;  /* ... of which the ideal distances (MS-BFS with its
+                              device-side level loop, or Bellman-Ford)          */
+    uint64_t bfs_bytes;    /* MS-BFS level-kernel gather bytes (neighbour frontier
+                              words, visited and new-frontier words; 128 B each per
+                              vertex searched per level), all batches and widths */
 } fdl_ctx_info;
 
 /* Kernel accounting of the hot path, accumulated since fdl_reset_stats. */

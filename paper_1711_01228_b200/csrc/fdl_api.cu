@@ -216,6 +216,8 @@ struct fdl_ctx {
     };
     std::vector<Mark> ev_marks;
     double setup_ms = 0.0;
+    double setup_dist_ms = 0.0;       // MS-BFS (or Bellman-Ford) part of the setup
+    unsigned long long bfs_bytes = 0;  // MS-BFS level-kernel gather bytes
     // errors
     std::string err;
     bool broken = false;
@@ -667,36 +669,53 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
         ctx->hop_bytes_total = dbytes;
         FDL_CUDA(cudaMemsetAsync(ctx->D, 0, dbytes, ctx->stream));
         const int maxhop = hb_max_hop(hb);
-        bool overflow = false;
-        int diam = 0;
+        // levels per batch: every BFS ends within diam <= 2 ecc(0) levels; one level past the
+        // width's maximum detects an overflow.  The loop runs on the device (level flags),
+        // with one host sync after all batches (MS-BFS)
+        const int nlev = std::max(1, std::min(2 * ecc0, maxhop + 1));
         uint8_t* bbuf = nullptr;
+        unsigned int* flags = nullptr;
         const size_t bbytes = (size_t)n * bfs_row_bytes_host(hb);
         FDL_CUDA(tmp.alloc(&bbuf, bbytes));
-        for (int s0 = src_lo; s0 < src_hi && !overflow; s0 += 32 * kBFSWords) {
+        FDL_CUDA(tmp.alloc(&flags, sizeof(unsigned int) * (size_t)(nlev + 2)));
+        FDL_CUDA(cudaMemsetAsync(&ctx->sc->bfs_diam, 0, sizeof(int), ctx->stream));
+        FDL_CUDA(cudaMemsetAsync(&ctx->sc->bfs_overflow, 0, sizeof(int), ctx->stream));
+        FDL_CUDA(cudaMemsetAsync(&ctx->sc->bfs_bytes, 0, sizeof(unsigned long long), ctx->stream));
+        const int grid = ctx->sm_count * 8;
+        // hubs (degree > kBfsHubDeg): a block each per level
+        std::vector<int> hub_list;
+        for (int v = 0; v < n; ++v)
+            if (rp[v + 1] - rp[v] > kBfsHubDeg) hub_list.push_back(v);
+        int* d_hubs = nullptr;
+        if (!hub_list.empty()) {
+            FDL_CUDA(tmp.alloc(&d_hubs, sizeof(int) * hub_list.size()));
+            FDL_CUDA(cudaMemcpyAsync(d_hubs, hub_list.data(), sizeof(int) * hub_list.size(), cudaMemcpyHostToDevice,
+                                     ctx->stream));
+        }
+        const int nhub = (int)hub_list.size();
+        for (int s0 = src_lo; s0 < src_hi; s0 += 32 * kBFSWords) {
             const int nsrc = std::min(32 * kBFSWords, src_hi - s0);
             FDL_CUDA(cudaMemsetAsync(bbuf, 0, bbytes, ctx->stream));
+            FDL_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned int) * (size_t)(nlev + 2), ctx->stream));
             FDL_LAUNCH(launch_bfs_init(fa, vis, n, s0, ctx->stream));
             uint32_t *fin = fa, *fout = fb;
-            for (int level = 1;; ++level) {
-                FDL_CUDA(cudaMemsetAsync(&ctx->sc->anynew, 0, sizeof(unsigned int), ctx->stream));
-                FDL_LAUNCH(launch_bfs_level_sym(d_rp, d_col, fin, fout, vis, bbuf, n, nsrc, level, hb,
-                                                &ctx->sc->anynew, ctx->stream));
-                FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost,
-                                         ctx->stream));
-                FDL_CUDA(cudaStreamSynchronize(ctx->stream));
-                if (!ctx->sc_host->anynew) break;
-                if (level > maxhop) {
-                    overflow = true;
-                    break;
-                }
-                diam = std::max(diam, level);
+            for (int level = 1; level <= nlev; ++level) {
+                FDL_LAUNCH(launch_bfs_level_sym(d_rp, d_col, fin, fout, vis, bbuf, n, nsrc, level, hb, flags,
+                                                &ctx->sc->bfs_bytes, d_hubs, nhub, grid, ctx->stream));
                 std::swap(fin, fout);
             }
-            if (!overflow)
-                FDL_LAUNCH(launch_bfs_retile(bbuf, ctx->D, n, s0, nsrc, ctx->nb, ctx->t0, ctx->t1, hb, ctx->stream));
+            FDL_LAUNCH(launch_bfs_batch_end(flags, nlev, maxhop, &ctx->sc->bfs_diam, &ctx->sc->bfs_overflow,
+                                            ctx->stream));
+            FDL_LAUNCH(launch_bfs_retile(bbuf, ctx->D, n, s0, nsrc, ctx->nb, ctx->t0, ctx->t1, hb, ctx->stream));
         }
+        FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, ctx->stream));
         FDL_CUDA(cudaStreamSynchronize(ctx->stream));
         tmp.release(bbuf);
+        tmp.release(flags);
+        if (d_hubs) tmp.release(d_hubs);
+        const bool overflow = ctx->sc_host->bfs_overflow != 0;
+        const int diam = ctx->sc_host->bfs_diam;
+        ctx->bfs_bytes += ctx->sc_host->bfs_bytes;
         if (!overflow) {
             ctx->diameter = diam;
             if (hb == 0) FDL_LAUNCH(launch_nib_encode(ctx->D, dbytes, ctx->stream));
@@ -742,8 +761,15 @@ fdl_status build_dists(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, cons
     FDL_CUDA(tmp.alloc(&d_col, sizeof(int32_t) * m));
     FDL_CUDA(tmp.alloc(&d_len, sizeof(double) * m));
     FDL_CUDA(tmp.alloc(&da, sizeof(double) * (size_t)n * S));
-    int* stamp = nullptr;
-    FDL_CUDA(tmp.alloc(&stamp, sizeof(int) * n));
+    // per (vertex, source) change bits of the last sweep, double-buffered
+    const int W = S / 32;
+    uint32_t *chg_a = nullptr, *chg_b = nullptr;
+    unsigned int* flags = nullptr;
+    constexpr int kChunk = 16;  // sweeps enqueued between host checks
+    const int max_sweeps = 4 * n + 8;
+    FDL_CUDA(tmp.alloc(&chg_a, sizeof(uint32_t) * (size_t)n * W));
+    FDL_CUDA(tmp.alloc(&chg_b, sizeof(uint32_t) * (size_t)n * W));
+    FDL_CUDA(tmp.alloc(&flags, sizeof(unsigned int) * (size_t)(max_sweeps + kChunk)));
     FDL_CUDA(tmp.alloc(&dmax, sizeof(double)));
     FDL_CUDA(cudaMemsetAsync(dmax, 0, sizeof(double), ctx->stream));
     std::vector<double> ones;
@@ -777,21 +803,73 @@ fdl_status build_dists(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, cons
     ctx->device_bytes += dbytes;
     ctx->hop_bytes_total = dbytes;
     FDL_CUDA(cudaMemsetAsync(ctx->D, 0, dbytes, ctx->stream));
-    for (int s0 = src_lo; s0 < src_hi; s0 += S) {
-        const int nsrc = std::min(S, src_hi - s0);
-        FDL_LAUNCH(launch_bf_init(da, n, s0, nsrc, S, ctx->stream));
-        FDL_CUDA(cudaMemsetAsync(stamp, 0xFF, sizeof(int) * n, ctx->stream));  // -1: never changed
-        // sweeps are idempotent at the fixed point, so 8 run between host checks
-        for (int it = 0; it < 4 * n + 8; it += 8) {
-            FDL_CUDA(cudaMemsetAsync(&ctx->sc->anynew, 0, sizeof(unsigned int), ctx->stream));
-            for (int k = 0; k < 8; ++k)
-                FDL_LAUNCH(launch_bf_relax(d_rp, d_col, d_len, da, stamp, n, S, nsrc, it + k, &ctx->sc->anynew,
-                                           ctx->stream));
-            FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, ctx->stream));
-            FDL_CUDA(cudaStreamSynchronize(ctx->stream));
-            if (!ctx->sc_host->anynew) break;
+    // Source batches as compact graph neighbourhoods: clusters of up to S sources of
+    // this rank's range, each grown by BFS (over vertices not yet taken) from the first
+    // untaken vertex.  Sources close to each other have nearly concentric wavefronts,
+    // so each sweep's change words are dense (many sources per vertex at once) instead
+    // of one bit per 32-lane word (measured: W4 setup 6.2 s with id-contiguous batches).
+    std::vector<int> order;
+    order.reserve((size_t)std::max(0, src_hi - src_lo));
+    {
+        std::vector<char> taken((size_t)n, 0);
+        std::vector<int> q;
+        q.reserve((size_t)n);
+        std::vector<int> mark((size_t)n, -1);
+        int cluster = 0;
+        for (int seed = src_lo; seed < src_hi; ++seed) {
+            if (taken[seed]) continue;
+            // BFS from seed; collect untaken vertices of [src_lo, src_hi) until S of them
+            q.clear();
+            q.push_back(seed);
+            mark[seed] = cluster;
+            int got = 0;
+            for (size_t h = 0; h < q.size() && got < S; ++h) {
+                const int u = q[h];
+                if (u >= src_lo && u < src_hi && !taken[u]) {
+                    taken[u] = 1;
+                    order.push_back(u);
+                    ++got;
+                }
+                for (int64_t e = rp[u]; e < rp[u + 1]; ++e) {
+                    const int w = col[e];
+                    if (mark[w] != cluster) {
+                        mark[w] = cluster;
+                        q.push_back(w);
+                    }
+                }
+            }
+            ++cluster;
         }
-        FDL_LAUNCH(launch_bf_store(da, n, s0, nsrc, S, ctx->nb, ctx->t0, ctx->t1, ctx->D, dmax, ctx->stream));
+    }
+    int* d_srcs = nullptr;
+    FDL_CUDA(tmp.alloc(&d_srcs, sizeof(int) * std::max<size_t>(order.size(), 1)));
+    if (!order.empty())
+        FDL_CUDA(cudaMemcpyAsync(d_srcs, order.data(), sizeof(int) * order.size(), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+    for (int b0 = 0; b0 < (int)order.size(); b0 += S) {
+        const int nsrc = std::min(S, (int)order.size() - b0);
+        const int* srcs = d_srcs + b0;
+        FDL_LAUNCH(launch_bf_init(da, n, srcs, nsrc, S, ctx->stream));
+        FDL_CUDA(cudaMemsetAsync(chg_a, 0, sizeof(uint32_t) * (size_t)n * W, ctx->stream));
+        FDL_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned int) * (size_t)(max_sweeps + kChunk), ctx->stream));
+        FDL_LAUNCH(launch_bf_seed(chg_a, srcs, nsrc, S, ctx->stream));
+        uint32_t *cin = chg_a, *cout = chg_b;
+        // sweeps on the device, kChunk between host checks of the last sweep's flag
+        // (a sweep after one without changes returns at once)
+        bool done = false;
+        for (int it = 0; it < max_sweeps && !done; it += kChunk) {
+            for (int k = 0; k < kChunk; ++k) {
+                FDL_LAUNCH(launch_bf_sweep(d_rp, d_col, d_len, da, cin, cout, n, S, nsrc, it + k, flags,
+                                           ctx->sm_count * 8, ctx->stream));
+                std::swap(cin, cout);
+            }
+            unsigned int last = 1;
+            FDL_CUDA(cudaMemcpyAsync(&last, flags + it + kChunk - 1, sizeof(unsigned int), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+            FDL_CUDA(cudaStreamSynchronize(ctx->stream));
+            done = last == 0u;
+        }
+        FDL_LAUNCH(launch_bf_store(da, n, srcs, nsrc, S, ctx->nb, ctx->t0, ctx->t1, ctx->D, dmax, ctx->stream));
     }
     double mx = 0.0;
     FDL_CUDA(cudaMemcpyAsync(&mx, dmax, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1053,10 +1131,12 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     FDL_CUDA(cudaMemcpyAsync(ctx->it_hi, hi.data(), sizeof(int) * ctx->nb, cudaMemcpyHostToDevice, ctx->stream));
 
     // hop matrix first (fixes the hop width), then grids, then the Jacobi diagonal
+    const auto td0 = std::chrono::steady_clock::now();
     if (ctx->general)
         FDL_TRY(build_dists(ctx, rp, col, edge_len));
     else
         FDL_TRY(build_hops(ctx, rp, col, ecc0));
+    ctx->setup_dist_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - td0).count();
     const int cap_items = std::max(ctx->nitems, 1);
     for (int s = 1; s <= 2; ++s)
         ctx->grid_p1[s] = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymP1, dim, s, ctx->hb)));
@@ -1924,6 +2004,8 @@ fdl_status fdl_get_info(fdl_ctx* ctx, fdl_ctx_info* info)
     r.local_pairs = ctx->local_pairs;
     r.device_bytes = ctx->device_bytes;
     r.setup_ms = ctx->setup_ms;
+    r.setup_dist_ms = ctx->setup_dist_ms;
+    r.bfs_bytes = ctx->bfs_bytes;
     *info = r;
     return FDL_OK;
 }

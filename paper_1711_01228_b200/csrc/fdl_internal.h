@@ -24,6 +24,7 @@ constexpr int kRB = 256;           // row block of all fp64 vector reductions
 constexpr int kGalMax = 8;         // history window of the recycled PCG start (R27)
 constexpr int kGalNV = kGalMax * (kGalMax + 1) / 2 + kGalMax;  // Gram entries + right-hand sides per column
 constexpr int kBFSWords = 32;      // MS-BFS source batch = 32 words x 32 bits = 1024
+constexpr int kBfsHubDeg = 256;    // MS-BFS: vertices of higher degree get a whole block per level
 
 // Device-resident scalars of the iteration (one struct per context).
 struct DevScalars {
@@ -55,6 +56,10 @@ struct DevScalars {
     int gal_use;           // vectors used by the current start
     int gal_dropped;       // dependent vectors skipped by the last solve
     int gal_m;             // window (fdl_params.cg_history, <= kGalMax)
+    // MS-BFS setup (device-driven level loop)
+    int bfs_diam;          // deepest level found so far
+    int bfs_overflow;      // a level beyond the stored width's maximum found a vertex
+    unsigned long long bfs_bytes;  // gather bytes of the level kernels (roofline)
 };
 
 // Host-mapped flag the host reads after a stream sync.
@@ -209,18 +214,22 @@ cudaError_t launch_sym_stress(const double* spart, int nitems, int nsets, double
                               cudaStream_t s);
 cudaError_t launch_bfs_level_sym(const int64_t* row_ptr, const int32_t* col, const uint32_t* fin, uint32_t* fout,
                                  uint32_t* visited, uint8_t* bbuf, int n, int nsrc, int level, int hb,
-                                 unsigned int* anynew, cudaStream_t s);
-// batch rows [s0, s0 + nsrc) of bbuf (cells [v][source]) -> the local triangle tiles
+                                 unsigned int* flags, unsigned long long* bytes, const int* hubs, int nhub, int grid,
+                                 cudaStream_t s);
+cudaError_t launch_bfs_batch_end(const unsigned int* flags, int nlevels, int maxhop, int* diam, int* overflow,
+                                 cudaStream_t s);
 cudaError_t launch_bfs_retile(const uint8_t* bbuf, uint8_t* D, int n, int s0, int nsrc, int nb, int64_t t0,
                               int64_t t1, int hb, cudaStream_t s);
 int bfs_row_bytes_host(int hb);  // batch-buffer bytes per vertex
 // weighted / general-alpha setup: multi-source Bellman-Ford in fp64 over the
 // CSR with edge lengths; dist[v * S + s] for the batch's sources s0..s0+S-1
-cudaError_t launch_bf_init(double* dist, int n, int s0, int nsrc, int S, cudaStream_t s);
-cudaError_t launch_bf_relax(const int64_t* row_ptr, const int32_t* col, const double* len, double* dist, int* stamp,
-                            int n, int S, int nsrc, int it, unsigned int* changed, cudaStream_t s);
-cudaError_t launch_bf_store(const double* dist, int n, int s0, int nsrc, int S, int nb, int64_t t0, int64_t t1,
-                            uint8_t* D, double* dmax, cudaStream_t s);
+cudaError_t launch_bf_init(double* dist, int n, const int* srcs, int nsrc, int S, cudaStream_t s);
+cudaError_t launch_bf_sweep(const int64_t* row_ptr, const int32_t* col, const double* len, double* dist,
+                            const uint32_t* chg_in, uint32_t* chg_out, int n, int S, int nsrc, int it,
+                            unsigned int* flags, int grid, cudaStream_t s);
+cudaError_t launch_bf_seed(uint32_t* chg, const int* srcs, int nsrc, int S, cudaStream_t s);
+cudaError_t launch_bf_store(const double* dist, int n, const int* srcs, int nsrc, int S, int nb, int64_t t0,
+                            int64_t t1, uint8_t* D, double* dmax, cudaStream_t s);
 cudaError_t launch_dist_rows(const uint8_t* D, int hb, int nb, int64_t t0, int64_t t1, const int* rows, int nrows,
                              int n, float* out, int* missing, cudaStream_t s);
 // 4-bit tiles: raw (lo | hi << 4) bytes written by the BFS -> nib_encode bytes

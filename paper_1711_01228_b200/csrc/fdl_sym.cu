@@ -39,7 +39,7 @@
 #define FDL_P1_SHFL 0  // 1: P1 hop decode by warp shuffle (experiment; slower)
 #endif
 #ifndef FDL_BFS_UNROLL
-#define FDL_BFS_UNROLL 4  // neighbour frontier loads in flight per warp (MS-BFS)
+#define FDL_BFS_UNROLL 16  // neighbour frontier loads in flight per warp (MS-BFS)
 #endif
 constexpr int kBfsUnroll = FDL_BFS_UNROLL;
 #ifndef FDL_P1S_CTAS
@@ -1571,41 +1571,148 @@ __host__ __device__ constexpr int bfs_row_bytes()  // batch-buffer bytes per ver
     return HB == 0 ? 512 : 1024 * HB;
 }
 
+// One level of the batch's BFS, with no host round trip: flags[L] = 1 when
+// level L found a new (vertex, source) pair, and a level whose predecessor
+// found none returns at once (the batch's search is over; diam <= 2 ecc(0)
+// bounds how many levels the host enqueues).  Grid-stride over vertices (warp
+// per vertex), so a finished level costs one short launch.  Gather bytes of
+// the level (neighbour frontier words + visited read + new-frontier write,
+// 128 B each per vertex searched) are added to *bytes (MS-BFS roofline).
+template <int HB>
+__device__ __forceinline__ uint32_t bfs_gather(const int32_t* __restrict__ col, const uint32_t* __restrict__ fin,
+                                               int64_t beg, int64_t end, int64_t stride, int lane)
+{
+    // OR of the neighbours' frontier words over col[beg, end) in chunks of 32 neighbours
+    // `stride` apart; kBfsUnroll independent 128-byte loads in flight per warp
+    uint32_t acc = 0;
+    for (int64_t e0 = beg; e0 < end; e0 += stride) {
+        const int myu = (e0 + lane < end) ? col[e0 + lane] : 0;
+        const int cnt = (int)min((int64_t)32, end - e0);
+        for (int k0 = 0; k0 < cnt; k0 += kBfsUnroll) {
+            uint32_t t[kBfsUnroll];
+#pragma unroll
+            for (int k = 0; k < kBfsUnroll; ++k) {
+                const int u = __shfl_sync(0xffffffffu, myu, (k0 + k) & 31);
+                t[k] = (k0 + k < cnt) ? __ldcg(&fin[(int64_t)u * kBFSWords + lane]) : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < kBfsUnroll; ++k) acc |= t[k];
+        }
+    }
+    return acc;
+}
+
+// One level of the batch's BFS, with no host round trip: flags[L] = 1 when
+// level L found a new (vertex, source) pair, and a level whose predecessor
+// found none returns at once (the batch's search is over; diam <= 2 ecc(0)
+// bounds how many levels the host enqueues).  Blocks [0, nhub) take one hub
+// (degree > kBfsHubDeg) each, its neighbour list split over the 8 warps (a
+// scale-free graph's hubs would otherwise be one warp's chain of deg / unroll
+// L2 round trips per level); the other blocks stride over the remaining
+// vertices, warp per vertex.  Gather bytes of the level (neighbour frontier
+// words + visited read + new-frontier write, 128 B each per vertex searched)
+// are added to *bytes (MS-BFS roofline).
 template <int HB>
 __global__ void __launch_bounds__(256) k_bfs_level_sym(const int64_t* __restrict__ row_ptr,
                                                        const int32_t* __restrict__ col,
                                                        const uint32_t* __restrict__ fin, uint32_t* __restrict__ fout,
                                                        uint32_t* __restrict__ visited, uint8_t* __restrict__ bbuf,
-                                                       int n, int nsrc, int level, unsigned int* anynew)
+                                                       int n, int nsrc, int level, unsigned int* flags,
+                                                       unsigned long long* bytes, const int* __restrict__ hubs,
+                                                       int nhub)
 {
-    const int v = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-    const int lane = threadIdx.x & 31;
-    if (v >= n) return;
+    if (level > 1 && *(volatile unsigned int*)&flags[level - 1] == 0u) return;  // uniform over the grid
+    __shared__ unsigned long long blk_bytes;
+    __shared__ unsigned int blk_new;
+    __shared__ uint32_t hub_acc[32];
+    __shared__ int hub_skip;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        blk_bytes = 0ull;
+        blk_new = 0u;
+    }
     const int nl = min(max(nsrc - 32 * lane, 0), 32);
     const uint32_t full = nl == 32 ? 0xffffffffu : ((1u << nl) - 1u);
-    const uint32_t vis = visited[(int64_t)v * kBFSWords + lane];
-    if (__all_sync(0xffffffffu, (vis & full) == full)) {
-        fout[(int64_t)v * kBFSWords + lane] = 0u;
+    if ((int)blockIdx.x < nhub) {
+        const int v = hubs[blockIdx.x];
+        if (wid == 0) {
+            const uint32_t vis = visited[(int64_t)v * kBFSWords + lane];
+            const bool done = __all_sync(0xffffffffu, (vis & full) == full);
+            hub_acc[lane] = 0u;
+            if (lane == 0) hub_skip = done ? 1 : 0;
+        }
+        __syncthreads();
+        const int64_t beg = row_ptr[v], end = row_ptr[v + 1];
+        if (!hub_skip) {
+            const uint32_t acc = bfs_gather<HB>(col, fin, beg + 32 * wid, end, 256, lane);
+            if (acc) atomicOr(&hub_acc[lane], acc);
+        }
+        __syncthreads();
+        if (wid == 0) {
+            const uint32_t vis = visited[(int64_t)v * kBFSWords + lane];
+            if (hub_skip) {
+                fout[(int64_t)v * kBFSWords + lane] = 0u;
+            } else {
+                const uint32_t nw = hub_acc[lane] & ~vis & full;
+                fout[(int64_t)v * kBFSWords + lane] = nw;
+                if (nw) {
+                    visited[(int64_t)v * kBFSWords + lane] = vis | nw;
+                    bfs_record<HB>(bbuf + (int64_t)v * bfs_row_bytes<HB>() + lane * (bfs_row_bytes<HB>() / 32), nw,
+                                   level);
+                }
+                if (__any_sync(0xffffffffu, nw != 0u) && lane == 0) flags[level] = 1u;
+                if (lane == 0) atomicAdd(bytes, (unsigned long long)(end - beg + 2) * 128ull);
+            }
+        }
         return;
     }
-    uint32_t acc = 0;
-    const int64_t beg = row_ptr[v], end = row_ptr[v + 1];
-    for (int64_t e0 = beg; e0 < end; e0 += 32) {
-        const int myu = (e0 + lane < end) ? col[e0 + lane] : 0;
-        const int cnt = (int)min((int64_t)32, end - e0);
-#pragma unroll kBfsUnroll
-        for (int k = 0; k < cnt; ++k) {
-            const int u = __shfl_sync(0xffffffffu, myu, k);
-            acc |= fin[(int64_t)u * kBFSWords + lane];
+    __syncthreads();
+    const int64_t nwarps = (int64_t)(gridDim.x - nhub) * (blockDim.x >> 5);
+    unsigned long long my_bytes = 0ull;
+    bool found = false;
+    for (int64_t vv = ((int64_t)(blockIdx.x - nhub) * blockDim.x + threadIdx.x) >> 5; vv < n; vv += nwarps) {
+        const int v = (int)vv;
+        const int64_t beg = row_ptr[v], end = row_ptr[v + 1];
+        if (end - beg > kBfsHubDeg) continue;  // a hub block's vertex
+        const uint32_t vis = visited[(int64_t)v * kBFSWords + lane];
+        if (__all_sync(0xffffffffu, (vis & full) == full)) {
+            fout[(int64_t)v * kBFSWords + lane] = 0u;
+            continue;
         }
+        const uint32_t acc = bfs_gather<HB>(col, fin, beg, end, 32, lane);
+        my_bytes += (unsigned long long)(end - beg + 2) * 128ull;
+        const uint32_t nw = acc & ~vis & full;
+        fout[(int64_t)v * kBFSWords + lane] = nw;
+        if (nw) {
+            visited[(int64_t)v * kBFSWords + lane] = vis | nw;
+            bfs_record<HB>(bbuf + (int64_t)v * bfs_row_bytes<HB>() + lane * (bfs_row_bytes<HB>() / 32), nw, level);
+        }
+        found |= __any_sync(0xffffffffu, nw != 0u);
     }
-    const uint32_t nw = acc & ~vis & full;
-    fout[(int64_t)v * kBFSWords + lane] = nw;
-    if (nw) {
-        visited[(int64_t)v * kBFSWords + lane] = vis | nw;
-        bfs_record<HB>(bbuf + (int64_t)v * bfs_row_bytes<HB>() + lane * (bfs_row_bytes<HB>() / 32), nw, level);
+    if (lane == 0) {
+        if (my_bytes) atomicAdd(&blk_bytes, my_bytes);
+        if (found) blk_new = 1u;
     }
-    if (__any_sync(0xffffffffu, nw != 0u) && lane == 0) *anynew = 1u;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (blk_bytes) atomicAdd(bytes, blk_bytes);
+        if (blk_new) flags[level] = 1u;
+    }
+}
+
+// After a batch's levels: the deepest level that found a vertex (running max
+// over batches = the diameter) and whether level maxhop + 1 found one (the
+// stored width cannot hold the hops: the host retries one width wider).
+__global__ void k_bfs_batch_end(const unsigned int* flags, int nlevels, int maxhop, int* diam, int* overflow)
+{
+    int d = 0;
+    for (int L = 1; L <= nlevels; ++L)
+        if (flags[L]) d = L;
+    if (d > maxhop) {
+        *overflow = 1;
+        d = maxhop;
+    }
+    if (d > *diam) *diam = d;
 }
 
 // Batch rows [s0, s0 + 1024) into the local triangle tiles: CTA per tile (I, J)
@@ -1664,16 +1771,26 @@ __global__ void __launch_bounds__(256) k_bfs_retile(const uint8_t* __restrict__ 
 
 cudaError_t launch_bfs_level_sym(const int64_t* row_ptr, const int32_t* col, const uint32_t* fin, uint32_t* fout,
                                  uint32_t* visited, uint8_t* bbuf, int n, int nsrc, int level, int hb,
-                                 unsigned int* anynew, cudaStream_t s)
+                                 unsigned int* flags, unsigned long long* bytes, const int* hubs, int nhub, int grid,
+                                 cudaStream_t s)
 {
-    const int64_t threads = (int64_t)n * 32;
-    const unsigned grid = (unsigned)((threads + 255) / 256);
+    const unsigned g = (unsigned)nhub + (unsigned)std::max(1, std::min(grid, (int)(((int64_t)n * 32 + 255) / 256)));
     if (hb == 0)
-        k_bfs_level_sym<0><<<grid, 256, 0, s>>>(row_ptr, col, fin, fout, visited, bbuf, n, nsrc, level, anynew);
+        k_bfs_level_sym<0><<<g, 256, 0, s>>>(row_ptr, col, fin, fout, visited, bbuf, n, nsrc, level, flags, bytes,
+                                             hubs, nhub);
     else if (hb == 1)
-        k_bfs_level_sym<1><<<grid, 256, 0, s>>>(row_ptr, col, fin, fout, visited, bbuf, n, nsrc, level, anynew);
+        k_bfs_level_sym<1><<<g, 256, 0, s>>>(row_ptr, col, fin, fout, visited, bbuf, n, nsrc, level, flags, bytes,
+                                             hubs, nhub);
     else
-        k_bfs_level_sym<2><<<grid, 256, 0, s>>>(row_ptr, col, fin, fout, visited, bbuf, n, nsrc, level, anynew);
+        k_bfs_level_sym<2><<<g, 256, 0, s>>>(row_ptr, col, fin, fout, visited, bbuf, n, nsrc, level, flags, bytes,
+                                             hubs, nhub);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bfs_batch_end(const unsigned int* flags, int nlevels, int maxhop, int* diam, int* overflow,
+                                 cudaStream_t s)
+{
+    k_bfs_batch_end<<<1, 1, 0, s>>>(flags, nlevels, maxhop, diam, overflow);
     return cudaGetLastError();
 }
 
@@ -1701,74 +1818,129 @@ int bfs_row_bytes_host(int hb) { return hb == 0 ? bfs_row_bytes<0>() : (hb == 1 
 // sources; iterated until no value changes.  Each stored value is the fp64
 // sum along a shortest path, so the result does not depend on the iteration
 // order; the tiles get its correctly rounded fp32 value.
-__global__ void k_bf_init(double* dist, int n, int s0, int nsrc, int S)
+__global__ void k_bf_init(double* dist, int n, const int* __restrict__ srcs, int nsrc, int S)
 {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (int64_t)n * S) return;
     const int v = (int)(idx / S), k = (int)(idx % S);
-    dist[idx] = (k < nsrc && v == s0 + k) ? 0.0 : INFINITY;
+    dist[idx] = (k < nsrc && v == srcs[k]) ? 0.0 : INFINITY;
 }
 
-cudaError_t launch_bf_init(double* dist, int n, int s0, int nsrc, int S, cudaStream_t s)
+cudaError_t launch_bf_init(double* dist, int n, const int* srcs, int nsrc, int S, cudaStream_t s)
 {
     const int64_t total = (int64_t)n * S;
-    k_bf_init<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(dist, n, s0, nsrc, S);
+    k_bf_init<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(dist, n, srcs, nsrc, S);
     return cudaGetLastError();
 }
 
-// In-place (Gauss-Seidel order) pull relaxation with a change frontier: vertex v
-// is recomputed only if a neighbour changed in this or the previous sweep
-// (stamp[u] >= it - 1).  Values only decrease and stay lengths of real paths
-// (aligned 64-bit stores are atomic), so the sweep converges to the same fixed
-// point as a Jacobi sweep, in fewer sweeps and touching only the wavefront.
-__global__ void __launch_bounds__(256) k_bf_relax(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-                                                  const double* __restrict__ len, double* dist, int* stamp, int n,
-                                                  int S, int nsrc, int it, unsigned int* changed)
+// Work-efficient sweep: per (vertex, source) change bits instead of a per-vertex
+// stamp.  chg_in[u] holds S bits (W = S/32 words): which of u's distances
+// improved in the previous sweep.  Vertex v ORs its neighbours' words (like the
+// MS-BFS gather) and re-relaxes only the sources whose bit is set somewhere in
+// its neighbourhood: dist[v][k] = min(dist[v][k], dist[u][k] + len(u, v)).
+// In place (Gauss-Seidel order); a value read before its neighbour improved in
+// the same sweep is re-checked in the next one, so the fixed point is the
+// shortest-path distance (each value an fp64 sum along a shortest path).  A
+// sweep whose predecessor changed nothing returns at once (flags[it - 1] = 0).
+__global__ void __launch_bounds__(256) k_bf_sweep(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                                                  const double* __restrict__ len, double* dist,
+                                                  const uint32_t* __restrict__ chg_in, uint32_t* __restrict__ chg_out,
+                                                  int n, int S, int nsrc, int it, unsigned int* flags)
 {
-    const int v = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (it > 0 && *(volatile unsigned int*)&flags[it - 1] == 0u) return;
+    __shared__ unsigned int blk_new;
+    if (threadIdx.x == 0) blk_new = 0u;
+    __syncthreads();
     const int lane = threadIdx.x & 31;
-    if (v >= n) return;
-    const int64_t beg = row_ptr[v], end = row_ptr[v + 1];
-    bool active = it == 0;
-    for (int64_t e = beg + lane; e < end && !active; e += 32) active = stamp[col[e]] >= it - 1;
-    if (!__any_sync(0xffffffffu, active)) return;
-    bool any = false;
-    for (int k = lane; k < nsrc; k += 32) {
-        volatile double* dv = dist;
-        const double old = dv[(int64_t)v * S + k];
-        double best = old;
-        for (int64_t e = beg; e < end; ++e) {
-            const double c = dv[(int64_t)col[e] * S + k] + len[e];
-            best = c < best ? c : best;
+    const int W = S >> 5;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    bool found = false;
+    for (int64_t vv = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; vv < n; vv += nwarps) {
+        const int v = (int)vv;
+        const int64_t beg = row_ptr[v], end = row_ptr[v + 1];
+        uint32_t act = 0;
+        for (int64_t e0 = beg; e0 < end; e0 += 32) {
+            const int myu = (e0 + lane < end) ? col[e0 + lane] : 0;
+            const int cnt = (int)min((int64_t)32, end - e0);
+            for (int k0 = 0; k0 < cnt; k0 += 8) {
+                uint32_t t[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int u = __shfl_sync(0xffffffffu, myu, (k0 + k) & 31);
+                    t[k] = (k0 + k < cnt && lane < W) ? __ldcg(&chg_in[(int64_t)u * W + lane]) : 0u;
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) act |= t[k];
+            }
         }
-        if (best < old) {
-            dv[(int64_t)v * S + k] = best;
-            any = true;
+        uint32_t outw = 0;
+        if (__any_sync(0xffffffffu, act != 0u)) {
+            for (int m = 0; m < W; ++m) {
+                const uint32_t wm = __shfl_sync(0xffffffffu, act, m);
+                if (!wm) continue;
+                const int k = 32 * m + lane;
+                bool imp = false;
+                if (((wm >> lane) & 1u) && k < nsrc) {
+                    volatile double* dv = dist;
+                    const double old = dv[(int64_t)v * S + k];
+                    double best = old;
+                    for (int64_t e = beg; e < end; e += 4) {
+                        double c[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            c[q] = e + q < end ? dv[(int64_t)col[e + q] * S + k] + len[e + q] : INFINITY;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) best = c[q] < best ? c[q] : best;
+                    }
+                    if (best < old) {
+                        dv[(int64_t)v * S + k] = best;
+                        imp = true;
+                    }
+                }
+                const uint32_t bw = __ballot_sync(0xffffffffu, imp);
+                if (lane == m) outw = bw;
+            }
         }
+        if (lane < W) chg_out[(int64_t)v * W + lane] = outw;
+        found |= __any_sync(0xffffffffu, outw != 0u);
     }
-    if (__any_sync(0xffffffffu, any) && lane == 0) {
-        stamp[v] = it;
-        *changed = 1u;
-    }
+    if (found && lane == 0) blk_new = 1u;
+    __syncthreads();
+    if (threadIdx.x == 0 && blk_new) flags[it] = 1u;
 }
 
-cudaError_t launch_bf_relax(const int64_t* row_ptr, const int32_t* col, const double* len, double* dist, int* stamp,
-                            int n, int S, int nsrc, int it, unsigned int* changed, cudaStream_t s)
+// change bits of the batch's sources: vertex s0 + k has source k's bit (its
+// distance 0 is the only finite value at the start)
+__global__ void k_bf_seed(uint32_t* chg, const int* __restrict__ srcs, int nsrc, int S)
 {
-    const int64_t threads = (int64_t)n * 32;
-    k_bf_relax<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(row_ptr, col, len, dist, stamp, n, S, nsrc, it,
-                                                                 changed);
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nsrc) return;
+    chg[(int64_t)srcs[k] * (S >> 5) + (k >> 5)] = 1u << (k & 31);
+}
+
+cudaError_t launch_bf_sweep(const int64_t* row_ptr, const int32_t* col, const double* len, double* dist,
+                            const uint32_t* chg_in, uint32_t* chg_out, int n, int S, int nsrc, int it,
+                            unsigned int* flags, int grid, cudaStream_t s)
+{
+    const unsigned g = (unsigned)std::max(1, std::min(grid, (int)(((int64_t)n * 32 + 255) / 256)));
+    k_bf_sweep<<<g, 256, 0, s>>>(row_ptr, col, len, dist, chg_in, chg_out, n, S, nsrc, it, flags);
     return cudaGetLastError();
 }
 
-// rows s0..s0+nsrc-1 of the upper-triangle tiles of the local range <- fp32(dist)
-__global__ void k_bf_store(const double* __restrict__ dist, int n, int s0, int nsrc, int S, int nb, int64_t t0,
-                           int64_t t1, float* D, double* dmax)
+cudaError_t launch_bf_seed(uint32_t* chg, const int* srcs, int nsrc, int S, cudaStream_t s)
+{
+    k_bf_seed<<<(nsrc + 255) / 256, 256, 0, s>>>(chg, srcs, nsrc, S);
+    return cudaGetLastError();
+}
+
+// rows srcs[0..nsrc) of the upper-triangle tiles of the local range <- fp32(dist)
+__global__ void k_bf_store(const double* __restrict__ dist, int n, const int* __restrict__ srcs, int nsrc, int S,
+                           int nb, int64_t t0, int64_t t1, float* D, double* dmax)
 {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (int64_t)n * nsrc) return;
     const int v = (int)(idx / nsrc), k = (int)(idx % nsrc);
-    const int src = s0 + k;
+    const int src = srcs[k];
     const int I = src / kT, J = v / kT;
     if (I > J) return;
     const int64_t t = tri_index(I, J, nb);
@@ -1780,11 +1952,11 @@ __global__ void k_bf_store(const double* __restrict__ dist, int n, int s0, int n
     }
 }
 
-cudaError_t launch_bf_store(const double* dist, int n, int s0, int nsrc, int S, int nb, int64_t t0, int64_t t1,
-                            uint8_t* D, double* dmax, cudaStream_t s)
+cudaError_t launch_bf_store(const double* dist, int n, const int* srcs, int nsrc, int S, int nb, int64_t t0,
+                            int64_t t1, uint8_t* D, double* dmax, cudaStream_t s)
 {
     const int64_t total = (int64_t)n * nsrc;
-    k_bf_store<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(dist, n, s0, nsrc, S, nb, t0, t1,
+    k_bf_store<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(dist, n, srcs, nsrc, S, nb, t0, t1,
                                                              reinterpret_cast<float*>(D), dmax);
     return cudaGetLastError();
 }

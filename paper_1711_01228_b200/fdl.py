@@ -80,6 +80,7 @@ class CtxInfo(ctypes.Structure):
         ("tile0", ctypes.c_int64), ("tile1", ctypes.c_int64), ("iterations", ctypes.c_int32),
         ("k", ctypes.c_double), ("f", ctypes.c_double), ("hop_matrix_bytes", ctypes.c_uint64),
         ("local_pairs", ctypes.c_uint64), ("device_bytes", ctypes.c_uint64), ("setup_ms", ctypes.c_double),
+        ("setup_dist_ms", ctypes.c_double), ("bfs_bytes", ctypes.c_uint64),
     ]
 
 

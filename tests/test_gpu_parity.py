@@ -929,3 +929,42 @@ def test_long_cycle_16_bit_hops(n):
     r = L.run_until_converged()
     o = layout.run_algorithm2(layout.Problem(g, 2, k), X0, 1.5, 1e-4, 500)
     _gates(r.iterations, r.f_final, o)
+
+
+@pytest.mark.parametrize("graphs_on", [0, 1])
+def test_solver_cap_leaves_state_untouched(graphs_on):
+    """S:223 NoConvergence: PCG capped at cg_max_iter before cg_rtol returns
+    FDL_E_SOLVER and the step is not applied -- positions, stress and the
+    iteration count stay those of X^k -- in eager and CUDA-graph launches alike
+    (the graph's lines 5-8 sit in an IF node on the solve's convergence flag)."""
+    cfg = configs.CONFIGS["C2"]
+    g = configs.graph_for("C2")
+    X0 = configs.positions_for("C2", g.n, 1)
+    p = fdl.make_params(dim=2, k=cfg.k_for(g.n), omega=1.5, tol=cfg.tol, max_iter=cfg.max_iter, cg_rtol=1e-12,
+                        cg_max_iter=2, use_graphs=graphs_on)
+    with fdl.Layout.from_graph(g, params=p, init_pos=X0) as L:
+        f0 = L.info.f
+        X = L.get_positions()
+        for _ in range(2):  # twice: the second call takes the captured graph in graph mode
+            with pytest.raises(fdl.FdlError) as e:
+                L.step()
+            assert e.value.name == "FDL_E_SOLVER"
+            assert np.array_equal(L.get_positions(), X)
+            assert L.info.f == f0 and L.info.iterations == 0
+
+
+def test_enumerating_strategy_32_candidates():
+    """enum_count = 32 (the ABI maximum; four candidate passes, the last one
+    partly filled): runs, and picks the first argmin of the 32 stresses."""
+    from oracle import strategies
+    g, k, X0, L = make("C1", strategy=fdl.STRAT_ENUM, enum_count=32, enum_step=0.25, cg_rtol=1e-10)
+    info = L.step()
+    L.close()
+    prob = layout.Problem(g, 2, k)
+    X = layout.pin(X0.astype(np.float64))
+    omegas = tuple(0.25 * c for c in range(32))
+    _, fbest, fs = strategies.enumerate_omega(prob, prob.H(X), X, omegas=omegas)
+    c = int(round(info.omega / 0.25))
+    assert 0 <= c < 32 and fs[c] <= fbest * (1 + STRESS_TOL)  # an argmin within the stress tolerance
+    # f_after comes from the chosen point's P1 pass, f_next from the candidate pass
+    assert info.f_after <= info.f_next * (1 + STRESS_TOL)
