@@ -49,6 +49,10 @@ struct NcclApi {
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
     bool load(std::string& err)
     {
@@ -66,8 +70,13 @@ struct NcclApi {
         CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
         CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
         AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
+        Send = (decltype(Send))dlsym(h, "ncclSend");
+        Recv = (decltype(Recv))dlsym(h, "ncclRecv");
+        GroupStart = (decltype(GroupStart))dlsym(h, "ncclGroupStart");
+        GroupEnd = (decltype(GroupEnd))dlsym(h, "ncclGroupEnd");
         GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
-        if (!GetUniqueId || !CommInitRank || !CommDestroy || !AllGather) {
+        if (!GetUniqueId || !CommInitRank || !CommDestroy || !AllGather || !Send || !Recv || !GroupStart ||
+            !GroupEnd) {
             err = "libnccl.so.2 lacks required symbols";
             return false;
         }
@@ -173,7 +182,12 @@ struct fdl_ctx {
     float* ipart = nullptr;
     double* spart = nullptr;
     double* stress_scratch = nullptr;  // chunk sums of the two-stage stress reduction
-    double *rparts = nullptr, *sparts = nullptr;  // world x partials
+    double *rparts = nullptr, *sparts = nullptr;  // this rank's dense partial [world * rslice rows][C]; stress partials
+    // row-slice exchange of the pair passes (several ranks): rank g owns rows
+    // [g * rslice, (g + 1) * rslice) of the reduction
+    int64_t rslice = 0;
+    double* xrecv = nullptr;  // [world][rslice * C]: the other ranks' partials of this rank's rows
+    double* xgath = nullptr;  // [world][rslice * C + 2]: reduced row slices + stress partials, all ranks
     double *diag = nullptr, *Xk = nullptr, *Xn = nullptr, *Xt = nullptr, *Rk = nullptr, *R1 = nullptr,
            *R2 = nullptr;
     double *cr = nullptr, *cz = nullptr, *cp = nullptr, *cy = nullptr;
@@ -469,6 +483,49 @@ fdl_status allgather_inplace(fdl_ctx* ctx, void* buf, size_t slice_elems, int nc
     return FDL_OK;
 }
 
+// Multi-GPU: all-to-all of row slices.  `src` holds world slices of `slice_elems`
+// doubles (slice h for rank h); rank h's slice of every rank lands in
+// dst[g * slice_elems] for source rank g (the reduce-scatter's data movement; the
+// sum is done by a kernel in rank order, so it is deterministic).
+fdl_status alltoall_slices(fdl_ctx* ctx, const double* src, double* dst, size_t slice_elems)
+{
+    const int G = ctx->world;
+    const size_t sb = slice_elems * sizeof(double);
+    if (ctx->group) {
+        fdl_group& Gr = *ctx->group;
+        FDL_CUDA(cudaStreamSynchronize(ctx->stream));
+        {
+            std::lock_guard<std::mutex> lk(Gr.m);
+            if (Gr.buf.size() < sb * G * G) Gr.buf.resize(sb * G * G);
+        }
+        Gr.barrier();
+        // rank g's whole partial at host row g (G slices)
+        FDL_CUDA(cudaMemcpyAsync(Gr.buf.data() + (size_t)ctx->rank * G * sb, src, sb * G, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+        FDL_CUDA(cudaStreamSynchronize(ctx->stream));
+        Gr.barrier();
+        // slice `rank` of every rank's partial: G rows of sb bytes, pitch G * sb
+        FDL_CUDA(cudaMemcpy2DAsync(dst, sb, Gr.buf.data() + (size_t)ctx->rank * sb, (size_t)G * sb, sb, G,
+                                   cudaMemcpyHostToDevice, ctx->stream));
+        FDL_CUDA(cudaStreamSynchronize(ctx->stream));
+        Gr.barrier();
+        return FDL_OK;
+    }
+    ncclResult_t r = g_nccl.GroupStart();
+    for (int h = 0; h < G && r == 0; ++h) {
+        r = g_nccl.Send(src + (size_t)h * slice_elems, slice_elems, ncclFloat64, h, ctx->comm, ctx->stream);
+        if (r == 0) r = g_nccl.Recv(dst + (size_t)h * slice_elems, slice_elems, ncclFloat64, h, ctx->comm, ctx->stream);
+    }
+    const ncclResult_t r2 = g_nccl.GroupEnd();
+    if (r == 0) r = r2;
+    if (r != 0) {
+        ctx->broken = true;
+        return set_err(ctx, FDL_E_NCCL,
+                       std::string("ncclSend/ncclRecv: ") + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
+    }
+    return FDL_OK;
+}
+
 // ------------------------------------------------------------ pair passes
 // One symmetric pass over the local tiles + the per-row fixed-order
 // reduction; with several ranks the dense rank partials are all-gathered and
@@ -525,25 +582,33 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
             FDL_LAUNCH(launch_p2_finish(out0, pos, ctx->diag, ctx->n, dim, ps_p2(dim), ctx->stream));
         if (p1) {
             FDL_LAUNCH2(launch_sym_stress(ctx->spart, ctx->nitems * 8, nsets, ctx->sparts, ctx->stress_scratch, ctx->stream));
-            FDL_LAUNCH(launch_stress_ranks(ctx->sparts, 1, nsets, ctx->sc, set_cur, ctx->stream));
+            FDL_LAUNCH(launch_stress_ranks(ctx->sparts, 2, 1, nsets, ctx->sc, set_cur, ctx->stream));
         }
         return FDL_OK;
     }
-    const size_t slice = (size_t)ctx->npad * C;
-    double* mine = ctx->rparts + (size_t)ctx->rank * slice;
+    // Several ranks: this rank's dense partial (rows of its tiles) -> all-to-all of row
+    // slices -> each rank sums its slice over the ranks in rank order -> all-gather of
+    // the reduced slices, with each rank's stress partial appended to its slice (one
+    // all-gather per pass).  Every element is the rank-order sum of the rank partials
+    // (as a sum of all-gathered partials would be), on 2 (G-1)/G of a dense vector
+    // per rank instead of G - 1 dense vectors.
+    const size_t rs = (size_t)ctx->rslice * C;  // elements of one row slice
+    const size_t gs = rs + 2;                   // ... plus the stress partials
+    double* mine = ctx->rparts;
     FDL_LAUNCH(launch_sym_reduce(ctx->ipart, ctx->jpart, ctx->it_lo, ctx->it_hi, ctx->nb, ctx->t0, ctx->t1, ctx->Ilo,
                                  ctx->Ihi, C, C, 0,
                                  mine, nullptr, ctx->stream));
-    FDL_TRY(allgather_inplace(ctx, ctx->rparts, slice, ncclFloat64, 8));
-    FDL_LAUNCH(launch_rank_sum(ctx->rparts, ctx->world, ctx->npad, C, D0, inter, out0, out1, ctx->stream));
+    FDL_TRY(alltoall_slices(ctx, mine, ctx->xrecv, rs));
+    double* myg = ctx->xgath + (size_t)ctx->rank * gs;
+    FDL_LAUNCH(launch_slice_sum(ctx->xrecv, ctx->world, rs, myg, ctx->stream));
+    if (p1)
+        FDL_LAUNCH2(launch_sym_stress(ctx->spart, ctx->nitems * 8, nsets, myg + rs, ctx->stress_scratch, ctx->stream));
+    FDL_TRY(allgather_inplace(ctx, ctx->xgath, gs, ncclFloat64, 8));
+    FDL_LAUNCH(launch_slice_unpack(ctx->xgath, ctx->world, ctx->rslice, ctx->npad, C, D0, inter, out0, out1,
+                                   ctx->stream));
     if (mode == kSymP2 && p2_finish)
         FDL_LAUNCH(launch_p2_finish(out0, pos, ctx->diag, ctx->n, dim, ps_p2(dim), ctx->stream));
-    if (p1) {
-        FDL_LAUNCH2(launch_sym_stress(ctx->spart, ctx->nitems * 8, nsets, ctx->sparts + 2 * ctx->rank, ctx->stress_scratch,
-                                     ctx->stream));
-        FDL_TRY(allgather_inplace(ctx, ctx->sparts, 2, ncclFloat64, 8));
-        FDL_LAUNCH(launch_stress_ranks(ctx->sparts, ctx->world, nsets, ctx->sc, set_cur, ctx->stream));
-    }
+    if (p1) FDL_LAUNCH(launch_stress_ranks(ctx->xgath + rs, gs, ctx->world, nsets, ctx->sc, set_cur, ctx->stream));
     return FDL_OK;
 }
 
@@ -1086,7 +1151,13 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
         // kEnumNC), so the buffer holds kEnumMax rounded up to whole passes
         FDL_ALLOC(ctx->enum_f, (size_t)((kEnumMax + kEnumNC - 1) / kEnumNC) * kEnumNC);
     }
-    if (ctx->distributed) FDL_ALLOC(ctx->rparts, (size_t)world * ctx->npad * Cmax);
+    if (ctx->distributed) {
+        ctx->rslice = (ctx->npad + world - 1) / world;
+        FDL_ALLOC(ctx->rparts, (size_t)world * ctx->rslice * Cmax);
+        FDL_ALLOC(ctx->xrecv, (size_t)world * ctx->rslice * Cmax);
+        FDL_ALLOC(ctx->xgath, (size_t)world * (ctx->rslice * Cmax + 2));
+        FDL_CUDA(cudaMemsetAsync(ctx->rparts, 0, sizeof(double) * (size_t)world * ctx->rslice * Cmax, ctx->stream));
+    }
     FDL_ALLOC(ctx->diag, (size_t)ctx->npad);
     FDL_ALLOC(ctx->Xk, vn);
     FDL_ALLOC(ctx->Xn, vn);

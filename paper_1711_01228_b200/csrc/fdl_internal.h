@@ -237,9 +237,10 @@ cudaError_t launch_nib_encode(uint8_t* D, size_t bytes, cudaStream_t s);
 cudaError_t launch_hop_rows(const uint8_t* D, int hb, int nb, int64_t t0, int64_t t1, const int* rows, int nrows,
                             int n, uint16_t* out, int* missing, cudaStream_t s);
 // sum of rank partials (world x len doubles, rank order) into out0/out1 split at D of C
-cudaError_t launch_rank_sum(const double* parts, int world, int64_t rows, int C, int D, int inter, double* out0,
-                            double* out1, cudaStream_t s);
-cudaError_t launch_stress_ranks(const double* parts, int world, int nsets, DevScalars* sc, int set_cur,
+cudaError_t launch_slice_sum(const double* recv, int world, int64_t elems, double* out, cudaStream_t s);
+cudaError_t launch_slice_unpack(const double* gath, int world, int64_t rslice, int64_t rows, int C, int D, int inter,
+                                double* out0, double* out1, cudaStream_t s);
+cudaError_t launch_stress_ranks(const double* parts, int64_t stride, int world, int nsets, DevScalars* sc, int set_cur,
                                 cudaStream_t s);
 cudaError_t launch_set_sigma_rows(const double* diag, int n, DevScalars* sc, cudaStream_t s);
 

@@ -1353,15 +1353,36 @@ cudaError_t launch_sym_reduce(const float* ipart, const float* jpart, const int*
 }
 
 // sum of rank partials in rank order (multi-GPU): parts[world][rows][C]
-__global__ void k_rank_sum(const double* __restrict__ parts, int world, int64_t rows, int C, int D, int inter,
-                           double* out0, double* out1)
+// Row-slice exchange of several ranks (fdl_api.cu run_sym): out[i] = sum over
+// source ranks g = 0..world-1, in rank order, of recv[g][i] (this rank's rows of
+// every rank's partial, as the all-to-all delivered them).
+__global__ void k_slice_sum(const double* __restrict__ recv, int world, int64_t elems, double* out)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= elems) return;
+    double s = 0.0;
+    for (int g = 0; g < world; ++g) s += recv[(size_t)g * elems + i];
+    out[i] = s;
+}
+
+cudaError_t launch_slice_sum(const double* recv, int world, int64_t elems, double* out, cudaStream_t s)
+{
+    k_slice_sum<<<(unsigned)((elems + 255) / 256), 256, 0, s>>>(recv, world, elems, out);
+    return cudaGetLastError();
+}
+
+// The all-gathered reduced slices ([world][rslice * C + 2]: rows of rank g's slice,
+// then its 2 stress partials) -> the dense outputs (components [0, D) -> out0, the
+// rest -> out1; inter: components interleaved by position set, out0 = set 0).
+__global__ void k_slice_unpack(const double* __restrict__ gath, int64_t rslice, int64_t rows, int C, int D, int inter,
+                               double* out0, double* out1)
 {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= rows * C) return;
     const int64_t row = idx / C;
     const int v = (int)(idx % C);
-    double s = 0.0;
-    for (int g = 0; g < world; ++g) s += parts[(size_t)g * rows * C + idx];
+    const int64_t g = row / rslice;
+    const double s = gath[(size_t)g * (rslice * C + 2) + (row - g * rslice) * C + v];
     if (inter)
         ((v & 1) ? out1 : out0)[row * D + (v >> 1)] = s;
     else if (v < D)
@@ -1370,22 +1391,25 @@ __global__ void k_rank_sum(const double* __restrict__ parts, int world, int64_t 
         out1[row * (C - D) + (v - D)] = s;
 }
 
-cudaError_t launch_rank_sum(const double* parts, int world, int64_t rows, int C, int D, int inter, double* out0,
-                            double* out1, cudaStream_t s)
+cudaError_t launch_slice_unpack(const double* gath, int world, int64_t rslice, int64_t rows, int C, int D, int inter,
+                                double* out0, double* out1, cudaStream_t s)
 {
+    (void)world;
     const int64_t total = rows * C;
-    k_rank_sum<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(parts, world, rows, C, D, inter, out0, out1);
+    k_slice_unpack<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(gath, rslice, rows, C, D, inter, out0, out1);
     return cudaGetLastError();
 }
 
-// f = sum over ranks (rank order) of the rank stress partials; Eq. 1 counts
-// each unordered pair once, as the symmetric pass does.
-__global__ void k_stress_ranks(const double* __restrict__ parts, int world, int nsets, DevScalars* sc, int set_cur)
+// f = sum over ranks (rank order) of the rank stress partials (rank g's pair at
+// parts + g * stride); Eq. 1 counts each unordered pair once, as the symmetric
+// pass does.
+__global__ void k_stress_ranks(const double* __restrict__ parts, int64_t stride, int world, int nsets, DevScalars* sc,
+                               int set_cur)
 {
     if (threadIdx.x != 0) return;
     for (int s = 0; s < nsets; ++s) {
         double v = 0.0;
-        for (int g = 0; g < world; ++g) v += parts[g * 2 + s];
+        for (int g = 0; g < world; ++g) v += parts[(size_t)g * stride + s];
         sc->f_set[s] = v;
         if (set_cur && s == 0) {
             sc->f_cur = v;
@@ -1394,10 +1418,10 @@ __global__ void k_stress_ranks(const double* __restrict__ parts, int world, int 
     }
 }
 
-cudaError_t launch_stress_ranks(const double* parts, int world, int nsets, DevScalars* sc, int set_cur,
+cudaError_t launch_stress_ranks(const double* parts, int64_t stride, int world, int nsets, DevScalars* sc, int set_cur,
                                 cudaStream_t s)
 {
-    k_stress_ranks<<<1, 32, 0, s>>>(parts, world, nsets, sc, set_cur);
+    k_stress_ranks<<<1, 32, 0, s>>>(parts, stride, world, nsets, sc, set_cur);
     return cudaGetLastError();
 }
 
