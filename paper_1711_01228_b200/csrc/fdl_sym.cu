@@ -48,6 +48,9 @@ constexpr int kBfsUnroll = FDL_BFS_UNROLL;
 #ifndef FDL_P1A_CTAS
 #define FDL_P1A_CTAS 2  // CTAs per SM of the 2-D fused evaluation pass
 #endif
+#ifndef FDL_P2_SHFLRED_CTAS
+#define FDL_P2_SHFLRED_CTAS 2  // CTAs per SM of the 2-D PCG matvec pass with the butterfly (16 more live registers)
+#endif
 #ifndef FDL_P2_CTAS
 #define FDL_P2_CTAS 3  // CTAs per SM of the 2-D PCG matvec pass
 #endif
@@ -56,6 +59,16 @@ constexpr int kBfsUnroll = FDL_BFS_UNROLL;
 #endif
 #ifndef FDL_TPS_P2
 #define FDL_TPS_P2 2  // 4-bit P2: tiles of one work item per TMA stage (one mbarrier wait / refill each)
+#endif
+#ifndef FDL_P2_SHFLRED
+#define FDL_P2_SHFLRED 0  // 1: 4-bit 2-D P2 j-side column sums by a warp butterfly (measured slower)
+#endif
+#ifndef FDL_P2_MUFU_COLS
+// 4-bit P2: bit cc set -> column cc of each 16-byte chunk (4 columns per chunk) takes
+// its weights from the MUFU (rcp.approx(h^2), bitwise the table's fp32(1/h^2) for
+// h <= 15) instead of the shared-memory table: moves that share of the table's
+// shared-memory wavefronts to the otherwise idle XU pipe
+#define FDL_P2_MUFU_COLS 0  // measured slower for every share: 0x8 -> 1762, 0xA -> 1613, 0xF -> 1377 vs 1913 GB/s
 #endif
 #ifndef FDL_MAXST
 #define FDL_MAXST 4  // deepest TMA ring of the pair passes
@@ -192,6 +205,15 @@ __host__ __device__ constexpr int sym_stage_bytes()
     return (int)tile_bytes(HB) + kT * sym_ps<MODE, DIM, NSETS>() * 4;
 }
 
+// j-side column sums of the tile by a warp butterfly (registers + SHFL) instead of
+// shared-memory stores and the warp flush: the 4-bit 2-D matvec pass, whose
+// shared-memory wavefronts bound it
+template <int MODE, int DIM, int NSETS, int HB>
+__host__ __device__ constexpr bool sym_shflred()
+{
+    return FDL_P2_SHFLRED && MODE == kSymP2 && DIM == 2 && NSETS == 1 && HB == 0;
+}
+
 // floats per lane row of a warp's j-side buffer: 9C keeps the 16 rows of a
 // half-warp on distinct banks for the C-wide vector stores
 template <int MODE, int DIM, int NSETS>
@@ -210,7 +232,7 @@ __host__ __device__ constexpr size_t sym_red_floats()  // the j-side warp buffer
 template <int MODE, int DIM>
 __host__ __device__ constexpr int sym_ctas_per_sm()
 {
-    return (MODE == kSymP2 && DIM == 2)    ? FDL_P2_CTAS
+    return (MODE == kSymP2 && DIM == 2)    ? (FDL_P2_SHFLRED ? FDL_P2_SHFLRED_CTAS : FDL_P2_CTAS)
            : (MODE == kSymP1A && DIM == 2) ? FDL_P1A_CTAS
            : (MODE == kSymP1S && DIM == 2) ? FDL_P1S_CTAS
                                            : ((DIM == 2 || (MODE != kSymP1 && MODE != kSymP1S && MODE != kSymP1A &&
@@ -546,9 +568,10 @@ template <int MODE, int DIM, int NSETS, int HB, bool SAFE>
 __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, const float* lut, const float2* lut2,
                                          const float2* lutw, uint32_t magic, float alpha, int ty, int tx, bool diag,
                                          const float (&xi)[8][NSETS * DIM], float (&ai)[8][sym_ncomp<MODE, DIM, NSETS>()],
-                                         float* myred, float (&sf)[2][NSETS])
+                                         float* myred, float (&sf)[2][NSETS], float (&jv)[8 * sym_ncomp<MODE, DIM, NSETS>()])
 {
     constexpr int C = sym_ncomp<MODE, DIM, NSETS>();
+    constexpr bool BFLY = sym_shflred<MODE, DIM, NSETS, HB>();
     constexpr int PS = sym_ps<MODE, DIM, NSETS>();
     constexpr int NCH = HB ? 4 * HB : 2;  // 16-byte chunks per thread
     constexpr int CPC = HB ? 2 / HB : 4;  // columns per chunk
@@ -617,6 +640,29 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
                 for (int v = 0; v < C; ++v) aj[0][v] = aj[1][v] = 0.0f;
                 const uint32_t w = word_of(ch, cc);
                 float2 e[4], ew[4];
+                if (MODE == kSymP2 && ((FDL_P2_MUFU_COLS >> cc) & 1)) {
+                    // the four bytes of the word at once: hi nibbles H, lo = (lo' - 4 hi) mod 16
+                    // per byte lane (lo' | 64 keeps each byte's difference from borrowing)
+                    const uint32_t H = (w >> 4) & 0x0F0F0F0Fu;
+                    const uint32_t L = (((w & 0x0F0F0F0Fu) | 0x40404040u) - (H << 2)) & 0x0F0F0F0Fu;
+#pragma unroll
+                    for (int rp = 0; rp < 4; ++rp) {
+                        uint32_t bl, bh;  // 0x4B0000hh = 2^23 + h
+                        switch (rp) {
+                            case 0: bl = prmt_imm<0x7650>(L, magic); bh = prmt_imm<0x7650>(H, magic); break;
+                            case 1: bl = prmt_imm<0x7651>(L, magic); bh = prmt_imm<0x7651>(H, magic); break;
+                            case 2: bl = prmt_imm<0x7652>(L, magic); bh = prmt_imm<0x7652>(H, magic); break;
+                            default: bl = prmt_imm<0x7653>(L, magic); bh = prmt_imm<0x7653>(H, magic); break;
+                        }
+                        const float hl = __uint_as_float(bl) - 8388608.0f, hh = __uint_as_float(bh) - 8388608.0f;
+                        float wl = rcp_approx(hl * hl), wh = rcp_approx(hh * hh);
+                        if (SAFE) {  // h = 0 (diagonal, padding): weight 0, as the table's entry
+                            wl = hl > 0.0f ? wl : 0.0f;
+                            wh = hh > 0.0f ? wh : 0.0f;
+                        }
+                        e[rp] = make_float2(wl, wh);
+                    }
+                } else
 #pragma unroll
                 for (int rp = 0; rp < 4; ++rp) {
                     const uint32_t off = rp == 0 ? ((w << 3) & 0x7f8u) : ((w >> (8 * rp - 3)) & 0x7f8u);
@@ -651,7 +697,12 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
                     }
                 }
 #pragma unroll
-                for (int v = 0; v < C; ++v) myred[c * C + v] = aj[0][v] + aj[1][v];
+                for (int v = 0; v < C; ++v) {
+                    if (BFLY)
+                        jv[c * C + v] = aj[0][v] + aj[1][v];
+                    else
+                        myred[c * C + v] = aj[0][v] + aj[1][v];
+                }
             }
         }
         return;
@@ -700,6 +751,40 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
             for (int v = 0; v < C; ++v) myred[c * C + v] = aj[0][v] + aj[1][v];
         }
     }
+}
+
+// j-side column sums by a warp butterfly: lane (h = tx & 1, ty) holds jv[e] =
+// its 8-row partial of output e = c * C + v (column tx * 8 + c).  Four halving
+// exchanges with lanes ty ^ 1, ^ 2, ^ 4, ^ 8 (each lane keeps the half of the
+// vector picked by that bit of ty and adds the partner's copy) leave lane ty
+// with the 16-row sum of output e = 8 b0 + 4 b1 + 2 b2 + b3 (b_k = bit k of ty).
+// The pairs added at each level are those of sym_flush_warp's tree (rows r and
+// r + w for w = 1, 2, 4, 8), so the sums are bitwise the same.  Needs 8C = 16.
+template <int MODE, int DIM, int NSETS>
+__device__ __forceinline__ void sym_bfly_warp(const float (&jv)[16], float* jpart_warp, int lane)
+{
+    const int ty = lane & 15, h = lane >> 4;
+    const bool b0 = ty & 1, b1 = ty & 2, b2 = ty & 4, b3 = ty & 8;
+    float l0[8], l1[4], l2[2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const float send = b0 ? jv[i] : jv[8 + i], keep = b0 ? jv[8 + i] : jv[i];
+        l0[i] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float send = b1 ? l0[i] : l0[4 + i], keep = b1 ? l0[4 + i] : l0[i];
+        l1[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const float send = b2 ? l1[i] : l1[2 + i], keep = b2 ? l1[2 + i] : l1[i];
+        l2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    const float send = b3 ? l2[0] : l2[1], keep = b3 ? l2[1] : l2[0];
+    const float tot = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    const int e = (b0 ? 8 : 0) + (b1 ? 4 : 0) + (b2 ? 2 : 0) + (b3 ? 1 : 0);
+    jpart_warp[h * 16 + e] = tot;  // P2: symmetric, no sign
 }
 
 // j-side flush of one tile by one warp (no CTA barrier): the warp's lanes are
@@ -840,10 +925,11 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
             float sf[2][NSETS];  // stress of the tile, even / odd rows (two independent FMA chains)
 #pragma unroll
             for (int s = 0; s < NSETS; ++s) sf[0][s] = sf[1][s] = 0.0f;
+            float jv[8 * C];  // j-side column partials (butterfly mode)
             if (safe)
-                sym_tile<MODE, DIM, NSETS, HB, true>(sD, sP, lut, lut2, lutw2, a.magic, a.alpha, ty, tx, diag, xi, ai, wrow, sf);
+                sym_tile<MODE, DIM, NSETS, HB, true>(sD, sP, lut, lut2, lutw2, a.magic, a.alpha, ty, tx, diag, xi, ai, wrow, sf, jv);
             else
-                sym_tile<MODE, DIM, NSETS, HB, false>(sD, sP, lut, lut2, lutw2, a.magic, a.alpha, ty, tx, diag, xi, ai, wrow, sf);
+                sym_tile<MODE, DIM, NSETS, HB, false>(sD, sP, lut, lut2, lutw2, a.magic, a.alpha, ty, tx, diag, xi, ai, wrow, sf, jv);
 #pragma unroll
             for (int s = 0; s < NSETS; ++s) s64[s] += (double)sf[0][s] + (double)sf[1][s];
             // stage consumed by this warp; the last of the 8 warps refills it
@@ -858,7 +944,10 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
                     }
                 }
             }
-            sym_flush_warp<MODE, DIM, NSETS>(wbuf, a.jpart + ((size_t)it.w + t) * kT * C + wid * 16 * C, lane);
+            if constexpr (sym_shflred<MODE, DIM, NSETS, HB>())
+                sym_bfly_warp<MODE, DIM, NSETS>(jv, a.jpart + ((size_t)it.w + t) * kT * C + wid * 16 * C, lane);
+            else
+                sym_flush_warp<MODE, DIM, NSETS>(wbuf, a.jpart + ((size_t)it.w + t) * kT * C + wid * 16 * C, lane);
             if (last && ++stage == NST) {
                 stage = 0;
                 phase ^= 1u;
@@ -984,7 +1073,11 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, 2>()) k_tile_mix(co
         float sf[2][NSETS];
 #pragma unroll
         for (int q = 0; q < NSETS; ++q) sf[0][q] = sf[1][q] = 0.0f;
-        sym_tile<MODE, 2, NSETS, 0, false>(sD, sP, lut, lut2, lut2, 0x4B000000u, -2.0f, ty, tx, false, xi, ai, wrow, sf);
+        float jv[8 * C];
+        sym_tile<MODE, 2, NSETS, 0, false>(sD, sP, lut, lut2, lut2, 0x4B000000u, -2.0f, ty, tx, false, xi, ai, wrow, sf,
+                                           jv);
+        if constexpr (sym_shflred<MODE, 2, NSETS, 0>())
+            sym_bfly_warp<MODE, 2, NSETS>(jv, red + wid * 2 * (16 * JP + 16), lane);  // the pass stores one float per lane
         s64 += (double)sf[0][0] + (double)sf[1][NSETS - 1];
         __syncwarp();
     }
