@@ -285,7 +285,10 @@ fdl_status fdl_get_positions(fdl_ctx* ctx, double* out, size_t count);
 /* Replace the placement (count n*dim, all finite, else FDL_E_INVALID_ARG);
  * re-pins x_0 = 0, recomputes f, L^X X and L^W X at it (one fused pass)
  * and clears the stop flag (checkpoint resume / interactive layouts / parity).
- * The recycled PCG basis (DESIGN R27) belongs to L^W and is kept. */
+ * The recycled PCG basis (DESIGN R27) belongs to L^W and is kept.  A placement
+ * bitwise equal to the current one as fdl_get_positions returns it (a caller
+ * that round-trips its layout through the host) keeps the context's state as it
+ * is (f, forces, PCG history; no evaluation pass) and only clears the stop flag. */
 fdl_status fdl_set_positions(fdl_ctx* ctx, const double* in, size_t count);
 
 /* Per-vertex relax factors omega_i >= 0 (§6 (1), line 410:

@@ -1927,6 +1927,18 @@ fdl_status fdl_set_positions(fdl_ctx* ctx, const double* in, size_t count)
     cudaSetDevice(ctx->device);
     ctx->stopped = false;
     ctx->stop_reason = 0;
+    if (ctx->a_valid && std::isfinite(ctx->f)) {
+        // the placement fdl_get_positions returned, passed back unchanged (a caller that
+        // round-trips its placement through the host every step): the context's f, R, L^W X
+        // and PCG history are already those of this placement, so no evaluation pass
+        FDL_CUDA(cudaMemcpyAsync(ctx->Xt, in, count * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        FDL_CUDA(cudaMemsetAsync(&ctx->sc->anynew, 0, sizeof(unsigned int), ctx->stream));
+        FDL_LAUNCH(launch_placement_differs(ctx->Xt, ctx->Xk, count, ctx->k, &ctx->sc->anynew, ctx->stream));
+        unsigned int differs = 1;
+        FDL_CUDA(cudaMemcpyAsync(&differs, &ctx->sc->anynew, sizeof differs, cudaMemcpyDeviceToHost, ctx->stream));
+        FDL_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (!differs) return FDL_OK;
+    }
     return upload_positions(ctx, in);
 }
 

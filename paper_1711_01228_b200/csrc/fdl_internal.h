@@ -49,7 +49,7 @@ struct DevScalars {
     int done;
     int cg_iters;
     double relres;
-    unsigned int anynew;   // MS-BFS level flag
+    unsigned int anynew;   // fdl_set_positions: the uploaded placement differs from X^k
     // recycled PCG start (R27): y of x0 = X^k + V y per column, basis vectors in use
     double gal_y[3][8];
     int gal_cnt;           // valid history vectors for the next start (<= kGalMax)
@@ -85,6 +85,8 @@ cudaError_t launch_extrap(const double* Xk, const double* Xprev, const double* A
                           double* y0, const DevScalars* sc, int n, int dim, int valid, cudaStream_t s);
 // ABI units: mode 0 y = (x - x_0) / k (upload, pin), mode 1 y = x k (download)
 cudaError_t launch_pin_scale(const double* x, double* y, int n, int dim, double k, int mode, cudaStream_t s);
+cudaError_t launch_placement_differs(const double* x, const double* Xk, size_t cnt, double k, unsigned int* differs,
+                                     cudaStream_t s);
 // Recycled PCG start (R27): Galerkin projection of the warm-start error onto the
 // last kGalMax step differences V (with AV = L^W V from the carried products).
 cudaError_t launch_gal_start(const double* V, const double* AV, const double* b, const double* Xk, const double* Ak,

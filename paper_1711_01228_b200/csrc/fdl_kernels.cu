@@ -399,6 +399,23 @@ __global__ void k_pin_scale(const double* __restrict__ x, double* __restrict__ y
     y[g] = mode == 0 ? (x[g] - x[g % dim]) / k : x[g] * k;
 }
 
+// fdl_set_positions: does the uploaded placement x (original units) differ from the
+// context's X^k as fdl_get_positions returns it (X^k * k, bitwise)?  *differs = 1 if so.
+__global__ void k_placement_differs(const double* __restrict__ x, const double* __restrict__ Xk, size_t cnt, double k,
+                                    unsigned int* differs)
+{
+    const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool d = g < cnt && x[g] != Xk[g] * k;
+    if (__any_sync(0xffffffffu, d) && (threadIdx.x & 31) == 0) *differs = 1u;
+}
+
+cudaError_t launch_placement_differs(const double* x, const double* Xk, size_t cnt, double k, unsigned int* differs,
+                                     cudaStream_t s)
+{
+    k_placement_differs<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(x, Xk, cnt, k, differs);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pin_scale(const double* x, double* y, int n, int dim, double k, int mode, cudaStream_t s)
 {
     const size_t cnt = (size_t)n * dim;

@@ -968,3 +968,31 @@ def test_enumerating_strategy_32_candidates():
     assert 0 <= c < 32 and fs[c] <= fbest * (1 + STRESS_TOL)  # an argmin within the stress tolerance
     # f_after comes from the chosen point's P1 pass, f_next from the candidate pass
     assert info.f_after <= info.f_next * (1 + STRESS_TOL)
+
+
+def test_set_positions_round_trip_keeps_state():
+    """fdl_set_positions with the placement fdl_get_positions just returned keeps
+    the context's state (no evaluation pass): the trajectory is bitwise that of
+    a run without the round trips; a changed placement is evaluated afresh."""
+    cfg = configs.CONFIGS["C2"]
+    g = configs.graph_for("C2")
+    X0 = configs.positions_for("C2", g.n, 4)
+    p = fdl.make_params(dim=2, k=cfg.k_for(g.n), omega=1.6, tol=cfg.tol, max_iter=cfg.max_iter, use_graphs=0)
+    runs = []
+    for round_trip in (False, True):
+        with fdl.Layout.from_graph(g, params=p, init_pos=X0) as L:
+            fs = []
+            for _ in range(12):
+                if round_trip:
+                    before = L.get_stats().p1_launches
+                    L.set_positions(L.get_positions())
+                    assert L.get_stats().p1_launches == before
+                fs.append(L.step().f_after)
+            runs.append((fs, L.get_positions()))
+            if round_trip:
+                before = L.get_stats().p1_launches
+                Y = L.get_positions()
+                Y[5, 0] += 1e-3 * cfg.k_for(g.n)
+                L.set_positions(Y)
+                assert L.get_stats().p1_launches == before + 1
+    assert runs[0][0] == runs[1][0] and np.array_equal(runs[0][1], runs[1][1])
