@@ -78,6 +78,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-rows", type=int, default=0)
     ap.add_argument("--no-run-leg", action="store_true", help="skip the whole-run (fdl_run_until_converged) leg")
+    ap.add_argument("--cg-rtol", type=float, default=0.0,
+                    help="PCG relative residual (0: 1e-2 tol for C5, the library default otherwise; DESIGN R8)")
     ap.add_argument("--plumbing-only", action="store_true",
                     help="test hook: ranks join a gloo group and report; no GPU work (tests/test_bench_spawn.py)")
     return ap.parse_args()
@@ -329,8 +331,12 @@ def run_gpu(args):
     n = g.n
     k = cfg.k_for(n)
     X0 = configs.positions_for(args.config, n, args.seed)
+    # PCG tolerance: C5 runs S:246's 1e-2 tol (its trajectory is the exact solve's at that
+    # tolerance: the BA20k/BA40k parity tests run this path, DESIGN R8); the other configs
+    # take the library default min(1e-2 tol, 1e-9) (C4's trajectory needs it)
+    cg_rtol = args.cg_rtol if args.cg_rtol > 0 else (1e-2 * cfg.tol if args.config == "C5" else 0.0)
     p = fdl.make_params(dim=cfg.dim, k=k, omega=cfg.omega, tol=cfg.tol, max_iter=cfg.max_iter, device=local_rank,
-                        cg_rtol=max(float(os.environ.get("FDL_CG_RTOL_F", "1e-2")) * cfg.tol, 1e-9),  # the config's solve tolerance (R8)
+                        cg_rtol=cg_rtol,
                         cg_extrap=int(os.environ.get("FDL_CG_EXTRAP", "2")),
                         p1_split=int(os.environ.get("FDL_P1_SPLIT", "-1")),
                         strategy={"fixed": fdl.STRAT_FIXED, "prob": fdl.STRAT_PROB, "enum": fdl.STRAT_ENUM}[args.strategy])
@@ -571,6 +577,7 @@ def run_gpu(args):
                        "dim": dim, "omega": cfg.omega, "k": k, "diameter": info.diameter,
                        "hop_bits": info.hop_bits, "parallelism": f"triangle-tile shard x{world} (NCCL all-gather of partials)",
                        "precision": "f32 pair arithmetic, f64 reductions, PCG state and positions",
+                       "cg_rtol": cg_rtol if cg_rtol > 0 else min(1e-2 * cfg.tol, 1e-9), "tol": cfg.tol,
                        "l2": ("inputs larger than L2 (hop matrix %.1f GB per GPU, L2 %.0f MB)"
                               % (info.hop_matrix_bytes / 1e9, l2_bytes / 1e6) if info.hop_matrix_bytes > l2_bytes else
                               "no L2 flush: the hop matrix (%.1f MB) fits in L2 (%.0f MB), as it does in every step "

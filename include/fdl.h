@@ -87,7 +87,9 @@ typedef struct {
     int32_t max_iter;     /* >= 1                                                                   */
     double weight_exp;    /* alpha in w = d^alpha, finite; -2 in the paper. alpha != -2 or
                              edge lengths use fp32 path-length tiles (NEXT-3)           */
-    double cg_rtol;       /* PCG relative residual; <= 0 -> max(1e-2*tol, 1e-9)             */
+    double cg_rtol;       /* PCG relative residual; <= 0 -> min(1e-2*tol, 1e-9): X^{k+1} solved to the
+                             precision at which the trajectory is the exact solve's (DESIGN R8);
+                             1e-2*tol is faster and reproduces it on C1-C3/C5 only    */
     int32_t cg_max_iter;  /* PCG cap per outer iteration; <= 0 -> min(10n, 10000)           */
     int32_t strategy;     /* fdl_strategy                                                           */
     uint64_t seed;        /* roulette stream seed (FDL_STRAT_PROB)                                  */

@@ -1,0 +1,32 @@
+"""Whole runs to the stop rule under different PCG tolerances: iterations, final f,
+PCG steps and wall time per iteration (the cost of a tighter solve, DESIGN R8)."""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1711_01228_b200 import fdl  # noqa: E402
+from workloads import configs, graphs  # noqa: E402
+
+name = sys.argv[1]
+rtols = [float(x) for x in sys.argv[2].split(",")]
+seed = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+if name.startswith("BA"):
+    g = graphs.barabasi_albert(int(name[2:-1]) * 1000, 3, seed=5)
+    cfg = configs.CONFIGS["C5"]
+    X0 = graphs.init_positions(g.n, 2, 5000 + seed)
+else:
+    cfg = configs.CONFIGS[name]
+    g = configs.graph_for(name)
+    X0 = configs.positions_for(name, g.n, seed)
+for rtol in rtols:
+    p = fdl.make_params(dim=cfg.dim, k=cfg.k_for(g.n), omega=cfg.omega, tol=cfg.tol, max_iter=cfg.max_iter,
+                        cg_rtol=rtol)
+    with fdl.Layout.from_graph(g, params=p, init_pos=X0) as L:
+        t0 = time.perf_counter()
+        r = L.run_until_converged()
+        dt = time.perf_counter() - t0
+    print(json.dumps({"cfg": name, "seed": seed, "cg_rtol": rtol, "iterations": r.iterations, "f": r.f_final,
+                      "pcg": r.cg_iters, "pcg_per_it": r.cg_iters / r.iterations, "ms_per_it": 1e3 * dt / r.iterations}),
+          flush=True)

@@ -358,7 +358,9 @@ TRACE_CASES = ["C3", "BA20k", "C2tol5", "C4", "BA40k"]
 # (fused + CUDA graph below n^2 = 2^30, split + eager above: C4, BA40k and C5), and
 # each one forced on every case
 PATHS = {"default": {}, "split_eager": {"p1_split": 1, "use_graphs": 0},
-         "fused_graph": {"p1_split": 0, "use_graphs": 1}}
+         "fused_graph": {"p1_split": 0, "use_graphs": 1},
+         # bench.py's C5 launch: S:246's solve tolerance 1e-2 tol (DESIGN R8)
+         "bench_c5": {"cg_rtol_tol": 1e-2}}
 
 
 def _trace_files(case):
@@ -373,6 +375,8 @@ def _trace_files(case):
 
 
 def _run_trace(d, g, **kw):
+    if "cg_rtol_tol" in kw:
+        kw["cg_rtol"] = kw.pop("cg_rtol_tol") * d["tol"]
     X0 = graphs.init_positions(g.n, d["dim"], d["position_seed"])
     p = fdl.make_params(dim=d["dim"], k=d["k"], omega=d["omega"], tol=d["tol"], max_iter=d["max_iter"], **kw)
     with fdl.Layout.from_graph(g, params=p, init_pos=X0) as L:
@@ -426,6 +430,17 @@ def test_end_to_end_launch_paths(case, path):
     one CUDA graph per step): the same end-to-end gates."""
     d = _trace_files(case)[0]
     _run_trace(d, _golden_graph(d), **PATHS[path])
+
+
+@pytest.mark.parametrize("case", ["BA20k", "BA40k"])
+def test_end_to_end_bench_c5_parameters(case):
+    """The C5 stand-ins over every stored seed with bench.py's C5 parameters
+    (solve to 1e-2 tol; the library default otherwise, DESIGN R8): the
+    gates hold, so the benchmarked configuration is parity-checked."""
+    ds = _trace_files(case)
+    g = _golden_graph(ds[0])
+    its = [_run_trace(d, g, **PATHS["bench_c5"]) for d in ds]
+    _mean_gate(its, [d["iterations"] for d in ds])
 
 
 def test_carried_lw_matches_full_refresh():
