@@ -749,7 +749,8 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
         const int grid = ctx->sm_count * 8;
         // hubs (degree > kBfsHubDeg): a block each per level
         std::vector<int> hub_list;
-        for (int v = 0; v < n; ++v)
+        static const bool no_hubs = getenv("FDL_BFS_NO_HUBS") != nullptr;  // A/B of the hub blocks
+        for (int v = 0; v < n && !no_hubs; ++v)
             if (rp[v + 1] - rp[v] > kBfsHubDeg) hub_list.push_back(v);
         int* d_hubs = nullptr;
         if (!hub_list.empty()) {

@@ -1790,7 +1790,7 @@ __global__ void __launch_bounds__(256) k_bfs_level_sym(const int64_t* __restrict
     for (int64_t vv = ((int64_t)(blockIdx.x - nhub) * blockDim.x + threadIdx.x) >> 5; vv < n; vv += nwarps) {
         const int v = (int)vv;
         const int64_t beg = row_ptr[v], end = row_ptr[v + 1];
-        if (end - beg > kBfsHubDeg) continue;  // a hub block's vertex
+        if (nhub > 0 && end - beg > kBfsHubDeg) continue;  // a hub block's vertex
         const uint32_t vis = visited[(int64_t)v * kBFSWords + lane];
         if (__all_sync(0xffffffffu, (vis & full) == full)) {
             fout[(int64_t)v * kBFSWords + lane] = 0u;
