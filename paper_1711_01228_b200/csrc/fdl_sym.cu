@@ -1992,31 +1992,46 @@ __global__ void __launch_bounds__(256) k_bf_sweep(const int64_t* __restrict__ ro
         }
         uint32_t outw = 0;
         if (__any_sync(0xffffffffu, act != 0u)) {
+            // the neighbour list in lane registers (one neighbour per lane, up to 32; longer
+            // lists are read in chunks of 32), so each relaxation issues all its distance
+            // loads at once instead of a col[] -> dist[] chain per neighbour
+            const int deg = (int)(end - beg);
+            const int nu = (int)min((int64_t)32, end - beg);
+            const int myu = lane < nu ? col[beg + lane] : 0;
+            const double myl = lane < nu ? len[beg + lane] : 0.0;
             for (int m = 0; m < W; ++m) {
                 const uint32_t wm = __shfl_sync(0xffffffffu, act, m);
                 if (!wm) continue;
                 const int k = 32 * m + lane;
+                const bool on = ((wm >> lane) & 1u) && k < nsrc;
+                volatile double* dv = dist;
+                const double old = on ? dv[(int64_t)v * S + k] : 0.0;
+                double best = old;
+                for (int q0 = 0; q0 < nu; q0 += 8) {
+                    double c[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int u = __shfl_sync(0xffffffffu, myu, (q0 + q) & 31);
+                        const double l = __shfl_sync(0xffffffffu, myl, (q0 + q) & 31);
+                        c[q] = (on && q0 + q < nu) ? dv[(int64_t)u * S + k] + l : INFINITY;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) best = c[q] < best ? c[q] : best;
+                }
+                for (int64_t e = beg + 32; e < end; ++e)  // lists longer than 32 (rare)
+                    if (on) {
+                        const double c = dv[(int64_t)col[e] * S + k] + len[e];
+                        best = c < best ? c : best;
+                    }
                 bool imp = false;
-                if (((wm >> lane) & 1u) && k < nsrc) {
-                    volatile double* dv = dist;
-                    const double old = dv[(int64_t)v * S + k];
-                    double best = old;
-                    for (int64_t e = beg; e < end; e += 4) {
-                        double c[4];
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            c[q] = e + q < end ? dv[(int64_t)col[e + q] * S + k] + len[e + q] : INFINITY;
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) best = c[q] < best ? c[q] : best;
-                    }
-                    if (best < old) {
-                        dv[(int64_t)v * S + k] = best;
-                        imp = true;
-                    }
+                if (on && best < old) {
+                    dv[(int64_t)v * S + k] = best;
+                    imp = true;
                 }
                 const uint32_t bw = __ballot_sync(0xffffffffu, imp);
                 if (lane == m) outw = bw;
             }
+            (void)deg;
         }
         if (lane < W) chg_out[(int64_t)v * W + lane] = outw;
         found |= __any_sync(0xffffffffu, outw != 0u);
