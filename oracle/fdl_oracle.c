@@ -108,9 +108,13 @@ static inline double weight(double d, double alpha) { return pow(d, alpha); }
  * Only a cache of the same values -- pow() per pair is 20x slower. */
 typedef struct { double* d; double* w; } dw_table;
 
+/* Largest hop of a matrix (sizes the table); a max over threads -- the table's values
+ * do not depend on how it is found.  (A serial scan of a full C4 matrix, 4.8 GB, cost
+ * ~1 s per call, i.e. most of an oracle iteration.) */
 static uint16_t max_hop(const uint16_t* h, size_t count)
 {
     uint16_t m = 0;
+#pragma omp parallel for reduction(max : m) schedule(static)
     for (size_t t = 0; t < count; ++t) if (h[t] > m) m = h[t];
     return m;
 }

@@ -746,7 +746,8 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
         FDL_CUDA(cudaMemsetAsync(&ctx->sc->bfs_diam, 0, sizeof(int), ctx->stream));
         FDL_CUDA(cudaMemsetAsync(&ctx->sc->bfs_overflow, 0, sizeof(int), ctx->stream));
         FDL_CUDA(cudaMemsetAsync(&ctx->sc->bfs_bytes, 0, sizeof(unsigned long long), ctx->stream));
-        const int grid = ctx->sm_count * 8;
+        static const int grid_mult = getenv("FDL_BFS_GRID") ? atoi(getenv("FDL_BFS_GRID")) : 8;  // A/B knob
+        const int grid = ctx->sm_count * std::max(1, grid_mult);
         // hubs (degree > kBfsHubDeg): a block each per level
         std::vector<int> hub_list;
         static const bool no_hubs = getenv("FDL_BFS_NO_HUBS") != nullptr;  // A/B of the hub blocks
