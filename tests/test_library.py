@@ -79,6 +79,10 @@ def test_parameter_validation():
     # edge lengths (NEXT-3): positive and finite per stored direction
     _expect("FDL_E_BAD_LENGTH", g.n, g.row_ptr, g.col, edge_len=np.array([1.0, 1.0, -2.0, -2.0]))
     _expect("FDL_E_BAD_LENGTH", g.n, g.row_ptr, g.col, edge_len=np.array([1.0, 1.0, np.inf, np.inf]))
+    # ... and equal in the two stored directions of an edge: path 0-1-2 stores
+    # (0,1), (1,0), (1,2), (2,1); edge (1,2) gets 2.0 one way and 3.0 the other
+    assert list(g.col) == [1, 0, 2, 1]
+    _expect("FDL_E_BAD_LENGTH", g.n, g.row_ptr, g.col, edge_len=np.array([1.0, 1.0, 2.0, 3.0]))
     p = fdl.make_params(strategy=fdl.STRAT_ENUM, weight_exp=-1.0)
     _expect("FDL_E_UNSUPPORTED", g.n, g.row_ptr, g.col, params=p)
     p = fdl.make_params(cg_history=9)  # recycled PCG start window: 0 (default 2) .. 8
