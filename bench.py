@@ -342,9 +342,16 @@ def run_gpu(args):
                         strategy={"fixed": fdl.STRAT_FIXED, "prob": fdl.STRAT_PROB, "enum": fdl.STRAT_ENUM}[args.strategy])
     if world > 1 or force_dist:
         from paper_1711_01228_b200 import dist as fdist
-        L = fdist.sharded_layout(g, p, X0, edge_len=configs.edge_lengths_for(args.config))
-    else:
-        L = fdl.Layout.from_graph(g, params=p, init_pos=X0, edge_len=configs.edge_lengths_for(args.config))
+
+    def new_layout():
+        """A fresh context: each leg (device-timed steps, e2e, whole run) starts from X0
+        with an empty recycled PCG basis (R27), so no leg replays another's trajectory
+        through the basis the earlier leg left behind."""
+        if world > 1 or force_dist:
+            return fdist.sharded_layout(g, p, X0, edge_len=configs.edge_lengths_for(args.config))
+        return fdl.Layout.from_graph(g, params=p, init_pos=X0, edge_len=configs.edge_lengths_for(args.config))
+
+    L = new_layout()
     # an explicit stream: the library enqueues everything on it and the timing events are
     # recorded on it (torch's default stream has handle 0, which the library would replace
     # by its own stream, unordered with events on the legacy stream)
@@ -489,12 +496,15 @@ def run_gpu(args):
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        # pinned host buffer (page-locked: the copies run at PCIe/C2C DMA speed). The run restarts
+        # pinned host buffer (page-locked: the copies run at PCIe/C2C DMA speed). A fresh context
         # from X0 with the same warm-up, so the timed e2e steps are the same iterations of the
         # trajectory as the device-timed ones (PCG counts depend on the phase of the run)
         Xh = torch.empty((n, dim), dtype=torch.float64, pin_memory=True).numpy()
         Xh[:] = X0
-        L.set_positions(X0)
+        L.close()
+        L = new_layout()
+        L.set_stream(stream.cuda_stream)
+        L.set_timing(True)
         for _ in range(args.warmup):
             L.set_positions(Xh)
             if L.step().stop:
@@ -527,7 +537,10 @@ def run_gpu(args):
     # iterations / time of fdl_run_until_converged, setup excluded)
     run_leg = None
     if not args.no_run_leg:
-        L.set_positions(X0)
+        L.close()
+        L = new_layout()
+        L.set_stream(stream.cuda_stream)
+        L.set_timing(True)
         L.reset_stats()
         barrier()
         e4 = torch.cuda.Event(enable_timing=True)

@@ -117,8 +117,8 @@ typedef struct {
                              sync per PCG iteration; -1 (default): 1 on one GPU when the split
                              line-6 pass is off (n^2 < 2^30). Same results either way (bitwise).
                              With graphs the stats time whole steps only (p1_ms = p2_ms = 0)     */
-    int32_t cg_history;   /* cg_extrap = 2: step differences kept for the start, 1..8 (0 = default 2;
-                             more vectors cut PCG counts a little further, DESIGN R27)           */
+    int32_t cg_history;   /* cg_extrap = 2: step differences kept for the start, 1..8 (0 = default 8;
+                             fewer vectors take more PCG steps, DESIGN R27)                      */
 } fdl_params;
 
 typedef struct {

@@ -33,6 +33,10 @@ using namespace fdl;
 
 namespace {
 
+#ifndef FDL_CG_HISTORY_DEFAULT
+#define FDL_CG_HISTORY_DEFAULT 8  // step differences kept for the recycled PCG start (R27)
+#endif
+
 // ------------------------------------------------------------- NCCL (dlopen)
 // NCCL is loaded at run time (the copy torch already loaded, if any), so the
 // single-GPU library has no link-time NCCL dependency.
@@ -1089,7 +1093,7 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     // valid trajectory on slowly converging inputs (C4 seeds 2-3: 169 / 179 iterations
     // against 160 / 189 for every solve at <= 1e-9)
     if (!(p.cg_rtol > 0)) ctx->p.cg_rtol = std::min(1e-2 * p.tol, 1e-9);
-    if (p.cg_history == 0) ctx->p.cg_history = 2;
+    if (p.cg_history == 0) ctx->p.cg_history = FDL_CG_HISTORY_DEFAULT;
     if (p.cg_max_iter <= 0) ctx->p.cg_max_iter = std::min(10 * n, 10000);
     if (p.a_refresh <= 0) ctx->p.a_refresh = 10;
     if (std::isfinite(p.step)) ctx->p.a_refresh = 1;  // the cap makes Xt non-linear in X^{k+1}
