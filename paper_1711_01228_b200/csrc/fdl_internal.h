@@ -227,9 +227,10 @@ int bfs_row_bytes_host(int hb);  // batch-buffer bytes per vertex
 // CSR with edge lengths; dist[v * S + s] for the batch's sources s0..s0+S-1
 cudaError_t launch_bf_init(double* dist, int n, const int* srcs, int nsrc, int S, cudaStream_t s);
 cudaError_t launch_bf_sweep(const int64_t* row_ptr, const int32_t* col, const double* len, double* dist,
-                            const uint32_t* chg_in, uint32_t* chg_out, int n, int S, int nsrc, int it,
-                            unsigned int* flags, int grid, cudaStream_t s);
-cudaError_t launch_bf_seed(uint32_t* chg, const int* srcs, int nsrc, int S, cudaStream_t s);
+                            const uint32_t* chg_in, uint32_t* chg_out, const uint8_t* pend_in, uint8_t* pend_out,
+                            int n, int S, int nsrc, int it, double delta, unsigned int* flags, int grid,
+                            cudaStream_t s);
+cudaError_t launch_bf_seed(uint32_t* chg, uint8_t* pend, const int* srcs, int nsrc, int S, cudaStream_t s);
 cudaError_t launch_bf_store(const double* dist, int n, const int* srcs, int nsrc, int S, int nb, int64_t t0,
                             int64_t t1, uint8_t* D, double* dmax, cudaStream_t s);
 cudaError_t launch_dist_rows(const uint8_t* D, int hb, int nb, int64_t t0, int64_t t1, const int* rows, int nrows,

@@ -1962,7 +1962,8 @@ cudaError_t launch_bf_init(double* dist, int n, const int* srcs, int nsrc, int S
 __global__ void __launch_bounds__(256) k_bf_sweep(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                                                   const double* __restrict__ len, double* dist,
                                                   const uint32_t* __restrict__ chg_in, uint32_t* __restrict__ chg_out,
-                                                  int n, int S, int nsrc, int it, unsigned int* flags)
+                                                  const uint8_t* __restrict__ pend_in, uint8_t* __restrict__ pend_out,
+                                                  int n, int S, int nsrc, int it, double delta, unsigned int* flags)
 {
     if (it > 0 && *(volatile unsigned int*)&flags[it - 1] == 0u) return;
     __shared__ unsigned int blk_new;
@@ -1970,71 +1971,86 @@ __global__ void __launch_bounds__(256) k_bf_sweep(const int64_t* __restrict__ ro
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int W = S >> 5;
+    const double T = delta * (double)(it + 1);  // this sweep's threshold (Delta-stepping buckets)
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
     bool found = false;
+    volatile double* dv = dist;
     for (int64_t vv = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; vv < n; vv += nwarps) {
         const int v = (int)vv;
         const int64_t beg = row_ptr[v], end = row_ptr[v + 1];
+        const int nu = (int)min((int64_t)32, end - beg);
+        const int myu = lane < nu ? col[beg + lane] : 0;
+        const bool selfp = pend_in[v] != 0;
+        // a vertex with nothing pending in its neighbourhood (the usual case away from the
+        // batch's wavefront band) costs its neighbours' 1-byte flags only
+        bool np = lane < nu && pend_in[myu] != 0;
+        for (int64_t e = beg + 32 + lane; e < end && !np; e += 32) np = pend_in[col[e]] != 0;
+        const unsigned pm = __ballot_sync(0xffffffffu, np);
+        if (!pm && !selfp) {
+            if (lane == 0) pend_out[v] = 0;
+            continue;
+        }
+        // candidate sources: pending bits of the neighbours that have any
         uint32_t act = 0;
-        for (int64_t e0 = beg; e0 < end; e0 += 32) {
-            const int myu = (e0 + lane < end) ? col[e0 + lane] : 0;
-            const int cnt = (int)min((int64_t)32, end - e0);
-            for (int k0 = 0; k0 < cnt; k0 += 8) {
-                uint32_t t[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const int u = __shfl_sync(0xffffffffu, myu, (k0 + k) & 31);
-                    t[k] = (k0 + k < cnt && lane < W) ? __ldcg(&chg_in[(int64_t)u * W + lane]) : 0u;
-                }
-#pragma unroll
-                for (int k = 0; k < 8; ++k) act |= t[k];
+        {
+            unsigned m = pm & (nu == 32 ? 0xffffffffu : ((1u << nu) - 1u));  // warp-uniform (a ballot)
+            while (m) {
+                const int q = __ffs(m) - 1;
+                m &= m - 1;
+                const int u = __shfl_sync(0xffffffffu, myu, q);
+                if (lane < W) act |= __ldcg(&chg_in[(int64_t)u * W + lane]);
             }
         }
-        uint32_t outw = 0;
-        if (__any_sync(0xffffffffu, act != 0u)) {
-            // the neighbour list in lane registers (one neighbour per lane, up to 32; longer
-            // lists are read in chunks of 32), so each relaxation issues all its distance
-            // loads at once instead of a col[] -> dist[] chain per neighbour
-            const int deg = (int)(end - beg);
-            const int nu = (int)min((int64_t)32, end - beg);
-            const int myu = lane < nu ? col[beg + lane] : 0;
-            const double myl = lane < nu ? len[beg + lane] : 0.0;
-            for (int m = 0; m < W; ++m) {
-                const uint32_t wm = __shfl_sync(0xffffffffu, act, m);
-                if (!wm) continue;
-                const int k = 32 * m + lane;
-                const bool on = ((wm >> lane) & 1u) && k < nsrc;
-                volatile double* dv = dist;
-                const double old = on ? dv[(int64_t)v * S + k] : 0.0;
-                double best = old;
-                for (int q0 = 0; q0 < nu; q0 += 8) {
-                    double c[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const int u = __shfl_sync(0xffffffffu, myu, (q0 + q) & 31);
-                        const double l = __shfl_sync(0xffffffffu, myl, (q0 + q) & 31);
-                        c[q] = (on && q0 + q < nu) ? dv[(int64_t)u * S + k] + l : INFINITY;
-                    }
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) best = c[q] < best ? c[q] : best;
-                }
-                for (int64_t e = beg + 32; e < end; ++e)  // lists longer than 32 (rare)
-                    if (on) {
-                        const double c = dv[(int64_t)col[e] * S + k] + len[e];
-                        best = c < best ? c : best;
-                    }
-                bool imp = false;
-                if (on && best < old) {
-                    dv[(int64_t)v * S + k] = best;
-                    imp = true;
-                }
-                const uint32_t bw = __ballot_sync(0xffffffffu, imp);
-                if (lane == m) outw = bw;
+        if (end - beg > 32)  // long lists: the rest in order (rare)
+            for (int64_t e = beg + 32; e < end; ++e) {
+                const int u = col[e];
+                if (pend_in[u] && lane < W) act |= __ldcg(&chg_in[(int64_t)u * W + lane]);
             }
-            (void)deg;
+        const uint32_t own = (selfp && lane < W) ? chg_in[(int64_t)v * W + lane] : 0u;
+        const double myl = lane < nu ? len[beg + lane] : 0.0;
+        uint32_t outw = 0;
+        for (int m = 0; m < W; ++m) {
+            const uint32_t wm = __shfl_sync(0xffffffffu, act, m), om = __shfl_sync(0xffffffffu, own, m);
+            if (!(wm | om)) continue;
+            const int k = 32 * m + lane;
+            const bool on = ((wm >> lane) & 1u) && k < nsrc;
+            const bool mine = (om >> lane) & 1u;
+            const double old = (on || mine) ? dv[(int64_t)v * S + k] : 0.0;
+            double best = old;
+            for (int q0 = 0; q0 < nu; q0 += 8) {
+                double c[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int u = __shfl_sync(0xffffffffu, myu, (q0 + q) & 31);
+                    const double l = __shfl_sync(0xffffffffu, myl, (q0 + q) & 31);
+                    const double du = (on && q0 + q < nu) ? dv[(int64_t)u * S + k] : INFINITY;
+                    c[q] = du <= T ? du + l : INFINITY;  // a distance above the threshold waits
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) best = c[q] < best ? c[q] : best;
+            }
+            for (int64_t e = beg + 32; e < end; ++e)  // lists longer than 32 (rare)
+                if (on) {
+                    const double du = dv[(int64_t)col[e] * S + k];
+                    const double c = du <= T ? du + len[e] : INFINITY;
+                    best = c < best ? c : best;
+                }
+            bool imp = false;
+            if (on && best < old) {
+                dv[(int64_t)v * S + k] = best;
+                imp = true;
+            }
+            // pending after this sweep: a new value, or an own pending value above the
+            // threshold (its neighbours did not take it yet); own values <= T were pulled
+            // by every neighbour in this sweep
+            const bool keep = imp || (mine && old > T);
+            const uint32_t bw = __ballot_sync(0xffffffffu, keep);
+            if (lane == m) outw = bw;
         }
         if (lane < W) chg_out[(int64_t)v * W + lane] = outw;
-        found |= __any_sync(0xffffffffu, outw != 0u);
+        const bool any = __any_sync(0xffffffffu, outw != 0u);
+        if (lane == 0) pend_out[v] = any ? 1 : 0;
+        found |= any;
     }
     if (found && lane == 0) blk_new = 1u;
     __syncthreads();
@@ -2043,25 +2059,28 @@ __global__ void __launch_bounds__(256) k_bf_sweep(const int64_t* __restrict__ ro
 
 // change bits of the batch's sources: vertex s0 + k has source k's bit (its
 // distance 0 is the only finite value at the start)
-__global__ void k_bf_seed(uint32_t* chg, const int* __restrict__ srcs, int nsrc, int S)
+__global__ void k_bf_seed(uint32_t* chg, uint8_t* pend, const int* __restrict__ srcs, int nsrc, int S)
 {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nsrc) return;
     chg[(int64_t)srcs[k] * (S >> 5) + (k >> 5)] = 1u << (k & 31);
+    pend[srcs[k]] = 1;
 }
 
 cudaError_t launch_bf_sweep(const int64_t* row_ptr, const int32_t* col, const double* len, double* dist,
-                            const uint32_t* chg_in, uint32_t* chg_out, int n, int S, int nsrc, int it,
-                            unsigned int* flags, int grid, cudaStream_t s)
+                            const uint32_t* chg_in, uint32_t* chg_out, const uint8_t* pend_in, uint8_t* pend_out,
+                            int n, int S, int nsrc, int it, double delta, unsigned int* flags, int grid,
+                            cudaStream_t s)
 {
     const unsigned g = (unsigned)std::max(1, std::min(grid, (int)(((int64_t)n * 32 + 255) / 256)));
-    k_bf_sweep<<<g, 256, 0, s>>>(row_ptr, col, len, dist, chg_in, chg_out, n, S, nsrc, it, flags);
+    k_bf_sweep<<<g, 256, 0, s>>>(row_ptr, col, len, dist, chg_in, chg_out, pend_in, pend_out, n, S, nsrc, it, delta,
+                                 flags);
     return cudaGetLastError();
 }
 
-cudaError_t launch_bf_seed(uint32_t* chg, const int* srcs, int nsrc, int S, cudaStream_t s)
+cudaError_t launch_bf_seed(uint32_t* chg, uint8_t* pend, const int* srcs, int nsrc, int S, cudaStream_t s)
 {
-    k_bf_seed<<<(nsrc + 255) / 256, 256, 0, s>>>(chg, srcs, nsrc, S);
+    k_bf_seed<<<(nsrc + 255) / 256, 256, 0, s>>>(chg, pend, srcs, nsrc, S);
     return cudaGetLastError();
 }
 
