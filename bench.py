@@ -67,7 +67,7 @@ def survey_flops_line6(dim: int) -> int:
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="fdl", choices=["fdl", "reference"])
     ap.add_argument("--config", default="C5", choices=list(configs.CONFIGS))
@@ -140,7 +140,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "25"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -148,7 +148,13 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))  # host arrival time of each sample
+
+    def mark(self, which: str):
+        """Host time at the start / end of the timed region: only samples that arrive
+        inside it count (the sampler starts before the warm-up, since nvidia-smi itself
+        needs ~0.1-0.3 s before its first sample)."""
+        setattr(self, which, time.time())
 
     def stop(self):
         if self.proc is None:
@@ -161,7 +167,9 @@ class ClockSampler:
         self.t.join(timeout=2)
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0, t1 = getattr(self, "t_begin", 0.0), getattr(self, "t_end", float("inf"))
+        inside = [ln for t, ln in self.lines if t0 <= t <= t1 + 0.05]
+        for ln in inside:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -174,7 +182,7 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "interval_ms": 25}
 
 
 def load_peaks():
@@ -378,13 +386,14 @@ def run_gpu(args):
             restarts += 1
         return inf
 
+    clocks = ClockSampler(local_rank)
+    clocks.start()
     for _ in range(args.warmup):
         step_or_restart()
     restarts = 0
     L.reset_stats()
-    clocks = ClockSampler(local_rank)
     barrier()
-    clocks.start()
+    clocks.mark("t_begin")
     marks = []
     accepted = 0
     st_excl = None  # stats of the untimed restarts (the P1A evaluation pass of set_positions)
@@ -402,6 +411,7 @@ def run_gpu(args):
             restarts += 1
             st_excl = _stats_add(st_excl, _stats_sub(L.get_stats(), before))
     barrier()
+    clocks.mark("t_end")
     clk = clocks.stop()
     ms = sum(a.elapsed_time(b) for a, b in marks)
     st = _stats_sub(L.get_stats(), st_excl) if st_excl is not None else L.get_stats()
