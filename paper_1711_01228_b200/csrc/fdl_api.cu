@@ -679,6 +679,46 @@ struct Scratch {
     }
 };
 
+// Source batches as compact graph neighbourhoods: clusters of up to S sources of
+// [lo, hi), each grown by BFS (over vertices not yet taken) from the first untaken
+// vertex.  Sources close to each other have nearly concentric wavefronts, so a batch's
+// searches touch a band of the graph at a time instead of all of it (geometric graphs:
+// MS-BFS on C4, the weighted sweeps on W4).
+std::vector<int> cluster_sources(int32_t n, const int64_t* rp, const int32_t* col, int lo, int hi, int S)
+{
+    std::vector<int> order;
+    order.reserve((size_t)std::max(0, hi - lo));
+    std::vector<char> taken((size_t)n, 0);
+    std::vector<int> q;
+    q.reserve((size_t)n);
+    std::vector<int> mark((size_t)n, -1);
+    int cluster = 0;
+    for (int seed = lo; seed < hi; ++seed) {
+        if (taken[seed]) continue;
+        q.clear();
+        q.push_back(seed);
+        mark[seed] = cluster;
+        int got = 0;
+        for (size_t h = 0; h < q.size() && got < S; ++h) {
+            const int u = q[h];
+            if (u >= lo && u < hi && !taken[u]) {
+                taken[u] = 1;
+                order.push_back(u);
+                ++got;
+            }
+            for (int64_t e = rp[u]; e < rp[u + 1]; ++e) {
+                const int w = col[e];
+                if (mark[w] != cluster) {
+                    mark[w] = cluster;
+                    q.push_back(w);
+                }
+            }
+        }
+        ++cluster;
+    }
+    return order;
+}
+
 // ------------------------------------------------------------------ MS-BFS
 // Sources: the rows of the blocks I of the local tiles.  Writes the upper
 // triangle tiles of the local range; the Jacobi diagonal follows from one
@@ -764,26 +804,60 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
                                      ctx->stream));
         }
         const int nhub = (int)hub_list.size();
+        // high-diameter graphs: clustered batches, per-vertex frontier flags and a scattered
+        // store into the tiles (id-contiguous batches spread their 1024 wavefronts over the
+        // whole graph: every vertex gathers at every level).  Low-diameter graphs keep
+        // id-contiguous batches and the tiled store (the whole graph is within a few levels
+        // of any batch anyway)
+        static const int cl_min_ecc = getenv("FDL_BFS_CLUSTER_ECC") ? atoi(getenv("FDL_BFS_CLUSTER_ECC")) : 24;
+        const bool clustered = ecc0 >= cl_min_ecc && src_hi - src_lo > 32 * kBFSWords;
+        std::vector<int> order;
+        int* d_srcs = nullptr;
+        uint8_t *fl_a = nullptr, *fl_b = nullptr;
+        if (clustered) {
+            order = cluster_sources(n, rp, col, src_lo, src_hi, 32 * kBFSWords);
+            FDL_CUDA(tmp.alloc(&d_srcs, sizeof(int) * order.size()));
+            FDL_CUDA(cudaMemcpyAsync(d_srcs, order.data(), sizeof(int) * order.size(), cudaMemcpyHostToDevice,
+                                     ctx->stream));
+            FDL_CUDA(tmp.alloc(&fl_a, (size_t)n));
+            FDL_CUDA(tmp.alloc(&fl_b, (size_t)n));
+        }
         for (int s0 = src_lo; s0 < src_hi; s0 += 32 * kBFSWords) {
             const int nsrc = std::min(32 * kBFSWords, src_hi - s0);
+            const int* srcs = clustered ? d_srcs + (s0 - src_lo) : nullptr;
             FDL_CUDA(cudaMemsetAsync(bbuf, 0, bbytes, ctx->stream));
             FDL_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned int) * (size_t)(nlev + 2), ctx->stream));
-            FDL_LAUNCH(launch_bfs_init(fa, vis, n, s0, ctx->stream));
+            if (clustered) {
+                FDL_CUDA(cudaMemsetAsync(fa, 0, masks * 4, ctx->stream));
+                FDL_CUDA(cudaMemsetAsync(vis, 0, masks * 4, ctx->stream));
+                FDL_CUDA(cudaMemsetAsync(fl_a, 0, (size_t)n, ctx->stream));
+                FDL_LAUNCH(launch_bfs_init_list(fa, vis, fl_a, srcs, nsrc, ctx->stream));
+            } else {
+                FDL_LAUNCH(launch_bfs_init(fa, vis, n, s0, ctx->stream));
+            }
             uint32_t *fin = fa, *fout = fb;
+            uint8_t *flin = fl_a, *flout = fl_b;
             for (int level = 1; level <= nlev; ++level) {
                 FDL_LAUNCH(launch_bfs_level_sym(d_rp, d_col, fin, fout, vis, bbuf, n, nsrc, level, hb, flags,
-                                                &ctx->sc->bfs_bytes, d_hubs, nhub, grid, ctx->stream));
+                                                &ctx->sc->bfs_bytes, d_hubs, nhub, grid, flin, flout, ctx->stream));
                 std::swap(fin, fout);
+                std::swap(flin, flout);
             }
             FDL_LAUNCH(launch_bfs_batch_end(flags, nlev, maxhop, &ctx->sc->bfs_diam, &ctx->sc->bfs_overflow,
                                             ctx->stream));
-            FDL_LAUNCH(launch_bfs_retile(bbuf, ctx->D, n, s0, nsrc, ctx->nb, ctx->t0, ctx->t1, hb, ctx->stream));
+            if (clustered)
+                FDL_LAUNCH(launch_bfs_scatter(bbuf, ctx->D, srcs, nsrc, n, ctx->nb, ctx->t0, ctx->t1, hb, ctx->stream));
+            else
+                FDL_LAUNCH(launch_bfs_retile(bbuf, ctx->D, n, s0, nsrc, ctx->nb, ctx->t0, ctx->t1, hb, ctx->stream));
         }
         FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, ctx->stream));
         FDL_CUDA(cudaStreamSynchronize(ctx->stream));
         tmp.release(bbuf);
         tmp.release(flags);
         if (d_hubs) tmp.release(d_hubs);
+        if (d_srcs) tmp.release(d_srcs);
+        if (fl_a) tmp.release(fl_a);
+        if (fl_b) tmp.release(fl_b);
         const bool overflow = ctx->sc_host->bfs_overflow != 0;
         const int diam = ctx->sc_host->bfs_diam;
         ctx->bfs_bytes += ctx->sc_host->bfs_bytes;
@@ -889,39 +963,7 @@ fdl_status build_dists(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, cons
     // untaken vertex.  Sources close to each other have nearly concentric wavefronts,
     // so each sweep's change words are dense (many sources per vertex at once) instead
     // of one bit per 32-lane word (measured: W4 setup 6.2 s with id-contiguous batches).
-    std::vector<int> order;
-    order.reserve((size_t)std::max(0, src_hi - src_lo));
-    {
-        std::vector<char> taken((size_t)n, 0);
-        std::vector<int> q;
-        q.reserve((size_t)n);
-        std::vector<int> mark((size_t)n, -1);
-        int cluster = 0;
-        for (int seed = src_lo; seed < src_hi; ++seed) {
-            if (taken[seed]) continue;
-            // BFS from seed; collect untaken vertices of [src_lo, src_hi) until S of them
-            q.clear();
-            q.push_back(seed);
-            mark[seed] = cluster;
-            int got = 0;
-            for (size_t h = 0; h < q.size() && got < S; ++h) {
-                const int u = q[h];
-                if (u >= src_lo && u < src_hi && !taken[u]) {
-                    taken[u] = 1;
-                    order.push_back(u);
-                    ++got;
-                }
-                for (int64_t e = rp[u]; e < rp[u + 1]; ++e) {
-                    const int w = col[e];
-                    if (mark[w] != cluster) {
-                        mark[w] = cluster;
-                        q.push_back(w);
-                    }
-                }
-            }
-            ++cluster;
-        }
-    }
+    const std::vector<int> order = cluster_sources(n, rp, col, src_lo, src_hi, S);
     int* d_srcs = nullptr;
     FDL_CUDA(tmp.alloc(&d_srcs, sizeof(int) * std::max<size_t>(order.size(), 1)));
     if (!order.empty())

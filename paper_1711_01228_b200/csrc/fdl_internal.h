@@ -217,7 +217,11 @@ cudaError_t launch_sym_stress(const double* spart, int nitems, int nsets, double
 cudaError_t launch_bfs_level_sym(const int64_t* row_ptr, const int32_t* col, const uint32_t* fin, uint32_t* fout,
                                  uint32_t* visited, uint8_t* bbuf, int n, int nsrc, int level, int hb,
                                  unsigned int* flags, unsigned long long* bytes, const int* hubs, int nhub, int grid,
+                                 const uint8_t* fl_in, uint8_t* fl_out, cudaStream_t s);
+cudaError_t launch_bfs_init_list(uint32_t* frontier, uint32_t* visited, uint8_t* fl, const int* srcs, int nsrc,
                                  cudaStream_t s);
+cudaError_t launch_bfs_scatter(const uint8_t* bbuf, uint8_t* D, const int* srcs, int nsrc, int n, int nb, int64_t t0,
+                               int64_t t1, int hb, cudaStream_t s);
 cudaError_t launch_bfs_batch_end(const unsigned int* flags, int nlevels, int maxhop, int* diam, int* overflow,
                                  cudaStream_t s);
 cudaError_t launch_bfs_retile(const uint8_t* bbuf, uint8_t* D, int n, int s0, int nsrc, int nb, int64_t t0,

@@ -1697,7 +1697,8 @@ __host__ __device__ constexpr int bfs_row_bytes()  // batch-buffer bytes per ver
 // 128 B each per vertex searched) are added to *bytes (MS-BFS roofline).
 template <int HB>
 __device__ __forceinline__ uint32_t bfs_gather(const int32_t* __restrict__ col, const uint32_t* __restrict__ fin,
-                                               int64_t beg, int64_t end, int64_t stride, int lane)
+                                               int64_t beg, int64_t end, int64_t stride, int lane,
+                                               const uint8_t* __restrict__ fl = nullptr)
 {
     // OR of the neighbours' frontier words over col[beg, end) in chunks of 32 neighbours
     // `stride` apart; kBfsUnroll independent 128-byte loads in flight per warp
@@ -1710,7 +1711,7 @@ __device__ __forceinline__ uint32_t bfs_gather(const int32_t* __restrict__ col, 
 #pragma unroll
             for (int k = 0; k < kBfsUnroll; ++k) {
                 const int u = __shfl_sync(0xffffffffu, myu, (k0 + k) & 31);
-                t[k] = (k0 + k < cnt) ? __ldcg(&fin[(int64_t)u * kBFSWords + lane]) : 0u;
+                t[k] = (k0 + k < cnt && (!fl || fl[u])) ? __ldcg(&fin[(int64_t)u * kBFSWords + lane]) : 0u;
             }
 #pragma unroll
             for (int k = 0; k < kBfsUnroll; ++k) acc |= t[k];
@@ -1736,7 +1737,8 @@ __global__ void __launch_bounds__(256) k_bfs_level_sym(const int64_t* __restrict
                                                        uint32_t* __restrict__ visited, uint8_t* __restrict__ bbuf,
                                                        int n, int nsrc, int level, unsigned int* flags,
                                                        unsigned long long* bytes, const int* __restrict__ hubs,
-                                                       int nhub)
+                                                       int nhub, const uint8_t* __restrict__ fl_in,
+                                                       uint8_t* __restrict__ fl_out)
 {
     if (level > 1 && *(volatile unsigned int*)&flags[level - 1] == 0u) return;  // uniform over the grid
     __shared__ unsigned long long blk_bytes;
@@ -1761,7 +1763,7 @@ __global__ void __launch_bounds__(256) k_bfs_level_sym(const int64_t* __restrict
         __syncthreads();
         const int64_t beg = row_ptr[v], end = row_ptr[v + 1];
         if (!hub_skip) {
-            const uint32_t acc = bfs_gather<HB>(col, fin, beg + 32 * wid, end, 256, lane);
+            const uint32_t acc = bfs_gather<HB>(col, fin, beg + 32 * wid, end, 256, lane, fl_in);
             if (acc) atomicOr(&hub_acc[lane], acc);
         }
         __syncthreads();
@@ -1769,6 +1771,7 @@ __global__ void __launch_bounds__(256) k_bfs_level_sym(const int64_t* __restrict
             const uint32_t vis = visited[(int64_t)v * kBFSWords + lane];
             if (hub_skip) {
                 fout[(int64_t)v * kBFSWords + lane] = 0u;
+                if (fl_out && lane == 0) fl_out[v] = 0;
             } else {
                 const uint32_t nw = hub_acc[lane] & ~vis & full;
                 fout[(int64_t)v * kBFSWords + lane] = nw;
@@ -1777,7 +1780,9 @@ __global__ void __launch_bounds__(256) k_bfs_level_sym(const int64_t* __restrict
                     bfs_record<HB>(bbuf + (int64_t)v * bfs_row_bytes<HB>() + lane * (bfs_row_bytes<HB>() / 32), nw,
                                    level);
                 }
-                if (__any_sync(0xffffffffu, nw != 0u) && lane == 0) flags[level] = 1u;
+                const bool anyn = __any_sync(0xffffffffu, nw != 0u);
+                if (anyn && lane == 0) flags[level] = 1u;
+                if (fl_out && lane == 0) fl_out[v] = anyn ? 1 : 0;
                 if (lane == 0) atomicAdd(bytes, (unsigned long long)(end - beg + 2) * 128ull);
             }
         }
@@ -1791,12 +1796,23 @@ __global__ void __launch_bounds__(256) k_bfs_level_sym(const int64_t* __restrict
         const int v = (int)vv;
         const int64_t beg = row_ptr[v], end = row_ptr[v + 1];
         if (nhub > 0 && end - beg > kBfsHubDeg) continue;  // a hub block's vertex
+        if (fl_in) {
+            // frontier flags (clustered batches): a vertex none of whose neighbours holds a
+            // frontier bit gathers nothing (its words are not read by anyone: flag 0)
+            bool nf = false;
+            for (int64_t e = beg + lane; e < end && !nf; e += 32) nf = fl_in[col[e]] != 0;
+            if (!__any_sync(0xffffffffu, nf)) {
+                if (lane == 0) fl_out[v] = 0;
+                continue;
+            }
+        }
         const uint32_t vis = visited[(int64_t)v * kBFSWords + lane];
         if (__all_sync(0xffffffffu, (vis & full) == full)) {
             fout[(int64_t)v * kBFSWords + lane] = 0u;
+            if (fl_out && lane == 0) fl_out[v] = 0;
             continue;
         }
-        const uint32_t acc = bfs_gather<HB>(col, fin, beg, end, 32, lane);
+        const uint32_t acc = bfs_gather<HB>(col, fin, beg, end, 32, lane, fl_in);
         my_bytes += (unsigned long long)(end - beg + 2) * 128ull;
         const uint32_t nw = acc & ~vis & full;
         fout[(int64_t)v * kBFSWords + lane] = nw;
@@ -1804,7 +1820,9 @@ __global__ void __launch_bounds__(256) k_bfs_level_sym(const int64_t* __restrict
             visited[(int64_t)v * kBFSWords + lane] = vis | nw;
             bfs_record<HB>(bbuf + (int64_t)v * bfs_row_bytes<HB>() + lane * (bfs_row_bytes<HB>() / 32), nw, level);
         }
-        found |= __any_sync(0xffffffffu, nw != 0u);
+        const bool anyn = __any_sync(0xffffffffu, nw != 0u);
+        if (fl_out && lane == 0) fl_out[v] = anyn ? 1 : 0;
+        found |= anyn;
     }
     if (lane == 0) {
         if (my_bytes) atomicAdd(&blk_bytes, my_bytes);
@@ -1889,18 +1907,91 @@ __global__ void __launch_bounds__(256) k_bfs_retile(const uint8_t* __restrict__ 
 cudaError_t launch_bfs_level_sym(const int64_t* row_ptr, const int32_t* col, const uint32_t* fin, uint32_t* fout,
                                  uint32_t* visited, uint8_t* bbuf, int n, int nsrc, int level, int hb,
                                  unsigned int* flags, unsigned long long* bytes, const int* hubs, int nhub, int grid,
-                                 cudaStream_t s)
+                                 const uint8_t* fl_in, uint8_t* fl_out, cudaStream_t s)
 {
     const unsigned g = (unsigned)nhub + (unsigned)std::max(1, std::min(grid, (int)(((int64_t)n * 32 + 255) / 256)));
     if (hb == 0)
         k_bfs_level_sym<0><<<g, 256, 0, s>>>(row_ptr, col, fin, fout, visited, bbuf, n, nsrc, level, flags, bytes,
-                                             hubs, nhub);
+                                             hubs, nhub, fl_in, fl_out);
     else if (hb == 1)
         k_bfs_level_sym<1><<<g, 256, 0, s>>>(row_ptr, col, fin, fout, visited, bbuf, n, nsrc, level, flags, bytes,
-                                             hubs, nhub);
+                                             hubs, nhub, fl_in, fl_out);
     else
         k_bfs_level_sym<2><<<g, 256, 0, s>>>(row_ptr, col, fin, fout, visited, bbuf, n, nsrc, level, flags, bytes,
-                                             hubs, nhub);
+                                             hubs, nhub, fl_in, fl_out);
+    return cudaGetLastError();
+}
+
+// Clustered batches (high-diameter graphs): the batch's sources are an arbitrary list
+// srcs[0..nsrc) (a compact graph neighbourhood, so the 1024 wavefronts travel
+// together); frontier / visited bit of slot k at vertex srcs[k], frontier flags set.
+__global__ void k_bfs_init_list(uint32_t* frontier, uint32_t* visited, uint8_t* fl, const int* __restrict__ srcs,
+                                int nsrc)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nsrc) return;
+    const int v = srcs[k];
+    frontier[(int64_t)v * kBFSWords + (k >> 5)] = 1u << (k & 31);  // one source per vertex: no conflict
+    visited[(int64_t)v * kBFSWords + (k >> 5)] = 1u << (k & 31);
+    fl[v] = 1;
+}
+
+cudaError_t launch_bfs_init_list(uint32_t* frontier, uint32_t* visited, uint8_t* fl, const int* srcs, int nsrc,
+                                 cudaStream_t s)
+{
+    k_bfs_init_list<<<(nsrc + 255) / 256, 256, 0, s>>>(frontier, visited, fl, srcs, nsrc);
+    return cudaGetLastError();
+}
+
+// Clustered batches: hop(srcs[k], v) from the batch buffer into the local upper-triangle
+// tiles, one thread per (v, k) (k fastest: coalesced bbuf reads), scattered stores; 4-bit
+// cells share a byte between rows 2p and 2p+1 (possibly of other batches): atomicOr of
+// the nibble into its zero-initialised word (raw layout, nib_encode runs after all batches).
+template <int HB>
+__global__ void k_bfs_scatter(const uint8_t* __restrict__ bbuf, uint8_t* D, const int* __restrict__ srcs, int nsrc,
+                              int n, int nb, int64_t t0, int64_t t1)
+{
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)n * nsrc) return;
+    const int v = (int)(idx / nsrc), k = (int)(idx % nsrc);
+    const int src = srcs[k];
+    const int I = src / kT, J = v / kT;
+    if (I > J) return;
+    const int64_t t = tri_index(I, J, nb);
+    if (t < t0 || t >= t1) return;
+    constexpr int RB = bfs_row_bytes<HB>();
+    const uint8_t* cells = bbuf + (int64_t)v * RB;
+    uint32_t h;
+    if (HB == 0)
+        h = (cells[k >> 1] >> (4 * (k & 1))) & 15u;  // lane-major nibbles: slot k = lane*32+j -> byte k/2
+    else if (HB == 1)
+        h = cells[k];
+    else
+        h = reinterpret_cast<const uint16_t*>(cells)[k];
+    if (!h) return;  // the diagonal (src == v); the tiles are zeroed
+    const int rl = src % kT, cl = v % kT;
+    const size_t off = sym_offset(t - t0, rl, cl, HB);
+    if (HB == 0) {
+        const size_t w = off & ~(size_t)3;
+        atomicOr(reinterpret_cast<unsigned int*>(D + w), h << (8 * (off & 3) + 4 * (rl & 1)));
+    } else if (HB == 1) {
+        D[off] = (uint8_t)h;
+    } else {
+        *reinterpret_cast<uint16_t*>(D + off) = (uint16_t)h;
+    }
+}
+
+cudaError_t launch_bfs_scatter(const uint8_t* bbuf, uint8_t* D, const int* srcs, int nsrc, int n, int nb, int64_t t0,
+                               int64_t t1, int hb, cudaStream_t s)
+{
+    const int64_t total = (int64_t)n * nsrc;
+    const unsigned g = (unsigned)((total + 255) / 256);
+    if (hb == 0)
+        k_bfs_scatter<0><<<g, 256, 0, s>>>(bbuf, D, srcs, nsrc, n, nb, t0, t1);
+    else if (hb == 1)
+        k_bfs_scatter<1><<<g, 256, 0, s>>>(bbuf, D, srcs, nsrc, n, nb, t0, t1);
+    else
+        k_bfs_scatter<2><<<g, 256, 0, s>>>(bbuf, D, srcs, nsrc, n, nb, t0, t1);
     return cudaGetLastError();
 }
 

@@ -1011,3 +1011,39 @@ def test_set_positions_round_trip_keeps_state():
                 L.set_positions(Y)
                 assert L.get_stats().p1_launches == before + 1
     assert runs[0][0] == runs[1][0] and np.array_equal(runs[0][1], runs[1][1])
+
+
+_CLUSTER_CHECK = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+from oracle import core
+from paper_1711_01228_b200 import fdl
+from workloads import configs, graphs
+cases = [("C3", configs.graph_for("C3"), 0), ("grid", graphs.grid_graph(40, 41), 0),
+         ("grid16", graphs.grid_graph(40, 41), 16), ("rgg", graphs.random_geometric_graph(3000, 6.0, seed=7), 0)]
+for name, g, bits in cases:
+    with fdl.Layout.from_graph(g, params=fdl.make_params(dim=2, hop_bits=bits),
+                               init_pos=graphs.init_positions(g.n, 2, 1)) as L:
+        got = L.get_hop_rows(0, g.n)
+        ref = core.hop_matrix(g)
+        assert np.array_equal(got, ref), name
+        assert L.info.diameter == int(ref.max()), name
+        R, A, f = L.eval_forces()
+    print(name, L.info.hop_bits, "ok")
+"""
+
+
+def test_hops_clustered_batches_bit_exact():
+    """MS-BFS with clustered source batches (compact graph neighbourhoods, frontier
+    flags, scattered tile stores; the default above eccentricity 24) forced on for
+    every graph (FDL_BFS_CLUSTER_ECC=1): hops bit-exact against the oracle BFS at
+    4, 8 and 16 bits, several batches and a ragged last one."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FDL_BFS_CLUSTER_ECC="1")
+    r = subprocess.run([sys.executable, "-c", _CLUSTER_CHECK.format(root=root)], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count(" ok") == 4, r.stdout
