@@ -896,8 +896,10 @@ fdl_status build_dists(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, cons
 {
     const int n = ctx->n;
     const int64_t m = std::max<int64_t>(rp[n], 1);
-    // sources per batch: up to 1024, within ~1 GB of fp64 distance buffers
-    const int S = (int)std::max<int64_t>(32, std::min<int64_t>(1024, ((int64_t)1 << 30) / (8 * (int64_t)n) / 32 * 32));
+    // sources per batch: up to 4096 (kBfWordsPerLane source words per lane), within ~2 GB of
+    // fp64 distances; fewer, larger batches mean fewer sweeps (each sweep has a fixed cost)
+    const int S = (int)std::max<int64_t>(
+        32, std::min<int64_t>(32 * 32 * kBfWordsPerLane, ((int64_t)1 << 31) / (8 * (int64_t)n) / 32 * 32));
     Scratch tmp;
     int64_t* d_rp = nullptr;
     int32_t* d_col = nullptr;

@@ -24,7 +24,8 @@ constexpr int kRB = 256;           // row block of all fp64 vector reductions
 constexpr int kGalMax = 8;         // history window of the recycled PCG start (R27)
 constexpr int kGalNV = kGalMax * (kGalMax + 1) / 2 + kGalMax;  // Gram entries + right-hand sides per column
 constexpr int kBFSWords = 32;      // MS-BFS source batch = 32 words x 32 bits = 1024
-constexpr int kBfsHubDeg = 256;    // MS-BFS: vertices of higher degree get a whole block per level
+constexpr int kBfsHubDeg = 256;
+constexpr int kBfWordsPerLane = 4;  // weighted APSP: up to 32 x 4 x 32 = 4096 sources per batch    // MS-BFS: vertices of higher degree get a whole block per level
 
 // Device-resident scalars of the iteration (one struct per context).
 struct DevScalars {

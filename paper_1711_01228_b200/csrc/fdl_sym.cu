@@ -2081,65 +2081,86 @@ __global__ void __launch_bounds__(256) k_bf_sweep(const int64_t* __restrict__ ro
             if (lane == 0) pend_out[v] = 0;
             continue;
         }
-        // candidate sources: pending bits of the neighbours that have any
-        uint32_t act = 0;
+        // candidate sources: pending bits of the neighbours that have any; lane holds words
+        // lane, lane + 32, ... of the W = S/32 source words (S <= 4096: up to 4 per lane)
+        uint32_t act[kBfWordsPerLane], own[kBfWordsPerLane], outw[kBfWordsPerLane];
+#pragma unroll
+        for (int j = 0; j < kBfWordsPerLane; ++j) act[j] = own[j] = outw[j] = 0u;
         {
             unsigned m = pm & (nu == 32 ? 0xffffffffu : ((1u << nu) - 1u));  // warp-uniform (a ballot)
             while (m) {
                 const int q = __ffs(m) - 1;
                 m &= m - 1;
                 const int u = __shfl_sync(0xffffffffu, myu, q);
-                if (lane < W) act |= __ldcg(&chg_in[(int64_t)u * W + lane]);
+#pragma unroll
+                for (int j = 0; j < kBfWordsPerLane; ++j)
+                    if (32 * j + lane < W) act[j] |= __ldcg(&chg_in[(int64_t)u * W + 32 * j + lane]);
             }
         }
         if (end - beg > 32)  // long lists: the rest in order (rare)
             for (int64_t e = beg + 32; e < end; ++e) {
                 const int u = col[e];
-                if (pend_in[u] && lane < W) act |= __ldcg(&chg_in[(int64_t)u * W + lane]);
+                if (pend_in[u])
+#pragma unroll
+                    for (int j = 0; j < kBfWordsPerLane; ++j)
+                        if (32 * j + lane < W) act[j] |= __ldcg(&chg_in[(int64_t)u * W + 32 * j + lane]);
             }
-        const uint32_t own = (selfp && lane < W) ? chg_in[(int64_t)v * W + lane] : 0u;
+        if (selfp)
+#pragma unroll
+            for (int j = 0; j < kBfWordsPerLane; ++j)
+                if (32 * j + lane < W) own[j] = chg_in[(int64_t)v * W + 32 * j + lane];
         const double myl = lane < nu ? len[beg + lane] : 0.0;
-        uint32_t outw = 0;
-        for (int m = 0; m < W; ++m) {
-            const uint32_t wm = __shfl_sync(0xffffffffu, act, m), om = __shfl_sync(0xffffffffu, own, m);
-            if (!(wm | om)) continue;
-            const int k = 32 * m + lane;
-            const bool on = ((wm >> lane) & 1u) && k < nsrc;
-            const bool mine = (om >> lane) & 1u;
-            const double old = (on || mine) ? dv[(int64_t)v * S + k] : 0.0;
-            double best = old;
-            for (int q0 = 0; q0 < nu; q0 += 8) {
-                double c[8];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int u = __shfl_sync(0xffffffffu, myu, (q0 + q) & 31);
-                    const double l = __shfl_sync(0xffffffffu, myl, (q0 + q) & 31);
-                    const double du = (on && q0 + q < nu) ? dv[(int64_t)u * S + k] : INFINITY;
-                    c[q] = du <= T ? du + l : INFINITY;  // a distance above the threshold waits
-                }
+        for (int j = 0; j < kBfWordsPerLane; ++j) {
+            if (32 * j >= W) break;
+            for (int mm = 0; mm < 32 && 32 * j + mm < W; ++mm) {
+                const int m = 32 * j + mm;
+                const uint32_t wm = __shfl_sync(0xffffffffu, act[j], mm), om = __shfl_sync(0xffffffffu, own[j], mm);
+                if (!(wm | om)) continue;
+                const int k = 32 * m + lane;
+                const bool on = ((wm >> lane) & 1u) && k < nsrc;
+                const bool mine = (om >> lane) & 1u;
+                const double old = (on || mine) ? dv[(int64_t)v * S + k] : 0.0;
+                double best = old;
+                for (int q0 = 0; q0 < nu; q0 += 8) {
+                    double c[8];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) best = c[q] < best ? c[q] : best;
-            }
-            for (int64_t e = beg + 32; e < end; ++e)  // lists longer than 32 (rare)
-                if (on) {
-                    const double du = dv[(int64_t)col[e] * S + k];
-                    const double c = du <= T ? du + len[e] : INFINITY;
-                    best = c < best ? c : best;
+                    for (int q = 0; q < 8; ++q) {
+                        const int u = __shfl_sync(0xffffffffu, myu, (q0 + q) & 31);
+                        const double l = __shfl_sync(0xffffffffu, myl, (q0 + q) & 31);
+                        const double du = (on && q0 + q < nu) ? dv[(int64_t)u * S + k] : INFINITY;
+                        c[q] = du <= T ? du + l : INFINITY;  // a distance above the threshold waits
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) best = c[q] < best ? c[q] : best;
                 }
-            bool imp = false;
-            if (on && best < old) {
-                dv[(int64_t)v * S + k] = best;
-                imp = true;
+                for (int64_t e = beg + 32; e < end; ++e)  // lists longer than 32 (rare)
+                    if (on) {
+                        const double du = dv[(int64_t)col[e] * S + k];
+                        const double c = du <= T ? du + len[e] : INFINITY;
+                        best = c < best ? c : best;
+                    }
+                bool imp = false;
+                if (on && best < old) {
+                    dv[(int64_t)v * S + k] = best;
+                    imp = true;
+                }
+                // pending after this sweep: a new value, or an own pending value above the
+                // threshold (its neighbours did not take it yet); own values <= T were pulled
+                // by every neighbour in this sweep
+                const bool keep = imp || (mine && old > T);
+                const uint32_t bw = __ballot_sync(0xffffffffu, keep);
+                if (lane == mm) outw[j] = bw;
             }
-            // pending after this sweep: a new value, or an own pending value above the
-            // threshold (its neighbours did not take it yet); own values <= T were pulled
-            // by every neighbour in this sweep
-            const bool keep = imp || (mine && old > T);
-            const uint32_t bw = __ballot_sync(0xffffffffu, keep);
-            if (lane == m) outw = bw;
         }
-        if (lane < W) chg_out[(int64_t)v * W + lane] = outw;
-        const bool any = __any_sync(0xffffffffu, outw != 0u);
+        bool anyw = false;
+#pragma unroll
+        for (int j = 0; j < kBfWordsPerLane; ++j)
+            if (32 * j + lane < W) {
+                chg_out[(int64_t)v * W + 32 * j + lane] = outw[j];
+                anyw |= outw[j] != 0u;
+            }
+        const bool any = __any_sync(0xffffffffu, anyw);
         if (lane == 0) pend_out[v] = any ? 1 : 0;
         found |= any;
     }
