@@ -290,6 +290,11 @@ fdl_status cuda_fail(fdl_ctx* c, cudaError_t e, const char* what)
         FDL_LAUNCH(call);      \
         ctx->stats.launches++; \
     } while (0)
+#define FDL_LAUNCH3(call)          \
+    do {                           \
+        FDL_LAUNCH(call);          \
+        ctx->stats.launches += 2;  \
+    } while (0)
 
 #define FDL_TRY(x)                     \
     do {                               \
@@ -1341,7 +1346,7 @@ fdl_status enqueue_prologue(fdl_ctx* ctx, const StepShape& sh, unsigned long lon
     const int dim = ctx->dim, n = ctx->n, pq = ps_p2(dim);
     const bool refresh = sh.refresh;
     cudaStream_t s = ctx->stream;
-    FDL_LAUNCH2(launch_cg_begin(ctx->Xk, ctx->Xn, ctx->pvec, n, 0, dim, pq, ctx->sc, s));
+    FDL_LAUNCH3(launch_cg_begin(ctx->Xk, ctx->Xn, ctx->pvec, n, 0, dim, pq, ctx->sc, ctx->blk_cg, s));
     if (refresh) FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->Ak, nullptr, 0));
     const double* y0 = ctx->Ak;
     if (ctx->p.cg_extrap == 2) {  // recycled start (R27): x0 into Xn, L^W x0 into cy
@@ -2026,7 +2031,8 @@ fdl_status fdl_eval_forces(fdl_ctx* ctx, double* R, double* A, double* stress)
     if (R) FDL_TRY(fetch(ctx->Rk, R));
     if (A) {
         // A = L^W X: one symmetric P2 pass with p = X
-        FDL_LAUNCH2(launch_cg_begin(ctx->Xk, ctx->cy, ctx->pvec, ctx->n, 0, dim, ps_p2(dim), ctx->sc, ctx->stream));
+        FDL_LAUNCH3(launch_cg_begin(ctx->Xk, ctx->cy, ctx->pvec, ctx->n, 0, dim, ps_p2(dim), ctx->sc, ctx->blk_cg,
+                                    ctx->stream));
         FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->cy, nullptr, 0));
         FDL_TRY(fetch(ctx->cy, A));
         collect_events(ctx);
@@ -2050,7 +2056,8 @@ fdl_status fdl_eval_partial(fdl_ctx* ctx, int32_t mode, const double* X, double*
         FDL_LAUNCH(launch_stage_pos1(ctx->Xt, ctx->posf, ctx->n, 0, dim, ps_p1(dim, 1), ctx->stream));
         FDL_TRY(run_sym(ctx, kSymP1, 1, ctx->posf, ctx->R1, nullptr, 0));
     } else {
-        FDL_LAUNCH2(launch_cg_begin(ctx->Xt, ctx->R1, ctx->pvec, ctx->n, 0, dim, ps_p2(dim), ctx->sc, ctx->stream));
+        FDL_LAUNCH3(launch_cg_begin(ctx->Xt, ctx->R1, ctx->pvec, ctx->n, 0, dim, ps_p2(dim), ctx->sc, ctx->blk_cg,
+                                    ctx->stream));
         FDL_TRY(run_sym(ctx, kSymP2, 1, ctx->pvec, ctx->R1, nullptr, 0));
     }
     FDL_CUDA(cudaMemcpyAsync(out, ctx->R1, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));

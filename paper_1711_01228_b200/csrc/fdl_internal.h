@@ -107,8 +107,9 @@ cudaError_t launch_get_pin(const double* x, double* slots, int rank, int dim, in
 cudaError_t launch_select(double* Xk, double* Rk, const double* Xn, const double* Xt, const double* R1,
                           const double* R2, const double* blk_max, int nloc, int dim, int nsets,
                           DevScalars* sc, double* Ak, const double* An, const double* At, cudaStream_t s);
-cudaError_t launch_cg_begin(const double* Xk, double* x, float* pvec, int nloc, int row0, int dim,
-                            int pq, DevScalars* sc, cudaStream_t s);
+cudaError_t launch_cg_begin(const double* Xk, double* x, float* pvec, int nloc, int row0, int dim, int pq,
+                            DevScalars* sc, double* blk /* >= 4 x ceil(nloc / kRB) doubles, scratch */,
+                            cudaStream_t s);
 cudaError_t launch_stage_p(const double* p, float* pvec, const DevScalars* sc, int n, int dim, int pq,
                            cudaStream_t s);
 cudaError_t launch_p2_finish(double* out, const float* pvec, const double* diag, int n, int dim, int pq,

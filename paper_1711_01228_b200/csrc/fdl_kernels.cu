@@ -607,24 +607,38 @@ cudaError_t launch_gal_push(const double* Xk, const double* Xprev, const double*
     return cudaGetLastError();
 }
 
-// column means of X (one block, fixed order) -> sc->cmean: the centring of the
-// staged P2 input (product form, k_p2_finish)
-__global__ void __launch_bounds__(1024) k_colmean(const double* __restrict__ X, int n, int dim, DevScalars* sc)
+// column means of X -> sc->cmean: the centring of the staged P2 input (product form,
+// k_p2_finish).  Block partials over kRB rows (warp butterfly, fixed order), then one
+// warp sums the blocks in block order: deterministic and independent of the grid.
+// (A single 1024-thread block took 0.14 ms per step at C5: it is on the critical path.)
+__global__ void k_colmean_part(const double* __restrict__ X, int n, int dim, double* blk)
 {
-    __shared__ double red[32];
+    __shared__ double red[kRB / 32][4];
+    const int i = blockIdx.x * kRB + threadIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int q = 0; q < dim; ++q) {
-        double v = 0.0;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) v += X[(size_t)i * dim + q];
+        double v = i < n ? X[(size_t)i * dim + q] : 0.0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0.0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-            sc->cmean[q] = t / n;
-        }
-        __syncthreads();
+        if (lane == 0) red[w][q] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < dim) {
+        double t = 0.0;
+        for (int k = 0; k < kRB / 32; ++k) t += red[k][threadIdx.x];
+        blk[(size_t)blockIdx.x * 4 + threadIdx.x] = t;
+    }
+}
+
+__global__ void k_colmean_fin(const double* __restrict__ blk, int nblk, int n, int dim, DevScalars* sc)
+{
+    const int lane = threadIdx.x;
+    for (int q = 0; q < dim; ++q) {
+        double v = 0.0;
+        for (int b = lane; b < nblk; b += 32) v += blk[(size_t)b * 4 + q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) sc->cmean[q] = v / n;
     }
 }
 
@@ -687,10 +701,14 @@ cudaError_t launch_p2_finish(double* out, const float* pvec, const double* diag,
 }
 
 cudaError_t launch_cg_begin(const double* Xk, double* x, float* pvec, int nloc, int row0, int dim, int pq,
-                            DevScalars* sc, cudaStream_t s)
+                            DevScalars* sc, double* blk, cudaStream_t s)
 {
-    k_colmean<<<1, 1024, 0, s>>>(Xk, nloc, dim, sc);
+    const int nblk = (nloc + kRB - 1) / kRB;
+    k_colmean_part<<<nblk, kRB, 0, s>>>(Xk, nloc, dim, blk);
     cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_colmean_fin<<<1, 32, 0, s>>>(blk, nblk, nloc, dim, sc);
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     k_cg_begin<<<(nloc + kRB - 1) / kRB, kRB, 0, s>>>(Xk, x, pvec, nloc, row0, dim, pq, sc);
     return cudaGetLastError();
