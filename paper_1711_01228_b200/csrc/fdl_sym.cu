@@ -1375,6 +1375,10 @@ int sym_max_ctas(int mode, int dim, int nsets, int hb)
 // combined in group order (fp64).  Blocks run largest B first.
 // Output: dense fp64 rank partial, components [0, D) -> out0, [D, C) -> out1.
 constexpr int kRedGroups = 8;
+#ifndef FDL_RED_UNROLL
+#define FDL_RED_UNROLL 4  // j-side tile partials in flight per thread (k_sym_reduce)
+#endif
+constexpr int kRedUnroll = FDL_RED_UNROLL;
 
 template <int C>
 __global__ void __launch_bounds__(kRedGroups * kT) k_sym_reduce(const float* __restrict__ ipart,
@@ -1393,7 +1397,7 @@ __global__ void __launch_bounds__(kRedGroups * kT) k_sym_reduce(const float* __r
     // only the local row blocks [Ilo, Ihi] (the rank's tile range); group g keeps I = g mod 8
     const int Ifirst = Ilo + ((g - Ilo) % kRedGroups + kRedGroups) % kRedGroups;
     const int Ilast = min(B, Ihi);
-#pragma unroll 4
+#pragma unroll kRedUnroll
     for (int I = Ifirst; I <= Ilast; I += kRedGroups) {
         const int64_t t = tri_index(I, B, nb);
         if (t < t0 || t >= t1) continue;

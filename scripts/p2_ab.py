@@ -37,4 +37,5 @@ print(json.dumps({"lib": os.path.basename(os.environ.get("FDL_LIB", "default")),
                   "p2_ms_per_launch": st.p2_ms / max(st.p2_launches, 1),
                   "p2_hop_gbs": st.p2_pairs * info.hop_bits / 8 / (st.p2_ms * 1e-3) / 1e9 if st.p2_ms else None,
                   "p1s_ms_per_launch": st.p1s_ms / max(st.p1s_launches, 1), "other_ms": st.other_ms,
+                  "other_ms_per_step": st.other_ms / max(st.steps, 1),
                   "steps": st.steps, "f": fs[-1], "xhash": hashlib.md5(X.tobytes()).hexdigest()}), flush=True)
