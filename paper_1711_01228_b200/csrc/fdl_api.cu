@@ -787,9 +787,19 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
         // width's maximum detects an overflow.  The loop runs on the device (level flags),
         // with one host sync after all batches (MS-BFS)
         const int nlev = std::max(1, std::min(2 * ecc0, maxhop + 1));
+        // high-diameter graphs: clustered batches of 4096 sources (compact graph
+        // neighbourhoods), per-vertex frontier flags and a scattered store into the tiles
+        // (id-contiguous batches spread their wavefronts over the whole graph: every vertex
+        // gathers at every level; a quarter of the batches is a quarter of the levels).
+        // Low-diameter graphs keep id-contiguous 1024-source batches and the tiled store (the
+        // whole graph is within a few levels of any batch anyway)
+        static const int cl_min_ecc = getenv("FDL_BFS_CLUSTER_ECC") ? atoi(getenv("FDL_BFS_CLUSTER_ECC")) : 24;
+        const bool clustered = ecc0 >= cl_min_ecc && src_hi - src_lo > 32 * kBFSWords;
+        const int bsrc = clustered ? 32 * kBfsWideWords : 32 * kBFSWords;  // sources per batch
+        const int64_t rb = (int64_t)bfs_row_bytes_host(hb) * (bsrc / (32 * kBFSWords));  // batch bytes / vertex
         uint8_t* bbuf = nullptr;
         unsigned int* flags = nullptr;
-        const size_t bbytes = (size_t)n * bfs_row_bytes_host(hb);
+        const size_t bbytes = (size_t)n * (size_t)rb;
         FDL_CUDA(tmp.alloc(&bbuf, bbytes));
         FDL_CUDA(tmp.alloc(&flags, sizeof(unsigned int) * (size_t)(nlev + 2)));
         FDL_CUDA(cudaMemsetAsync(&ctx->sc->bfs_diam, 0, sizeof(int), ctx->stream));
@@ -809,49 +819,55 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
                                      ctx->stream));
         }
         const int nhub = (int)hub_list.size();
-        // high-diameter graphs: clustered batches, per-vertex frontier flags and a scattered
-        // store into the tiles (id-contiguous batches spread their 1024 wavefronts over the
-        // whole graph: every vertex gathers at every level).  Low-diameter graphs keep
-        // id-contiguous batches and the tiled store (the whole graph is within a few levels
-        // of any batch anyway)
-        static const int cl_min_ecc = getenv("FDL_BFS_CLUSTER_ECC") ? atoi(getenv("FDL_BFS_CLUSTER_ECC")) : 24;
-        const bool clustered = ecc0 >= cl_min_ecc && src_hi - src_lo > 32 * kBFSWords;
         std::vector<int> order;
         int* d_srcs = nullptr;
         uint8_t *fl_a = nullptr, *fl_b = nullptr;
+        uint32_t *wa = nullptr, *wb = nullptr, *wv = nullptr;  // 128-word frontier / visited sets
+        const size_t wmasks = (size_t)n * kBfsWideWords;
         if (clustered) {
-            order = cluster_sources(n, rp, col, src_lo, src_hi, 32 * kBFSWords);
+            order = cluster_sources(n, rp, col, src_lo, src_hi, bsrc);
             FDL_CUDA(tmp.alloc(&d_srcs, sizeof(int) * order.size()));
             FDL_CUDA(cudaMemcpyAsync(d_srcs, order.data(), sizeof(int) * order.size(), cudaMemcpyHostToDevice,
                                      ctx->stream));
             FDL_CUDA(tmp.alloc(&fl_a, (size_t)n));
             FDL_CUDA(tmp.alloc(&fl_b, (size_t)n));
+            FDL_CUDA(tmp.alloc(&wa, wmasks * 4));
+            FDL_CUDA(tmp.alloc(&wb, wmasks * 4));
+            FDL_CUDA(tmp.alloc(&wv, wmasks * 4));
         }
-        for (int s0 = src_lo; s0 < src_hi; s0 += 32 * kBFSWords) {
-            const int nsrc = std::min(32 * kBFSWords, src_hi - s0);
+        for (int s0 = src_lo; s0 < src_hi; s0 += bsrc) {
+            const int nsrc = std::min(bsrc, src_hi - s0);
             const int* srcs = clustered ? d_srcs + (s0 - src_lo) : nullptr;
             FDL_CUDA(cudaMemsetAsync(bbuf, 0, bbytes, ctx->stream));
             FDL_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned int) * (size_t)(nlev + 2), ctx->stream));
             if (clustered) {
-                FDL_CUDA(cudaMemsetAsync(fa, 0, masks * 4, ctx->stream));
-                FDL_CUDA(cudaMemsetAsync(vis, 0, masks * 4, ctx->stream));
+                FDL_CUDA(cudaMemsetAsync(wa, 0, wmasks * 4, ctx->stream));
+                FDL_CUDA(cudaMemsetAsync(wv, 0, wmasks * 4, ctx->stream));
                 FDL_CUDA(cudaMemsetAsync(fl_a, 0, (size_t)n, ctx->stream));
-                FDL_LAUNCH(launch_bfs_init_list(fa, vis, fl_a, srcs, nsrc, ctx->stream));
+                FDL_LAUNCH(launch_bfs_init_list(wa, wv, fl_a, srcs, nsrc, kBfsWideWords, ctx->stream));
+                uint32_t *fin = wa, *fout = wb;
+                uint8_t *flin = fl_a, *flout = fl_b;
+                for (int level = 1; level <= nlev; ++level) {
+                    FDL_LAUNCH(launch_bfs_level_wide(d_rp, d_col, fin, fout, wv, bbuf, n, nsrc, level, hb, flags,
+                                                     &ctx->sc->bfs_bytes, grid, flin, flout, ctx->stream));
+                    std::swap(fin, fout);
+                    std::swap(flin, flout);
+                }
             } else {
                 FDL_LAUNCH(launch_bfs_init(fa, vis, n, s0, ctx->stream));
-            }
-            uint32_t *fin = fa, *fout = fb;
-            uint8_t *flin = fl_a, *flout = fl_b;
-            for (int level = 1; level <= nlev; ++level) {
-                FDL_LAUNCH(launch_bfs_level_sym(d_rp, d_col, fin, fout, vis, bbuf, n, nsrc, level, hb, flags,
-                                                &ctx->sc->bfs_bytes, d_hubs, nhub, grid, flin, flout, ctx->stream));
-                std::swap(fin, fout);
-                std::swap(flin, flout);
+                uint32_t *fin = fa, *fout = fb;
+                for (int level = 1; level <= nlev; ++level) {
+                    FDL_LAUNCH(launch_bfs_level_sym(d_rp, d_col, fin, fout, vis, bbuf, n, nsrc, level, hb, flags,
+                                                    &ctx->sc->bfs_bytes, d_hubs, nhub, grid, nullptr, nullptr,
+                                                    ctx->stream));
+                    std::swap(fin, fout);
+                }
             }
             FDL_LAUNCH(launch_bfs_batch_end(flags, nlev, maxhop, &ctx->sc->bfs_diam, &ctx->sc->bfs_overflow,
                                             ctx->stream));
             if (clustered)
-                FDL_LAUNCH(launch_bfs_scatter(bbuf, ctx->D, srcs, nsrc, n, ctx->nb, ctx->t0, ctx->t1, hb, ctx->stream));
+                FDL_LAUNCH(launch_bfs_scatter(bbuf, ctx->D, srcs, nsrc, n, ctx->nb, ctx->t0, ctx->t1, hb, rb,
+                                              ctx->stream));
             else
                 FDL_LAUNCH(launch_bfs_retile(bbuf, ctx->D, n, s0, nsrc, ctx->nb, ctx->t0, ctx->t1, hb, ctx->stream));
         }
@@ -863,6 +879,9 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
         if (d_srcs) tmp.release(d_srcs);
         if (fl_a) tmp.release(fl_a);
         if (fl_b) tmp.release(fl_b);
+        if (wa) tmp.release(wa);
+        if (wb) tmp.release(wb);
+        if (wv) tmp.release(wv);
         const bool overflow = ctx->sc_host->bfs_overflow != 0;
         const int diam = ctx->sc_host->bfs_diam;
         ctx->bfs_bytes += ctx->sc_host->bfs_bytes;

@@ -25,6 +25,7 @@ constexpr int kGalMax = 8;         // history window of the recycled PCG start (
 constexpr int kGalNV = kGalMax * (kGalMax + 1) / 2 + kGalMax;  // Gram entries + right-hand sides per column
 constexpr int kBFSWords = 32;      // MS-BFS source batch = 32 words x 32 bits = 1024
 constexpr int kBfsHubDeg = 256;
+constexpr int kBfsWideWords = 128;  // clustered MS-BFS batches: 128 words x 32 = 4096 sources
 constexpr int kBfWordsPerLane = 4;  // weighted APSP: up to 32 x 4 x 32 = 4096 sources per batch    // MS-BFS: vertices of higher degree get a whole block per level
 
 // Device-resident scalars of the iteration (one struct per context).
@@ -221,9 +222,13 @@ cudaError_t launch_bfs_level_sym(const int64_t* row_ptr, const int32_t* col, con
                                  unsigned int* flags, unsigned long long* bytes, const int* hubs, int nhub, int grid,
                                  const uint8_t* fl_in, uint8_t* fl_out, cudaStream_t s);
 cudaError_t launch_bfs_init_list(uint32_t* frontier, uint32_t* visited, uint8_t* fl, const int* srcs, int nsrc,
-                                 cudaStream_t s);
+                                 int nw, cudaStream_t s);
+cudaError_t launch_bfs_level_wide(const int64_t* row_ptr, const int32_t* col, const uint32_t* fin, uint32_t* fout,
+                                  uint32_t* visited, uint8_t* bbuf, int n, int nsrc, int level, int hb,
+                                  unsigned int* flags, unsigned long long* bytes, int grid, const uint8_t* fl_in,
+                                  uint8_t* fl_out, cudaStream_t s);
 cudaError_t launch_bfs_scatter(const uint8_t* bbuf, uint8_t* D, const int* srcs, int nsrc, int n, int nb, int64_t t0,
-                               int64_t t1, int hb, cudaStream_t s);
+                               int64_t t1, int hb, int64_t rb, cudaStream_t s);
 cudaError_t launch_bfs_batch_end(const unsigned int* flags, int nlevels, int maxhop, int* diam, int* overflow,
                                  cudaStream_t s);
 cudaError_t launch_bfs_retile(const uint8_t* bbuf, uint8_t* D, int n, int s0, int nsrc, int nb, int64_t t0,

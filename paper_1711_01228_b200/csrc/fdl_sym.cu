@@ -1927,33 +1927,156 @@ cudaError_t launch_bfs_level_sym(const int64_t* row_ptr, const int32_t* col, con
 }
 
 // Clustered batches (high-diameter graphs): the batch's sources are an arbitrary list
-// srcs[0..nsrc) (a compact graph neighbourhood, so the 1024 wavefronts travel
-// together); frontier / visited bit of slot k at vertex srcs[k], frontier flags set.
+// srcs[0..nsrc) (a compact graph neighbourhood, so the wavefronts travel together); frontier /
+// visited bit of slot k at vertex srcs[k] (nw words per vertex), frontier flags set.
 __global__ void k_bfs_init_list(uint32_t* frontier, uint32_t* visited, uint8_t* fl, const int* __restrict__ srcs,
-                                int nsrc)
+                                int nsrc, int nw)
 {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nsrc) return;
     const int v = srcs[k];
-    frontier[(int64_t)v * kBFSWords + (k >> 5)] = 1u << (k & 31);  // one source per vertex: no conflict
-    visited[(int64_t)v * kBFSWords + (k >> 5)] = 1u << (k & 31);
+    frontier[(int64_t)v * nw + (k >> 5)] = 1u << (k & 31);  // one source per vertex: no conflict
+    visited[(int64_t)v * nw + (k >> 5)] = 1u << (k & 31);
     fl[v] = 1;
 }
 
 cudaError_t launch_bfs_init_list(uint32_t* frontier, uint32_t* visited, uint8_t* fl, const int* srcs, int nsrc,
-                                 cudaStream_t s)
+                                 int nw, cudaStream_t s)
 {
-    k_bfs_init_list<<<(nsrc + 255) / 256, 256, 0, s>>>(frontier, visited, fl, srcs, nsrc);
+    k_bfs_init_list<<<(nsrc + 255) / 256, 256, 0, s>>>(frontier, visited, fl, srcs, nsrc, nw);
     return cudaGetLastError();
 }
 
-// Clustered batches: hop(srcs[k], v) from the batch buffer into the local upper-triangle
+// One level of a clustered batch of up to kBfsWideWords x 32 = 4096 sources: lane holds
+// source words lane + 32 j (j < 4).  Four times the sources of k_bfs_level_sym per
+// level pass: a compact batch's search needs about as many levels as a 1024-source one
+// (the graph's eccentricity), so a quarter of the batches means a quarter of the levels,
+// each of which costs a pass over every vertex's frontier flags.  Frontier flags, the
+// all-visited skip, device level flags and the gather-byte count as k_bfs_level_sym.
+template <int HB>
+__global__ void __launch_bounds__(256) k_bfs_level_wide(const int64_t* __restrict__ row_ptr,
+                                                        const int32_t* __restrict__ col,
+                                                        const uint32_t* __restrict__ fin, uint32_t* __restrict__ fout,
+                                                        uint32_t* __restrict__ visited, uint8_t* __restrict__ bbuf,
+                                                        int n, int nsrc, int level, unsigned int* flags,
+                                                        unsigned long long* bytes, const uint8_t* __restrict__ fl_in,
+                                                        uint8_t* __restrict__ fl_out)
+{
+    constexpr int NW = kBfsWideWords;
+    constexpr int J = NW / 32;
+    constexpr int CB = bfs_row_bytes<HB>() / 32;  // cell bytes of one source word (32 sources)
+    if (level > 1 && *(volatile unsigned int*)&flags[level - 1] == 0u) return;
+    __shared__ unsigned long long blk_bytes;
+    __shared__ unsigned int blk_new;
+    if (threadIdx.x == 0) {
+        blk_bytes = 0ull;
+        blk_new = 0u;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    uint32_t full[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        const int nl = min(max(nsrc - 32 * (32 * j + lane), 0), 32);
+        full[j] = nl == 32 ? 0xffffffffu : ((1u << nl) - 1u);
+    }
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    unsigned long long my_bytes = 0ull;
+    bool found = false;
+    for (int64_t vv = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; vv < n; vv += nwarps) {
+        const int v = (int)vv;
+        const int64_t beg = row_ptr[v], end = row_ptr[v + 1];
+        bool nf = false;
+        for (int64_t e = beg + lane; e < end && !nf; e += 32) nf = fl_in[col[e]] != 0;
+        if (!__any_sync(0xffffffffu, nf)) {
+            if (lane == 0) fl_out[v] = 0;
+            continue;
+        }
+        uint32_t vis[J];
+        bool done = true;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            vis[j] = visited[(int64_t)v * NW + 32 * j + lane];
+            done &= (vis[j] & full[j]) == full[j];
+        }
+        if (__all_sync(0xffffffffu, done)) {
+            if (lane == 0) fl_out[v] = 0;
+            continue;
+        }
+        uint32_t acc[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) acc[j] = 0u;
+        for (int64_t e0 = beg; e0 < end; e0 += 32) {
+            const int myu = (e0 + lane < end) ? col[e0 + lane] : 0;
+            const int cnt = (int)min((int64_t)32, end - e0);
+            for (int k0 = 0; k0 < cnt; k0 += 4) {
+                uint32_t t[4][J];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int u = __shfl_sync(0xffffffffu, myu, (k0 + k) & 31);
+                    const bool ok = k0 + k < cnt && fl_in[u];
+#pragma unroll
+                    for (int j = 0; j < J; ++j) t[k][j] = ok ? __ldcg(&fin[(int64_t)u * NW + 32 * j + lane]) : 0u;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                    for (int j = 0; j < J; ++j) acc[j] |= t[k][j];
+            }
+        }
+        my_bytes += (unsigned long long)(end - beg + 2) * (128ull * J);
+        bool anyw = false;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const uint32_t nw = acc[j] & ~vis[j] & full[j];
+            fout[(int64_t)v * NW + 32 * j + lane] = nw;
+            if (nw) {
+                visited[(int64_t)v * NW + 32 * j + lane] = vis[j] | nw;
+                bfs_record<HB>(bbuf + ((int64_t)v * NW + 32 * j + lane) * CB, nw, level);
+                anyw = true;
+            }
+        }
+        const bool anyn = __any_sync(0xffffffffu, anyw);
+        if (lane == 0) fl_out[v] = anyn ? 1 : 0;
+        found |= anyn;
+    }
+    if (lane == 0) {
+        if (my_bytes) atomicAdd(&blk_bytes, my_bytes);
+        if (found) blk_new = 1u;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (blk_bytes) atomicAdd(bytes, blk_bytes);
+        if (blk_new) flags[level] = 1u;
+    }
+}
+
+cudaError_t launch_bfs_level_wide(const int64_t* row_ptr, const int32_t* col, const uint32_t* fin, uint32_t* fout,
+                                  uint32_t* visited, uint8_t* bbuf, int n, int nsrc, int level, int hb,
+                                  unsigned int* flags, unsigned long long* bytes, int grid, const uint8_t* fl_in,
+                                  uint8_t* fl_out, cudaStream_t s)
+{
+    const unsigned g = (unsigned)std::max(1, std::min(grid, (int)(((int64_t)n * 32 + 255) / 256)));
+    if (hb == 0)
+        k_bfs_level_wide<0><<<g, 256, 0, s>>>(row_ptr, col, fin, fout, visited, bbuf, n, nsrc, level, flags, bytes,
+                                              fl_in, fl_out);
+    else if (hb == 1)
+        k_bfs_level_wide<1><<<g, 256, 0, s>>>(row_ptr, col, fin, fout, visited, bbuf, n, nsrc, level, flags, bytes,
+                                              fl_in, fl_out);
+    else
+        k_bfs_level_wide<2><<<g, 256, 0, s>>>(row_ptr, col, fin, fout, visited, bbuf, n, nsrc, level, flags, bytes,
+                                              fl_in, fl_out);
+    return cudaGetLastError();
+}
+
+// Clustered batches: hop(srcs[k], v) from the batch buffer (rb bytes per vertex: the
+// cells of slot k at k/2 (4-bit), k (8-bit), 2k (16-bit)) into the local upper-triangle
 // tiles, one thread per (v, k) (k fastest: coalesced bbuf reads), scattered stores; 4-bit
 // cells share a byte between rows 2p and 2p+1 (possibly of other batches): atomicOr of
 // the nibble into its zero-initialised word (raw layout, nib_encode runs after all batches).
 template <int HB>
 __global__ void k_bfs_scatter(const uint8_t* __restrict__ bbuf, uint8_t* D, const int* __restrict__ srcs, int nsrc,
-                              int n, int nb, int64_t t0, int64_t t1)
+                              int n, int nb, int64_t t0, int64_t t1, int64_t rb)
 {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (int64_t)n * nsrc) return;
@@ -1963,11 +2086,10 @@ __global__ void k_bfs_scatter(const uint8_t* __restrict__ bbuf, uint8_t* D, cons
     if (I > J) return;
     const int64_t t = tri_index(I, J, nb);
     if (t < t0 || t >= t1) return;
-    constexpr int RB = bfs_row_bytes<HB>();
-    const uint8_t* cells = bbuf + (int64_t)v * RB;
+    const uint8_t* cells = bbuf + (int64_t)v * rb;
     uint32_t h;
     if (HB == 0)
-        h = (cells[k >> 1] >> (4 * (k & 1))) & 15u;  // lane-major nibbles: slot k = lane*32+j -> byte k/2
+        h = (cells[k >> 1] >> (4 * (k & 1))) & 15u;
     else if (HB == 1)
         h = cells[k];
     else
@@ -1986,16 +2108,16 @@ __global__ void k_bfs_scatter(const uint8_t* __restrict__ bbuf, uint8_t* D, cons
 }
 
 cudaError_t launch_bfs_scatter(const uint8_t* bbuf, uint8_t* D, const int* srcs, int nsrc, int n, int nb, int64_t t0,
-                               int64_t t1, int hb, cudaStream_t s)
+                               int64_t t1, int hb, int64_t rb, cudaStream_t s)
 {
     const int64_t total = (int64_t)n * nsrc;
     const unsigned g = (unsigned)((total + 255) / 256);
     if (hb == 0)
-        k_bfs_scatter<0><<<g, 256, 0, s>>>(bbuf, D, srcs, nsrc, n, nb, t0, t1);
+        k_bfs_scatter<0><<<g, 256, 0, s>>>(bbuf, D, srcs, nsrc, n, nb, t0, t1, rb);
     else if (hb == 1)
-        k_bfs_scatter<1><<<g, 256, 0, s>>>(bbuf, D, srcs, nsrc, n, nb, t0, t1);
+        k_bfs_scatter<1><<<g, 256, 0, s>>>(bbuf, D, srcs, nsrc, n, nb, t0, t1, rb);
     else
-        k_bfs_scatter<2><<<g, 256, 0, s>>>(bbuf, D, srcs, nsrc, n, nb, t0, t1);
+        k_bfs_scatter<2><<<g, 256, 0, s>>>(bbuf, D, srcs, nsrc, n, nb, t0, t1, rb);
     return cudaGetLastError();
 }
 
