@@ -603,7 +603,7 @@ def run_gpu(args):
             "config": {"workload": f"{args.config}: BA n={n} m=3 |E|={g.num_edges}" if args.config == "C5"
                        else f"{args.config} n={n} |E|={g.num_edges}",
                        "dim": dim, "omega": cfg.omega, "k": k, "diameter": info.diameter,
-                       "hop_bits": info.hop_bits, "parallelism": f"triangle-tile shard x{world} (NCCL all-gather of partials)",
+                       "hop_bits": info.hop_bits, "parallelism": f"triangle-tile shard x{world} (NCCL row-slice all-to-all + all-gather per pair pass)",
                        "precision": "f32 pair arithmetic, f64 reductions, PCG state and positions",
                        "cg_rtol": cg_rtol if cg_rtol > 0 else min(1e-2 * cfg.tol, 1e-9), "tol": cfg.tol,
                        "l2": ("inputs larger than L2 (hop matrix %.1f GB per GPU, L2 %.0f MB)"
