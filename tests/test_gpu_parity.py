@@ -618,16 +618,18 @@ def test_enumerating_strategy_one_step():
     tolerance may resolve either way)."""
     from oracle import strategies
     cfg = configs.CONFIGS["C2"]
-    g, k, X0, L = make("C2", strategy=fdl.STRAT_ENUM)
+    # a tight solve (as test_first_iteration): the comparison isolates the candidate pass's
+    # arithmetic from the PCG tolerance (round 1's 10x wider gate came from a 1e-6 solve)
+    g, k, X0, L = make("C2", strategy=fdl.STRAT_ENUM, cg_rtol=1e-10)
     info = L.step()
     prob = layout.Problem(g, 2, k)
     Xn = prob.H(layout.pin(X0.astype(np.float64)))
     w, fbest, fs = strategies.enumerate_omega(prob, Xn, layout.pin(X0.astype(np.float64)))
     c = int(round(info.omega / 0.5))
-    assert abs(info.f_next - fs[0]) / fs[0] <= STRESS_TOL * 10
-    assert abs(info.f_relaxed - fs[c]) / fs[c] <= STRESS_TOL * 10
-    assert fs[c] <= fbest * (1 + 1e-5)
-    assert abs(info.f_after - fs[c]) / fs[c] <= STRESS_TOL * 10
+    assert abs(info.f_next - fs[0]) / fs[0] <= STRESS_TOL
+    assert abs(info.f_relaxed - fs[c]) / fs[c] <= STRESS_TOL
+    assert fs[c] <= fbest * (1 + STRESS_TOL)
+    assert abs(info.f_after - fs[c]) / fs[c] <= STRESS_TOL
     np.testing.assert_allclose(L.get_positions(), (1 + info.omega) * Xn - info.omega * layout.pin(X0.astype(np.float64)),
                                rtol=0, atol=1e-5 * np.abs(Xn).max())
 
