@@ -52,6 +52,16 @@ def run(case: str, seed: int = 1):
     t0 = time.time()
     prob = layout.Problem(g, cfg.dim, k)
     t1 = time.time()
+    H = prob.H
+    calls = [0]
+
+    def H_progress(X):  # progress on stderr every 10 majorization steps (no change to the step)
+        calls[0] += 1
+        if calls[0] % 10 == 0:
+            print(f"  {case}:{seed} step {calls[0]} at {time.time() - t1:.0f}s", file=sys.stderr, flush=True)
+        return H(X)
+
+    prob.H = H_progress
     res = layout.run_algorithm2(prob, X0, cfg.omega, tol, cfg.max_iter)
     t2 = time.time()
     out = {
