@@ -7,8 +7,10 @@ Passages followed, in the paper's order and notation:
   * Line 125: "always taking x_1 = 0 and removing the first row and first
     column of L^W ... Cholesky factorization ... or conjugate gradient".  The
     paper's vertex 1 is id 0 here.  Cholesky (a library primitive,
-    scipy.linalg.cho_factor) when the dense reduced matrix fits in memory,
-    otherwise fp64 Jacobi-preconditioned CG to relative residual 1e-12.
+    scipy.linalg.cho_factor, or numpy's 64-bit-index np.linalg.cholesky with
+    blocked triangular solves above 2^31 entries) when the dense reduced matrix
+    fits in memory, otherwise fp64 Jacobi-preconditioned CG to relative residual
+    1e-12.
   * Algorithm 1 (lines 130-145): repeat X <- H(X).
   * Algorithm 2 (lines 147-162) with Eq. 10 (line 232): Xt = (1+w) X^{k+1} - w X^k;
     if f(Xt) <= f(X^{k+1}) then X^{k+1} <- Xt.
@@ -29,10 +31,34 @@ import scipy.linalg
 
 from . import core
 
-# Dense reduced matrix (fp64, (n-1)^2 entries) is used up to this many bytes and
-# below 2^31 entries (scipy's bundled LAPACK uses 32-bit indices).
+# Dense reduced matrix (fp64, (n-1)^2 entries) is used up to this many bytes: below 2^31
+# entries through scipy's cho_factor / cho_solve (its bundled LAPACK uses 32-bit
+# indices), above through numpy's 64-bit-index LAPACK (np.linalg.cholesky) and the
+# blocked triangular solves below ("cholesky64", e.g. C4: 2.4e9 entries, 19 GB).
 DENSE_LIMIT_BYTES = 24 << 30
 DENSE_LIMIT_ENTRIES = (1 << 31) - 1
+_TRI_BLOCK = 2048
+
+
+def _chol64_solve(Lc: np.ndarray, B: np.ndarray) -> np.ndarray:
+    """Z with (Lc Lc^T) Z = B for a lower Cholesky factor Lc of any size: forward then
+    back substitution by blocks of _TRI_BLOCK rows -- each diagonal block by
+    scipy.linalg.solve_triangular, the coupling to the rows already solved by one
+    matrix product.  The same substitutions as an unblocked solve, in the usual
+    blocked order."""
+    m = Lc.shape[0]
+    Y = np.empty_like(B)
+    for i0 in range(0, m, _TRI_BLOCK):
+        i1 = min(m, i0 + _TRI_BLOCK)
+        rhs = B[i0:i1] - Lc[i0:i1, :i0] @ Y[:i0] if i0 else B[i0:i1]
+        Y[i0:i1] = scipy.linalg.solve_triangular(Lc[i0:i1, i0:i1], rhs, lower=True, check_finite=False)
+    Z = np.empty_like(B)
+    for i1 in range(m, 0, -_TRI_BLOCK):
+        i0 = max(0, i1 - _TRI_BLOCK)
+        rhs = Y[i0:i1] - Lc[i1:, i0:i1].T @ Z[i1:] if i1 < m else Y[i0:i1]
+        Z[i0:i1] = scipy.linalg.solve_triangular(Lc[i0:i1, i0:i1], rhs, lower=True, trans="T",
+                                                 check_finite=False)
+    return Z
 
 
 @dataclass
@@ -73,7 +99,8 @@ class Problem:
         self.rows = np.arange(self.n, dtype=np.int32)
         if solver == "auto":
             m2 = (self.n - 1) ** 2
-            solver = "cholesky" if (8 * m2 <= DENSE_LIMIT_BYTES and m2 <= DENSE_LIMIT_ENTRIES) else "cg"
+            solver = ("cg" if 8 * m2 > DENSE_LIMIT_BYTES else
+                      ("cholesky" if m2 <= DENSE_LIMIT_ENTRIES else "cholesky64"))
         self.solver = solver
         self.cg_rtol = cg_rtol
         self.cg_iters = []
@@ -83,6 +110,10 @@ class Problem:
                 # the reduced system is SPD; factor once (L^W never changes).
                 self.cho = scipy.linalg.cho_factor(Lr, lower=False, overwrite_a=True,
                                                    check_finite=False)
+                del Lr
+            elif solver == "cholesky64":
+                Lr = core.lw_red_dense(self.hop, self.k, self.alpha)
+                self.chol64 = np.linalg.cholesky(Lr)  # P:125, 64-bit-index LAPACK
                 del Lr
             else:
                 self.diag = core.lw_diag(self.hop, self.k, self.alpha)
@@ -104,6 +135,9 @@ class Problem:
             return Z
         if self.solver == "cholesky":
             Z[1:] = scipy.linalg.cho_solve(self.cho, B[1:], check_finite=False)
+            return Z
+        if self.solver == "cholesky64":
+            Z[1:] = _chol64_solve(self.chol64, np.ascontiguousarray(B[1:]))
             return Z
         return self._pcg(B, X0 if X0 is not None else np.zeros_like(B))
 

@@ -214,6 +214,23 @@ def test_cg_matches_cholesky():
 
 # ---------------------------------------------------- one majorization step
 
+def test_blocked_64bit_cholesky_matches_cholesky(monkeypatch):
+    """The oracle's solve for reduced matrices above 2^31 entries (C4): numpy's
+    64-bit-index Cholesky with blocked forward/back substitution.  On a small system
+    with several ragged blocks it equals scipy's cho_solve and meets S:213's residual
+    bound ||L^W_red z - b|| <= 1e-10 (1 + ||b||)."""
+    monkeypatch.setattr(layout, "_TRI_BLOCK", 97)
+    g = graphs.random_geometric_graph(600, 6.0, seed=11)
+    a = layout.Problem(g, 3, 0.05, solver="cholesky")
+    b = layout.Problem(g, 3, 0.05, solver="cholesky64")
+    B = np.random.default_rng(5).normal(size=(g.n, 3))
+    za, zb = a.solve_reduced(B), b.solve_reduced(B)
+    assert zb[0].tolist() == [0.0, 0.0, 0.0]
+    np.testing.assert_allclose(zb, za, rtol=0, atol=1e-12 * np.abs(za).max())
+    Lr = core.lw_red_dense(a.hop, 0.05)
+    assert np.linalg.norm(Lr @ zb[1:] - B[1:]) <= 1e-10 * (1 + np.linalg.norm(B[1:]))
+
+
 def test_majorize_single_edge_1d():
     """single edge, d = 1, x = (0, 3) -> next placement has distance 1."""
     prob = layout.Problem(graphs.path_graph(2), 1, 1.0)
