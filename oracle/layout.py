@@ -31,13 +31,40 @@ import scipy.linalg
 
 from . import core
 
-# Dense reduced matrix (fp64, (n-1)^2 entries) is used up to this many bytes: below 2^31
-# entries through scipy's cho_factor / cho_solve (its bundled LAPACK uses 32-bit
-# indices), above through numpy's 64-bit-index LAPACK (np.linalg.cholesky) and the
-# blocked triangular solves below ("cholesky64", e.g. C4: 2.4e9 entries, 19 GB).
+# Dense reduced matrix (fp64, (n-1)^2 entries) is used up to this many bytes: small ones
+# through scipy's cho_factor / cho_solve, large ones (C4: 2.4e9 entries, 19 GB; BA-40k)
+# through the blocked factorisation and blocked triangular solves below ("cholesky64").
 DENSE_LIMIT_BYTES = 24 << 30
 DENSE_LIMIT_ENTRIES = (1 << 31) - 1
+# above this many entries the factorisation is blocked (_blocked_cholesky): scipy's
+# cho_factor on BA-40k (1.6e9 entries) and numpy's cholesky on C4 (2.4e9) crashed in
+# OpenBLAS here; BA-20k (4e8) works either way
+BLOCKED_CHOLESKY_ENTRIES = 1 << 29
 _TRI_BLOCK = 2048
+
+
+def _blocked_cholesky(A: np.ndarray, b: int = _TRI_BLOCK) -> np.ndarray:
+    """Lower Cholesky factor of the SPD matrix A, in place (the strict upper triangle is
+    left as it was), by the textbook right-looking blocked algorithm: factor the
+    diagonal block (scipy.linalg.cholesky), solve the panel below it against that
+    factor (solve_triangular), subtract the panel's outer product from the trailing
+    lower triangle (matrix products in row chunks).  Every library call works on blocks
+    of at most _TRI_BLOCK rows or columns: one LAPACK potrf on the whole C4 / BA-40k
+    matrix (1.6e9-2.4e9 entries) crashed inside OpenBLAS on this host."""
+    m = A.shape[0]
+    for k0 in range(0, m, b):
+        k1 = min(m, k0 + b)
+        A[k0:k1, k0:k1] = scipy.linalg.cholesky(A[k0:k1, k0:k1], lower=True, check_finite=False)
+        if k1 == m:
+            break
+        # panel L21 = A21 L11^-T
+        P = scipy.linalg.solve_triangular(A[k0:k1, k0:k1], A[k1:, k0:k1].T, lower=True, check_finite=False).T
+        A[k1:, k0:k1] = P
+        # trailing lower triangle: A22 -= L21 L21^T, one row chunk at a time
+        for i0 in range(k1, m, b):
+            i1 = min(m, i0 + b)
+            A[i0:i1, k1:i1] -= P[i0 - k1:i1 - k1] @ P[:i1 - k1].T
+    return A
 
 
 def _chol64_solve(Lc: np.ndarray, B: np.ndarray) -> np.ndarray:
@@ -100,7 +127,7 @@ class Problem:
         if solver == "auto":
             m2 = (self.n - 1) ** 2
             solver = ("cg" if 8 * m2 > DENSE_LIMIT_BYTES else
-                      ("cholesky" if m2 <= DENSE_LIMIT_ENTRIES else "cholesky64"))
+                      ("cholesky" if m2 <= BLOCKED_CHOLESKY_ENTRIES else "cholesky64"))
         self.solver = solver
         self.cg_rtol = cg_rtol
         self.cg_iters = []
@@ -112,9 +139,8 @@ class Problem:
                                                    check_finite=False)
                 del Lr
             elif solver == "cholesky64":
-                Lr = core.lw_red_dense(self.hop, self.k, self.alpha)
-                self.chol64 = np.linalg.cholesky(Lr)  # P:125, 64-bit-index LAPACK
-                del Lr
+                # the same factorisation, blocked (see _blocked_cholesky), in place
+                self.chol64 = _blocked_cholesky(core.lw_red_dense(self.hop, self.k, self.alpha))
             else:
                 self.diag = core.lw_diag(self.hop, self.k, self.alpha)
 
