@@ -1,6 +1,6 @@
 # usage: bash scripts/prof.sh <tag>  -- launch list + ncu --set full of P1 (split two-set pass) and P2 at C5
 TAG=${1:-r01}
-CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
+CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-run-leg"
 $CMD > gpurun_out/${TAG}_plain.log 2>&1; echo "plain rc=$?"; tail -1 gpurun_out/${TAG}_plain.log | cut -c1-300
 ncu --kernel-name-base demangled -k regex:"fdl::k_(sym|cg|combine|select|stage|get_pin|rank|slice|stress|extrap|rho|colmean|p2_finish|carry|gal|bfs|nib)" \
     --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
