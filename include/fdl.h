@@ -282,7 +282,7 @@ fdl_status fdl_run_until_converged(fdl_ctx* ctx, fdl_run_info* info);
 /* Current placement into the caller's buffer (count must be n*dim, else
  * FDL_E_INVALID_ARG), original units, x_0 = 0.  Synchronises the stream; a
  * page-locked buffer is filled by one DMA. */
-fdl_status fdl_get_positions(fdl_ctx* ctx, double* out, size_t count);
+fdl_status fdl_get_positions(const fdl_ctx* ctx, double* out, size_t count);
 
 /* Replace the placement (count n*dim, all finite, else FDL_E_INVALID_ARG);
  * re-pins x_0 = 0, recomputes f, L^X X and L^W X at it (one fused pass)

@@ -1993,8 +1993,11 @@ fdl_status fdl_run_until_converged(fdl_ctx* ctx, fdl_run_info* info)
     return s;
 }
 
-fdl_status fdl_get_positions(fdl_ctx* ctx, double* out, size_t count)
+fdl_status fdl_get_positions(const fdl_ctx* cctx, double* out, size_t count)
 {
+    // logically const: the placement is only read; the x k scaling runs
+    // in the context's PCG scratch vector and on its stream
+    fdl_ctx* ctx = const_cast<fdl_ctx*>(cctx);
     if (!ctx || !out) return FDL_E_INVALID_ARG;
     if (ctx->emulated) return set_err(ctx, FDL_E_UNSUPPORTED, "emulated rank: only fdl_eval_partial");
     if (count != (size_t)ctx->n * ctx->dim) return set_err(ctx, FDL_E_INVALID_ARG, "count must be n*dim");
