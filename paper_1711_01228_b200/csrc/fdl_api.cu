@@ -858,8 +858,7 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
                 uint32_t *fin = fa, *fout = fb;
                 for (int level = 1; level <= nlev; ++level) {
                     FDL_LAUNCH(launch_bfs_level_sym(d_rp, d_col, fin, fout, vis, bbuf, n, nsrc, level, hb, flags,
-                                                    &ctx->sc->bfs_bytes, d_hubs, nhub, grid, nullptr, nullptr,
-                                                    ctx->stream));
+                                                    &ctx->sc->bfs_bytes, d_hubs, nhub, grid, ctx->stream));
                     std::swap(fin, fout);
                 }
             }

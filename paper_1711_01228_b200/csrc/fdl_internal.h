@@ -220,7 +220,7 @@ cudaError_t launch_sym_stress(const double* spart, int nitems, int nsets, double
 cudaError_t launch_bfs_level_sym(const int64_t* row_ptr, const int32_t* col, const uint32_t* fin, uint32_t* fout,
                                  uint32_t* visited, uint8_t* bbuf, int n, int nsrc, int level, int hb,
                                  unsigned int* flags, unsigned long long* bytes, const int* hubs, int nhub, int grid,
-                                 const uint8_t* fl_in, uint8_t* fl_out, cudaStream_t s);
+                                 cudaStream_t s);
 cudaError_t launch_bfs_init_list(uint32_t* frontier, uint32_t* visited, uint8_t* fl, const int* srcs, int nsrc,
                                  int nw, cudaStream_t s);
 cudaError_t launch_bfs_level_wide(const int64_t* row_ptr, const int32_t* col, const uint32_t* fin, uint32_t* fout,

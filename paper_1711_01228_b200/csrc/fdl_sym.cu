@@ -1701,8 +1701,7 @@ __host__ __device__ constexpr int bfs_row_bytes()  // batch-buffer bytes per ver
 // 128 B each per vertex searched) are added to *bytes (MS-BFS roofline).
 template <int HB>
 __device__ __forceinline__ uint32_t bfs_gather(const int32_t* __restrict__ col, const uint32_t* __restrict__ fin,
-                                               int64_t beg, int64_t end, int64_t stride, int lane,
-                                               const uint8_t* __restrict__ fl = nullptr)
+                                               int64_t beg, int64_t end, int64_t stride, int lane)
 {
     // OR of the neighbours' frontier words over col[beg, end) in chunks of 32 neighbours
     // `stride` apart; kBfsUnroll independent 128-byte loads in flight per warp
@@ -1715,7 +1714,7 @@ __device__ __forceinline__ uint32_t bfs_gather(const int32_t* __restrict__ col, 
 #pragma unroll
             for (int k = 0; k < kBfsUnroll; ++k) {
                 const int u = __shfl_sync(0xffffffffu, myu, (k0 + k) & 31);
-                t[k] = (k0 + k < cnt && (!fl || fl[u])) ? __ldcg(&fin[(int64_t)u * kBFSWords + lane]) : 0u;
+                t[k] = (k0 + k < cnt) ? __ldcg(&fin[(int64_t)u * kBFSWords + lane]) : 0u;
             }
 #pragma unroll
             for (int k = 0; k < kBfsUnroll; ++k) acc |= t[k];
@@ -1741,8 +1740,7 @@ __global__ void __launch_bounds__(256) k_bfs_level_sym(const int64_t* __restrict
                                                        uint32_t* __restrict__ visited, uint8_t* __restrict__ bbuf,
                                                        int n, int nsrc, int level, unsigned int* flags,
                                                        unsigned long long* bytes, const int* __restrict__ hubs,
-                                                       int nhub, const uint8_t* __restrict__ fl_in,
-                                                       uint8_t* __restrict__ fl_out)
+                                                       int nhub)
 {
     if (level > 1 && *(volatile unsigned int*)&flags[level - 1] == 0u) return;  // uniform over the grid
     __shared__ unsigned long long blk_bytes;
@@ -1767,7 +1765,7 @@ __global__ void __launch_bounds__(256) k_bfs_level_sym(const int64_t* __restrict
         __syncthreads();
         const int64_t beg = row_ptr[v], end = row_ptr[v + 1];
         if (!hub_skip) {
-            const uint32_t acc = bfs_gather<HB>(col, fin, beg + 32 * wid, end, 256, lane, fl_in);
+            const uint32_t acc = bfs_gather<HB>(col, fin, beg + 32 * wid, end, 256, lane);
             if (acc) atomicOr(&hub_acc[lane], acc);
         }
         __syncthreads();
@@ -1775,7 +1773,6 @@ __global__ void __launch_bounds__(256) k_bfs_level_sym(const int64_t* __restrict
             const uint32_t vis = visited[(int64_t)v * kBFSWords + lane];
             if (hub_skip) {
                 fout[(int64_t)v * kBFSWords + lane] = 0u;
-                if (fl_out && lane == 0) fl_out[v] = 0;
             } else {
                 const uint32_t nw = hub_acc[lane] & ~vis & full;
                 fout[(int64_t)v * kBFSWords + lane] = nw;
@@ -1784,9 +1781,7 @@ __global__ void __launch_bounds__(256) k_bfs_level_sym(const int64_t* __restrict
                     bfs_record<HB>(bbuf + (int64_t)v * bfs_row_bytes<HB>() + lane * (bfs_row_bytes<HB>() / 32), nw,
                                    level);
                 }
-                const bool anyn = __any_sync(0xffffffffu, nw != 0u);
-                if (anyn && lane == 0) flags[level] = 1u;
-                if (fl_out && lane == 0) fl_out[v] = anyn ? 1 : 0;
+                if (__any_sync(0xffffffffu, nw != 0u) && lane == 0) flags[level] = 1u;
                 if (lane == 0) atomicAdd(bytes, (unsigned long long)(end - beg + 2) * 128ull);
             }
         }
@@ -1800,23 +1795,12 @@ __global__ void __launch_bounds__(256) k_bfs_level_sym(const int64_t* __restrict
         const int v = (int)vv;
         const int64_t beg = row_ptr[v], end = row_ptr[v + 1];
         if (nhub > 0 && end - beg > kBfsHubDeg) continue;  // a hub block's vertex
-        if (fl_in) {
-            // frontier flags (clustered batches): a vertex none of whose neighbours holds a
-            // frontier bit gathers nothing (its words are not read by anyone: flag 0)
-            bool nf = false;
-            for (int64_t e = beg + lane; e < end && !nf; e += 32) nf = fl_in[col[e]] != 0;
-            if (!__any_sync(0xffffffffu, nf)) {
-                if (lane == 0) fl_out[v] = 0;
-                continue;
-            }
-        }
         const uint32_t vis = visited[(int64_t)v * kBFSWords + lane];
         if (__all_sync(0xffffffffu, (vis & full) == full)) {
             fout[(int64_t)v * kBFSWords + lane] = 0u;
-            if (fl_out && lane == 0) fl_out[v] = 0;
             continue;
         }
-        const uint32_t acc = bfs_gather<HB>(col, fin, beg, end, 32, lane, fl_in);
+        const uint32_t acc = bfs_gather<HB>(col, fin, beg, end, 32, lane);
         my_bytes += (unsigned long long)(end - beg + 2) * 128ull;
         const uint32_t nw = acc & ~vis & full;
         fout[(int64_t)v * kBFSWords + lane] = nw;
@@ -1824,9 +1808,7 @@ __global__ void __launch_bounds__(256) k_bfs_level_sym(const int64_t* __restrict
             visited[(int64_t)v * kBFSWords + lane] = vis | nw;
             bfs_record<HB>(bbuf + (int64_t)v * bfs_row_bytes<HB>() + lane * (bfs_row_bytes<HB>() / 32), nw, level);
         }
-        const bool anyn = __any_sync(0xffffffffu, nw != 0u);
-        if (fl_out && lane == 0) fl_out[v] = anyn ? 1 : 0;
-        found |= anyn;
+        found |= __any_sync(0xffffffffu, nw != 0u);
     }
     if (lane == 0) {
         if (my_bytes) atomicAdd(&blk_bytes, my_bytes);
@@ -1911,18 +1893,18 @@ __global__ void __launch_bounds__(256) k_bfs_retile(const uint8_t* __restrict__ 
 cudaError_t launch_bfs_level_sym(const int64_t* row_ptr, const int32_t* col, const uint32_t* fin, uint32_t* fout,
                                  uint32_t* visited, uint8_t* bbuf, int n, int nsrc, int level, int hb,
                                  unsigned int* flags, unsigned long long* bytes, const int* hubs, int nhub, int grid,
-                                 const uint8_t* fl_in, uint8_t* fl_out, cudaStream_t s)
+                                 cudaStream_t s)
 {
     const unsigned g = (unsigned)nhub + (unsigned)std::max(1, std::min(grid, (int)(((int64_t)n * 32 + 255) / 256)));
     if (hb == 0)
         k_bfs_level_sym<0><<<g, 256, 0, s>>>(row_ptr, col, fin, fout, visited, bbuf, n, nsrc, level, flags, bytes,
-                                             hubs, nhub, fl_in, fl_out);
+                                             hubs, nhub);
     else if (hb == 1)
         k_bfs_level_sym<1><<<g, 256, 0, s>>>(row_ptr, col, fin, fout, visited, bbuf, n, nsrc, level, flags, bytes,
-                                             hubs, nhub, fl_in, fl_out);
+                                             hubs, nhub);
     else
         k_bfs_level_sym<2><<<g, 256, 0, s>>>(row_ptr, col, fin, fout, visited, bbuf, n, nsrc, level, flags, bytes,
-                                             hubs, nhub, fl_in, fl_out);
+                                             hubs, nhub);
     return cudaGetLastError();
 }
 
