@@ -558,6 +558,8 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
     a.items = ctx->items;
     a.nitems = ctx->nitems;
     a.n = ctx->n;
+    a.ntiles = ctx->t1 - ctx->t0;
+    a.nstage = ctx->npad;
     a.magic = 0x4B000000u;
     a.alpha = (float)ctx->alpha;
     const int grid = mode == kSymP1S   ? ctx->grid_p1s
@@ -1452,6 +1454,8 @@ fdl_status enqueue_epilogue(fdl_ctx* ctx, const StepShape& sh)
             a.items = ctx->items;
             a.nitems = ctx->nitems;
             a.n = ctx->n;
+            a.ntiles = ctx->t1 - ctx->t0;
+            a.nstage = ctx->npad;
             a.magic = 0x4B000000u;
             if (ctx->nitems > 0) FDL_LAUNCH(launch_enum(a, w, dim, ctx->hb, ctx->grid_enum, s));
             FDL_LAUNCH2(launch_sym_stress(ctx->spart_enum, ctx->nitems, kEnumNC, ctx->enum_f + c0, ctx->stress_scratch, s));

@@ -8,6 +8,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 namespace fdl {
 
@@ -18,6 +19,26 @@ __host__ __device__ inline int64_t stage_slot(int64_t v)
 {
     return (v & ~(int64_t)127) | ((v & 7) << 4) | ((v & 127) >> 3);
 }
+
+// ------------------------------------------------------------ debug bounds
+// FDL_DEBUG_BOUNDS builds (scripts/debug_build.sh, tests run against them through
+// FDL_LIB) check the global-memory indices of the pair, reduction and setup kernels and
+// trap on a violation: the pool's compute-sanitizer is closed, so out-of-range accesses
+// are caught by the kernels themselves.
+#ifdef FDL_DEBUG_BOUNDS
+#define FDL_DCHECK(c)                                                                        \
+    do {                                                                                     \
+        if (!(c)) {                                                                          \
+            printf("FDL_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                       \
+            __trap();                                                                        \
+        }                                                                                    \
+    } while (0)
+#else
+#define FDL_DCHECK(c) \
+    do {              \
+    } while (0)
+#endif
 
 // ------------------------------------------------------------ constants
 constexpr int kRB = 256;           // row block of all fp64 vector reductions
@@ -197,6 +218,8 @@ struct SymArgs {
     uint32_t magic;        // 0x4B000000 (2^23 as fp32 bits) for the hop decode, passed as a
                            // parameter so the PRMT selector can stay an immediate
     float alpha;           // weight exponent w = d^alpha (fp32 distance tiles, hb = 4)
+    int64_t ntiles;        // local tiles (bounds checks of the debug build)
+    int64_t nstage;        // vertices of the staged position vector (nb * kT)
 };
 
 cudaError_t launch_sym(const SymArgs& a, int mode, int dim, int nsets, int hb, int grid, cudaStream_t s);

@@ -870,6 +870,7 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
             const int J = it.y + p_t + k;
             const int64_t lt = (int64_t)it.w + p_t + k;
             uint8_t* base = smem + (size_t)stage * SLOT + (size_t)k * STAGE;
+            FDL_DCHECK(lt >= 0 && lt < a.ntiles && J >= 0 && (int64_t)(J + 1) * kT <= a.nstage);
             tma_load_1d(base, a.D + lt * DT, DT, &full[stage]);
             tma_load_1d(base + DT, a.pos + (int64_t)J * kT * PS, kT * PS * 4, &full[stage]);
         }
@@ -900,6 +901,8 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
     for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
         const int4 it = a.items[item];
         const int I = it.x;
+        FDL_DCHECK(it.z >= 1 && it.w >= 0 && (int64_t)it.w + it.z <= a.ntiles && I <= it.y &&
+                   (int64_t)(I + 1) * kT <= a.nstage);
         float xi[8][NSETS * DIM];
         float ai[8][C];
 #pragma unroll
@@ -944,6 +947,7 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
                     }
                 }
             }
+            FDL_DCHECK((int64_t)it.w + t < a.ntiles);
             if constexpr (sym_shflred<MODE, DIM, NSETS, HB>())
                 sym_bfly_warp<MODE, DIM, NSETS>(jv, a.jpart + ((size_t)it.w + t) * kT * C + wid * 16 * C, lane);
             else
@@ -1232,6 +1236,7 @@ __global__ void __launch_bounds__(256, 2) k_enum(const SymArgs a, const EnumOmeg
         uint8_t* base = smem + (size_t)stage * STAGE;
         fence_proxy_async();
         mbar_arrive_expect_tx(&full[stage], STAGE);
+        FDL_DCHECK(lt >= 0 && lt < a.ntiles && J >= 0 && (int64_t)(J + 1) * kT <= a.nstage);
         tma_load_1d(base, a.D + lt * DT, DT, &full[stage]);
         tma_load_1d(base + DT, a.pos + (int64_t)J * kT * PS, kT * PS * 4, &full[stage]);
         if (++p_t == it.z) {
@@ -2079,6 +2084,7 @@ __global__ void k_bfs_scatter(const uint8_t* __restrict__ bbuf, uint8_t* D, cons
     if (!h) return;  // the diagonal (src == v); the tiles are zeroed
     const int rl = src % kT, cl = v % kT;
     const size_t off = sym_offset(t - t0, rl, cl, HB);
+    FDL_DCHECK(off < (size_t)(t1 - t0) * tile_bytes(HB) && k < nsrc && v < n);
     if (HB == 0) {
         const size_t w = off & ~(size_t)3;
         atomicOr(reinterpret_cast<unsigned int*>(D + w), h << (8 * (off & 3) + 4 * (rl & 1)));
@@ -2317,6 +2323,7 @@ __global__ void k_bf_store(const double* __restrict__ dist, int n, const int* __
     const int64_t t = tri_index(I, J, nb);
     if (t < t0 || t >= t1) return;
     const double d = dist[(int64_t)v * S + k];
+    FDL_DCHECK(sym_offset(t - t0, src % kT, v % kT, kHbDist) < (size_t)(t1 - t0) * tile_bytes(kHbDist));
     D[sym_offset(t - t0, src % kT, v % kT, kHbDist) / 4] = (float)d;
     if (d > 0.0) {  // max distance (positive doubles order like their bit patterns)
         atomicMax(reinterpret_cast<unsigned long long*>(dmax), (unsigned long long)__double_as_longlong(d));
