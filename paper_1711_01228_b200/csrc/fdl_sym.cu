@@ -70,6 +70,9 @@ constexpr int kBfsUnroll = FDL_BFS_UNROLL;
 // shared-memory wavefronts to the otherwise idle XU pipe
 #define FDL_P2_MUFU_COLS 0  // measured slower for every share: 0x8 -> 1762, 0xA -> 1613, 0xF -> 1377 vs 1913 GB/s
 #endif
+#ifndef FDL_P1S_SQRT
+#define FDL_P1S_SQRT 0  // 1: P1S stress of X^{k+1} by MUFU.SQRT and 1/h (experiment)
+#endif
 #ifndef FDL_MAXST
 #define FDL_MAXST 4  // deepest TMA ring of the pair passes
 #endif
@@ -312,7 +315,39 @@ template <int MODE, int DIM, int NSETS, bool SAFE>
 __device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float h2, float wlut, bool valid,
                                          float* ai, float* aj, float* s)
 {
-    if (MODE == kSymP1S) {
+    if (MODE == kSymP1S && FDL_P1S_SQRT) {
+        // experiment: set 0 (stress only) as r0 = sqrt(r2) and u0 = r0 / h - 1 with 1/h from
+        // the table (wlut), so only set 1 needs r2 h^2 for its rsqrt
+        u64 d[DIM];
+        u64 r2 = pk(FLT_MIN, FLT_MIN);
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+            d[c] = fsub2(pk(xi[2 * c], xi[2 * c + 1]), pk(xj[2 * c], xj[2 * c + 1]));
+            r2 = ffma2(d[c], d[c], r2);
+        }
+        float r20, r21;
+        upk(r2, r20, r21);
+        float r0;
+        asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(r20));
+        float q1 = rsqrt_approx(r21 * h2);
+        if (SAFE) q1 = valid ? q1 : 0.0f;
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+            float dlo, dhi;
+            upk(d[c], dlo, dhi);
+            ai[c] = fmaf(q1, dhi, ai[c]);
+            aj[c] = fmaf(q1, dhi, aj[c]);
+        }
+        float u0 = fmaf(r0, wlut, -1.0f), u1 = fmaf(r21, q1, -1.0f);
+        if (SAFE) {
+            u0 = valid ? u0 : 0.0f;
+            u1 = valid ? u1 : 0.0f;
+        }
+        float s0, s1;
+        upk(ffma2(pk(u0, u1), pk(u0, u1), pk(s[0], s[1])), s0, s1);
+        s[0] = s0;
+        s[1] = s1;
+    } else if (MODE == kSymP1S) {
         // two sets, stress of both, R of set 1 only (Xt; R(X^{k+1}) is needed only
         // when the guard rejects, and is then computed by a 1-set pass): the
         // stress arithmetic is the packed 2-set code, R the scalar FMAs of set 1
@@ -666,7 +701,7 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
 #pragma unroll
                 for (int rp = 0; rp < 4; ++rp) {
                     const uint32_t off = rp == 0 ? ((w << 3) & 0x7f8u) : ((w >> (8 * rp - 3)) & 0x7f8u);
-                    if (MODE == kSymP1A)  // w' = 1/h^2 of the same byte (the P2 table values)
+                    if (MODE == kSymP1A || (MODE == kSymP1S && FDL_P1S_SQRT))  // w' = 1/h^2 (P1A) or 1/h (P1S exp.)
                         ew[rp] = *reinterpret_cast<const float2*>(reinterpret_cast<const char*>(lutw) + off);
                     if ((FDL_P2_SHFL && MODE == kSymP2) || (FDL_P1_SHFL && (MODE == kSymP1 || MODE == kSymP1S))) {
                         // experiment (off): weights by warp shuffle from a 16-entry register
@@ -690,7 +725,8 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
                     for (int hh = 0; hh < 2; ++hh) {
                         const int r = 2 * rp + hh;
                         const float v = hh ? e[rp].y : e[rp].x;
-                        const float vw = MODE == kSymP1A ? (hh ? ew[rp].y : ew[rp].x) : v;
+                        const float vw = (MODE == kSymP1A || (MODE == kSymP1S && FDL_P1S_SQRT))
+                                             ? (hh ? ew[rp].y : ew[rp].x) : v;
                         bool valid = true;
                         if (SAFE) valid = (v > 0.0f) && (!diag || (ty * 8 + r < jl));
                         sym_pair<MODE, DIM, NSETS, SAFE>(&xi[r][0], xj, v, vw, valid, &ai[r][0], &aj[hh][0], &sf[hh][0]);
@@ -837,7 +873,7 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
     __shared__ int prod[2];       // producer cursor {item, tile in item}
     __shared__ float lut[256];
     __shared__ float2 lut2[HB == 0 ? 256 : 1];
-    __shared__ float2 lutw2[(HB == 0 && MODE == kSymP1A) ? 256 : 1];
+    __shared__ float2 lutw2[(HB == 0 && (MODE == kSymP1A || (MODE == kSymP1S && FDL_P1S_SQRT))) ? 256 : 1];
     constexpr int TPS = sym_tps<MODE, HB>();
     constexpr int SLOT = TPS * STAGE;  // one stage: up to TPS consecutive tiles of one item
     float* red = reinterpret_cast<float*>(smem + (size_t)NST * SLOT);
@@ -856,6 +892,8 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
                                    : make_float2((float)(lo * lo), (float)(hi * hi));
         if (MODE == kSymP1A)
             lutw2[tid] = make_float2(lo ? 1.0f / (float)(lo * lo) : 0.0f, hi ? 1.0f / (float)(hi * hi) : 0.0f);
+        if (MODE == kSymP1S && FDL_P1S_SQRT)
+            lutw2[tid] = make_float2(lo ? 1.0f / (float)lo : 0.0f, hi ? 1.0f / (float)hi : 0.0f);
     }
     // producer: the next tile of this CTA's items (cursor in shared memory; it is
     // advanced by whichever warp frees a stage last, see below)
