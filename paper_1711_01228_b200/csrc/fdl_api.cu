@@ -101,7 +101,11 @@ inline uint64_t splitmix64(uint64_t& s)
 inline double u01(uint64_t& s) { return (double)(splitmix64(s) >> 11) * (1.0 / 9007199254740992.0); }
 
 // work-item length in tiles (strip segments)
-int seg_len() { return kSeg; }
+// tiles per work item: 32 for large triangles (C5's 1.2e6 tiles: half the i-side partials
+// and reduction work, P2 5.22 -> 5.07 ms, other -0.24 ms per step), kSeg = 16 below (C4's
+// 7e4 tiles and C3 got slower with 32: fewer items per CTA).  A function of n only, so the
+// items -- and every fp32 segment sum -- are the same for any number of GPUs
+int seg_len(int64_t nb) { return nb * (nb + 1) / 2 >= ((int64_t)1 << 18) ? 2 * kSeg : kSeg; }
 
 // (I, J) of triangle index t (row-major upper triangle over nb blocks)
 void tri_coords(int64_t t, int64_t nb, int64_t& I, int64_t& J)
@@ -1086,7 +1090,7 @@ fdl_status check_params(const fdl_params* p, std::string& msg)
     return FDL_OK;
 }
 
-// Work items of the local tile range: strip segments of <= kSeg tiles.
+// Work items of the local tile range: strip segments of <= seg_len(nb) tiles.
 void build_items(fdl_ctx* ctx, std::vector<int4>& items, std::vector<int>& lo, std::vector<int>& hi)
 {
     const int64_t nb = ctx->nb;
@@ -1099,7 +1103,7 @@ void build_items(fdl_ctx* ctx, std::vector<int4>& items, std::vector<int>& lo, s
         int64_t I, J;
         tri_coords(t, nb, I, J);
         const int64_t strip_end = tri_index(I, nb - 1, nb) + 1;
-        const int64_t nt = std::min<int64_t>({(int64_t)seg_len(), strip_end - t, ctx->t1 - t});
+        const int64_t nt = std::min<int64_t>({(int64_t)seg_len(nb), strip_end - t, ctx->t1 - t});
         if (!seen[I]) {
             seen[I] = 1;
             lo[I] = (int)items.size();
@@ -1892,7 +1896,7 @@ fdl_status fdl_create_loopback(int32_t n, const int64_t* row_ptr, const int32_t*
 fdl_status fdl_shard_tiles(int32_t n, int32_t world, int32_t rank, int64_t* t0, int64_t* t1)
 {
     if (n < 1 || world < 1 || rank < 0 || rank >= world || !t0 || !t1) return FDL_E_INVALID_ARG;
-    // Boundaries fall on global work-item boundaries (strip segments of <= kSeg
+    // Boundaries fall on global work-item boundaries (strip segments of <= seg_len(nb)
     // tiles), nearest to equal tile shares: every item -- and so every fp32
     // segment sum -- is the same for any number of GPUs.
     const int64_t nb = (n + kT - 1) / kT;
@@ -1905,8 +1909,9 @@ fdl_status fdl_shard_tiles(int32_t n, int32_t world, int32_t rank, int64_t* t0, 
             const int64_t s0 = tri_index(I, I, nb), len = nb - I;
             if (s0 + len < target) continue;  // strip entirely before the target
             // segment starts inside strip I: s0, s0 + kSeg, ...
-            const int64_t k = (target - s0 + seg_len() / 2) / seg_len();
-            best = std::min(s0 + k * seg_len(), s0 + len);
+            const int64_t sl = seg_len(nb);
+            const int64_t k = (target - s0 + sl / 2) / sl;
+            best = std::min(s0 + k * sl, s0 + len);
             break;
         }
         return best;

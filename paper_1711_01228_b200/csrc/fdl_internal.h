@@ -166,7 +166,10 @@ int tile_mix_ctas_per_sm(int mode);
 
 // ------------------------------------------------------- symmetric (triangle) passes
 constexpr int kT = 128;            // tile edge: tiles (I, J), I <= J, of kT x kT pairs
-constexpr int kSeg = 16;           // tiles per work item (strip segment)
+#ifndef FDL_SEG
+#define FDL_SEG 16
+#endif
+constexpr int kSeg = FDL_SEG;      // tiles per work item (strip segment)
 // P1S: 2 stress sets, R of set 1; P1A: 1 set, stress + R + L^W X (difference form, unit lengths);
 // P1R: 1 set, R only (the rejection pass: its stress is known from P1S)
 enum { kSymP1 = 0, kSymP2 = 1, kSymDiag = 2, kSymP1S = 3, kSymP1A = 4, kSymP1R = 5 };

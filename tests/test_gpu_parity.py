@@ -86,9 +86,12 @@ def test_jacobi_diagonal(name):
     rows = sample_rows(g.n) if g.n > 20000 else np.arange(g.n, dtype=np.int32)
     ref = core.lw_diag_rows(rows, core.hop_rows(g, rows), k)
     got = L.get_diag()[rows]
-    # Jacobi preconditioner only: fp32 weights, fp32 tile partials (<= 128
-    # terms) summed in fp64 -> relative 1e-6
-    np.testing.assert_allclose(got, ref, rtol=1e-6)
+    # Jacobi preconditioner only: fp32 weights, fp32 sums within one work item
+    # (<= 32 tiles x 8 terms per thread at C5, 16 x 8 below, DESIGN R22) plus a
+    # 4-level fp32 shuffle tree, item sums in fp64.  Positive terms, so the
+    # recursive-summation bound (K - 1) u with K <= 256 + 4, u = 2^-24, holds:
+    # relative 1.6e-5 (measured: 1.4e-6 at C5, below 1e-6 for C1-C4)
+    np.testing.assert_allclose(got, ref, rtol=260 * 2.0 ** -24)
 
 
 # ------------------------------------------------- a2/a3 forces at X0 (single iteration)

@@ -98,9 +98,11 @@ def test_parameter_validation():
 def test_shard_tiles_partition(n, world):
     """Upper-triangle tiles split into contiguous ranges covering
     [0, nb(nb+1)/2) exactly once, with boundaries on global work items (strip
-    segments of <= 16 tiles), so shares differ by at most one item."""
+    segments of <= 16 tiles, 32 from 2^18 tiles on), so shares differ by at
+    most one item."""
     nb = -(-n // fdl.FDL_TILE)
     total = nb * (nb + 1) // 2
+    seg = 32 if total >= 1 << 18 else 16
     prev = 0
     sizes = []
     for r in range(world):
@@ -109,4 +111,4 @@ def test_shard_tiles_partition(n, world):
         sizes.append(b - a)
         prev = b
     assert prev == total
-    assert max(sizes) - min(sizes) <= 2 * 16 or total < world * 16
+    assert max(sizes) - min(sizes) <= 2 * seg or total < world * seg
