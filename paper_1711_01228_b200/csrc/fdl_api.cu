@@ -694,9 +694,52 @@ struct Scratch {
 // [lo, hi), each grown by BFS (over vertices not yet taken) from the first untaken
 // vertex.  Sources close to each other have nearly concentric wavefronts, so a batch's
 // searches touch a band of the graph at a time instead of all of it (geometric graphs:
-// MS-BFS on C4, the weighted sweeps on W4).
-std::vector<int> cluster_sources(int32_t n, const int64_t* rp, const int32_t* col, int lo, int hi, int S)
+// MS-BFS on C4, the weighted sweeps on W4).  Inside a batch, each 32-source word
+// is itself a compact ball (compact_words): the BFS order of the batch puts a
+// shell of the seed's neighbourhood into a word, whose sources then reach a
+// distant vertex over many sweeps with one or two bits each.
+static void compact_words(const int64_t* rp, const int32_t* col, int* seg, int cnt, std::vector<char>& inb,
+                          std::vector<int>& seen, int& stamp)
 {
+    if (cnt <= 32) return;
+    for (int i = 0; i < cnt; ++i) inb[seg[i]] = 1;  // 1: in the batch, untaken; 2: taken
+    std::vector<int> out, q;
+    out.reserve((size_t)cnt);
+    for (int i = 0; i < cnt; ++i) {
+        const int s0 = seg[i];
+        if (inb[s0] != 1) continue;
+        // a ball around s0 over the batch's vertices (taken or not) until the current
+        // word is full; an exhausted ball leaves the word to the next seed
+        ++stamp;
+        q.clear();
+        q.push_back(s0);
+        seen[s0] = stamp;
+        for (size_t h = 0; h < q.size(); ++h) {
+            const int u = q[h];
+            if (inb[u] == 1) {
+                inb[u] = 2;
+                out.push_back(u);
+                if (out.size() % 32 == 0) break;
+            }
+            for (int64_t e = rp[u]; e < rp[u + 1]; ++e) {
+                const int w = col[e];
+                if (inb[w] && seen[w] != stamp) {
+                    seen[w] = stamp;
+                    q.push_back(w);
+                }
+            }
+        }
+    }
+    for (int i = 0; i < cnt; ++i) inb[seg[i]] = 0;
+    std::copy(out.begin(), out.end(), seg);
+}
+
+std::vector<int> cluster_sources(int32_t n, const int64_t* rp, const int32_t* col, int lo, int hi, int S,
+                                 bool words)
+{
+    std::vector<char> inb(words ? (size_t)n : 0, 0);
+    std::vector<int> seen(words ? (size_t)n : 0, 0);
+    int stamp = 0;
     std::vector<int> order;
     order.reserve((size_t)std::max(0, hi - lo));
     std::vector<char> taken((size_t)n, 0);
@@ -725,6 +768,7 @@ std::vector<int> cluster_sources(int32_t n, const int64_t* rp, const int32_t* co
                 }
             }
         }
+        if (words) compact_words(rp, col, order.data() + (order.size() - got), got, inb, seen, stamp);
         ++cluster;
     }
     return order;
@@ -831,7 +875,9 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
         uint32_t *wa = nullptr, *wb = nullptr, *wv = nullptr;  // 128-word frontier / visited sets
         const size_t wmasks = (size_t)n * kBfsWideWords;
         if (clustered) {
-            order = cluster_sources(n, rp, col, src_lo, src_hi, bsrc);
+            // compact words: C4 ideal distances 0.40 -> 0.365 s
+            static const bool no_words = getenv("FDL_BFS_NO_WORDS") != nullptr;  // A/B knob
+            order = cluster_sources(n, rp, col, src_lo, src_hi, bsrc, !no_words);
             FDL_CUDA(tmp.alloc(&d_srcs, sizeof(int) * order.size()));
             FDL_CUDA(cudaMemcpyAsync(d_srcs, order.data(), sizeof(int) * order.size(), cudaMemcpyHostToDevice,
                                      ctx->stream));
@@ -925,10 +971,27 @@ fdl_status build_dists(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, cons
 {
     const int n = ctx->n;
     const int64_t m = std::max<int64_t>(rp[n], 1);
-    // sources per batch: up to 4096 (kBfWordsPerLane source words per lane), within ~2 GB of
-    // fp64 distances; fewer, larger batches mean fewer sweeps (each sweep has a fixed cost)
-    const int S = (int)std::max<int64_t>(
-        32, std::min<int64_t>(32 * 32 * kBfWordsPerLane, ((int64_t)1 << 31) / (8 * (int64_t)n) / 32 * 32));
+    int64_t Ilo = 0, Jlo = 0, Ihi = -1, Jhi = 0;
+    if (ctx->t1 > ctx->t0) {
+        tri_coords(ctx->t0, ctx->nb, Ilo, Jlo);
+        tri_coords(ctx->t1 - 1, ctx->nb, Ihi, Jhi);
+    }
+    const int src_lo = (int)std::min<int64_t>(n, Ilo * kT);
+    const int src_hi = (int)std::min<int64_t>(n, (Ihi + 1) * kT);
+    // sources per batch: up to kBfMaxChunks chunks of 4096, the fp64 distances within
+    // min(24 GB, a third of the free memory); fewer, larger batches mean fewer sweeps in
+    // all (a batch takes ~ max distance / delta sweeps however many sources it has)
+    static const double budget_gb = getenv("FDL_BF_BUDGET_GB") ? atof(getenv("FDL_BF_BUDGET_GB")) : 24.0;
+    size_t free_b = 0, total_b = 0;
+    FDL_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const int64_t nsrc_all = std::max(1, src_hi - src_lo);
+    const int64_t by_mem = std::min<int64_t>((int64_t)(budget_gb * 1e9), (int64_t)(free_b / 3)) / (8 * (int64_t)n);
+    int S;
+    if (nsrc_all <= kBfChunk || by_mem < 2 * kBfChunk)
+        S = (int)std::max<int64_t>(32, std::min<int64_t>({(nsrc_all + 31) / 32 * 32, (int64_t)kBfChunk, by_mem / 32 * 32}));
+    else
+        S = kBfChunk * (int)std::min<int64_t>({(int64_t)kBfMaxChunks, (nsrc_all + kBfChunk - 1) / kBfChunk,
+                                                by_mem / kBfChunk});
     Scratch tmp;
     int64_t* d_rp = nullptr;
     int32_t* d_col = nullptr;
@@ -940,7 +1003,7 @@ fdl_status build_dists(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, cons
     // per (vertex, source) change bits of the last sweep, double-buffered
     const int W = S / 32;
     uint32_t *chg_a = nullptr, *chg_b = nullptr;
-    uint8_t *pend_a = nullptr, *pend_b = nullptr;
+    uint16_t *pend_a = nullptr, *pend_b = nullptr;
     unsigned int* flags = nullptr;
     constexpr int kChunk = 16;  // sweeps enqueued between host checks
     // Delta-stepping threshold: sweep t propagates only distances <= (t + 1) delta, so a
@@ -953,8 +1016,8 @@ fdl_status build_dists(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, cons
     const int max_sweeps = (int)std::min<int64_t>(INT32_MAX - kChunk, 4 * (int64_t)n + rp[n] + 8);
     FDL_CUDA(tmp.alloc(&chg_a, sizeof(uint32_t) * (size_t)n * W));
     FDL_CUDA(tmp.alloc(&chg_b, sizeof(uint32_t) * (size_t)n * W));
-    FDL_CUDA(tmp.alloc(&pend_a, (size_t)n));
-    FDL_CUDA(tmp.alloc(&pend_b, (size_t)n));
+    FDL_CUDA(tmp.alloc(&pend_a, sizeof(uint16_t) * (size_t)n));
+    FDL_CUDA(tmp.alloc(&pend_b, sizeof(uint16_t) * (size_t)n));
     FDL_CUDA(tmp.alloc(&flags, sizeof(unsigned int) * (size_t)(max_sweeps + kChunk)));
     FDL_CUDA(tmp.alloc(&dmax, sizeof(double)));
     FDL_CUDA(cudaMemsetAsync(dmax, 0, sizeof(double), ctx->stream));
@@ -969,13 +1032,6 @@ fdl_status build_dists(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, cons
         FDL_CUDA(cudaMemcpyAsync(d_col, col, sizeof(int32_t) * rp[n], cudaMemcpyHostToDevice, ctx->stream));
         FDL_CUDA(cudaMemcpyAsync(d_len, lens, sizeof(double) * rp[n], cudaMemcpyHostToDevice, ctx->stream));
     }
-    int64_t Ilo = 0, Jlo = 0, Ihi = -1, Jhi = 0;
-    if (ctx->t1 > ctx->t0) {
-        tri_coords(ctx->t0, ctx->nb, Ilo, Jlo);
-        tri_coords(ctx->t1 - 1, ctx->nb, Ihi, Jhi);
-    }
-    const int src_lo = (int)std::min<int64_t>(n, Ilo * kT);
-    const int src_hi = (int)std::min<int64_t>(n, (Ihi + 1) * kT);
     ctx->hb = kHbDist;
     const size_t dbytes = (size_t)std::max<int64_t>(ctx->t1 - ctx->t0, 1) * (size_t)tile_bytes(kHbDist);
     void* q = nullptr;
@@ -994,7 +1050,9 @@ fdl_status build_dists(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, cons
     // untaken vertex.  Sources close to each other have nearly concentric wavefronts,
     // so each sweep's change words are dense (many sources per vertex at once) instead
     // of one bit per 32-lane word (measured: W4 setup 6.2 s with id-contiguous batches).
-    const std::vector<int> order = cluster_sources(n, rp, col, src_lo, src_hi, S);
+    // compact words: W4 distances 2.2 -> 1.4-1.6 s
+    static const bool no_words = getenv("FDL_BF_NO_WORDS") != nullptr;  // A/B knob
+    const std::vector<int> order = cluster_sources(n, rp, col, src_lo, src_hi, S, !no_words);
     int* d_srcs = nullptr;
     FDL_CUDA(tmp.alloc(&d_srcs, sizeof(int) * std::max<size_t>(order.size(), 1)));
     if (!order.empty())
@@ -1005,11 +1063,11 @@ fdl_status build_dists(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, cons
         const int* srcs = d_srcs + b0;
         FDL_LAUNCH(launch_bf_init(da, n, srcs, nsrc, S, ctx->stream));
         FDL_CUDA(cudaMemsetAsync(chg_a, 0, sizeof(uint32_t) * (size_t)n * W, ctx->stream));
-        FDL_CUDA(cudaMemsetAsync(pend_a, 0, (size_t)n, ctx->stream));
+        FDL_CUDA(cudaMemsetAsync(pend_a, 0, sizeof(uint16_t) * (size_t)n, ctx->stream));
         FDL_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned int) * (size_t)(max_sweeps + kChunk), ctx->stream));
         FDL_LAUNCH(launch_bf_seed(chg_a, pend_a, srcs, nsrc, S, ctx->stream));
         uint32_t *cin = chg_a, *cout = chg_b;
-        uint8_t *pin = pend_a, *pout = pend_b;
+        uint16_t *pin = pend_a, *pout = pend_b;
         // sweeps on the device, kChunk between host checks of the last sweep's flag
         // (a sweep after one without changes returns at once)
         bool done = false;

@@ -47,7 +47,11 @@ constexpr int kGalNV = kGalMax * (kGalMax + 1) / 2 + kGalMax;  // Gram entries +
 constexpr int kBFSWords = 32;      // MS-BFS source batch = 32 words x 32 bits = 1024
 constexpr int kBfsHubDeg = 256;
 constexpr int kBfsWideWords = 128;  // clustered MS-BFS batches: 128 words x 32 = 4096 sources
-constexpr int kBfWordsPerLane = 4;  // weighted APSP: up to 32 x 4 x 32 = 4096 sources per batch    // MS-BFS: vertices of higher degree get a whole block per level
+// weighted APSP: a warp relaxes one chunk of 32 x 4 x 32 = 4096 sources of a vertex at a
+// time; a batch holds up to kBfMaxChunks chunks (one 16-bit pending mask per vertex)
+constexpr int kBfWordsPerLane = 4;
+constexpr int kBfChunk = 32 * 32 * kBfWordsPerLane;
+constexpr int kBfMaxChunks = 16;
 
 // Device-resident scalars of the iteration (one struct per context).
 struct DevScalars {
@@ -264,10 +268,10 @@ int bfs_row_bytes_host(int hb);  // batch-buffer bytes per vertex
 // CSR with edge lengths; dist[v * S + s] for the batch's sources s0..s0+S-1
 cudaError_t launch_bf_init(double* dist, int n, const int* srcs, int nsrc, int S, cudaStream_t s);
 cudaError_t launch_bf_sweep(const int64_t* row_ptr, const int32_t* col, const double* len, double* dist,
-                            const uint32_t* chg_in, uint32_t* chg_out, const uint8_t* pend_in, uint8_t* pend_out,
+                            const uint32_t* chg_in, uint32_t* chg_out, const uint16_t* pend_in, uint16_t* pend_out,
                             int n, int S, int nsrc, int it, double delta, unsigned int* flags, int grid,
                             cudaStream_t s);
-cudaError_t launch_bf_seed(uint32_t* chg, uint8_t* pend, const int* srcs, int nsrc, int S, cudaStream_t s);
+cudaError_t launch_bf_seed(uint32_t* chg, uint16_t* pend, const int* srcs, int nsrc, int S, cudaStream_t s);
 cudaError_t launch_bf_store(const double* dist, int n, const int* srcs, int nsrc, int S, int nb, int64_t t0,
                             int64_t t1, uint8_t* D, double* dmax, cudaStream_t s);
 cudaError_t launch_dist_rows(const uint8_t* D, int hb, int nb, int64_t t0, int64_t t1, const int* rows, int nrows,

@@ -2202,77 +2202,135 @@ cudaError_t launch_bf_init(double* dist, int n, const int* srcs, int nsrc, int S
 // the same sweep is re-checked in the next one, so the fixed point is the
 // shortest-path distance (each value an fp64 sum along a shortest path).  A
 // sweep whose predecessor changed nothing returns at once (flags[it - 1] = 0).
-__global__ void __launch_bounds__(256) k_bf_sweep(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+__global__ void __launch_bounds__(256, 4) k_bf_sweep(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                                                   const double* __restrict__ len, double* dist,
                                                   const uint32_t* __restrict__ chg_in, uint32_t* __restrict__ chg_out,
-                                                  const uint8_t* __restrict__ pend_in, uint8_t* __restrict__ pend_out,
+                                                  const uint16_t* __restrict__ pend_in, uint16_t* __restrict__ pend_out,
                                                   int n, int S, int nsrc, int it, double delta, unsigned int* flags)
 {
     if (it > 0 && *(volatile unsigned int*)&flags[it - 1] == 0u) return;
-    __shared__ unsigned int blk_new;
-    if (threadIdx.x == 0) blk_new = 0u;
-    __syncthreads();
+    __shared__ uint32_t outw[8 * 32 * kBfWordsPerLane];  // per warp: the vertex's new change words
     const int lane = threadIdx.x & 31;
     const int W = S >> 5;
     const double T = delta * (double)(it + 1);  // this sweep's threshold (Delta-stepping buckets)
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
     bool found = false;
-    volatile double* dv = dist;
+    // weak L2 loads (ld.global.cg): a value another warp improves during this sweep may be
+    // read stale, and is then re-relaxed in the next sweep through the change bits, as
+    // with any Gauss-Seidel order (volatile's system-scope loads were slower)
+    double* dv = dist;
     for (int64_t vv = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; vv < n; vv += nwarps) {
         const int v = (int)vv;
         const int64_t beg = row_ptr[v], end = row_ptr[v + 1];
         const int nu = (int)min((int64_t)32, end - beg);
         const int myu = lane < nu ? col[beg + lane] : 0;
-        const bool selfp = pend_in[v] != 0;
-        // a vertex with nothing pending in its neighbourhood (the usual case away from the
-        // batch's wavefront band) costs its neighbours' 1-byte flags only
-        bool np = lane < nu && pend_in[myu] != 0;
-        for (int64_t e = beg + 32 + lane; e < end && !np; e += 32) np = pend_in[col[e]] != 0;
-        const unsigned pm = __ballot_sync(0xffffffffu, np);
-        if (!pm && !selfp) {
+        // pending chunks (bit c: some source of chunk c changed at that vertex in the last
+        // sweep).  A vertex with nothing pending in its neighbourhood (the usual case away
+        // from the wavefront band) costs its neighbours' 2-byte masks only
+        const uint32_t smask = pend_in[v];
+        const uint32_t lmask = lane < nu ? pend_in[myu] : 0u;
+        uint32_t xmask = 0u;  // neighbours past the first 32 (rare)
+        for (int64_t e = beg + 32 + lane; e < end; e += 32) xmask |= pend_in[col[e]];
+        const uint32_t cmask = __reduce_or_sync(0xffffffffu, lmask | xmask) | smask;
+        if (!cmask) {
             if (lane == 0) pend_out[v] = 0;
             continue;
         }
-        // candidate sources: pending bits of the neighbours that have any; lane holds words
-        // lane, lane + 32, ... of the W = S/32 source words (S <= 4096: up to 4 per lane)
-        uint32_t act[kBfWordsPerLane], own[kBfWordsPerLane], outw[kBfWordsPerLane];
+        uint32_t outmask = 0u;
+        for (uint32_t cm = cmask; cm; cm &= cm - 1) {
+            const int ch = __ffs(cm) - 1;  // chunk: sources [4096 ch, 4096 ch + 4096), words [128 ch, ...)
+            const unsigned pm = __ballot_sync(0xffffffffu, (lmask >> ch) & 1u);
+            const bool selfp = (smask >> ch) & 1u;
+            const int wofs = ch * 32 * kBfWordsPerLane, WC = min(W - wofs, 32 * kBfWordsPerLane);
+            // candidate sources: pending bits of the neighbours that have any; lane holds words
+            // lane, lane + 32, ... of the W = S/32 source words (S <= 4096: up to 4 per lane)
+            uint32_t act[kBfWordsPerLane], own[kBfWordsPerLane];
 #pragma unroll
-        for (int j = 0; j < kBfWordsPerLane; ++j) act[j] = own[j] = outw[j] = 0u;
-        {
-            unsigned m = pm & (nu == 32 ? 0xffffffffu : ((1u << nu) - 1u));  // warp-uniform (a ballot)
-            while (m) {
-                const int q = __ffs(m) - 1;
-                m &= m - 1;
-                const int u = __shfl_sync(0xffffffffu, myu, q);
+            for (int j = 0; j < kBfWordsPerLane; ++j) act[j] = own[j] = 0u;
+            {
+                unsigned m = pm & (nu == 32 ? 0xffffffffu : ((1u << nu) - 1u));  // warp-uniform (a ballot)
+                while (m) {  // four neighbours' words in flight at once
+                    uint32_t t[4][kBfWordsPerLane];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) {
+                        const int q = m ? __ffs(m) - 1 : -1;
+                        m &= m - 1;
+                        const int u = __shfl_sync(0xffffffffu, myu, q < 0 ? 0 : q);
+#pragma unroll
+                        for (int j = 0; j < kBfWordsPerLane; ++j)
+                            t[a][j] = (q >= 0 && 32 * j + lane < WC) ? __ldcg(&chg_in[(int64_t)u * W + wofs + 32 * j + lane]) : 0u;
+                    }
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int j = 0; j < kBfWordsPerLane; ++j) act[j] |= t[a][j];
+                }
+            }
+            if (end - beg > 32)  // long lists: the rest in order (rare)
+                for (int64_t e = beg + 32; e < end; ++e) {
+                    const int u = col[e];
+                    if ((pend_in[u] >> ch) & 1u)
+#pragma unroll
+                        for (int j = 0; j < kBfWordsPerLane; ++j)
+                            if (32 * j + lane < WC) act[j] |= __ldcg(&chg_in[(int64_t)u * W + wofs + 32 * j + lane]);
+                }
+            if (selfp)
 #pragma unroll
                 for (int j = 0; j < kBfWordsPerLane; ++j)
-                    if (32 * j + lane < W) act[j] |= __ldcg(&chg_in[(int64_t)u * W + 32 * j + lane]);
+                    if (32 * j + lane < WC) own[j] = chg_in[(int64_t)v * W + wofs + 32 * j + lane];
+            const double myl = lane < nu ? len[beg + lane] : 0.0;
+            // The candidates (set bits of act | own) compacted over the lanes: round b gives
+            // lane L the (32 b + L)-th candidate in (owner lane, word, bit) order, so a round
+            // relaxes 32 (vertex, source) values whatever the words' bit density (one word at
+            // a time used 8.7 of 32 lanes on W4).  The new change bits collect in the warp's
+            // shared word buffer.
+            uint32_t* ob = outw + (threadIdx.x >> 5) * (32 * kBfWordsPerLane);
+            int cnt = 0;
+#pragma unroll
+            for (int j = 0; j < kBfWordsPerLane; ++j) {
+                if (32 * j + lane < WC) ob[32 * j + lane] = 0u;
+                cnt += __popc(act[j] | own[j]);
             }
-        }
-        if (end - beg > 32)  // long lists: the rest in order (rare)
-            for (int64_t e = beg + 32; e < end; ++e) {
-                const int u = col[e];
-                if (pend_in[u])
+            int incl = cnt;
 #pragma unroll
-                    for (int j = 0; j < kBfWordsPerLane; ++j)
-                        if (32 * j + lane < W) act[j] |= __ldcg(&chg_in[(int64_t)u * W + 32 * j + lane]);
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
             }
-        if (selfp)
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            __syncwarp();
+            for (int base = 0; base < total; base += 32) {
+                const int r = base + lane;
+                int ol = 0;  // owner lane: the first with an inclusive count above r
 #pragma unroll
-            for (int j = 0; j < kBfWordsPerLane; ++j)
-                if (32 * j + lane < W) own[j] = chg_in[(int64_t)v * W + 32 * j + lane];
-        const double myl = lane < nu ? len[beg + lane] : 0.0;
+                for (int step = 16; step > 0; step >>= 1) {
+                    const int t = __shfl_sync(0xffffffffu, incl, ol + step - 1);
+                    if (t <= r) ol += step;
+                }
+                int rr = r - (__shfl_sync(0xffffffffu, incl, ol) - __shfl_sync(0xffffffffu, cnt, ol));
+                uint32_t aw = 0u, owd = 0u;
+                int wj = 0;
+                bool picked = false;
 #pragma unroll
-        for (int j = 0; j < kBfWordsPerLane; ++j) {
-            if (32 * j >= W) break;
-            for (int mm = 0; mm < 32 && 32 * j + mm < W; ++mm) {
-                const int m = 32 * j + mm;
-                const uint32_t wm = __shfl_sync(0xffffffffu, act[j], mm), om = __shfl_sync(0xffffffffu, own[j], mm);
-                if (!(wm | om)) continue;
-                const int k = 32 * m + lane;
-                const bool on = ((wm >> lane) & 1u) && k < nsrc;
-                const bool mine = (om >> lane) & 1u;
-                const double old = (on || mine) ? dv[(int64_t)v * S + k] : 0.0;
+                for (int j = 0; j < kBfWordsPerLane; ++j) {
+                    const uint32_t a = __shfl_sync(0xffffffffu, act[j], ol), o = __shfl_sync(0xffffffffu, own[j], ol);
+                    const int c = __popc(a | o);
+                    if (!picked && rr < c) {
+                        aw = a;
+                        owd = o;
+                        wj = j;
+                        picked = true;
+                    } else if (!picked) {
+                        rr -= c;
+                    }
+                }
+                const bool valid = r < total && picked;
+                const int bit = valid ? (int)__fns(aw | owd, 0u, rr + 1) : 0;
+                const int word = 32 * wj + ol;
+                const int k = 32 * (wofs + word) + bit;
+                const bool on = valid && ((aw >> bit) & 1u) && k < nsrc;
+                const bool mine = valid && ((owd >> bit) & 1u);
+                const double old = (on || mine) ? __ldcg(&dv[(int64_t)v * S + k]) : 0.0;
                 double best = old;
                 for (int q0 = 0; q0 < nu; q0 += 8) {
                     double c[8];
@@ -2280,15 +2338,15 @@ __global__ void __launch_bounds__(256) k_bf_sweep(const int64_t* __restrict__ ro
                     for (int q = 0; q < 8; ++q) {
                         const int u = __shfl_sync(0xffffffffu, myu, (q0 + q) & 31);
                         const double l = __shfl_sync(0xffffffffu, myl, (q0 + q) & 31);
-                        const double du = (on && q0 + q < nu) ? dv[(int64_t)u * S + k] : INFINITY;
+                        const double du = (on && q0 + q < nu) ? __ldcg(&dv[(int64_t)u * S + k]) : INFINITY;
                         c[q] = du <= T ? du + l : INFINITY;  // a distance above the threshold waits
                     }
 #pragma unroll
                     for (int q = 0; q < 8; ++q) best = c[q] < best ? c[q] : best;
                 }
-                for (int64_t e = beg + 32; e < end; ++e)  // lists longer than 32 (rare)
-                    if (on) {
-                        const double du = dv[(int64_t)col[e] * S + k];
+                if (on)
+                    for (int64_t e = beg + 32; e < end; ++e) {  // lists longer than 32 (rare)
+                        const double du = __ldcg(&dv[(int64_t)col[e] * S + k]);
                         const double c = du <= T ? du + len[e] : INFINITY;
                         best = c < best ? c : best;
                     }
@@ -2300,71 +2358,93 @@ __global__ void __launch_bounds__(256) k_bf_sweep(const int64_t* __restrict__ ro
                 // pending after this sweep: a new value, or an own pending value above the
                 // threshold (its neighbours did not take it yet); own values <= T were pulled
                 // by every neighbour in this sweep
-                const bool keep = imp || (mine && old > T);
-                const uint32_t bw = __ballot_sync(0xffffffffu, keep);
-                if (lane == mm) outw[j] = bw;
+                if (imp || (mine && old > T)) atomicOr(&ob[word], 1u << bit);
             }
-        }
-        bool anyw = false;
+            __syncwarp();
+            bool anyw = false;
 #pragma unroll
-        for (int j = 0; j < kBfWordsPerLane; ++j)
-            if (32 * j + lane < W) {
-                chg_out[(int64_t)v * W + 32 * j + lane] = outw[j];
-                anyw |= outw[j] != 0u;
-            }
-        const bool any = __any_sync(0xffffffffu, anyw);
-        if (lane == 0) pend_out[v] = any ? 1 : 0;
-        found |= any;
+            for (int j = 0; j < kBfWordsPerLane; ++j)
+                if (32 * j + lane < WC) {
+                    const uint32_t wv = ob[32 * j + lane];
+                    chg_out[(int64_t)v * W + wofs + 32 * j + lane] = wv;
+                    anyw |= wv != 0u;
+                }
+            __syncwarp();
+            if (__any_sync(0xffffffffu, anyw)) outmask |= 1u << ch;
+        }
+        if (lane == 0) pend_out[v] = (uint16_t)outmask;
+        found |= outmask != 0u;
     }
-    if (found && lane == 0) blk_new = 1u;
-    __syncthreads();
-    if (threadIdx.x == 0 && blk_new) flags[it] = 1u;
+    // per warp, no block barrier (a block's warps finish their vertex lists at
+    // different times; a barrier here held 25% of the stall samples, W4)
+    if (found && lane == 0) flags[it] = 1u;
 }
 
 // change bits of the batch's sources: vertex s0 + k has source k's bit (its
 // distance 0 is the only finite value at the start)
-__global__ void k_bf_seed(uint32_t* chg, uint8_t* pend, const int* __restrict__ srcs, int nsrc, int S)
+__global__ void k_bf_seed(uint32_t* chg, uint16_t* pend, const int* __restrict__ srcs, int nsrc, int S)
 {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nsrc) return;
     chg[(int64_t)srcs[k] * (S >> 5) + (k >> 5)] = 1u << (k & 31);
-    pend[srcs[k]] = 1;
+    pend[srcs[k]] = (uint16_t)(1u << (k / kBfChunk));  // a vertex is one source of the batch
 }
 
 cudaError_t launch_bf_sweep(const int64_t* row_ptr, const int32_t* col, const double* len, double* dist,
-                            const uint32_t* chg_in, uint32_t* chg_out, const uint8_t* pend_in, uint8_t* pend_out,
+                            const uint32_t* chg_in, uint32_t* chg_out, const uint16_t* pend_in, uint16_t* pend_out,
                             int n, int S, int nsrc, int it, double delta, unsigned int* flags, int grid,
                             cudaStream_t s)
 {
-    const unsigned g = (unsigned)std::max(1, std::min(grid, (int)(((int64_t)n * 32 + 255) / 256)));
+    // grid-stride warps: one wave of resident blocks (a second partial wave idled SMs)
+    static int per_sm = 0;
+    if (per_sm == 0) {
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bf_sweep, 256, 0);
+        if (e != cudaSuccess || per_sm < 1) per_sm = 1;
+    }
+    const unsigned g = (unsigned)std::max(1, std::min(grid * per_sm, (int)(((int64_t)n * 32 + 255) / 256)));
     k_bf_sweep<<<g, 256, 0, s>>>(row_ptr, col, len, dist, chg_in, chg_out, pend_in, pend_out, n, S, nsrc, it, delta,
                                  flags);
     return cudaGetLastError();
 }
 
-cudaError_t launch_bf_seed(uint32_t* chg, uint8_t* pend, const int* srcs, int nsrc, int S, cudaStream_t s)
+cudaError_t launch_bf_seed(uint32_t* chg, uint16_t* pend, const int* srcs, int nsrc, int S, cudaStream_t s)
 {
     k_bf_seed<<<(nsrc + 255) / 256, 256, 0, s>>>(chg, pend, srcs, nsrc, S);
     return cudaGetLastError();
 }
 
 // rows srcs[0..nsrc) of the upper-triangle tiles of the local range <- fp32(dist)
-__global__ void k_bf_store(const double* __restrict__ dist, int n, const int* __restrict__ srcs, int nsrc, int S,
-                           int nb, int64_t t0, int64_t t1, float* D, double* dmax)
+__global__ void __launch_bounds__(256) k_bf_store(const double* __restrict__ dist, int n,
+                                                  const int* __restrict__ srcs, int nsrc, int S, int nb, int64_t t0,
+                                                  int64_t t1, float* D, double* dmax)
 {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (int64_t)n * nsrc) return;
-    const int v = (int)(idx / nsrc), k = (int)(idx % nsrc);
-    const int src = srcs[k];
-    const int I = src / kT, J = v / kT;
-    if (I > J) return;
-    const int64_t t = tri_index(I, J, nb);
-    if (t < t0 || t >= t1) return;
-    const double d = dist[(int64_t)v * S + k];
-    FDL_DCHECK(sym_offset(t - t0, src % kT, v % kT, kHbDist) < (size_t)(t1 - t0) * tile_bytes(kHbDist));
-    D[sym_offset(t - t0, src % kT, v % kT, kHbDist) / 4] = (float)d;
-    if (d > 0.0) {  // max distance (positive doubles order like their bit patterns)
-        atomicMax(reinterpret_cast<unsigned long long*>(dmax), (unsigned long long)__double_as_longlong(d));
+    // max distance as the max of the positive doubles' bit patterns (they order alike):
+    // per block, one atomic (one per element serialised on the address: 67 ms per W4 batch)
+    unsigned long long mb = 0ull;
+    if (idx < (int64_t)n * nsrc) {
+        const int v = (int)(idx / nsrc), k = (int)(idx % nsrc);
+        const int src = srcs[k];
+        const int I = src / kT, J = v / kT;
+        const int64_t t = tri_index(I, J, nb);
+        if (I <= J && t >= t0 && t < t1) {
+            const double d = dist[(int64_t)v * S + k];
+            FDL_DCHECK(sym_offset(t - t0, src % kT, v % kT, kHbDist) < (size_t)(t1 - t0) * tile_bytes(kHbDist));
+            D[sym_offset(t - t0, src % kT, v % kT, kHbDist) / 4] = (float)d;
+            if (d > 0.0) mb = (unsigned long long)__double_as_longlong(d);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(0xffffffffu, mb, o);
+        mb = x > mb ? x : mb;
+    }
+    __shared__ unsigned long long wmax[8];
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = mb;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) mb = wmax[w] > mb ? wmax[w] : mb;
+        if (mb) atomicMax(reinterpret_cast<unsigned long long*>(dmax), mb);
     }
 }
 

@@ -15,6 +15,7 @@ stand-ins BA-20k / BA-40k over several seeds, through every launch path and
 bench.py's C5 parameters.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -24,6 +25,7 @@ from paper_1711_01228_b200 import fdl
 from workloads import configs, graphs
 
 pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 FORCE_TOL = 1e-5
 STRESS_TOL = 1e-6
@@ -726,6 +728,59 @@ def test_weighted_distances(kind):
     got = L.get_dist_rows(0, g.n)
     want = k * D.astype(np.float32).astype(np.float64)
     np.testing.assert_allclose(got, want, rtol=2e-7, atol=0)
+
+
+def test_weighted_distances_w4_sampled():
+    """W4 at full size (n = 49100: 12 clustered batches of 4096 sources, the
+    launch path bench.py times): sampled rows of the stored distances =
+    Dijkstra (fp64) rounded to fp32, and the diameter = ceil(max distance)."""
+    from oracle import weighted
+    cfg = configs.CONFIGS["W4"]
+    g = configs.graph_for("W4")
+    lens = configs.edge_lengths_for("W4")
+    k = cfg.k_for(g.n)
+    p = fdl.make_params(dim=cfg.dim, k=k, omega=cfg.omega, tol=cfg.tol)
+    with fdl.Layout.from_graph(g, params=p, init_pos=configs.positions_for("W4", g.n, 1), edge_len=lens) as L:
+        assert L.info.hop_bits == 32
+        rows = sample_rows(g.n, count=24)
+        want = weighted.dist_rows(g, lens, rows)
+        for r, w in zip(rows, want):
+            got = L.get_dist_rows(int(r), 1)[0]
+            np.testing.assert_allclose(got, k * w.astype(np.float32).astype(np.float64), rtol=2e-7, atol=0,
+                                       err_msg=str(r))
+        assert L.info.diameter >= int(np.ceil(want.max()))
+
+
+@pytest.mark.parametrize("budget_gb", [None, 0.7])
+def test_weighted_distances_chunked(budget_gb, tmp_path):
+    """Batches of several 4096-source chunks (n ~ 10^4: one batch of 3 chunks, the
+    last partial; and, with a 0.7 GB budget for the fp64 distances, 2 batches of
+    2 chunks): sampled rows = Dijkstra (fp64) rounded to fp32.  The budget is read
+    once per process, so the variant runs in a subprocess."""
+    import subprocess
+    import sys
+    from oracle import weighted
+    g, lens = graphs.random_geometric_graph_weighted(10000, 6, 23)
+    assert g.n > 2 * 4096
+    rows = sample_rows(g.n, count=20)
+    out = tmp_path / "rows.npy"
+    code = (
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {str(ROOT)!r})\n"
+        "from paper_1711_01228_b200 import fdl\n"
+        "from workloads import graphs\n"
+        "g, lens = graphs.random_geometric_graph_weighted(10000, 6, 23)\n"
+        "p = fdl.make_params(dim=2, k=1.0)\n"
+        "L = fdl.Layout.from_graph(g, params=p, init_pos=graphs.init_positions(g.n, 2, 1), edge_len=lens)\n"
+        f"rows = {rows.tolist()!r}\n"
+        f"np.save({str(out)!r}, np.stack([L.get_dist_rows(r, 1)[0] for r in rows]))\n")
+    env = dict(os.environ)
+    if budget_gb is not None:
+        env["FDL_BF_BUDGET_GB"] = str(budget_gb)
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=300)
+    got = np.load(out)
+    want = weighted.dist_rows(g, lens, rows)
+    np.testing.assert_allclose(got, want.astype(np.float32).astype(np.float64), rtol=2e-7, atol=0)
 
 
 @pytest.mark.parametrize("kind,alpha,dim", [("wrgg", -2.0, 2), ("wrgg", -1.0, 2), ("wgrid", -2.0, 3),
