@@ -2330,6 +2330,7 @@ __global__ void __launch_bounds__(256, 4) k_bf_sweep(const int64_t* __restrict__
                 const int k = 32 * (wofs + word) + bit;
                 const bool on = valid && ((aw >> bit) & 1u) && k < nsrc;
                 const bool mine = valid && ((owd >> bit) & 1u);
+                FDL_DCHECK(!valid || (k < nsrc && k < S && word < WC));
                 const double old = (on || mine) ? __ldcg(&dv[(int64_t)v * S + k]) : 0.0;
                 double best = old;
                 for (int q0 = 0; q0 < nu; q0 += 8) {

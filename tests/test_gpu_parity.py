@@ -710,6 +710,9 @@ def _weighted_case(kind):
     elif kind == "wgrid":
         g = graphs.grid_graph(12, 13)
         lens = graphs.edge_lengths_uniform(g, 0.5, 2.0, 22)
+    elif kind == "wba":  # hubs: neighbour lists longer than a warp (the sweep's long-list path)
+        g = graphs.barabasi_albert(1500, 2, 24)
+        lens = graphs.edge_lengths_uniform(g, 0.5, 2.0, 25)
     else:  # unit lengths (general alpha on hop distances)
         g = graphs.grid_graph(10, 10)
         lens = None
@@ -717,10 +720,12 @@ def _weighted_case(kind):
     return g, lens, D
 
 
-@pytest.mark.parametrize("kind", ["wrgg", "wgrid"])
+@pytest.mark.parametrize("kind", ["wrgg", "wgrid", "wba"])
 def test_weighted_distances(kind):
     """Multi-source Bellman-Ford (fp64, stored fp32) = Dijkstra (fp64) rounded."""
     g, lens, D = _weighted_case(kind)
+    if kind == "wba":
+        assert np.diff(g.row_ptr).max() > 64
     k = 0.05
     p = fdl.make_params(dim=2, k=k)
     L = fdl.Layout.from_graph(g, params=p, init_pos=graphs.init_positions(g.n, 2, 1), edge_len=lens)
