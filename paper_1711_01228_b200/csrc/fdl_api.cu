@@ -774,6 +774,19 @@ std::vector<int> cluster_sources(int32_t n, const int64_t* rp, const int32_t* co
     return order;
 }
 
+// FDL_SETUP_TRACE=1: host timestamps of the setup phases on stderr (each after a
+// stream sync, so only for diagnosis)
+void setup_trace(fdl_ctx* ctx, const char* what)
+{
+    static const bool on = getenv("FDL_SETUP_TRACE") != nullptr;
+    if (!on) return;
+    static auto t_last = std::chrono::steady_clock::now();
+    cudaStreamSynchronize(ctx->stream);
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "fdl setup: %-28s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+}
+
 // ------------------------------------------------------------------ MS-BFS
 // Sources: the rows of the blocks I of the local tiles.  Writes the upper
 // triangle tiles of the local range; the Jacobi diagonal follows from one
@@ -831,7 +844,9 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
         ctx->allocs.push_back(q);
         ctx->device_bytes += dbytes;
         ctx->hop_bytes_total = dbytes;
+        setup_trace(ctx, "hop tiles allocated");
         FDL_CUDA(cudaMemsetAsync(ctx->D, 0, dbytes, ctx->stream));
+        setup_trace(ctx, "hop tiles zeroed");
         const int maxhop = hb_max_hop(hb);
         // levels per batch: every BFS ends within diam <= 2 ecc(0) levels; one level past the
         // width's maximum detects an overflow.  The loop runs on the device (level flags),
@@ -922,6 +937,7 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
             else
                 FDL_LAUNCH(launch_bfs_retile(bbuf, ctx->D, n, s0, nsrc, ctx->nb, ctx->t0, ctx->t1, hb, ctx->stream));
         }
+        setup_trace(ctx, "MS-BFS batches");
         FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, ctx->stream));
         FDL_CUDA(cudaStreamSynchronize(ctx->stream));
         tmp.release(bbuf);
@@ -933,12 +949,14 @@ fdl_status build_hops(fdl_ctx* ctx, const int64_t* rp, const int32_t* col, int e
         if (wa) tmp.release(wa);
         if (wb) tmp.release(wb);
         if (wv) tmp.release(wv);
+        setup_trace(ctx, "batch buffers freed");
         const bool overflow = ctx->sc_host->bfs_overflow != 0;
         const int diam = ctx->sc_host->bfs_diam;
         ctx->bfs_bytes += ctx->sc_host->bfs_bytes;
         if (!overflow) {
             ctx->diameter = diam;
             if (hb == 0) FDL_LAUNCH(launch_nib_encode(ctx->D, dbytes, ctx->stream));
+            setup_trace(ctx, "nibble encode");
             break;
         }
         if (hb == 2) {
@@ -1356,12 +1374,14 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     FDL_CUDA(cudaMemcpyAsync(ctx->it_hi, hi.data(), sizeof(int) * ctx->nb, cudaMemcpyHostToDevice, ctx->stream));
 
     // hop matrix first (fixes the hop width), then grids, then the Jacobi diagonal
+    setup_trace(ctx, "create: buffers");
     const auto td0 = std::chrono::steady_clock::now();
     if (ctx->general)
         FDL_TRY(build_dists(ctx, rp, col, edge_len));
     else
         FDL_TRY(build_hops(ctx, rp, col, ecc0));
     ctx->setup_dist_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - td0).count();
+    setup_trace(ctx, "ideal distances");
     const int cap_items = std::max(ctx->nitems, 1);
     for (int s = 1; s <= 2; ++s)
         ctx->grid_p1[s] = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymP1, dim, s, ctx->hb)));
@@ -1380,6 +1400,7 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     // Jacobi diagonal sum_{j != i} w'_ij (one symmetric DIAG pass) and sigma = mean(diag)/n
     FDL_TRY(run_sym(ctx, kSymDiag, 1, ctx->posf, ctx->diag, nullptr, 0));
     FDL_LAUNCH(launch_set_sigma_rows(ctx->diag, ctx->n, ctx->sc, ctx->stream));
+    setup_trace(ctx, "Jacobi diagonal");
 
     // initial placement: caller's, else seeded uniform on the unit cube
     std::vector<double> X0;
@@ -1393,6 +1414,7 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     for (size_t i = 0; i < (size_t)n * dim; ++i)
         if (!std::isfinite(X[i])) return set_err(ctx, FDL_E_INVALID_ARG, "init_pos has a non-finite value");
     FDL_TRY(upload_positions(ctx, X));
+    setup_trace(ctx, "positions + first evaluation");
     ctx->setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return FDL_OK;
 }

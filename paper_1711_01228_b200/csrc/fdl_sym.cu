@@ -1688,30 +1688,44 @@ cudaError_t launch_sym_stress(const double* spart, int nitems, int nsets, double
 // of the stored width, each lane's 32 cells contiguous: one vector
 // read-modify-write per lane and level).  k_bfs_retile then moves the batch's
 // rows into the triangle tiles with coalesced 16-byte chunk stores.
+// Bit k of the low bits of x moved to the lowest bit of cell k (cells of 4, 8 or 16
+// bits); times the level, each cell of a set bit holds the level (no carries: the
+// level fits the cell).
+__device__ __forceinline__ uint32_t spread_nib(uint32_t x)  // 8 bits -> 8 nibbles
+{
+    x &= 0xffu;
+    x = (x | (x << 12)) & 0x000F000Fu;
+    x = (x | (x << 6)) & 0x03030303u;
+    return (x | (x << 3)) & 0x11111111u;
+}
+__device__ __forceinline__ uint32_t spread_byte(uint32_t x)  // 4 bits -> 4 bytes
+{
+    x &= 0xfu;
+    x = (x | (x << 14)) & 0x00030003u;
+    return (x | (x << 7)) & 0x01010101u;
+}
+
 template <int HB>
 __device__ __forceinline__ void bfs_record(uint8_t* cells, uint32_t nw, int level)
 {
+    const uint32_t L = (uint32_t)level;
     if (HB == 0) {  // 32 nibbles = 16 bytes
         uint4 c = *reinterpret_cast<uint4*>(cells);
-        uint32_t w[4] = {c.x, c.y, c.z, c.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if ((nw >> (8 * q + k)) & 1u) w[q] |= (uint32_t)level << (4 * k);
-        *reinterpret_cast<uint4*>(cells) = make_uint4(w[0], w[1], w[2], w[3]);
+        c.x |= spread_nib(nw) * L;
+        c.y |= spread_nib(nw >> 8) * L;
+        c.z |= spread_nib(nw >> 16) * L;
+        c.w |= spread_nib(nw >> 24) * L;
+        *reinterpret_cast<uint4*>(cells) = c;
     } else if (HB == 1) {  // 32 bytes
         uint4* p = reinterpret_cast<uint4*>(cells);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             uint4 c = p[h];
-            uint32_t w[4] = {c.x, c.y, c.z, c.w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if ((nw >> (16 * h + 4 * q + k)) & 1u) w[q] |= (uint32_t)level << (8 * k);
-            p[h] = make_uint4(w[0], w[1], w[2], w[3]);
+            c.x |= spread_byte(nw >> (16 * h)) * L;
+            c.y |= spread_byte(nw >> (16 * h + 4)) * L;
+            c.z |= spread_byte(nw >> (16 * h + 8)) * L;
+            c.w |= spread_byte(nw >> (16 * h + 12)) * L;
+            p[h] = c;
         }
     } else {  // 32 x uint16 = 64 bytes
         uint4* p = reinterpret_cast<uint4*>(cells);
@@ -1720,10 +1734,10 @@ __device__ __forceinline__ void bfs_record(uint8_t* cells, uint32_t nw, int leve
             uint4 c = p[h];
             uint32_t w[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-                for (int k = 0; k < 2; ++k)
-                    if ((nw >> (8 * h + 2 * q + k)) & 1u) w[q] |= (uint32_t)level << (16 * k);
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t b = nw >> (8 * h + 2 * q);
+                w[q] |= ((b & 1u) | ((b & 2u) << 15)) * L;
+            }
             p[h] = make_uint4(w[0], w[1], w[2], w[3]);
         }
     }
@@ -1749,15 +1763,27 @@ __device__ __forceinline__ uint32_t bfs_gather(const int32_t* __restrict__ col, 
     // OR of the neighbours' frontier words over col[beg, end) in chunks of 32 neighbours
     // `stride` apart; kBfsUnroll independent 128-byte loads in flight per warp
     uint32_t acc = 0;
+    const uint32_t* fl = fin + lane;
     for (int64_t e0 = beg; e0 < end; e0 += stride) {
         const int myu = (e0 + lane < end) ? col[e0 + lane] : 0;
-        const int cnt = (int)min((int64_t)32, end - e0);
+        const int cnt = (int)min((int64_t)32, end - e0);  // warp-uniform
+        if (cnt <= 8) {  // the usual degree: 8 slots instead of kBfsUnroll predicated ones
+            uint32_t t[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t u = (uint32_t)__shfl_sync(0xffffffffu, myu, k);
+                t[k] = k < cnt ? __ldcg(fl + (size_t)u * kBFSWords) : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc |= t[k];
+            continue;
+        }
         for (int k0 = 0; k0 < cnt; k0 += kBfsUnroll) {
             uint32_t t[kBfsUnroll];
 #pragma unroll
             for (int k = 0; k < kBfsUnroll; ++k) {
-                const int u = __shfl_sync(0xffffffffu, myu, (k0 + k) & 31);
-                t[k] = (k0 + k < cnt) ? __ldcg(&fin[(int64_t)u * kBFSWords + lane]) : 0u;
+                const uint32_t u = (uint32_t)__shfl_sync(0xffffffffu, myu, (k0 + k) & 31);
+                t[k] = (k0 + k < cnt) ? __ldcg(fl + (size_t)u * kBFSWords) : 0u;
             }
 #pragma unroll
             for (int k = 0; k < kBfsUnroll; ++k) acc |= t[k];
