@@ -830,6 +830,7 @@ def test_weighted_end_to_end(kind, alpha, omega):
 @pytest.mark.parametrize("name,world,omega,kw", [("C2", 2, 1.6, {}), ("C3", 3, 1.5, {}), ("C3", 2, 0.0, {}),
                                                  ("C3", 2, 1.5, {"dim": 3, "hop_bits": 16}),
                                                  ("wrgg", 2, 1.5, {"weight_exp": -1.0}),
+                                                 ("wrgg10k", 2, 1.5, {}),
                                                  ("C2", 3, 1.5, {"strategy": fdl.STRAT_PROB, "seed": 4}),
                                                  ("BA40k", 2, 1.5, {})])
 def test_loopback_ranks_bitwise(name, world, omega, kw):
@@ -843,6 +844,9 @@ def test_loopback_ranks_bitwise(name, world, omega, kw):
     lens = None
     if name == "wrgg":
         g, lens = graphs.random_geometric_graph_weighted(700, 6, 21)
+        cfg = configs.CONFIGS["C3"]
+    elif name == "wrgg10k":  # each rank's sources in one batch of 2 Bellman-Ford chunks
+        g, lens = graphs.random_geometric_graph_weighted(10000, 6, 23)
         cfg = configs.CONFIGS["C3"]
     elif name == "BA40k":  # C5's launch shape (n^2 >= 2^30: split line-6 pass, eager, 4-bit) over two ranks
         g = graphs.barabasi_albert(40000, 3, seed=5)
