@@ -90,6 +90,36 @@ for kern in ("p1", "p2"):
         out.append("| raw | top stall reasons (warps per issue) | " + ", ".join(
             f"{s.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', '')}={float(v):.2f}"
             for s, v in stalls) + " |")
+        for k in ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+                  "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum",
+                  "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+                  "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum"):
+            if k in hh:
+                j = hh.index(k)
+                out.append(f"| raw | {k} | {vals[j]} {units[j]} |")
+    # per-opcode executed instructions and shared-memory wavefronts (SASS source page)
+    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    sr = list(csv.reader(io.StringIO(src)))
+    hs = [i for i, r in enumerate(sr[:10]) if "Source" in r]
+    if hs:
+        h = sr[hs[0]]
+        ix = {k: j for j, k in enumerate(h)}
+        agg = collections.defaultdict(lambda: [0.0, 0.0])
+        for r in sr[hs[0] + 1:]:
+            if len(r) < len(h) or not r[ix["Source"]].strip():
+                continue
+            toks = r[ix["Source"]].split()
+            op = toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]
+            parts = op.split(".")
+            key = parts[0] + ("." + parts[1] if parts[0] in ("LDS", "STS", "MUFU") and len(parts) > 1 else "")
+            agg[key][0] += float(r[ix["Instructions Executed"]] or 0)
+            agg[key][1] += float(r[ix["L1 Wavefronts Shared"]] or 0)
+        tot = sum(v[0] for v in agg.values()) or 1.0
+        out.append("\nper opcode (warp instructions executed, shared-memory wavefronts):\n")
+        out.append("| opcode | instructions | share | shared wavefronts | wavefronts / instruction |\n|---|---|---|---|---|")
+        for k, v in sorted(agg.items(), key=lambda x: -x[1][0])[:16]:
+            out.append(f"| {k} | {v[0]:.3e} | {100 * v[0] / tot:.1f}% | {v[1]:.3e} | {v[1] / max(v[0], 1):.2f} |")
     out.append("")
 
 if traffic:  # per-launch DRAM bytes of the captured kernels (bench.py roofline.traffic)
