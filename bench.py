@@ -347,6 +347,7 @@ def run_gpu(args):
                         cg_rtol=cg_rtol,
                         cg_extrap=int(os.environ.get("FDL_CG_EXTRAP", "2")),
                         p1_split=int(os.environ.get("FDL_P1_SPLIT", "-1")),
+                        use_graphs=int(os.environ.get("FDL_USE_GRAPHS", "-1")),
                         strategy={"fixed": fdl.STRAT_FIXED, "prob": fdl.STRAT_PROB, "enum": fdl.STRAT_ENUM}[args.strategy])
     if world > 1 or force_dist:
         from paper_1711_01228_b200 import dist as fdist

@@ -536,7 +536,9 @@ __device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float
             aj[2] = fmaf(w, xi[2], aj[2]);
         }
     } else {
-        float w = __frcp_rn(h2);
+        // DIAG: w' = fp32(1/h^2) correctly rounded -- the table value at 4 bits (the
+        // P2 table), __frcp_rn(h^2) at 8/16 bits (sym_tile); the same number either way
+        float w = wlut;
         if (SAFE) w = valid ? w : 0.0f;
         ai[0] += w;
         aj[0] += w;
@@ -777,6 +779,7 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
                     hf = chunk_hop<HB>(ch, r, cc, magic);
                     h2 = hf * hf;
                     if (MODE == kSymP2) wl = rcp_approx(h2);
+                    if (MODE == kSymDiag) wl = __frcp_rn(h2);
                     if (MODE == kSymP1A) wl = HB == 1 ? lut[(int)hf] : rcp_approx(h2);  // as P2 at this width
                 }
                 bool valid = true;
@@ -887,9 +890,9 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
     lut[tid] = tid ? 1.0f / (float)(tid * tid) : 0.0f;  // w'_h = fp32(1/h^2), correctly rounded
     if (HB == 0) {  // entry of encoded byte tid: (row 2p, row 2p+1) -> h^2 (P1, DIAG) or w' (P2)
         const int lo = (int)nib_decode_lo((uint32_t)tid), hi = (int)nib_decode_hi((uint32_t)tid);
-        lut2[tid] = MODE == kSymP2 ? make_float2(lo ? 1.0f / (float)(lo * lo) : 0.0f,
-                                                 hi ? 1.0f / (float)(hi * hi) : 0.0f)
-                                   : make_float2((float)(lo * lo), (float)(hi * hi));
+        lut2[tid] = (MODE == kSymP2 || MODE == kSymDiag)
+                        ? make_float2(lo ? 1.0f / (float)(lo * lo) : 0.0f, hi ? 1.0f / (float)(hi * hi) : 0.0f)
+                        : make_float2((float)(lo * lo), (float)(hi * hi));
         if (MODE == kSymP1A)
             lutw2[tid] = make_float2(lo ? 1.0f / (float)(lo * lo) : 0.0f, hi ? 1.0f / (float)(hi * hi) : 0.0f);
         if (MODE == kSymP1S && FDL_P1S_SQRT)
