@@ -619,6 +619,8 @@ def run_gpu(args):
                        % (cfg.tol, restarts)),
             "pcg_iters_per_step": st.cg_iters / max(st.steps, 1),
             "sor_accept_rate": accepted / max(args.steps, 1), "p1_rejected_passes": st.p1_rejected,
+            # line-6 steps run as the two-set pass because a rejection was predicted (DESIGN R30)
+            "p1_predicted_twoset": {"passes": st.p1_predicted, "rejected": st.p1_predicted_rejected},
             "kernel_share": ({"p1": p1_share, "p2": p2_share, "other": max(0.0, 1 - p1_share - p2_share)}
                              if (st.p1_ms > 0 or st.p2_ms > 0) else None),
             "p1_tflops": p1_tf, "p2_hop_gbs": p2_gbs,

@@ -40,7 +40,8 @@
 extern "C" {
 #endif
 
-#define FDL_ABI_VERSION 2  /* 2: fdl_strategy ENUM = 1, PROB = 2; fdl_ctx_info setup breakdown */
+#define FDL_ABI_VERSION 3  /* 2: fdl_strategy ENUM = 1, PROB = 2; fdl_ctx_info setup breakdown;
+                              3: p1_split = 2 (predicted two-set steps), fdl_stats.p1_predicted* */
 
 typedef struct fdl_ctx fdl_ctx; /* opaque; owned by the library */
 
@@ -110,8 +111,11 @@ typedef struct {
     double enum_step;     /* FDL_STRAT_ENUM candidate spacing > 0 (default 0.5)                */
     int32_t p1_split;     /* line 6 pass over {X^{k+1}, Xt}: 1 = stresses of both + R(Xt) only, with a
                              1-set pass for R(X^{k+1}) when the guard rejects Xt (one host sync per
-                             step); 0 = stresses and R of both in one pass; -1 (default) = 1 when
-                             n^2 >= 2^30. Same results either way (bitwise)                       */
+                             step); 0 = stresses and R of both in one pass; 2 = 1, but a step whose
+                             guard is predicted to reject (the first step of a run, or the last
+                             step accepted Xt with f(X^{k+1}) - f(Xt) < 1/2 of f(X^k) - f(X^{k+1}))
+                             runs the two-set pass of 0 instead (DESIGN R30); -1 (default) = 2
+                             when n^2 >= 2^30, else 0. Same results either way (bitwise)           */
     int32_t use_graphs;   /* 1: each step is one CUDA-graph launch (the PCG loop a device-side WHILE
                              node), one host sync per step; 0: kernels launched eagerly with a host
                              sync per PCG iteration; -1 (default): 1 on one GPU when the split
@@ -181,6 +185,8 @@ typedef struct {
     uint64_t p1_rejected;     /* split P1 steps whose guard rejected Xt (extra 1-set pass) */
     uint64_t p1s_launches;    /* ... of the P1 launches: split line-6 passes (P1S)         */
     double p1s_ms;            /* ... and their CUDA-event time (included in p1_ms)       */
+    uint64_t p1_predicted;    /* p1_split = 2: two-set line-6 passes run on a predicted rejection */
+    uint64_t p1_predicted_rejected; /* ... of which the guard did reject Xt                */
 } fdl_stats;
 
 /* Fill *p with defaults: dim 2, k auto, omega 1.5, step +INF, tol 1e-4,

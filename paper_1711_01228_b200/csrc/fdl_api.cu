@@ -181,6 +181,9 @@ struct fdl_ctx {
     int nblk = 0;  // 256-row reduction blocks of the vector kernels
     int grid_p1[3] = {0, 0, 0}, grid_p2 = 0, grid_diag = 0, grid_enum = 0, grid_p1s = 0, grid_p1a = 0, grid_p1r = 0;
     bool p1_split = false;  // P1 over {X^{k+1}, Xt} computes R of Xt only (R(X^{k+1}) on rejection)
+    bool p1_predict = false;     // p1_split = 2: a step whose guard is predicted to reject runs the two-set pass
+    bool p1_fused_next = true;   // ... the prediction for the next step (the first step of a run: reject)
+    bool p1_fused_now = false;   // ... the current step runs the two-set pass
     cudaStream_t stream = nullptr, own_stream = nullptr;
     // device memory
     uint8_t* D = nullptr;
@@ -644,6 +647,7 @@ fdl_status eval_current(fdl_ctx* ctx)
     FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, ctx->stream));
     FDL_CUDA(cudaStreamSynchronize(ctx->stream));
     collect_events(ctx);
+    ctx->p1_fused_next = true;  // a new placement: its first relaxed step is predicted to be rejected (R30)
     ctx->f = ctx->sc_host->f_cur;
     if (!std::isfinite(ctx->f)) return set_err(ctx, FDL_E_NONFINITE, "stress is not finite");
     return FDL_OK;
@@ -1395,8 +1399,9 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
     }
     // large problems: the extra host sync of the split P1 is negligible against the pass
     ctx->use_graphs = ctx->p.use_graphs == 1 || (ctx->p.use_graphs < 0 && !ctx->distributed && (int64_t)n * n < (int64_t)1 << 30);
-    ctx->p1_split = !ctx->general &&
-                    (ctx->p.p1_split == 1 || (ctx->p.p1_split < 0 && (int64_t)n * n >= (int64_t)1 << 30));
+    ctx->p1_split = !ctx->general && (ctx->p.p1_split == 1 || ctx->p.p1_split == 2 ||
+                                      (ctx->p.p1_split < 0 && (int64_t)n * n >= (int64_t)1 << 30));
+    ctx->p1_predict = ctx->p1_split && ctx->p.p1_split != 1;
     // Jacobi diagonal sum_{j != i} w'_ij (one symmetric DIAG pass) and sigma = mean(diag)/n
     FDL_TRY(run_sym(ctx, kSymDiag, 1, ctx->posf, ctx->diag, nullptr, 0));
     FDL_LAUNCH(launch_set_sigma_rows(ctx->diag, ctx->n, ctx->sc, ctx->stream));
@@ -1558,7 +1563,7 @@ fdl_status enqueue_epilogue(fdl_ctx* ctx, const StepShape& sh)
             FDL_LAUNCH2(launch_rho(ctx->Xn, ctx->Xk, ctx->Xprev, ctx->Ak, ctx->Aprev, ctx->blk_cg, n, dim,
                                   ctx->ext_ok ? 1 : 0, ctx->sc, s));
         // ---- line 6: f(Xt), f(X^{k+1}) and the next right-hand side, one fused pass
-        if (nsets == 2 && ctx->p1_split) {
+        if (nsets == 2 && ctx->p1_split && !ctx->p1_fused_now) {
             // stress of both candidates + R(Xt); R(X^{k+1}) only if the guard rejects Xt
             FDL_TRY(run_sym(ctx, kSymP1S, 2, ctx->posf, ctx->R2, nullptr, 0));
             FDL_CUDA(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, s));
@@ -1736,6 +1741,9 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
     // per-vertex omega: Xt is not a scalar combination, At cannot be carried
     const bool refresh = !ctx->a_valid || ctx->a_age + 1 >= ctx->p.a_refresh || ctx->omega_v;
     const StepShape sh{refresh, enumerate, nsets, omega};
+    // p1_split = 2 (R30): the two-set line-6 pass when a rejection is predicted (the same
+    // results as the split pass plus the rejection pass, bitwise; R25)
+    ctx->p1_fused_now = ctx->p1_predict && nsets == 2 && !enumerate && ctx->p1_fused_next;
     int cg = 0;
     // graph mode: one launch per step; not with a host decision inside the step
     // (split line 6, enumeration) or host-side exchanges (several ranks)
@@ -1810,6 +1818,15 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
         f_rel = h.enum_fbest;
         f_after = h.f_set[0];
     }
+    if (ctx->p1_fused_now) {
+        ctx->stats.p1_predicted++;
+        if (!accepted) ctx->stats.p1_predicted_rejected++;
+    }
+    // R30: predict the next guard decision from this one -- after an accepted Xt whose
+    // extra decrease f(X^{k+1}) - f(Xt) fell below half of the solve's own decrease
+    // f(X^k) - f(X^{k+1}), the relaxation is running out and the next Xt tends to overshoot
+    if (ctx->p1_predict && nsets == 2 && !enumerate)
+        ctx->p1_fused_next = accepted && (f_next - f_rel) < 0.5 * (f_before - f_next);
     ctx->iterations++;
     ctx->f = f_after;
     fdl_iter_info inf{};

@@ -73,6 +73,12 @@ constexpr int kBfsUnroll = FDL_BFS_UNROLL;
 #ifndef FDL_P1S_SQRT
 #define FDL_P1S_SQRT 0  // 1: P1S stress of X^{k+1} by MUFU.SQRT and 1/h (experiment)
 #endif
+#ifndef FDL_P1R_SCALAR
+#define FDL_P1R_SCALAR 0  // 1: the 2-D one-set R updates (P1R, 1-set P1) as scalar FFMAs instead of FFMA2
+#endif
+#ifndef FDL_P1S_PACKR
+#define FDL_P1S_PACKR 0  // 1: the line-6 pass's R updates of set 1 as FFMA2 on (x, y) instead of 4 FFMA
+#endif
 #ifndef FDL_MAXST
 #define FDL_MAXST 4  // deepest TMA ring of the pair passes
 #endif
@@ -365,12 +371,27 @@ __device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float
             q0 = valid ? q0 : 0.0f;
             q1 = valid ? q1 : 0.0f;
         }
+        if (FDL_P1S_PACKR && DIM == 2) {
+            // R of set 1 as two FFMA2 on (x, y) with q1 broadcast (same fma per element)
+            float dx0, dx1, dy0, dy1;
+            upk(d[0], dx0, dx1);
+            upk(d[1], dy0, dy1);
+            const u64 d1 = pk(dx1, dy1), qq = pk(q1, q1);
+            float lo, hi;
+            upk(ffma2(qq, d1, pk(ai[0], ai[1])), lo, hi);
+            ai[0] = lo;
+            ai[1] = hi;
+            upk(ffma2(qq, d1, pk(aj[0], aj[1])), lo, hi);
+            aj[0] = lo;
+            aj[1] = hi;
+        } else {
 #pragma unroll
-        for (int c = 0; c < DIM; ++c) {
-            float dlo, dhi;
-            upk(d[c], dlo, dhi);
-            ai[c] = fmaf(q1, dhi, ai[c]);
-            aj[c] = fmaf(q1, dhi, aj[c]);
+            for (int c = 0; c < DIM; ++c) {
+                float dlo, dhi;
+                upk(d[c], dlo, dhi);
+                ai[c] = fmaf(q1, dhi, ai[c]);
+                aj[c] = fmaf(q1, dhi, aj[c]);
+            }
         }
         float u0, u1;
         upk(ffma2(r2, pk(q0, q1), pk(-1.0f, -1.0f)), u0, u1);
@@ -432,14 +453,22 @@ __device__ __forceinline__ void sym_pair(const float* xi, const float* xj, float
             q = valid ? q : 0.0f;
             u = valid ? u : 0.0f;
         }
-        const u64 qq = pk(q, q);
-        float lo, hi;
-        upk(ffma2(qq, d, pk(ai[0], ai[1])), lo, hi);
-        ai[0] = lo;
-        ai[1] = hi;
-        upk(ffma2(qq, d, pk(aj[0], aj[1])), lo, hi);
-        aj[0] = lo;
-        aj[1] = hi;
+        if (FDL_P1R_SCALAR) {
+            // four scalar FFMAs (the same IEEE fma per element as the packed pair)
+            ai[0] = fmaf(q, dx, ai[0]);
+            ai[1] = fmaf(q, dy, ai[1]);
+            aj[0] = fmaf(q, dx, aj[0]);
+            aj[1] = fmaf(q, dy, aj[1]);
+        } else {
+            const u64 qq = pk(q, q);
+            float lo, hi;
+            upk(ffma2(qq, d, pk(ai[0], ai[1])), lo, hi);
+            ai[0] = lo;
+            ai[1] = hi;
+            upk(ffma2(qq, d, pk(aj[0], aj[1])), lo, hi);
+            aj[0] = lo;
+            aj[1] = hi;
+        }
         if (MODE == kSymP1) s[0] = fmaf(u, u, s[0]);
     } else if (MODE == kSymP1 || MODE == kSymP1R) {
         float d[DIM];

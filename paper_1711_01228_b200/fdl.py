@@ -91,6 +91,7 @@ class Stats(ctypes.Structure):
         ("p1_ms", ctypes.c_double), ("p2_ms", ctypes.c_double), ("other_ms", ctypes.c_double),
         ("steps", ctypes.c_uint64), ("cg_iters", ctypes.c_uint64), ("p1_pairs_nor", ctypes.c_uint64),
         ("p1_rejected", ctypes.c_uint64), ("p1s_launches", ctypes.c_uint64), ("p1s_ms", ctypes.c_double),
+        ("p1_predicted", ctypes.c_uint64), ("p1_predicted_rejected", ctypes.c_uint64),
     ]
 
     def as_dict(self):

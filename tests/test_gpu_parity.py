@@ -493,12 +493,16 @@ def test_hop_width_invariance(name, dim):
             got = L.info.hop_bits
             assert got == max(bits, 4 if L.info.diameter <= 15 else (8 if L.info.diameter <= 255 else 16))
             R, A, f = L.eval_forces()
+            diag = L.get_diag()
             info = L.step()
-            out[got] = (R, A, f, L.get_positions(), info.f_after)
+            out[got] = (R, A, f, L.get_positions(), info.f_after, diag)
     widths = sorted(out)
-    R0, A0, f0, X1, fa = out[widths[-1]]
+    # the Jacobi diagonal sum_j fp32(1/h^2): the 4-bit table value and __frcp_rn(h^2)
+    # at 8/16 bits are the same correctly rounded number, summed in the same order
+    assert all(np.array_equal(out[w][5], out[widths[0]][5]) for w in widths)
+    R0, A0, f0, X1, fa, _ = out[widths[-1]]
     for w in widths:
-        R, A, f, X, fw = out[w]
+        R, A, f, X, fw, _ = out[w]
         assert np.array_equal(R, R0) and f == f0
         assert relL2(A, A0) <= 1e-6
     if 4 in out and 8 in out:
@@ -681,12 +685,13 @@ def test_split_p1_bitwise(name):
     """The split line-6 pass (stresses of both candidates, R of Xt only, and a
     R-only 1-set pass for R(X^{k+1}) when the guard rejects) gives bitwise the same
     trajectory as the fused two-set pass (same per-pair fp32 arithmetic and
-    the same fixed summation orders)."""
+    the same fixed summation orders), and so does the split pass with predicted
+    two-set steps (p1_split = 2, DESIGN R30)."""
     cfg = configs.CONFIGS[name]
     g = configs.graph_for(name)
     X0 = configs.positions_for(name, g.n, 1)
     out = []
-    for split in (0, 1):
+    for split in (0, 1, 2):
         p = fdl.make_params(dim=2, k=cfg.k_for(g.n), omega=1.9, tol=cfg.tol, max_iter=60, p1_split=split)
         with fdl.Layout.from_graph(g, params=p, init_pos=X0) as L:
             fs = []
@@ -695,11 +700,18 @@ def test_split_p1_bitwise(name):
                 fs.append((info.f_next, info.f_relaxed, info.accepted))
                 if info.stop:
                     break
-            out.append((fs, L.get_positions(), L.get_stats().p1_rejected))
-    assert out[0][0] == out[1][0]
-    assert np.array_equal(out[0][1], out[1][1])
-    assert out[1][2] == sum(1 for a in out[1][0] if not a[2])
-    assert out[1][2] > 0  # the R-only rejection pass (kSymP1R) ran
+            out.append((fs, L.get_positions(), L.get_stats()))
+    for o in out[1:]:
+        assert o[0] == out[0][0]
+        assert np.array_equal(o[1], out[0][1])
+    rejected = sum(1 for a in out[0][0] if not a[2])
+    assert out[1][2].p1_rejected == rejected > 0  # the R-only rejection pass (kSymP1R) ran
+    # p1_split = 2 (R30): predicted steps ran the two-set pass, the others the split pass
+    # with the R-only pass on a rejection; every step is one or the other
+    st = out[2][2]
+    assert st.p1_predicted >= 1 and st.p1_predicted_rejected >= 1  # the first step is predicted
+    assert st.p1_rejected + st.p1_predicted_rejected == rejected
+    assert st.p1s_launches + st.p1_predicted == len(out[0][0])
 
 
 # --------------------------------------------- NEXT-3: weighted graphs, general alpha

@@ -30,7 +30,7 @@ def test_exports_every_declared_symbol():
 
 
 def test_abi_version_and_defaults():
-    assert fdl.lib.fdl_abi_version() == 2
+    assert fdl.lib.fdl_abi_version() == 3
     p = fdl.params_default()
     assert p.struct_size == 88 or p.struct_size == __import__("ctypes").sizeof(fdl.Params)
     assert p.dim == 2 and p.omega == 1.5 and math.isinf(p.step) and p.tol == 1e-4
