@@ -113,7 +113,7 @@ typedef struct {
                              1-set pass for R(X^{k+1}) when the guard rejects Xt (one host sync per
                              step); 0 = stresses and R of both in one pass; 2 = 1, but a step whose
                              guard is predicted to reject (the first step of a run, or the last
-                             step accepted Xt with f(X^{k+1}) - f(Xt) < 1/2 of f(X^k) - f(X^{k+1}))
+                             step accepted Xt with f(X^{k+1}) - f(Xt) < 0.6 (f(X^k) - f(X^{k+1})))
                              runs the two-set pass of 0 instead (DESIGN R30); -1 (default) = 2
                              when n^2 >= 2^30, else 0. Same results either way (bitwise)           */
     int32_t use_graphs;   /* 1: each step is one CUDA-graph launch (the PCG loop a device-side WHILE

@@ -1823,10 +1823,10 @@ fdl_status step_impl(fdl_ctx* ctx, fdl_iter_info* info)
         if (!accepted) ctx->stats.p1_predicted_rejected++;
     }
     // R30: predict the next guard decision from this one -- after an accepted Xt whose
-    // extra decrease f(X^{k+1}) - f(Xt) fell below half of the solve's own decrease
+    // extra decrease f(X^{k+1}) - f(Xt) fell below 0.6 of the solve's own decrease
     // f(X^k) - f(X^{k+1}), the relaxation is running out and the next Xt tends to overshoot
     if (ctx->p1_predict && nsets == 2 && !enumerate)
-        ctx->p1_fused_next = accepted && (f_next - f_rel) < 0.5 * (f_before - f_next);
+        ctx->p1_fused_next = accepted && (f_next - f_rel) < 0.6 * (f_before - f_next);
     ctx->iterations++;
     ctx->f = f_after;
     fdl_iter_info inf{};
