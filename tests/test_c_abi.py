@@ -27,7 +27,7 @@ def test_c_program_validation_errors(exe):
     r = subprocess.run([exe, "--check-errors"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "disconnected: FDL_E_DISCONNECTED, ctx NULL" in r.stdout
-    assert "self loop: FDL_E_SELF_LOOP" in r.stdout and "abi 2 ok" in r.stdout
+    assert "self loop: FDL_E_SELF_LOOP" in r.stdout and "abi 3 ok" in r.stdout
 
 
 @pytest.mark.gpu
