@@ -273,9 +273,14 @@ __global__ void __launch_bounds__(kRB) k_select(double* Xk, double* Rk, const do
             if (Ak) Ak[i] = accept ? At[i] : An[i];
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        // max of the block maxima by warp 0 (fmax is exact, so any order gives the same value;
+        // one thread walking C5's 782 maxima took ~30 us)
         double m = 0.0;
-        for (int b = 0; b < nblk_loc; ++b) m = fmax(m, blk_max[b]);
+        for (int b = threadIdx.x; b < nblk_loc; b += 32) m = fmax(m, blk_max[b]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (threadIdx.x != 0) return;
         sc->maxdisp = sqrt(m);
         sc->f_next = f0;
         sc->f_relaxed = nsets == 2 ? f1 : NAN;
@@ -492,7 +497,13 @@ __global__ void __launch_bounds__(256) k_gal_solve(const double* __restrict__ bl
     const int cnt = sc->gal_cnt;
     for (int e = threadIdx.x; e < dim * kGalNV && cnt > 0; e += blockDim.x) {
         double t = 0.0;
-        for (int q = 0; q < nblk; ++q) t += blk[(size_t)e * nblk + q];
+        for (int q0 = 0; q0 < nblk; q0 += 8) {  // in order; 8 loads in flight (+0.0 padding is exact)
+            double v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = q0 + k < nblk ? __ldg(blk + (size_t)e * nblk + q0 + k) : 0.0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) t += v[k];
+        }
         tot[e] = t;
     }
     __syncthreads();
@@ -859,18 +870,43 @@ __device__ __forceinline__ void cg_finalize_warp(const double* __restrict__ blk,
                                                  cudaGraphConditionalHandle cond, int use_cond, int cg_max)
 {
     const int lane = threadIdx.x & 31;
+    // per (quantity, column): the lane's partials b = lane, lane + 32, ... summed in that
+    // order, then a butterfly.  The loads of a chunk of 4 x 32 partials of every array are
+    // staged in registers before the adds, so they are in flight together (a dependent L2
+    // round trip per partial made this ~15 us at C5's 782 blocks); the +0.0 padding past
+    // nblk leaves the sums bitwise unchanged (they start at +0.0 and never become -0.0)
+    const bool use[4] = {true, mode != 1, mode == 0, mode != 1};
     double sums[4][3];
-    for (int qq = 0; qq < 4; ++qq)
-        for (int c = 0; c < dim; ++c) {
-            sums[qq][c] = 0.0;
-            if (mode == 1 && qq > 0) continue;
-            if (mode == 2 && qq == 2) continue;
-            const double* src = blk + (size_t)(qq * 4 + c) * nblk;
-            double v = 0.0;
-            for (int b = lane; b < nblk; b += 32) v += src[b];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            sums[qq][c] = v;
+    for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) sums[qq][c] = 0.0;
+    for (int b0 = lane; b0 < nblk; b0 += 4 * 32) {
+        double v[4][3][4];
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int bb = b0 + 32 * k;
+                    v[qq][c][k] = (use[qq] && c < dim && bb < nblk) ? __ldg(blk + (size_t)(qq * 4 + c) * nblk + bb) : 0.0;
+                }
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) sums[qq][c] += v[qq][c][k];
+    }
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            double t = sums[qq][c];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            sums[qq][c] = t;
         }
     if (lane != 0) return;
     const double rt2 = rtol * rtol;
