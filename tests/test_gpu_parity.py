@@ -680,19 +680,24 @@ def test_enumerating_strategy_end_to_end(name):
     assert all(b <= a * (1 + 1e-9) for a, b in zip([L.info.f] + fs, fs))
 
 
-@pytest.mark.parametrize("name", ["C2", "C3"])
+@pytest.mark.parametrize("name", ["C2", "C3", "rgg3"])
 def test_split_p1_bitwise(name):
     """The split line-6 pass (stresses of both candidates, R of Xt only, and a
     R-only 1-set pass for R(X^{k+1}) when the guard rejects) gives bitwise the same
     trajectory as the fused two-set pass (same per-pair fp32 arithmetic and
     the same fixed summation orders), and so does the split pass with predicted
     two-set steps (p1_split = 2, DESIGN R30)."""
-    cfg = configs.CONFIGS[name]
-    g = configs.graph_for(name)
-    X0 = configs.positions_for(name, g.n, 1)
+    if name == "rgg3":  # 3-D: the split and two-set passes of DIM = 3 (C4's line-6 kernels)
+        cfg = configs.CONFIGS["C4"]
+        g, dim = graphs.random_geometric_graph(2500, 6.0, seed=44), 3
+        X0 = graphs.init_positions(g.n, 3, 45)
+    else:
+        cfg = configs.CONFIGS[name]
+        g, dim = configs.graph_for(name), 2
+        X0 = configs.positions_for(name, g.n, 1)
     out = []
     for split in (0, 1, 2):
-        p = fdl.make_params(dim=2, k=cfg.k_for(g.n), omega=1.9, tol=cfg.tol, max_iter=60, p1_split=split)
+        p = fdl.make_params(dim=dim, k=cfg.k_for(g.n), omega=1.9, tol=cfg.tol, max_iter=60, p1_split=split)
         with fdl.Layout.from_graph(g, params=p, init_pos=X0) as L:
             fs = []
             for _ in range(40):
@@ -712,6 +717,26 @@ def test_split_p1_bitwise(name):
     assert st.p1_predicted >= 1 and st.p1_predicted_rejected >= 1  # the first step is predicted
     assert st.p1_rejected + st.p1_predicted_rejected == rejected
     assert st.p1s_launches + st.p1_predicted == len(out[0][0])
+
+
+def test_predicted_twoset_default_at_c5_shape():
+    """At C5's launch shape (BA-40k, n^2 >= 2^30) the default line-6 schedule is the
+    split pass with predicted two-set steps (p1_split = 2, DESIGN R30): both passes run
+    in a short run, and the trajectory is bitwise that of the plain split pass."""
+    d = _trace_files("BA40k")[0]
+    g = _golden_graph(d)
+    X0 = graphs.init_positions(g.n, d["dim"], d["position_seed"])
+    out = []
+    for split in (-1, 1):
+        p = fdl.make_params(dim=d["dim"], k=d["k"], omega=d["omega"], tol=d["tol"], max_iter=d["max_iter"],
+                            p1_split=split)
+        with fdl.Layout.from_graph(g, params=p, init_pos=X0) as L:
+            infos = [L.step() for _ in range(6)]
+            out.append(([(i.f_next, i.f_relaxed, i.accepted) for i in infos], L.get_positions(), L.get_stats()))
+    assert out[0][0] == out[1][0] and np.array_equal(out[0][1], out[1][1])
+    st = out[0][2]
+    assert st.p1_predicted >= 1 and st.p1s_launches >= 1 and st.p1s_launches + st.p1_predicted == 6
+    assert out[1][2].p1_predicted == 0
 
 
 # --------------------------------------------- NEXT-3: weighted graphs, general alpha
