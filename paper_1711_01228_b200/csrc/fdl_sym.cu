@@ -63,6 +63,9 @@ constexpr int kBfsUnroll = FDL_BFS_UNROLL;
 #ifndef FDL_P2_SHFLRED
 #define FDL_P2_SHFLRED 0  // 1: 4-bit 2-D P2 j-side column sums by a warp butterfly (measured slower)
 #endif
+#ifndef FDL_P2_PBFLY
+#define FDL_P2_PBFLY 0  // 1: 4-bit 2-D P2 j-side column sums by a progressive warp butterfly (no j-side buffer)
+#endif
 #ifndef FDL_P2_MUFU_COLS
 // 4-bit P2: bit cc set -> column cc of each 16-byte chunk (4 columns per chunk) takes
 // its weights from the MUFU (rcp.approx(h^2), bitwise the table's fp32(1/h^2) for
@@ -225,6 +228,17 @@ __host__ __device__ constexpr bool sym_shflred()
 
 // floats per lane row of a warp's j-side buffer: 9C keeps the 16 rows of a
 // half-warp on distinct banks for the C-wide vector stores
+// ... the same butterfly done column by column inside the tile (sym_tile): after
+// each column the pair of rows (ty, ty^1) is combined, after each column pair
+// the rows (ty, ty^2), and so on, so at most ~3 partial values are live per
+// lane (the end-of-tile butterfly holds 16 and needs 2 CTAs/SM); no j-side
+// shared-memory buffer, so the TMA ring gets its space
+template <int MODE, int DIM, int NSETS, int HB>
+__host__ __device__ constexpr bool sym_pbfly()
+{
+    return FDL_P2_PBFLY && !FDL_P2_SHFLRED && MODE == kSymP2 && DIM == 2 && NSETS == 1 && HB == 0;
+}
+
 template <int MODE, int DIM, int NSETS>
 __host__ __device__ constexpr int sym_jpitch()
 {
@@ -252,10 +266,16 @@ __host__ __device__ constexpr int sym_ctas_per_sm()
 // reduction buffers allows at sym_ctas_per_sm CTAs per SM (228 KB per SM,
 // ~1 KB per CTA reserved, ~4 KB static).
 template <int MODE, int DIM, int NSETS, int HB>
+__host__ __device__ constexpr size_t sym_red_floats_hb()  // j-side warp buffers of this pass (none with sym_pbfly)
+{
+    return sym_pbfly<MODE, DIM, NSETS, HB>() ? 0 : sym_red_floats<MODE, DIM, NSETS>();
+}
+
+template <int MODE, int DIM, int NSETS, int HB>
 __host__ __device__ constexpr int sym_stages()
 {
     constexpr int budget = 228 * 1024 / sym_ctas_per_sm<MODE, DIM>() - 5 * 1024 -
-                           (int)sym_red_floats<MODE, DIM, NSETS>() * 4;
+                           (int)sym_red_floats_hb<MODE, DIM, NSETS, HB>() * 4;
     constexpr int st = budget / (sym_tps<MODE, HB>() * sym_stage_bytes<MODE, DIM, NSETS, HB>());
     return st < 2 ? 2 : (st > FDL_MAXST ? FDL_MAXST : st);
 }
@@ -264,7 +284,7 @@ template <int MODE, int DIM, int NSETS, int HB>
 __host__ __device__ constexpr size_t sym_smem_bytes()
 {
     return (size_t)sym_stages<MODE, DIM, NSETS, HB>() * sym_tps<MODE, HB>() * sym_stage_bytes<MODE, DIM, NSETS, HB>() +
-           sym_red_floats<MODE, DIM, NSETS>() * 4;
+           sym_red_floats_hb<MODE, DIM, NSETS, HB>() * 4;
 }
 
 // ------------------------------------------------------------ packed FP32x2
@@ -638,6 +658,7 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
 {
     constexpr int C = sym_ncomp<MODE, DIM, NSETS>();
     constexpr bool BFLY = sym_shflred<MODE, DIM, NSETS, HB>();
+    constexpr bool PBFLY = sym_pbfly<MODE, DIM, NSETS, HB>();
     constexpr int PS = sym_ps<MODE, DIM, NSETS>();
     constexpr int NCH = HB ? 4 * HB : 2;  // 16-byte chunks per thread
     constexpr int CPC = HB ? 2 / HB : 4;  // columns per chunk
@@ -678,6 +699,8 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
         // j-side sum of a column is split over even/odd rows (two 4-long FFMA
         // chains instead of one 8-long chain).
         uint4 chs[NCH];
+        float pv1[8], pv2[4], pv3[2];  // progressive butterfly partials (PBFLY)
+        const bool b0 = ty & 1, b1 = ty & 2, b2 = ty & 4, b3 = ty & 8;
         const float wtab = MODE == kSymP2 ? lut[threadIdx.x & 15]  // w'_h for h = lane & 15 (w'_0 = 0)
                                           : (float)((threadIdx.x & 15) * (threadIdx.x & 15));  // h^2 (shuffle experiments)
 #pragma unroll
@@ -763,12 +786,31 @@ __device__ __forceinline__ void sym_tile(const uint8_t* sD, const float* sP, con
                         sym_pair<MODE, DIM, NSETS, SAFE>(&xi[r][0], xj, v, vw, valid, &ai[r][0], &aj[hh][0], &sf[hh][0]);
                     }
                 }
+                if constexpr (PBFLY) {
+                    // rows (ty, ty^1) of column c: the lane keeps component b0; then column
+                    // pairs with lane ty^2 (keeps column 2m + b1), column quads with ty^4,
+                    // the two halves with ty^8: the pairs added are those of
+                    // sym_flush_warp's tree, so the sums are bitwise the same, and lane ty
+                    // ends with output (column 4 b3 + 2 b2 + b1, component b0) = e = ty
+                    const float s0 = aj[0][0] + aj[1][0], s1 = aj[0][1] + aj[1][1];
+                    pv1[c] = (b0 ? s1 : s0) + __shfl_xor_sync(0xffffffffu, b0 ? s0 : s1, 1);
+                    if (c & 1) {
+                        const float lo = pv1[c - 1], hi = pv1[c];
+                        pv2[c >> 1] = (b1 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b1 ? lo : hi, 2);
+                    }
+                    if ((c & 3) == 3) {
+                        const float lo = pv2[(c >> 1) - 1], hi = pv2[c >> 1];
+                        pv3[c >> 2] = (b2 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b2 ? lo : hi, 4);
+                    }
+                    if (c == 7) jv[0] = (b3 ? pv3[1] : pv3[0]) + __shfl_xor_sync(0xffffffffu, b3 ? pv3[0] : pv3[1], 8);
+                } else {
 #pragma unroll
-                for (int v = 0; v < C; ++v) {
-                    if (BFLY)
-                        jv[c * C + v] = aj[0][v] + aj[1][v];
-                    else
-                        myred[c * C + v] = aj[0][v] + aj[1][v];
+                    for (int v = 0; v < C; ++v) {
+                        if (BFLY)
+                            jv[c * C + v] = aj[0][v] + aj[1][v];
+                        else
+                            myred[c * C + v] = aj[0][v] + aj[1][v];
+                    }
                 }
             }
         }
@@ -1020,6 +1062,8 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
             FDL_DCHECK((int64_t)it.w + t < a.ntiles);
             if constexpr (sym_shflred<MODE, DIM, NSETS, HB>())
                 sym_bfly_warp<MODE, DIM, NSETS>(jv, a.jpart + ((size_t)it.w + t) * kT * C + wid * 16 * C, lane);
+            else if constexpr (sym_pbfly<MODE, DIM, NSETS, HB>())
+                a.jpart[((size_t)it.w + t) * kT * C + wid * 16 * C + lane] = jv[0];  // P2: symmetric, no sign
             else
                 sym_flush_warp<MODE, DIM, NSETS>(wbuf, a.jpart + ((size_t)it.w + t) * kT * C + wid * 16 * C, lane);
             if (last && ++stage == NST) {
@@ -1152,6 +1196,8 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, 2>()) k_tile_mix(co
                                            jv);
         if constexpr (sym_shflred<MODE, 2, NSETS, 0>())
             sym_bfly_warp<MODE, 2, NSETS>(jv, red + wid * 2 * (16 * JP + 16), lane);  // the pass stores one float per lane
+        else if constexpr (sym_pbfly<MODE, 2, NSETS, 0>())
+            red[wid * 2 * (16 * JP + 16) + lane] = jv[0];
         s64 += (double)sf[0][0] + (double)sf[1][NSETS - 1];
         __syncwarp();
     }
