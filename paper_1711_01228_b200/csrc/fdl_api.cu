@@ -188,6 +188,8 @@ struct fdl_ctx {
     // device memory
     uint8_t* D = nullptr;
     int4* items = nullptr;
+    // per grid size: slot -> item schedule of the pair passes (item_order)
+    std::vector<std::pair<int, int*>> item_orders;
     int *it_lo = nullptr, *it_hi = nullptr;
     float* jpart = nullptr;
     float* ipart = nullptr;
@@ -463,6 +465,63 @@ void collect_events(fdl_ctx* ctx)
     ctx->ev_marks.clear();
 }
 
+// Schedule of the pair passes' work items over `grid` CTAs (CTA b takes slots b, b + grid,
+// ...): items sorted by tile count, longest first, dealt to the CTAs in snake order (round r
+// left to right when r is even, right to left when odd).  Work items are strip segments of
+// up to kSeg tiles and each row ends in a shorter one, so plain round-robin over triangle
+// order leaves per-CTA work uneven (C5: the busiest CTA has 2.3% more tiles than the mean,
+// the pass waits for it); the snake deal is within 0.05%.  Outputs are indexed by item and
+// tile, so the schedule does not change any sum.  FDL_ITEM_ORDER=rr: plain round-robin.
+static std::vector<int> snake_order(const std::vector<int4>& items, int grid)
+{
+    const int m = (int)items.size();
+    std::vector<int> order(std::max(m, 1), 0);
+    static const bool rr = [] {
+        const char* e = getenv("FDL_ITEM_ORDER");
+        return e && std::string(e) == "rr";
+    }();
+    if (rr || grid <= 1) {
+        for (int i = 0; i < m; ++i) order[i] = i;
+        return order;
+    }
+    std::vector<int> srt(m);
+    for (int i = 0; i < m; ++i) srt[i] = i;
+    std::stable_sort(srt.begin(), srt.end(), [&](int a, int b) { return items[a].z > items[b].z; });
+    for (int s = 0; s < m; ++s) {
+        const int r = s / grid, c = s % grid;
+        const int cnt = std::min(grid, m - r * grid);  // items in this round
+        const int b = (r & 1) ? cnt - 1 - c : c;
+        order[r * grid + b] = srt[s];
+    }
+    return order;
+}
+
+static fdl_status build_item_orders(fdl_ctx* ctx, const std::vector<int4>& items)
+{
+    const int grids[] = {ctx->grid_p1[1], ctx->grid_p1[2], ctx->grid_p2, ctx->grid_diag,
+                         ctx->grid_enum,  ctx->grid_p1s,   ctx->grid_p1a, ctx->grid_p1r};
+    for (int g : grids) {
+        if (g <= 0) continue;
+        bool have = false;
+        for (auto& e : ctx->item_orders) have = have || e.first == g;
+        if (have) continue;
+        const std::vector<int> o = snake_order(items, g);
+        int* d = nullptr;
+        FDL_ALLOC(d, o.size());
+        FDL_CUDA(cudaMemcpyAsync(d, o.data(), sizeof(int) * o.size(), cudaMemcpyHostToDevice, ctx->stream));
+        FDL_CUDA(cudaStreamSynchronize(ctx->stream));  // `o` is a host temporary
+        ctx->item_orders.emplace_back(g, d);
+    }
+    return FDL_OK;
+}
+
+static const int* item_order(const fdl_ctx* ctx, int grid)
+{
+    for (auto& e : ctx->item_orders)
+        if (e.first == grid) return e.second;
+    return nullptr;
+}
+
 // Multi-GPU: all-gather the rank slices (slice_elems each, rank slice at
 // rank * slice_elems) of `buf` in place.
 fdl_status allgather_inplace(fdl_ctx* ctx, void* buf, size_t slice_elems, int nccl_type, size_t esize)
@@ -573,6 +632,8 @@ fdl_status run_sym(fdl_ctx* ctx, int mode, int nsets, const float* pos, double* 
                      : mode == kSymP1A ? ctx->grid_p1a
                      : mode == kSymP1R ? ctx->grid_p1r
                      : (mode == kSymP1 ? ctx->grid_p1[nsets] : (mode == kSymP2 ? ctx->grid_p2 : ctx->grid_diag));
+    a.order = item_order(ctx, grid);
+    if (ctx->nitems > 0 && !a.order) return set_err(ctx, FDL_E_STATE, "no work-item schedule for the grid");
     const int mk = mark_begin(ctx, mode == kSymP1S ? 4 : ((p1 || mode == kSymP1R) ? 1 : (mode == kSymP2 ? 2 : 3)));
     if (ctx->nitems > 0) FDL_LAUNCH(launch_sym(a, mode, dim, nsets, ctx->hb, grid, ctx->stream));
     mark_end(ctx, mk);
@@ -1397,6 +1458,7 @@ fdl_status create_impl(int32_t n, const int64_t* rp, const int32_t* col, const d
         ctx->grid_p1a = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymP1A, dim, 1, ctx->hb)));
         ctx->grid_p1r = std::max(1, std::min(cap_items, ctx->sm_count * sym_max_ctas(kSymP1R, dim, 1, ctx->hb)));
     }
+    FDL_TRY(build_item_orders(ctx, items));
     // large problems: the extra host sync of the split P1 is negligible against the pass
     ctx->use_graphs = ctx->p.use_graphs == 1 || (ctx->p.use_graphs < 0 && !ctx->distributed && (int64_t)n * n < (int64_t)1 << 30);
     ctx->p1_split = !ctx->general && (ctx->p.p1_split == 1 || ctx->p.p1_split == 2 ||
@@ -1541,11 +1603,13 @@ fdl_status enqueue_epilogue(fdl_ctx* ctx, const StepShape& sh)
             a.ipart = nullptr;
             a.spart = ctx->spart_enum;
             a.items = ctx->items;
+            a.order = item_order(ctx, ctx->grid_enum);
             a.nitems = ctx->nitems;
             a.n = ctx->n;
             a.ntiles = ctx->t1 - ctx->t0;
             a.nstage = ctx->npad;
             a.magic = 0x4B000000u;
+            if (ctx->nitems > 0 && !a.order) return set_err(ctx, FDL_E_STATE, "no work-item schedule for the grid");
             if (ctx->nitems > 0) FDL_LAUNCH(launch_enum(a, w, dim, ctx->hb, ctx->grid_enum, s));
             FDL_LAUNCH2(launch_sym_stress(ctx->spart_enum, ctx->nitems, kEnumNC, ctx->enum_f + c0, ctx->stress_scratch, s));
         }

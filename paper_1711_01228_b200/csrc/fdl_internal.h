@@ -220,6 +220,7 @@ struct SymArgs {
     float* ipart;          // [item][warp][kT][C] fp32 i-side partials
     double* spart;         // [item][warp][nsets] fp64 stress partials (P1); k_enum: [item][kEnumNC]
     const int4* items;     // {I, J0, ntiles, first local tile}
+    const int* order;      // schedule: CTA b takes items order[b], order[b + grid], ... (item_order)
     int nitems;
     int n;
     uint32_t magic;        // 0x4B000000 (2^23 as fp32 bits) for the hop decode, passed as a

@@ -987,7 +987,7 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
     auto issue = [&](int stage) {
         int p_item = prod[0], p_t = prod[1];
         if (p_item >= a.nitems) return;
-        const int4 it = a.items[p_item];  // {I, J0, ntiles, first local tile}
+        const int4 it = a.items[a.order[p_item]];  // {I, J0, ntiles, first local tile}
         const int cnt = min(TPS, it.z - p_t);  // tiles of this item in the stage
         fence_proxy_async();
         mbar_arrive_expect_tx(&full[stage], cnt * STAGE);
@@ -1023,7 +1023,8 @@ __global__ void __launch_bounds__(256, sym_ctas_per_sm<MODE, DIM>()) k_sym(const
     const float* wbuf = red + wid * 2 * (16 * JP + 16);
     int stage = 0;
     uint32_t phase = 0;
-    for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
+    for (int slot = blockIdx.x; slot < a.nitems; slot += gridDim.x) {
+        const int item = a.order[slot];  // outputs are indexed by item: any schedule gives the same sums
         const int4 it = a.items[item];
         const int I = it.x;
         FDL_DCHECK(it.z >= 1 && it.w >= 0 && (int64_t)it.w + it.z <= a.ntiles && I <= it.y &&
@@ -1359,7 +1360,7 @@ __global__ void __launch_bounds__(256, 2) k_enum(const SymArgs a, const EnumOmeg
     auto issue = [&](int stage) {
         int p_item = prod[0], p_t = prod[1];
         if (p_item >= a.nitems) return;
-        const int4 it = a.items[p_item];
+        const int4 it = a.items[a.order[p_item]];
         const int J = it.y + p_t;
         const int64_t lt = (int64_t)it.w + p_t;
         uint8_t* base = smem + (size_t)stage * STAGE;
@@ -1388,7 +1389,8 @@ __global__ void __launch_bounds__(256, 2) k_enum(const SymArgs a, const EnumOmeg
     __syncthreads();
     int stage = 0;
     uint32_t phase = 0;
-    for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
+    for (int slot = blockIdx.x; slot < a.nitems; slot += gridDim.x) {
+        const int item = a.order[slot];  // outputs are indexed by item: any schedule gives the same sums
         const int4 it = a.items[item];
         const int I = it.x;
         float xi[8][2 * DIM];
