@@ -17,7 +17,8 @@
 // conflict-free.
 //
 // Work item = strip segment: row block I and up to kSeg consecutive column
-// blocks J (the rank's tile range in triangle order).  i-side sums stay in
+// blocks J (the rank's tile range in triangle order); CTA b takes the items
+// order[b], order[b + grid], ... (longest first, dealt in snake order: item_order).  i-side sums stay in
 // registers over the segment; j-side sums are reduced across the 16 thread
 // rows through padded shared memory after every tile.  Outputs are fp32 tile
 // partials (j side, per tile) and fp64 segment partials (i side, stress),
