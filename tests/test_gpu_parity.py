@@ -296,6 +296,34 @@ def test_bitwise_determinism():
     assert np.array_equal(a.get_positions(), b.get_positions())
 
 
+def test_item_schedule_does_not_change_sums():
+    """The pair passes' work-item schedule (snake deal, FDL_ITEM_ORDER; read once per process)
+    only decides which CTA runs an item: outputs are indexed by item and tile, so the
+    round-robin schedule gives a bitwise-equal trajectory (C3, and C4's 3-D 16-bit split path)."""
+    import subprocess
+    import sys
+
+    code = ("import sys, numpy as np; sys.path.insert(0, %r)\n"
+            "from paper_1711_01228_b200 import fdl\n"
+            "from workloads import configs\n"
+            "for name in ('C3', 'C4'):\n"
+            "    cfg = configs.CONFIGS[name]; g = configs.graph_for(name)\n"
+            "    p = fdl.make_params(dim=cfg.dim, k=cfg.k_for(g.n), omega=cfg.omega, tol=cfg.tol, max_iter=cfg.max_iter)\n"
+            "    L = fdl.Layout.from_graph(g, params=p, init_pos=configs.positions_for(name, g.n, 1))\n"
+            "    for _ in range(3): L.step()\n"
+            "    np.save(sys.argv[1] + name + '.npy', L.get_positions())\n") % ROOT
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as td:
+        for order in ("snake", "rr"):
+            env = dict(os.environ, FDL_ITEM_ORDER=order)
+            subprocess.run([sys.executable, "-c", code, os.path.join(td, order)], env=env, check=True, cwd=ROOT)
+        for name in ("C3", "C4"):
+            a = np.load(os.path.join(td, "snake" + name + ".npy"))
+            b = np.load(os.path.join(td, "rr" + name + ".npy"))
+            assert np.array_equal(a, b), name
+
+
 # ------------------------------------------------- closed forms and edge cases
 def _run_small(g, dim, X0, omega=1.5, tol=1e-12, k=1.0, max_iter=2000):
     p = fdl.make_params(dim=dim, k=k, omega=omega, tol=tol, max_iter=max_iter, cg_rtol=1e-12)
