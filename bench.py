@@ -326,9 +326,9 @@ def run_gpu(args):
     force_dist = world == 1 and os.environ.get("FDL_BENCH_FORCE_DIST") == "1"
     if world > 1 or force_dist:
         import torch.distributed as dist
-        if os.environ.get("NCCL_DEBUG"):
-            # NCCL logs to stdout by default: keep stdout to the one JSON line of rank 0
-            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        # NCCL logs (and its version banner) go to stdout by default: keep stdout to the one
+        # JSON line of rank 0
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         os.environ.setdefault("RANK", "0")
