@@ -326,9 +326,6 @@ def run_gpu(args):
     force_dist = world == 1 and os.environ.get("FDL_BENCH_FORCE_DIST") == "1"
     if world > 1 or force_dist:
         import torch.distributed as dist
-        # NCCL logs (and its version banner) go to stdout by default: keep stdout to the one
-        # JSON line of rank 0
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         os.environ.setdefault("RANK", "0")
@@ -651,6 +648,15 @@ def run_gpu(args):
 
 def main():
     args = parse_args()
+    if args.gpus > 1 or "WORLD_SIZE" in os.environ or os.environ.get("FDL_BENCH_FORCE_DIST") == "1":
+        # NCCL logs go to stdout by default, and at NCCL_DEBUG=VERSION (this image's default) the
+        # version banner ignores NCCL_DEBUG_FILE: log the communicator INIT lines (they include
+        # the version and count the ranks) to stderr instead, so stdout is rank 0's one JSON
+        # line.  Set before torch loads NCCL (its debug setup reads these once)
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+            os.environ["NCCL_DEBUG"] = "INFO"
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         raise SystemExit(spawn_ranks(args))
     if args.plumbing_only:
